@@ -1,0 +1,49 @@
+"""BASELINE.json's five workloads as parameter sets.
+
+Pure data: no method arithmetic.  ``frames(cfg)`` draws the synthetic input of
+a config with the seeded generator in ``mosaic.py`` (seed = 1000 * index).
+Readings Q4 (n_levels counts block levels), Q12 (I = 4 where unstated) and Q13
+(gamma: 1 for c1-c3 and c5, 0 for the warm-started video c4) are DESIGN.md's.
+"""
+from __future__ import annotations
+
+from . import mosaic
+
+CONFIGS = {
+    "c1": dict(index=0, W=160, H=120, C=3, K=48, L=2, bpc=5, gamma=1, iters=2,
+               R=12, sigma=8.0, grad=0.0, frames=1),
+    "c2": dict(index=1, W=481, H=321, C=3, K=200, L=4, bpc=5, gamma=1, iters=4,
+               R=40, sigma=10.0, grad=30.0, frames=1),
+    "c3": dict(index=2, W=481, H=321, C=3, K=400, L=4, bpc=5, gamma=1, iters=4,
+               R=(40, 80), sigma=(5.0, 15.0), grad=30.0, frames=256),
+    "c4": dict(index=3, W=1920, H=1080, C=3, K=1000, L=5, bpc=5, gamma=0, iters=4,
+               R=150, sigma=8.0, grad=30.0, frames=64, clip=8),
+    "c5": dict(index=4, W=8192, H=8192, C=3, K=20000, L=6, bpc=8, gamma=1, iters=4,
+               R=5000, sigma=10.0, grad=30.0, frames=1),
+}
+
+
+def params(cfg: str) -> dict:
+    c = CONFIGS[cfg]
+    return dict(n_superpixels=c["K"], n_levels=c["L"], bins_per_channel=c["bpc"],
+                smoothness_prior=c["gamma"], iters_per_level=c["iters"])
+
+
+def frames(cfg: str, n: int | None = None):
+    """(n, H, W, C) uint8 frames of config ``cfg``."""
+    c = CONFIGS[cfg]
+    seed = 1000 * c["index"]
+    n = c["frames"] if n is None else n
+    if cfg == "c3":
+        return mosaic.mosaic_batch(n, c["W"], c["H"], c["R"][0], c["R"][1], c["sigma"][0],
+                                   c["sigma"][1], seed=seed, grad=c["grad"], C=c["C"])
+    if cfg == "c4":
+        f, _ = mosaic.moving_mosaic(n, c["W"], c["H"], c["R"], c["sigma"], seed=seed,
+                                    grad=c["grad"], C=c["C"])
+        return f
+    import numpy as np
+    out = np.empty((n, c["H"], c["W"], c["C"]), np.uint8)
+    for i in range(n):
+        out[i] = mosaic.mosaic(c["W"], c["H"], c["R"], c["sigma"], seed=seed + i, C=c["C"],
+                               grad=c["grad"])
+    return out
