@@ -1,0 +1,186 @@
+/*
+ * seeds.h -- C ABI of libseeds.so, the B200 (sm_100a) implementation of the
+ * SEEDS hill-climbing refinement of a grid superpixel partition
+ * (Van den Bergh et al., "SEEDS: Superpixels Extracted via Energy-Driven
+ * Sampling", arXiv 1309.3848).  Citations "PAPER.md:L" are lines of the
+ * paper's LaTeX source; "reading Qn/On" are DESIGN.md section 3.
+ *
+ * The problem: given an image I of N pixels and a
+ * target number K of superpixels, return a partition s : {1..N} -> {1..K}
+ * into 4-connected superpixels (the valid set S) that increases the energy
+ * E(s) = H(s) + gamma G(s) (Eq. 4) by hill climbing from a
+ * regular grid (S5.1), moving blocks of decreasing size
+ * and then single pixels between neighbouring superpixels (S5.2,
+ * PAPER.md:501-526), accepting a move by the histogram-intersection test of
+ * Proposition 1 and, with gamma = 1 at the pixel level, the
+ * boundary test of Proposition 2, and updating colour
+ * histograms incrementally (S5.3.3).
+ *
+ * Schedule: the coloured snapshot sub-sweeps of reading O7 -- every unit of
+ * one colour class is decided against the histograms as they stood at the
+ * start of the sub-sweep, then all accepted moves are applied.  The output
+ * is bit-identical to the CPU oracle (oracle/seeds_oracle.c, schedule COL,
+ * rule R1).
+ *
+ * Conventions shared by every entry point:
+ *  - All image / label / histogram pointers are DEVICE pointers unless the
+ *    name ends in _host.  The caller owns them and keeps them alive until the
+ *    work enqueued on `stream` has completed; the context owns everything
+ *    else.
+ *  - Enqueue-only: seeds_iterate / seeds_batch return after enqueueing work on
+ *    `stream` (a CUDA graph launch).  Kernel faults surface as SEEDS_ECUDA from
+ *    a later call that synchronises (seeds_sync, seeds_read_state,
+ *    seeds_destroy, the *_host entry points).
+ *  - A context is not thread-safe; use one context per host thread/stream.
+ *    Distinct contexts are independent.
+ *  - On an error return nothing was enqueued and *out pointers are unchanged.
+ */
+#ifndef SEEDS_H
+#define SEEDS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct seeds_ctx seeds_ctx; /* opaque; owns all device workspaces */
+
+typedef enum {
+    SEEDS_OK = 0,
+    SEEDS_EINVAL = -1, /* an argument is out of its documented range */
+    SEEDS_ENOMEM = -2, /* a device or pinned-host allocation failed */
+    SEEDS_ECUDA = -3,  /* a CUDA runtime error; seeds_last_error() has the text */
+    SEEDS_ENCCL = -4,  /* reserved for the row-band multi-GPU mode */
+    SEEDS_ESTATE = -5, /* call out of order (e.g. read_state before any run) */
+    SEEDS_ERANGE = -6  /* the problem exceeds an integer width (see seeds_create) */
+} seeds_status;
+
+/* Values derived at seeds_create (reading O2).  K_act != n_superpixels and
+ * levels_eff < n_levels are not errors. */
+typedef struct {
+    int width, height, channels;
+    int nx, ny;          /* superpixel grid: K_act = nx * ny */
+    int k_actual;
+    int levels_eff;      /* block levels actually used (finest blocks >= 1 px) */
+    int grid_x, grid_y;  /* level-0 block grid nx 2^L_eff x ny 2^L_eff */
+    int colour_period;   /* P: 2 (gamma = 0) or 3 (gamma = 1), reading Q11 */
+    int bins_total;      /* B = bins_per_channel ^ channels */
+    int bin_bytes;       /* 1 if B <= 256 else 2 */
+    int subsweeps;       /* 4 L_eff I + P^2 I sub-sweeps per cold frame */
+    int max_block_area;  /* largest top-level block, pixels */
+    int kernels_per_run; /* kernel launches of one cold run (graph kernel nodes) */
+    size_t workspace_bytes_per_frame;
+} seeds_info;
+
+/* seeds_create -- validate, derive the geometry and allocate a context on the
+ * current CUDA device.  Host-only; nothing is enqueued.
+ *   width, height      image size in pixels, >= 1, width*height < 2^31
+ *   channels           1..4 interleaved uint8 channels (HWC)
+ *   n_superpixels      requested K >= 1; the grid gets
+ *                      K_act = nx*ny (seeds_query)
+ *   n_levels           block levels below the superpixels, 0..15 (reading Q4:
+ *                      the pixel level is not counted); clamped to L_eff so
+ *                      that the finest blocks have >= 1 pixel
+ *   bins_per_channel   1..256 uniform bins per 8-bit channel (reading Q1);
+ *                      B = bins_per_channel^channels must be <= 4096
+ *   smoothness_prior   gamma in {0, 1}: 1 adds the 3x3 boundary term G at the
+ *                      pixel level
+ *   iters_per_level    I >= 0 iterations (each = every colour class once) per
+ *                      block level and at the pixel level (reading Q12);
+ *                      I = 0 returns the grid
+ *   out                receives the context
+ * Errors: SEEDS_EINVAL (an argument out of range, out == NULL),
+ *         SEEDS_ERANGE (K_act > 65535, or a top-level block of > 65535 px),
+ *         SEEDS_ECUDA, SEEDS_ENOMEM. */
+seeds_status seeds_create(int width, int height, int channels, int n_superpixels, int n_levels,
+                          int bins_per_channel, int smoothness_prior, int iters_per_level,
+                          seeds_ctx **out);
+
+/* seeds_iterate -- refine one frame from the grid (cold start).
+ *   image_u8    device, height*width*channels bytes, row stride width*channels
+ *   labels_out  device, height*width int32, receives s(i) in [0, K_act)
+ *   stream      cudaStream_t (NULL = legacy default stream) */
+seeds_status seeds_iterate(seeds_ctx *ctx, const uint8_t *image_u8, int32_t *labels_out,
+                           void *stream);
+
+/* seeds_batch -- refine n_frames independent frames of the context's size.
+ *   images       device, n_frames*height*width*channels bytes, frame-major
+ *   init_labels  NULL: every frame starts from the grid (cold).  Otherwise
+ *                device n_frames*height*width int32 labels in [0, K_act),
+ *                every superpixel non-empty and 4-connected: the frame's
+ *                histograms are recounted from them, the block phase is
+ *                skipped and only the pixel phase runs (warm start, reading
+ *                O9).  Labels violating the precondition give undefined
+ *                (but memory-safe) results.
+ *   labels_out   device, n_frames*height*width int32 */
+seeds_status seeds_batch(seeds_ctx *ctx, const uint8_t *images, int n_frames,
+                         const int32_t *init_labels, int32_t *labels_out, void *stream);
+
+/* seeds_batch_host -- seeds_batch from and to HOST memory: copies the frames
+ * in, runs, copies the labels out and synchronises `stream`.  Pinned host
+ * buffers give the fastest copies; pageable ones work.  init_labels_host may
+ * be NULL (cold). */
+seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
+                              const int32_t *init_labels_host, int32_t *labels_out_host,
+                              void *stream);
+
+/* seeds_query -- derived geometry and sizes (see seeds_info). */
+seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *out);
+
+/* seeds_read_state -- copy frame `frame`'s superpixel histograms and sizes as
+ * they stand after the last run (for parity tests, Eq. 6
+ * unnormalised):
+ *   hist_out   device, K_act*B int32, row k = counts of superpixel k per bin
+ *   sizes_out  device, K_act int32 (|A_k|)
+ * Either may be NULL.  Synchronises `stream`.  SEEDS_ESTATE before any run
+ * or if frame is outside the last batch. */
+seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int32_t *sizes_out,
+                              void *stream);
+
+/* seeds_debug_limit -- stop every later run after max_subsweeps sub-sweeps
+ * (the block maps are still pushed down and expanded, so the labels are the
+ * valid partition reached at that point); -1 turns the limit off.  Used to
+ * bisect a divergence against the oracle's max_subsweeps. */
+seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps);
+
+/* seeds_stats -- accepted moves per sub-sweep of frame `frame` of the last
+ * run: moves_out[s] for s < min(cap, subsweeps).  Host pointer.  Synchronises.
+ * For a block sub-sweep the count is of histogram delta entries (one per
+ * non-empty bin of each moved block); for a pixel sub-sweep, of moved pixels. */
+seeds_status seeds_stats(seeds_ctx *ctx, int frame, int32_t *moves_out_host, int cap, void *stream);
+
+/* Kernel classes timed by seeds_profile. */
+enum {
+    SEEDS_KIND_SEED = 0,  /* quantise + initial labels + histograms */
+    SEEDS_KIND_BLOCK = 1, /* one block-level sub-sweep */
+    SEEDS_KIND_PIXEL = 2, /* one pixel-level sub-sweep */
+    SEEDS_KIND_EMIT = 3,  /* labels -> int32 output */
+    SEEDS_KIND_COUNT = 4
+};
+
+/* seeds_profile -- enable (1) or disable (0) per-kernel device timing: later
+ * runs record a CUDA event pair around every seed / block / pixel / emit
+ * launch inside the captured graph.  Resets the accumulators. */
+seeds_status seeds_profile(seeds_ctx *ctx, int enable);
+
+/* seeds_profile_collect -- synchronise `stream`, add the event durations of the
+ * last run to per-kind accumulators and return them: ms_out[SEEDS_KIND_COUNT]
+ * total milliseconds and launches_out[SEEDS_KIND_COUNT] launch counts (host
+ * pointers, either may be NULL).  Call once after every profiled run. */
+seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out, long long *launches_out);
+
+/* seeds_sync -- wait for `stream` and report any pending CUDA error. */
+seeds_status seeds_sync(seeds_ctx *ctx, void *stream);
+
+/* seeds_destroy -- synchronise the context's work and free it (NULL is ok). */
+void seeds_destroy(seeds_ctx *ctx);
+
+const char *seeds_status_string(seeds_status s);
+const char *seeds_last_error(const seeds_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEEDS_H */

@@ -1,0 +1,632 @@
+// seeds_engine.cu -- host engine and C ABI of libseeds.so (include/seeds.h).
+//
+// Integer geometry, workspaces, the sub-sweep schedule and its CUDA-graph
+// capture.  Every step of the hot path runs in the kernels of
+// seeds_kernels.cuh; this file only allocates, launches and copies.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../include/seeds.h"
+#include "seeds_kernels.cuh"
+
+using namespace seeds;
+
+namespace {
+
+struct GraphKey {
+    const void *img = nullptr;
+    const void *init = nullptr;
+    void *out = nullptr;
+    int nf = -1;
+    int limit = -2;
+    bool prof = false;
+    bool operator==(const GraphKey &o) const
+    {
+        return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof;
+    }
+};
+
+}  // namespace
+
+struct seeds_ctx {
+    // arguments
+    int W, H, C, Kreq, Lreq, bpc, gamma, iters;
+    // derived (reading O2)
+    int nx, ny, K, L, GX, GY, B, bb, P, amax, S;
+    long long N;
+    int dev;
+    // level-0 block geometry
+    std::vector<int> colstart, rowstart, bxof, byof;
+    int *d_colstart = nullptr, *d_rowstart = nullptr, *d_bxof = nullptr, *d_byof = nullptr;
+    // per-frame workspaces (capacity cap_frames)
+    int cap_frames = 0;
+    void *d_bins = nullptr;
+    uint16_t *d_lab = nullptr;
+    uint16_t *d_M[2] = {nullptr, nullptr};
+    int *d_H[2] = {nullptr, nullptr};
+    int *d_A[2] = {nullptr, nullptr};
+    Rec *d_rec[2] = {nullptr, nullptr};
+    int *d_cnt = nullptr;    // (S + 1) rows x cap_frames: delta entries per sub-sweep
+    int *d_moves = nullptr;  // (S + 1) rows x cap_frames: accepted units per sub-sweep
+    long long map_fs = 0, H_fs = 0, rec_fs = 0;
+    // host staging for the *_host entry point
+    int stage_frames = 0;
+    uint8_t *d_img_stage = nullptr;
+    int32_t *d_init_stage = nullptr, *d_out_stage = nullptr;
+    // graph
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    GraphKey key;
+    // state of the last run
+    int limit = -1;
+    int last_nf = 0;
+    int last_final = 0;  // H buffer holding the final state
+    int last_done = 0;   // sub-sweeps run
+    bool ran = false;
+    char err[512] = {0};
+    // optional per-kernel timing: event pairs captured into the graph
+    bool prof = false;
+    std::vector<cudaEvent_t> ev;   // 2 per profiled launch
+    std::vector<int> ev_kind;      // kind of each pair
+    int ev_used = 0;
+    double prof_ms[SEEDS_KIND_COUNT] = {0};
+    long long prof_n[SEEDS_KIND_COUNT] = {0};
+    int kernels_per_run = 0;
+};
+
+static seeds_status cuda_fail(seeds_ctx *c, cudaError_t e, const char *what)
+{
+    if (c) snprintf(c->err, sizeof c->err, "%s: %s", what, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SEEDS_ENOMEM : SEEDS_ECUDA;
+}
+
+#define CK(call)                                                    \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);   \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Geometry (reading O2).  nx = sqrt(K W / H) rounded half up (exact integer
+// test), ny = K / nx rounded half up, both clamped; L_eff = the largest level
+// count whose finest blocks still have >= 1 pixel in each direction.
+// ---------------------------------------------------------------------------
+static void derive_geometry(seeds_ctx *c)
+{
+    const long long KW4 = 4LL * c->Kreq * c->W;
+    long long nx = (long long)std::floor(std::sqrt((double)c->Kreq * c->W / c->H) + 0.5);
+    if (nx < 1) nx = 1;
+    // exact correction: want (2nx-1)^2 H <= 4KW < (2nx+1)^2 H
+    while (nx > 1 && (2 * nx - 1) * (2 * nx - 1) * (long long)c->H > KW4) nx--;
+    while ((2 * nx + 1) * (2 * nx + 1) * (long long)c->H <= KW4) nx++;
+    nx = std::min<long long>(nx, c->W);
+    long long ny = (2LL * c->Kreq + nx) / (2 * nx);  // floor(K/nx + 1/2)
+    ny = std::max<long long>(1, std::min<long long>(ny, c->H));
+    c->nx = (int)nx;
+    c->ny = (int)ny;
+    c->K = c->nx * c->ny;
+    int L = c->Lreq;
+    while (L > 0 && (((long long)c->nx << L) > c->W || ((long long)c->ny << L) > c->H)) L--;
+    c->L = L;
+    c->GX = c->nx << L;
+    c->GY = c->ny << L;
+    c->B = 1;
+    for (int i = 0; i < c->C; i++) c->B *= c->bpc;
+    c->bb = c->B <= 256 ? 1 : 2;
+    c->P = c->gamma ? 3 : 2;
+    c->S = 4 * c->L * c->iters + c->P * c->P * c->iters;
+    c->N = (long long)c->W * c->H;
+    c->colstart.resize(c->GX + 1);
+    c->rowstart.resize(c->GY + 1);
+    for (int i = 0; i <= c->GX; i++) c->colstart[i] = (int)((long long)i * c->W / c->GX);
+    for (int j = 0; j <= c->GY; j++) c->rowstart[j] = (int)((long long)j * c->H / c->GY);
+    c->bxof.resize(c->W);
+    c->byof.resize(c->H);
+    for (int i = 0; i < c->GX; i++)
+        for (int x = c->colstart[i]; x < c->colstart[i + 1]; x++) c->bxof[x] = i;
+    for (int j = 0; j < c->GY; j++)
+        for (int y = c->rowstart[j]; y < c->rowstart[j + 1]; y++) c->byof[y] = j;
+    // largest block at the top block level (the largest alpha of any move)
+    const int top = c->L > 0 ? c->L - 1 : 0;
+    int mw = 0, mh = 0;
+    for (int i = 0; i < (c->GX >> top); i++)
+        mw = std::max(mw, c->colstart[(i + 1) << top] - c->colstart[i << top]);
+    for (int j = 0; j < (c->GY >> top); j++)
+        mh = std::max(mh, c->rowstart[(j + 1) << top] - c->rowstart[j << top]);
+    c->amax = mw * mh;
+    c->kernels_per_run = 2 + c->P * c->P * c->iters + (c->L > 0 ? 2 + (c->L - 1) + 4 * c->L * c->iters : 0);
+}
+
+// Event pair around a launch when profiling (recorded into the captured graph).
+static cudaError_t prof_begin(seeds_ctx *c, cudaStream_t st, int kind)
+{
+    if (!c->prof) return cudaSuccess;
+    const size_t need = 2 * (size_t)(c->ev_used + 1);
+    while (c->ev.size() < need) {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreate(&e);
+        if (r != cudaSuccess) return r;
+        c->ev.push_back(e);
+    }
+    if (c->ev_kind.size() < (size_t)c->ev_used + 1) c->ev_kind.resize(c->ev_used + 1);
+    c->ev_kind[c->ev_used] = kind;
+    return cudaEventRecordWithFlags(c->ev[2 * c->ev_used], st, cudaEventRecordExternal);
+}
+
+static cudaError_t prof_end(seeds_ctx *c, cudaStream_t st)
+{
+    if (!c->prof) return cudaSuccess;
+    cudaError_t r = cudaEventRecordWithFlags(c->ev[2 * c->ev_used + 1], st, cudaEventRecordExternal);
+    c->ev_used++;
+    return r;
+}
+
+static int max_block_area(const seeds_ctx *c, int l)
+{
+    int mw = 0, mh = 0;
+    for (int i = 0; i < (c->GX >> l); i++) mw = std::max(mw, c->colstart[(i + 1) << l] - c->colstart[i << l]);
+    for (int j = 0; j < (c->GY >> l); j++) mh = std::max(mh, c->rowstart[(j + 1) << l] - c->rowstart[j << l]);
+    return mw * mh;
+}
+
+// Removable ring masks (reading Q8): label positions 0..7 around the unit
+// (N, NE, E, SE, S, SW, W, NW); union consecutive same-label ring cells (they
+// are 4-adjacent) and require that the edge cells carrying the label are all
+// in one union and that there is at least one.
+static void build_removable(uint32_t lut[8])
+{
+    memset(lut, 0, 8 * sizeof(uint32_t));
+    for (int m = 0; m < 256; m++) {
+        int comp[8];
+        for (int r = 0; r < 8; r++) comp[r] = r;
+        auto find = [&](int a) {
+            while (comp[a] != a) a = comp[a];
+            return a;
+        };
+        for (int r = 0; r < 8; r++) {
+            const int s = (r + 1) & 7;
+            if ((m >> r & 1) && (m >> s & 1)) comp[find(r)] = find(s);
+        }
+        int root = -1;
+        bool ok = true;
+        for (int r = 0; r < 8; r += 2) {
+            if (!(m >> r & 1)) continue;
+            if (root < 0) root = find(r);
+            else if (find(r) != root) ok = false;
+        }
+        if (root >= 0 && ok) lut[m >> 5] |= 1u << (m & 31);
+    }
+}
+
+static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
+{
+    if (nf <= ctx->cap_frames) return SEEDS_OK;
+    CK(cudaDeviceSynchronize());
+    if (ctx->exec) {  // the cached graph points at the buffers freed below
+        cudaGraphExecDestroy(ctx->exec);
+        ctx->exec = nullptr;
+        ctx->key = GraphKey();
+    }
+    auto release = [](void *&p) {
+        if (p) cudaFree(p);
+        p = nullptr;
+    };
+    release(ctx->d_bins);
+    release((void *&)ctx->d_lab);
+    for (int i = 0; i < 2; i++) {
+        release((void *&)ctx->d_M[i]);
+        release((void *&)ctx->d_H[i]);
+        release((void *&)ctx->d_A[i]);
+        release((void *&)ctx->d_rec[i]);
+    }
+    release((void *&)ctx->d_cnt);
+    release((void *&)ctx->d_moves);
+    ctx->cap_frames = 0;
+    const size_t F = nf;
+    ctx->map_fs = ((long long)ctx->GX * ctx->GY + 7) / 8 * 8;
+    ctx->H_fs = (long long)ctx->K * ctx->B;
+    ctx->rec_fs = ctx->N;
+    CK(cudaMalloc(&ctx->d_bins, F * ctx->N * ctx->bb + 16));
+    CK(cudaMalloc(&ctx->d_lab, F * ctx->N * 2 + 16));
+    for (int i = 0; i < 2; i++) {
+        CK(cudaMalloc(&ctx->d_M[i], F * ctx->map_fs * 2));
+        CK(cudaMalloc(&ctx->d_H[i], F * ctx->H_fs * 4));
+        CK(cudaMalloc(&ctx->d_A[i], F * ctx->K * 4));
+        CK(cudaMalloc(&ctx->d_rec[i], F * ctx->rec_fs * sizeof(Rec)));
+    }
+    CK(cudaMalloc(&ctx->d_cnt, (size_t)(ctx->S + 1) * F * 4));
+    CK(cudaMalloc(&ctx->d_moves, (size_t)(ctx->S + 1) * F * 4));
+    ctx->cap_frames = nf;
+    return SEEDS_OK;
+}
+
+static dim3 grid1(long long work, int threads, int frames, long long maxblocks = 148LL * 16)
+{
+    long long b = (work + threads - 1) / threads;
+    b = std::max(1LL, std::min(b, maxblocks));
+    return dim3((unsigned)b, (unsigned)frames);
+}
+
+template <int G, typename BinT>
+static cudaError_t launch_block(seeds_ctx *ctx, const SweepParams &p, int nf, cudaStream_t st)
+{
+    const size_t per_group = (2 * (size_t)p.B + 2) * 4;
+    int gpc = 256 / G;
+    while (gpc > 1 && gpc * per_group > 160 * 1024) gpc >>= 1;
+    const size_t shm = gpc * per_group;
+    auto kern = k_block<G, BinT>;
+    const long long units = (long long)p.uw * p.uh;
+    const long long blocks = std::max(1LL, std::min((units + gpc - 1) / gpc, 148LL * 32));
+    kern<<<dim3((unsigned)blocks, nf), gpc * G, shm, st>>>(p, gpc);
+    return cudaGetLastError();
+}
+
+template <typename BinT>
+static cudaError_t launch_pixel(seeds_ctx *ctx, const SweepParams &p, int nf, cudaStream_t st)
+{
+    const long long units = (long long)p.uw * p.uh;
+    const dim3 g = grid1(units, 256, nf, 148LL * 32);
+    if (ctx->gamma) k_pixel<BinT, 1, 3><<<g, 256, 0, st>>>(p);
+    else k_pixel<BinT, 0, 2><<<g, 256, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+// Enqueue one whole run (cold or warm) of nf frames on stream st.
+template <typename BinT>
+static seeds_status enqueue(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
+                            cudaStream_t st)
+{
+    const bool warm = init != nullptr;
+    const int bufsz = (int)(ctx->S + 1) * nf;
+    CK(cudaMemsetAsync(ctx->d_cnt, 0, (size_t)bufsz * 4, st));
+    CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)bufsz * 4, st));
+    CK(cudaMemsetAsync(ctx->d_H[0], 0, (size_t)nf * ctx->H_fs * 4, st));
+    CK(cudaMemsetAsync(ctx->d_A[0], 0, (size_t)nf * ctx->K * 4, st));
+    const bool blocks = !warm && ctx->L > 0;
+    ctx->ev_used = 0;
+    CK(prof_begin(ctx, st, SEEDS_KIND_SEED));
+    {
+        const dim3 g = grid1(ctx->N, 256, nf);
+        k_seed<BinT><<<g, 256, 0, st>>>(img, ctx->W, ctx->C, ctx->bpc, ctx->N, ctx->L, ctx->nx, ctx->B,
+                                        ctx->d_bxof, ctx->d_byof, init, (BinT *)ctx->d_bins,
+                                        blocks ? nullptr : ctx->d_lab, ctx->d_H[0], ctx->d_A[0], ctx->H_fs,
+                                        ctx->K);
+        CK(cudaGetLastError());
+    }
+    CK(prof_end(ctx, st));
+    CK(cudaMemcpyAsync(ctx->d_H[1], ctx->d_H[0], (size_t)nf * ctx->H_fs * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->d_A[1], ctx->d_A[0], (size_t)nf * ctx->K * 4, cudaMemcpyDeviceToDevice, st));
+
+    SweepParams p{};
+    p.W = ctx->W; p.H = ctx->H; p.B = ctx->B; p.K = ctx->K;
+    p.bins = ctx->d_bins;
+    p.N = ctx->N; p.H_fs = ctx->H_fs; p.rec_fs = ctx->rec_fs;
+    p.colstart = ctx->d_colstart; p.rowstart = ctx->d_rowstart;
+    int s = 0;
+    const int limit = ctx->limit;
+    auto set_sweep = [&](int sidx) {
+        p.Hx = ctx->d_H[sidx & 1]; p.Ax = ctx->d_A[sidx & 1];
+        p.Hy = ctx->d_H[(sidx + 1) & 1]; p.Ay = ctx->d_A[(sidx + 1) & 1];
+        p.rec_prev = ctx->d_rec[(sidx + 1) & 1]; p.cnt_prev = ctx->d_cnt + (size_t)sidx * nf;
+        p.rec_out = ctx->d_rec[sidx & 1]; p.cnt_out = ctx->d_cnt + (size_t)(sidx + 1) * nf;
+        p.moves_out = ctx->d_moves + (size_t)(sidx + 1) * nf;
+    };
+    int mb = 0;  // map buffer holding the current level
+    if (blocks) {
+        const int wt = ctx->GX >> (ctx->L - 1), ht = ctx->GY >> (ctx->L - 1);
+        k_topmap<<<grid1((long long)wt * ht, 256, nf), 256, 0, st>>>(ctx->d_M[0], wt, ht, ctx->map_fs, ctx->nx);
+        CK(cudaGetLastError());
+        for (int l = ctx->L - 1; l >= 0; l--) {
+            const int w = ctx->GX >> l, h = ctx->GY >> l;
+            p.w = w; p.h = h; p.level = l;
+            p.map = ctx->d_M[mb]; p.map_fs = ctx->map_fs;
+            const int am = max_block_area(ctx, l);
+            for (int it = 0; it < ctx->iters; it++)
+                for (int c = 0; c < 4; c++) {
+                    if (limit >= 0 && s >= limit) break;
+                    p.cx = c & 1; p.cy = c >> 1;
+                    p.uw = (w - p.cx + 1) / 2; p.uh = (h - p.cy + 1) / 2;
+                    set_sweep(s);
+                    CK(prof_begin(ctx, st, SEEDS_KIND_BLOCK));
+                    cudaError_t e = am > 8 ? launch_block<32, BinT>(ctx, p, nf, st)
+                                           : launch_block<8, BinT>(ctx, p, nf, st);
+                    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_block launch");
+                    CK(prof_end(ctx, st));
+                    s++;
+                }
+            if (l > 0) {
+                const int wc = ctx->GX >> (l - 1), hc = ctx->GY >> (l - 1);
+                k_pushdown<<<grid1((long long)wc * hc, 256, nf), 256, 0, st>>>(ctx->d_M[mb], ctx->d_M[mb ^ 1], wc,
+                                                                             hc, ctx->map_fs);
+                CK(cudaGetLastError());
+                mb ^= 1;
+            }
+        }
+        k_expand<<<grid1(ctx->N, 256, nf), 256, 0, st>>>(ctx->d_M[mb], ctx->d_lab, ctx->W, ctx->N, ctx->GX,
+                                                         ctx->map_fs, ctx->d_bxof, ctx->d_byof);
+        CK(cudaGetLastError());
+    }
+    // pixel level
+    p.w = ctx->W; p.h = ctx->H; p.level = 0;
+    p.map = ctx->d_lab; p.map_fs = ctx->N;
+    for (int it = 0; it < ctx->iters; it++)
+        for (int c = 0; c < ctx->P * ctx->P; c++) {
+            if (limit >= 0 && s >= limit) break;
+            p.cx = c % ctx->P; p.cy = c / ctx->P;
+            p.uw = (ctx->W - p.cx + ctx->P - 1) / ctx->P;
+            p.uh = (ctx->H - p.cy + ctx->P - 1) / ctx->P;
+            set_sweep(s);
+            CK(prof_begin(ctx, st, SEEDS_KIND_PIXEL));
+            cudaError_t e = launch_pixel<BinT>(ctx, p, nf, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "k_pixel launch");
+            CK(prof_end(ctx, st));
+            s++;
+        }
+    CK(prof_begin(ctx, st, SEEDS_KIND_EMIT));
+    k_emit<<<grid1(ctx->N * nf, 256, 1), 256, 0, st>>>(ctx->d_lab, out, ctx->N * nf);
+    CK(cudaGetLastError());
+    CK(prof_end(ctx, st));
+    ctx->last_done = s;
+    ctx->last_final = s & 1;
+    return SEEDS_OK;
+}
+
+static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
+                        cudaStream_t st)
+{
+    seeds_status r = ensure_frames(ctx, nf);
+    if (r != SEEDS_OK) return r;
+    GraphKey key;
+    key.img = img; key.init = init; key.out = out; key.nf = nf; key.limit = ctx->limit; key.prof = ctx->prof;
+    if (!ctx->exec || !(key == ctx->key)) {
+        if (ctx->exec) {
+            cudaGraphExecDestroy(ctx->exec);
+            ctx->exec = nullptr;
+        }
+        CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+        seeds_status er = ctx->bb == 1 ? enqueue<uint8_t>(ctx, img, init, out, nf, ctx->cap_stream)
+                                       : enqueue<uint16_t>(ctx, img, init, out, nf, ctx->cap_stream);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
+        if (er != SEEDS_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return er;
+        }
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+        e = cudaGraphInstantiate(&ctx->exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+        ctx->key = key;
+    }
+    CK(cudaGraphLaunch(ctx->exec, st));
+    ctx->last_nf = nf;
+    ctx->ran = true;
+    return SEEDS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+seeds_status seeds_create(int width, int height, int channels, int n_superpixels, int n_levels,
+                          int bins_per_channel, int smoothness_prior, int iters_per_level, seeds_ctx **out)
+{
+    seeds_ctx *ctx = nullptr;
+    if (!out || width < 1 || height < 1 || channels < 1 || channels > 4 || n_superpixels < 1 || n_levels < 0 ||
+        n_levels > 15 || bins_per_channel < 1 || bins_per_channel > 256 ||
+        (smoothness_prior != 0 && smoothness_prior != 1) || iters_per_level < 0)
+        return SEEDS_EINVAL;
+    if ((long long)width * height >= (1LL << 31)) return SEEDS_ERANGE;
+    long long B = 1;
+    for (int i = 0; i < channels; i++) B *= bins_per_channel;
+    if (B > 4096) return SEEDS_EINVAL;
+    ctx = new seeds_ctx();
+    ctx->W = width; ctx->H = height; ctx->C = channels; ctx->Kreq = n_superpixels; ctx->Lreq = n_levels;
+    ctx->bpc = bins_per_channel; ctx->gamma = smoothness_prior; ctx->iters = iters_per_level;
+    derive_geometry(ctx);
+    if (ctx->K > 65535 || ctx->amax > 65535) {
+        delete ctx;
+        return SEEDS_ERANGE;
+    }
+    cudaError_t e = cudaGetDevice(&ctx->dev);
+    if (e == cudaSuccess) {
+        uint32_t lut[8];
+        build_removable(lut);
+        e = cudaMemcpyToSymbol(c_removable, lut, sizeof lut);
+    }
+    auto up = [&](int *&d, const std::vector<int> &h) {
+        if (e != cudaSuccess) return;
+        e = cudaMalloc(&d, h.size() * sizeof(int));
+        if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice);
+    };
+    up(ctx->d_colstart, ctx->colstart);
+    up(ctx->d_rowstart, ctx->rowstart);
+    up(ctx->d_bxof, ctx->bxof);
+    up(ctx->d_byof, ctx->byof);
+    // shared-memory opt-in of the block kernels (set outside any graph capture)
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block<32, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block<8, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block<32, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block<8, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        seeds_status st = e == cudaErrorMemoryAllocation ? SEEDS_ENOMEM : SEEDS_ECUDA;
+        seeds_destroy(ctx);
+        return st;
+    }
+    *out = ctx;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_batch(seeds_ctx *ctx, const uint8_t *images, int n_frames, const int32_t *init_labels,
+                         int32_t *labels_out, void *stream)
+{
+    if (!ctx || !images || !labels_out || n_frames < 1 || n_frames > 65535) return SEEDS_EINVAL;
+    return run(ctx, images, init_labels, labels_out, n_frames, (cudaStream_t)stream);
+}
+
+seeds_status seeds_iterate(seeds_ctx *ctx, const uint8_t *image_u8, int32_t *labels_out, void *stream)
+{
+    return seeds_batch(ctx, image_u8, 1, nullptr, labels_out, stream);
+}
+
+seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
+                              const int32_t *init_labels_host, int32_t *labels_out_host, void *stream)
+{
+    if (!ctx || !images_host || !labels_out_host || n_frames < 1 || n_frames > 65535) return SEEDS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_frames > ctx->stage_frames) {
+        CK(cudaStreamSynchronize(st));
+        if (ctx->d_img_stage) cudaFree(ctx->d_img_stage);
+        if (ctx->d_out_stage) cudaFree(ctx->d_out_stage);
+        if (ctx->d_init_stage) cudaFree(ctx->d_init_stage);
+        ctx->d_img_stage = nullptr; ctx->d_out_stage = nullptr; ctx->d_init_stage = nullptr;
+        ctx->stage_frames = 0;
+        CK(cudaMalloc(&ctx->d_img_stage, (size_t)n_frames * ctx->N * ctx->C));
+        CK(cudaMalloc(&ctx->d_out_stage, (size_t)n_frames * ctx->N * 4));
+        CK(cudaMalloc(&ctx->d_init_stage, (size_t)n_frames * ctx->N * 4));
+        ctx->stage_frames = n_frames;
+    }
+    CK(cudaMemcpyAsync(ctx->d_img_stage, images_host, (size_t)n_frames * ctx->N * ctx->C,
+                       cudaMemcpyHostToDevice, st));
+    const int32_t *init = nullptr;
+    if (init_labels_host) {
+        CK(cudaMemcpyAsync(ctx->d_init_stage, init_labels_host, (size_t)n_frames * ctx->N * 4,
+                           cudaMemcpyHostToDevice, st));
+        init = ctx->d_init_stage;
+    }
+    seeds_status r = run(ctx, ctx->d_img_stage, init, ctx->d_out_stage, n_frames, st);
+    if (r != SEEDS_OK) return r;
+    CK(cudaMemcpyAsync(labels_out_host, ctx->d_out_stage, (size_t)n_frames * ctx->N * 4, cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    return SEEDS_OK;
+}
+
+seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *o)
+{
+    if (!ctx || !o) return SEEDS_EINVAL;
+    o->width = ctx->W; o->height = ctx->H; o->channels = ctx->C;
+    o->nx = ctx->nx; o->ny = ctx->ny; o->k_actual = ctx->K; o->levels_eff = ctx->L;
+    o->grid_x = ctx->GX; o->grid_y = ctx->GY; o->colour_period = ctx->P; o->bins_total = ctx->B;
+    o->bin_bytes = ctx->bb; o->subsweeps = ctx->S; o->max_block_area = ctx->amax;
+    o->kernels_per_run = ctx->kernels_per_run;
+    o->workspace_bytes_per_frame = (size_t)ctx->N * (ctx->bb + 2) +
+                                   (size_t)(((long long)ctx->GX * ctx->GY + 7) / 8 * 8) * 4 +
+                                   (size_t)ctx->K * (ctx->B + 1) * 8 + (size_t)ctx->N * sizeof(Rec) * 2;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int32_t *sizes_out, void *stream)
+{
+    if (!ctx) return SEEDS_EINVAL;
+    if (!ctx->ran || frame < 0 || frame >= ctx->last_nf) return SEEDS_ESTATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int b = ctx->last_final;
+    if (hist_out)
+        CK(cudaMemcpyAsync(hist_out, ctx->d_H[b] + (size_t)frame * ctx->H_fs, (size_t)ctx->H_fs * 4,
+                           cudaMemcpyDeviceToDevice, st));
+    if (sizes_out)
+        CK(cudaMemcpyAsync(sizes_out, ctx->d_A[b] + (size_t)frame * ctx->K, (size_t)ctx->K * 4,
+                           cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return SEEDS_OK;
+}
+
+seeds_status seeds_stats(seeds_ctx *ctx, int frame, int32_t *moves_out_host, int cap, void *stream)
+{
+    if (!ctx || !moves_out_host || cap < 0) return SEEDS_EINVAL;
+    if (!ctx->ran || frame < 0 || frame >= ctx->last_nf) return SEEDS_ESTATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaStreamSynchronize(st));
+    const int n = std::min(cap, ctx->last_done);
+    std::vector<int32_t> all((size_t)(ctx->S + 1) * ctx->last_nf);
+    CK(cudaMemcpy(all.data(), ctx->d_moves, all.size() * 4, cudaMemcpyDeviceToHost));
+    for (int s = 0; s < n; s++) moves_out_host[s] = all[(size_t)(s + 1) * ctx->last_nf + frame];
+    return SEEDS_OK;
+}
+
+seeds_status seeds_profile(seeds_ctx *ctx, int enable)
+{
+    if (!ctx) return SEEDS_EINVAL;
+    ctx->prof = enable != 0;
+    for (int k = 0; k < SEEDS_KIND_COUNT; k++) {
+        ctx->prof_ms[k] = 0;
+        ctx->prof_n[k] = 0;
+    }
+    return SEEDS_OK;
+}
+
+seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out, long long *launches_out)
+{
+    if (!ctx) return SEEDS_EINVAL;
+    if (ctx->prof && ctx->ran) {
+        CK(cudaStreamSynchronize((cudaStream_t)stream));
+        for (int i = 0; i < ctx->ev_used; i++) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ctx->ev[2 * i], ctx->ev[2 * i + 1]));
+            ctx->prof_ms[ctx->ev_kind[i]] += ms;
+            ctx->prof_n[ctx->ev_kind[i]] += 1;
+        }
+    }
+    for (int k = 0; k < SEEDS_KIND_COUNT; k++) {
+        if (ms_out) ms_out[k] = ctx->prof_ms[k];
+        if (launches_out) launches_out[k] = ctx->prof_n[k];
+    }
+    return SEEDS_OK;
+}
+
+seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps)
+{
+    if (!ctx || max_subsweeps < -1) return SEEDS_EINVAL;
+    ctx->limit = max_subsweeps;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_sync(seeds_ctx *ctx, void *stream)
+{
+    if (!ctx) return SEEDS_EINVAL;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    CK(cudaGetLastError());
+    return SEEDS_OK;
+}
+
+void seeds_destroy(seeds_ctx *ctx)
+{
+    if (!ctx) return;
+    cudaDeviceSynchronize();
+    if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
+    void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
+                    ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1],
+                    ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage,
+                    ctx->d_init_stage, ctx->d_out_stage};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    delete ctx;
+}
+
+const char *seeds_status_string(seeds_status s)
+{
+    switch (s) {
+    case SEEDS_OK: return "ok";
+    case SEEDS_EINVAL: return "invalid argument";
+    case SEEDS_ENOMEM: return "out of memory";
+    case SEEDS_ECUDA: return "CUDA error";
+    case SEEDS_ENCCL: return "NCCL error";
+    case SEEDS_ESTATE: return "invalid state";
+    case SEEDS_ERANGE: return "problem exceeds an integer width";
+    }
+    return "unknown status";
+}
+
+const char *seeds_last_error(const seeds_ctx *ctx) { return ctx ? ctx->err : "no context"; }
+
+}  // extern "C"

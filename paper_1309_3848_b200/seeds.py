@@ -1,0 +1,219 @@
+"""Python binding of libseeds.so (include/seeds.h): argument marshalling only.
+
+Every step of the refinement runs in the CUDA kernels behind the C ABI; this
+module converts torch tensors / numpy arrays to pointers and streams.  There
+is no CPU fallback: if the library is missing or no CUDA device is present,
+the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libseeds.so")
+
+_STATUS = {0: "ok", -1: "invalid argument", -2: "out of memory", -3: "CUDA error",
+           -4: "NCCL error", -5: "invalid state", -6: "problem exceeds an integer width"}
+
+EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "seeds_query",
+           "seeds_read_state", "seeds_debug_limit", "seeds_stats", "seeds_sync", "seeds_destroy",
+           "seeds_profile", "seeds_profile_collect",
+           "seeds_status_string", "seeds_last_error"]
+
+
+class SeedsError(RuntimeError):
+    def __init__(self, status: int, detail: str = ""):
+        super().__init__(f"{_STATUS.get(status, status)}" + (f": {detail}" if detail else ""))
+        self.status = status
+
+
+class Info(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "width", "height", "channels", "nx", "ny", "k_actual", "levels_eff", "grid_x", "grid_y",
+        "colour_period", "bins_total", "bin_bytes", "subsweeps", "max_block_area",
+        "kernels_per_run")] + [
+        ("workspace_bytes_per_frame", ctypes.c_size_t)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libseeds.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built: run `python -m paper_1309_3848_b200.build`")
+    lib = ctypes.CDLL(path)
+    vp, i = ctypes.c_void_p, ctypes.c_int
+    sig = {
+        "seeds_create": ([i] * 8 + [ctypes.POINTER(vp)], i),
+        "seeds_iterate": ([vp, vp, vp, vp], i),
+        "seeds_batch": ([vp, vp, i, vp, vp, vp], i),
+        "seeds_batch_host": ([vp, vp, i, vp, vp, vp], i),
+        "seeds_query": ([vp, ctypes.POINTER(Info)], i),
+        "seeds_read_state": ([vp, i, vp, vp, vp], i),
+        "seeds_debug_limit": ([vp, i], i),
+        "seeds_stats": ([vp, i, vp, i, vp], i),
+        "seeds_sync": ([vp, vp], i),
+        "seeds_profile": ([vp, i], i),
+        "seeds_profile_collect": ([vp, vp, vp, vp], i),
+        "seeds_destroy": ([vp], None),
+        "seeds_status_string": ([i], ctypes.c_char_p),
+        "seeds_last_error": ([vp], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+@dataclass
+class Geometry:
+    nx: int
+    ny: int
+    k_actual: int
+    levels_eff: int
+    grid_x: int
+    grid_y: int
+    colour_period: int
+    bins_total: int
+    bin_bytes: int
+    subsweeps: int
+    max_block_area: int
+    kernels_per_run: int
+    workspace_bytes_per_frame: int
+
+
+class Seeds:
+    """One refinement context (seeds_create ... seeds_destroy)."""
+
+    def __init__(self, width: int, height: int, channels: int, n_superpixels: int, n_levels: int,
+                 bins_per_channel: int, smoothness_prior: int, iters_per_level: int):
+        self._lib = load()
+        self._ctx = ctypes.c_void_p()
+        st = self._lib.seeds_create(width, height, channels, n_superpixels, n_levels,
+                                    bins_per_channel, int(smoothness_prior), iters_per_level,
+                                    ctypes.byref(self._ctx))
+        if st != 0:
+            raise SeedsError(st)
+        self.width, self.height, self.channels = width, height, channels
+        info = Info()
+        self._check(self._lib.seeds_query(self._ctx, ctypes.byref(info)))
+        self.info = Geometry(**{f: getattr(info, f) for f in Geometry.__dataclass_fields__})
+
+    def _check(self, st: int):
+        if st != 0:
+            raise SeedsError(st, self._lib.seeds_last_error(self._ctx).decode())
+
+    def close(self):
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            self._lib.seeds_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device entry points (torch tensors on the current CUDA device) -------
+    def _frames(self, images):
+        import torch
+        if not (isinstance(images, torch.Tensor) and images.is_cuda and images.dtype == torch.uint8
+                and images.is_contiguous()):
+            raise TypeError("images must be a contiguous uint8 CUDA tensor")
+        n = images.numel() // (self.width * self.height * self.channels)
+        if n * self.width * self.height * self.channels != images.numel() or n < 1:
+            raise ValueError("images do not hold whole frames of the context's size")
+        return n
+
+    def iterate(self, image, labels_out=None, stream=None):
+        """Cold refinement of one frame: (H, W, C) uint8 CUDA tensor -> (H, W) int32."""
+        import torch
+        self._frames(image)
+        if labels_out is None:
+            labels_out = torch.empty((self.height, self.width), dtype=torch.int32, device=image.device)
+        self._check(self._lib.seeds_iterate(self._ctx, image.data_ptr(), labels_out.data_ptr(),
+                                            _stream_ptr(stream)))
+        return labels_out
+
+    def batch(self, images, init_labels=None, labels_out=None, stream=None):
+        """(n, H, W, C) uint8 CUDA tensor [+ (n, H, W) int32 warm-start labels] -> (n, H, W) int32."""
+        import torch
+        n = self._frames(images)
+        if labels_out is None:
+            labels_out = torch.empty((n, self.height, self.width), dtype=torch.int32,
+                                     device=images.device)
+        init_ptr = None
+        if init_labels is not None:
+            if not (init_labels.is_cuda and init_labels.dtype == torch.int32
+                    and init_labels.is_contiguous() and init_labels.numel() == labels_out.numel()):
+                raise TypeError("init_labels must be a contiguous int32 CUDA tensor of n*H*W")
+            init_ptr = init_labels.data_ptr()
+        self._check(self._lib.seeds_batch(self._ctx, images.data_ptr(), n, init_ptr,
+                                          labels_out.data_ptr(), _stream_ptr(stream)))
+        return labels_out
+
+    def batch_host(self, images: np.ndarray, labels_out: np.ndarray, init_labels=None, stream=None):
+        """Host-memory entry point (copies in, runs, copies out, synchronises)."""
+        n = images.size // (self.width * self.height * self.channels)
+        assert images.flags.c_contiguous and images.dtype == np.uint8
+        assert labels_out.flags.c_contiguous and labels_out.dtype == np.int32
+        init_ptr = None
+        if init_labels is not None:
+            init_ptr = init_labels.ctypes.data
+        self._check(self._lib.seeds_batch_host(self._ctx, images.ctypes.data, n, init_ptr,
+                                               labels_out.ctypes.data, _stream_ptr(stream)))
+        return labels_out
+
+    def read_state(self, frame: int = 0, stream=None):
+        """(hist (K_act, B) int32, sizes (K_act,) int32) CUDA tensors after the last run."""
+        import torch
+        K, B = self.info.k_actual, self.info.bins_total
+        h = torch.empty((K, B), dtype=torch.int32, device="cuda")
+        a = torch.empty((K,), dtype=torch.int32, device="cuda")
+        self._check(self._lib.seeds_read_state(self._ctx, frame, h.data_ptr(), a.data_ptr(),
+                                               _stream_ptr(stream)))
+        return h, a
+
+    def stats(self, frame: int = 0, stream=None) -> np.ndarray:
+        out = np.zeros(self.info.subsweeps, np.int32)
+        self._check(self._lib.seeds_stats(self._ctx, frame, out.ctypes.data, out.size,
+                                          _stream_ptr(stream)))
+        return out
+
+    KINDS = ("seed", "block", "pixel", "emit")
+
+    def profile(self, enable: bool = True):
+        self._check(self._lib.seeds_profile(self._ctx, int(enable)))
+
+    def profile_collect(self, stream=None):
+        """{kind: (total ms, launches)} accumulated over profiled runs."""
+        ms = np.zeros(4, np.float64)
+        n = np.zeros(4, np.int64)
+        self._check(self._lib.seeds_profile_collect(self._ctx, _stream_ptr(stream), ms.ctypes.data,
+                                                    n.ctypes.data))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.KINDS)}
+
+    def debug_limit(self, max_subsweeps: int):
+        self._check(self._lib.seeds_debug_limit(self._ctx, max_subsweeps))
+
+    def sync(self, stream=None):
+        self._check(self._lib.seeds_sync(self._ctx, _stream_ptr(stream)))

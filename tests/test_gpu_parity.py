@@ -1,0 +1,168 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle's
+coloured schedule (COL, rule R1), element by element.  Labels, histograms
+and sizes are integers, so the bar is bit-exactness (BASELINE.json
+north_star).  Needs a B200: every test is marked gpu."""
+import numpy as np
+import pytest
+
+from paper_1309_3848_b200 import configs, mosaic
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1309_3848_b200 import build
+    build.build()
+    return torch
+
+
+def gpu_run(torch, img, p, init=None, limit=-1):
+    from paper_1309_3848_b200.seeds import Seeds
+    imgs = img if img.ndim == 4 else img[None]
+    n, H, W, C = imgs.shape
+    s = Seeds(W, H, C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
+              p["smoothness_prior"], p["iters_per_level"])
+    if limit >= 0:
+        s.debug_limit(limit)
+    d = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
+    di = None if init is None else torch.from_numpy(np.ascontiguousarray(init, np.int32)).cuda()
+    lab = s.batch(d, init_labels=di)
+    torch.cuda.synchronize()
+    hs, as_ = [], []
+    for f in range(n):
+        h, a = s.read_state(f)
+        hs.append(h.cpu().numpy())
+        as_.append(a.cpu().numpy())
+    out = lab.cpu().numpy(), np.stack(hs), np.stack(as_), s
+    return out
+
+
+def assert_parity(torch, orc, img, p, init=None, limit=-1):
+    lab, h, a, s = gpu_run(torch, img, p, init=init, limit=limit)
+    imgs = img if img.ndim == 4 else img[None]
+    for f in range(imgs.shape[0]):
+        r = orc.run(imgs[f], **p, init_labels=None if init is None else init[f], max_subsweeps=limit)
+        assert s.info.k_actual == r.k_act
+        np.testing.assert_array_equal(lab[f], r.labels, err_msg=f"labels frame {f}")
+        np.testing.assert_array_equal(h[f], r.hist, err_msg=f"hist frame {f}")
+        np.testing.assert_array_equal(a[f], r.sizes, err_msg=f"sizes frame {f}")
+        # accepted moves per pixel sub-sweep equal the oracle's
+        mv = s.stats(f)
+        for i, t in enumerate(r.trace):
+            if t["level"] == -1:
+                assert mv[i] == t["moves"], (f, i)
+    return lab, s
+
+
+def test_c1_full(torch_cuda, orc):
+    assert_parity(torch_cuda, orc, configs.frames("c1")[0], configs.params("c1"))
+
+
+@pytest.mark.parametrize("gamma", [0, 1])
+def test_c2_full(torch_cuda, orc, gamma):
+    p = configs.params("c2")
+    p["smoothness_prior"] = gamma
+    assert_parity(torch_cuda, orc, configs.frames("c2")[0], p)
+
+
+def test_c1_every_subsweep(torch_cuda, orc):
+    """Bisection hook: the state after s sub-sweeps matches for every s."""
+    img = configs.frames("c1")[0]
+    p = configs.params("c1")
+    for s in range(0, 35):
+        assert_parity(torch_cuda, orc, img, p, limit=s)
+
+
+def test_c2_subsweeps(torch_cuda, orc):
+    img = configs.frames("c2")[0]
+    p = configs.params("c2")
+    for s in (1, 4, 17, 63, 64, 65, 80):
+        assert_parity(torch_cuda, orc, img, p, limit=s)
+
+
+@pytest.mark.parametrize("W,H,K,L,bpc,C,gamma,iters", [
+    (37, 23, 7, 3, 5, 3, 1, 3),     # ragged: blocks of unequal size, odd grid
+    (37, 23, 7, 3, 5, 3, 0, 3),
+    (64, 48, 12, 0, 5, 3, 1, 4),    # n_levels = 0: pixel level only (SPH)
+    (64, 48, 12, 2, 5, 3, 1, 0),    # iters = 0: the grid (GRID baseline)
+    (1, 1, 1, 2, 5, 3, 1, 2),       # one pixel
+    (1, 40, 3, 2, 4, 1, 1, 3),      # one column
+    (50, 1, 4, 2, 4, 1, 0, 3),      # one row
+    (3, 2, 6, 1, 2, 1, 0, 2),       # K_act = N (every superpixel one pixel)
+    (90, 70, 30, 2, 1, 3, 1, 2),    # bpc = 1: one bin, no move can pass (strict test)
+    (80, 60, 20, 2, 8, 3, 1, 3),    # B = 512: uint16 bin plane
+    (80, 60, 20, 2, 4, 4, 0, 3),    # 4 channels, B = 256
+    (64, 64, 4, 5, 16, 2, 1, 2),    # deep levels (clamped), B = 256
+    (200, 150, 2000, 3, 5, 3, 1, 2),  # many tiny superpixels, L clamped
+])
+def test_shapes_and_degenerate_cases(torch_cuda, orc, W, H, K, L, bpc, C, gamma, iters):
+    img = mosaic.mosaic(W, H, max(1, min(20, W * H // 30)), 9.0, seed=W * 1000 + H, C=C, grad=20.0)
+    p = dict(n_superpixels=K, n_levels=L, bins_per_channel=bpc, smoothness_prior=gamma,
+             iters_per_level=iters)
+    assert_parity(torch_cuda, orc, img, p)
+
+
+def test_constant_image(torch_cuda, orc):
+    img = np.full((61, 47, 3), 99, np.uint8)
+    p = dict(n_superpixels=12, n_levels=2, bins_per_channel=5, smoothness_prior=1, iters_per_level=3)
+    lab, s = assert_parity(torch_cuda, orc, img, p)
+    assert s.stats(0).sum() == 0
+
+
+def test_batch_independent_frames(torch_cuda, orc):
+    """c3-shaped batch (K=400): every frame equals its own oracle run."""
+    imgs = configs.frames("c3", n=6)
+    assert_parity(torch_cuda, orc, imgs, configs.params("c3"))
+
+
+def test_warm_start(torch_cuda, orc):
+    """Warm start (reading O9): labels of frame t seed frame t+1."""
+    f, _ = mosaic.moving_mosaic(3, 160, 96, 15, 8.0, seed=42)
+    p = dict(n_superpixels=40, n_levels=3, bins_per_channel=5, smoothness_prior=0, iters_per_level=3)
+    r0 = orc.run(f[0], **p)
+    init = np.stack([r0.labels, r0.labels])
+    assert_parity(torch_cuda, orc, f[1:], p, init=init)
+
+
+def test_c3_sampled_full_batch(torch_cuda, orc):
+    """The full 256-frame c3 batch in one launch; frames 0, 85, 170, 255 checked
+    against the oracle, every frame checked for histogram/size invariants."""
+    imgs = configs.frames("c3")
+    p = configs.params("c3")
+    lab, h, a, s = gpu_run(torch_cuda, imgs, p)
+    N = imgs.shape[1] * imgs.shape[2]
+    assert (a.sum(1) == N).all()
+    assert (h.sum(2) == a).all()
+    for f in (0, 85, 170, 255):
+        r = orc.run(imgs[f], **p)
+        np.testing.assert_array_equal(lab[f], r.labels)
+        np.testing.assert_array_equal(h[f], r.hist)
+
+
+def test_repeat_launch_is_deterministic(torch_cuda):
+    """Graph replays give identical output (no order dependence on the GPU)."""
+    from paper_1309_3848_b200.seeds import Seeds
+    img = configs.frames("c2")[0]
+    p = configs.params("c2")
+    s = Seeds(img.shape[1], img.shape[0], 3, *[p[k] for k in (
+        "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    d = torch_cuda.from_numpy(img).cuda()
+    out = torch_cuda.empty(img.shape[:2], dtype=torch_cuda.int32, device="cuda")
+    ref = s.iterate(d, out).clone()
+    for _ in range(5):
+        s.iterate(d, out)
+        assert torch_cuda.equal(out, ref)
+
+
+def test_host_entry_point(torch_cuda, orc):
+    from paper_1309_3848_b200.seeds import Seeds
+    img = configs.frames("c1")[0]
+    p = configs.params("c1")
+    s = Seeds(img.shape[1], img.shape[0], 3, *[p[k] for k in (
+        "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    out = np.empty(img.shape[:2], np.int32)
+    s.batch_host(np.ascontiguousarray(img), out)
+    np.testing.assert_array_equal(out, orc.run(img, **p).labels)
