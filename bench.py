@@ -181,6 +181,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "graph", "resident"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--json-out", default=None)
@@ -209,6 +210,7 @@ def main():
     p = configs.params(name)
     s = Seeds(W, H, C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
               p["smoothness_prior"], p["iters_per_level"])
+    s.set_mode(args.mode)
     info = s.info
     stream = torch.cuda.current_stream()
     d_img = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
@@ -259,6 +261,7 @@ def main():
     s.profile(False)
     torch.cuda.synchronize()
     ab = algorithmic_bytes(info, C, nf, N)
+    ab["frame"] = frame_bytes(info, C, N, p["iters_per_level"]) * nf
     kinds = {k: {"ms_total": v[0] / kp, "launches": v[1] // kp,
                  "avg_launch_us": 1e3 * v[0] / max(1, v[1]),
                  "gbps": (ab[k] / (v[0] / max(1, v[1]) / 1e3) / 1e9) if v[1] else None}
@@ -309,6 +312,8 @@ def main():
                                    f"L={info.levels_eff}, I={p['iters_per_level']}, "
                                    f"B={info.bins_total}, gamma={p['smoothness_prior']}",
                        "frames_per_step_per_rank": nf,
+                       "exec_mode": {1: "graph", 2: "resident"}[info.exec_mode],
+                       "cluster_size": info.cluster_size,
                        "parallelism": "replicas" if scaling == "weak" else f"frames/{world}",
                        "l2": "512 MiB buffer rewritten between timed steps (outside events)"},
             "frames_per_s": nf * world * args.steps / (tot_ms_max / 1e3),

@@ -70,7 +70,9 @@ typedef struct {
     int bin_bytes;       /* 1 if B <= 256 else 2 */
     int subsweeps;       /* 4 L_eff I + P^2 I sub-sweeps per cold frame */
     int max_block_area;  /* largest top-level block, pixels */
-    int kernels_per_run; /* kernel launches of one cold run (graph kernel nodes) */
+    int kernels_per_run; /* kernel launches of one cold run in the resolved mode */
+    int exec_mode;       /* resolved execution mode (SEEDS_MODE_GRAPH or _RESIDENT) */
+    int cluster_size;    /* CTAs per cluster of the resident kernel (0: frame does not fit) */
     size_t workspace_bytes_per_frame;
 } seeds_info;
 
@@ -145,6 +147,13 @@ seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int3
  * bisect a divergence against the oracle's max_subsweeps. */
 seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps);
 
+/* seeds_debug_trace -- resident mode only: enable (1) per-CTA clock64 stamps of
+ * every sub-sweep of frame 0 (work finished / barrier passed), copy them to
+ * host_out[min(cap, cluster_size*(subsweeps+4)*2)] (int64, layout
+ * [cta][phase][2]), or disable (0) and free the buffer.  Synchronises the
+ * device when host_out is given.  Diagnostic; not part of the hot path. */
+seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap);
+
 /* seeds_stats -- accepted moves per sub-sweep of frame `frame` of the last
  * run: moves_out[s] for s < min(cap, subsweeps).  Host pointer.  Synchronises.
  * For a block sub-sweep the count is of histogram delta entries (one per
@@ -157,8 +166,25 @@ enum {
     SEEDS_KIND_BLOCK = 1, /* one block-level sub-sweep */
     SEEDS_KIND_PIXEL = 2, /* one pixel-level sub-sweep */
     SEEDS_KIND_EMIT = 3,  /* labels -> int32 output */
-    SEEDS_KIND_COUNT = 4
+    SEEDS_KIND_FRAME = 4, /* one resident whole-refinement launch */
+    SEEDS_KIND_COUNT = 5
 };
+
+/* Execution modes (seeds_set_mode).  Both give bit-identical results.
+ *  GRAPH:    one kernel per sub-sweep, the run captured as a CUDA graph with
+ *            programmatic dependent launch; every kernel spans all frames of
+ *            the batch, state in HBM/L2 (any frame size).
+ *  RESIDENT: one launch for the whole run; a thread-block cluster per frame
+ *            keeps labels, bins and histograms in (distributed) shared memory
+ *            and separates sub-sweeps by cluster barriers; clusters loop over
+ *            the frames of the batch (frames that fit a cluster, e.g. 481x321).
+ *  AUTO:     GRAPH (RESIDENT is selected explicitly). */
+enum { SEEDS_MODE_AUTO = 0, SEEDS_MODE_GRAPH = 1, SEEDS_MODE_RESIDENT = 2 };
+
+/* seeds_set_mode -- pick the execution mode for later runs.  SEEDS_EINVAL for
+ * an unknown mode; SEEDS_ESTATE if RESIDENT is requested but the frame does
+ * not fit a co-schedulable cluster. */
+seeds_status seeds_set_mode(seeds_ctx *ctx, int mode);
 
 /* seeds_profile -- enable (1) or disable (0) per-kernel device timing: later
  * runs record a CUDA event pair around every seed / block / pixel / emit

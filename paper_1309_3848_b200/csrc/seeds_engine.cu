@@ -14,6 +14,7 @@
 
 #include "../../include/seeds.h"
 #include "seeds_kernels.cuh"
+#include "seeds_resident.cuh"
 
 using namespace seeds;
 
@@ -78,6 +79,17 @@ struct seeds_ctx {
     double prof_ms[SEEDS_KIND_COUNT] = {0};
     long long prof_n[SEEDS_KIND_COUNT] = {0};
     int kernels_per_run = 0;
+    // execution mode: SEEDS_MODE_AUTO / _GRAPH / _RESIDENT
+    int mode = SEEDS_MODE_AUTO;
+    int cluster = 0;          // resident kernel cluster size (0 = unavailable)
+    int max_clusters = 0;     // co-resident clusters of that size
+    size_t res_smem = 0;
+    int ntab = 0;
+    ResParams rp{};           // resident layout (pointers filled per run)
+    int *d_band = nullptr;    // band_y (CS+1) then band_top (CS+1)
+    long long *d_trace = nullptr;  // resident-kernel phase clocks (seeds_debug_trace)
+    int n_sm = 148;
+    bool pixel_tiled = true;  // SEEDS_PIXEL_TILED=0 selects the untiled pixel kernel
 };
 
 static seeds_status cuda_fail(seeds_ctx *c, cudaError_t e, const char *what)
@@ -143,6 +155,17 @@ static void derive_geometry(seeds_ctx *c)
     c->kernels_per_run = 2 + c->P * c->P * c->iters + (c->L > 0 ? 2 + (c->L - 1) + 4 * c->L * c->iters : 0);
 }
 
+// Inside a stream capture an event record must be external to become a graph
+// node; outside a capture it is an ordinary record.
+static cudaError_t record_event(cudaEvent_t e, cudaStream_t st)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t r = cudaStreamIsCapturing(st, &cs);
+    if (r != cudaSuccess) return r;
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, st);
+}
+
 // Event pair around a launch when profiling (recorded into the captured graph).
 static cudaError_t prof_begin(seeds_ctx *c, cudaStream_t st, int kind)
 {
@@ -156,13 +179,13 @@ static cudaError_t prof_begin(seeds_ctx *c, cudaStream_t st, int kind)
     }
     if (c->ev_kind.size() < (size_t)c->ev_used + 1) c->ev_kind.resize(c->ev_used + 1);
     c->ev_kind[c->ev_used] = kind;
-    return cudaEventRecordWithFlags(c->ev[2 * c->ev_used], st, cudaEventRecordExternal);
+    return record_event(c->ev[2 * c->ev_used], st);
 }
 
 static cudaError_t prof_end(seeds_ctx *c, cudaStream_t st)
 {
     if (!c->prof) return cudaSuccess;
-    cudaError_t r = cudaEventRecordWithFlags(c->ev[2 * c->ev_used + 1], st, cudaEventRecordExternal);
+    cudaError_t r = record_event(c->ev[2 * c->ev_used + 1], st);
     c->ev_used++;
     return r;
 }
@@ -253,28 +276,74 @@ static dim3 grid1(long long work, int threads, int frames, long long maxblocks =
     return dim3((unsigned)b, (unsigned)frames);
 }
 
-template <int G, typename BinT>
-static cudaError_t launch_block(seeds_ctx *ctx, const SweepParams &p, int nf, cudaStream_t st)
+// Launch with programmatic dependent launch (the kernel calls pdl_enter()), so
+// consecutive sub-sweep kernels of the graph overlap launch with execution.
+// SEEDS_PDL=0 in the environment launches them as ordinary kernels.
+static bool pdl_enabled()
 {
-    const size_t per_group = (2 * (size_t)p.B + 2) * 4;
-    int gpc = 256 / G;
-    while (gpc > 1 && gpc * per_group > 160 * 1024) gpc >>= 1;
-    const size_t shm = gpc * per_group;
-    auto kern = k_block<G, BinT>;
+    static int on = -1;
+    if (on < 0) {
+        const char *v = getenv("SEEDS_PDL");
+        on = (v && atoi(v) == 0) ? 0 : 1;
+    }
+    return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// CTAs per frame for `work` items (units or warps) of `per_cta` items each:
+// enough to cover the work, but over all frames not more than ~8 waves.
+static unsigned ctas_per_frame(const seeds_ctx *c, long long work, int per_cta, int nf)
+{
+    const long long need = std::max(1LL, (work + per_cta - 1) / per_cta);
+    const long long cap = std::max(1LL, (long long)c->n_sm * 8 * 8 / nf);
+    return (unsigned)std::min(need, cap);
+}
+
+template <typename BinT>
+static cudaError_t launch_block(seeds_ctx *ctx, const SweepParams &p, int nf, cudaStream_t st, bool large)
+{
     const long long units = (long long)p.uw * p.uh;
-    const long long blocks = std::max(1LL, std::min((units + gpc - 1) / gpc, 148LL * 32));
-    kern<<<dim3((unsigned)blocks, nf), gpc * G, shm, st>>>(p, gpc);
-    return cudaGetLastError();
+    if (!large) {
+        const dim3 g(ctas_per_frame(ctx, units, 256, nf), nf);
+        return launch_pdl(k_block_small<BinT>, g, dim3(256), 0, st, p);
+    }
+    const size_t per_warp = (2 * (size_t)p.B + 2) * 4;
+    int warps = 8;
+    while (warps > 1 && warps * per_warp > 160 * 1024) warps >>= 1;
+    const dim3 g(ctas_per_frame(ctx, units, warps, nf), nf);
+    return launch_pdl(k_block_large<BinT>, g, dim3(32 * warps), warps * per_warp, st, p);
 }
 
 template <typename BinT>
 static cudaError_t launch_pixel(seeds_ctx *ctx, const SweepParams &p, int nf, cudaStream_t st)
 {
+    if (ctx->pixel_tiled) {
+        const int tx = (ctx->W + TILE_W - 1) / TILE_W, ty = (ctx->H + TILE_H - 1) / TILE_H;
+        const int ntiles = tx * ty;
+        const dim3 g(ctas_per_frame(ctx, ntiles, 1, nf), nf);
+        if (ctx->gamma) return launch_pdl(k_pixel_tile<BinT, 1, 3>, g, dim3(256), 0, st, p, tx, ntiles);
+        return launch_pdl(k_pixel_tile<BinT, 0, 2>, g, dim3(256), 0, st, p, tx, ntiles);
+    }
     const long long units = (long long)p.uw * p.uh;
-    const dim3 g = grid1(units, 256, nf, 148LL * 32);
-    if (ctx->gamma) k_pixel<BinT, 1, 3><<<g, 256, 0, st>>>(p);
-    else k_pixel<BinT, 0, 2><<<g, 256, 0, st>>>(p);
-    return cudaGetLastError();
+    const dim3 g(ctas_per_frame(ctx, units, 256, nf), nf);
+    if (ctx->gamma) return launch_pdl(k_pixel<BinT, 1, 3>, g, dim3(256), 0, st, p);
+    return launch_pdl(k_pixel<BinT, 0, 2>, g, dim3(256), 0, st, p);
 }
 
 // Enqueue one whole run (cold or warm) of nf frames on stream st.
@@ -293,11 +362,10 @@ static seeds_status enqueue(seeds_ctx *ctx, const uint8_t *img, const int32_t *i
     CK(prof_begin(ctx, st, SEEDS_KIND_SEED));
     {
         const dim3 g = grid1(ctx->N, 256, nf);
-        k_seed<BinT><<<g, 256, 0, st>>>(img, ctx->W, ctx->C, ctx->bpc, ctx->N, ctx->L, ctx->nx, ctx->B,
-                                        ctx->d_bxof, ctx->d_byof, init, (BinT *)ctx->d_bins,
-                                        blocks ? nullptr : ctx->d_lab, ctx->d_H[0], ctx->d_A[0], ctx->H_fs,
-                                        ctx->K);
-        CK(cudaGetLastError());
+        SeedArgs a{img, ctx->W, ctx->C, ctx->bpc, ctx->L, ctx->nx, ctx->B, ctx->K, ctx->N, ctx->H_fs,
+                   ctx->d_bxof, ctx->d_byof, init, ctx->d_bins, blocks ? nullptr : ctx->d_lab,
+                   ctx->d_H[0], ctx->d_A[0]};
+        CK(launch_pdl(k_seed<BinT>, g, dim3(256), 0, st, a));
     }
     CK(prof_end(ctx, st));
     CK(cudaMemcpyAsync(ctx->d_H[1], ctx->d_H[0], (size_t)nf * ctx->H_fs * 4, cudaMemcpyDeviceToDevice, st));
@@ -320,8 +388,8 @@ static seeds_status enqueue(seeds_ctx *ctx, const uint8_t *img, const int32_t *i
     int mb = 0;  // map buffer holding the current level
     if (blocks) {
         const int wt = ctx->GX >> (ctx->L - 1), ht = ctx->GY >> (ctx->L - 1);
-        k_topmap<<<grid1((long long)wt * ht, 256, nf), 256, 0, st>>>(ctx->d_M[0], wt, ht, ctx->map_fs, ctx->nx);
-        CK(cudaGetLastError());
+        CK(launch_pdl(k_topmap, grid1((long long)wt * ht, 256, nf), dim3(256), 0, st, ctx->d_M[0], wt, ht,
+                      (long long)ctx->map_fs, ctx->nx));
         for (int l = ctx->L - 1; l >= 0; l--) {
             const int w = ctx->GX >> l, h = ctx->GY >> l;
             p.w = w; p.h = h; p.level = l;
@@ -334,23 +402,21 @@ static seeds_status enqueue(seeds_ctx *ctx, const uint8_t *img, const int32_t *i
                     p.uw = (w - p.cx + 1) / 2; p.uh = (h - p.cy + 1) / 2;
                     set_sweep(s);
                     CK(prof_begin(ctx, st, SEEDS_KIND_BLOCK));
-                    cudaError_t e = am > 8 ? launch_block<32, BinT>(ctx, p, nf, st)
-                                           : launch_block<8, BinT>(ctx, p, nf, st);
+                    cudaError_t e = launch_block<BinT>(ctx, p, nf, st, am > GRAPH_SMALL_ALPHA);
                     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_block launch");
                     CK(prof_end(ctx, st));
                     s++;
                 }
             if (l > 0) {
                 const int wc = ctx->GX >> (l - 1), hc = ctx->GY >> (l - 1);
-                k_pushdown<<<grid1((long long)wc * hc, 256, nf), 256, 0, st>>>(ctx->d_M[mb], ctx->d_M[mb ^ 1], wc,
-                                                                             hc, ctx->map_fs);
-                CK(cudaGetLastError());
+                CK(launch_pdl(k_pushdown, grid1((long long)wc * hc, 256, nf), dim3(256), 0, st,
+                              (const uint16_t *)ctx->d_M[mb], ctx->d_M[mb ^ 1], wc, hc, (long long)ctx->map_fs));
                 mb ^= 1;
             }
         }
-        k_expand<<<grid1(ctx->N, 256, nf), 256, 0, st>>>(ctx->d_M[mb], ctx->d_lab, ctx->W, ctx->N, ctx->GX,
-                                                         ctx->map_fs, ctx->d_bxof, ctx->d_byof);
-        CK(cudaGetLastError());
+        CK(launch_pdl(k_expand, grid1(ctx->N, 256, nf), dim3(256), 0, st, (const uint16_t *)ctx->d_M[mb],
+                      ctx->d_lab, ctx->W, (long long)ctx->N, ctx->GX, (long long)ctx->map_fs,
+                      (const int *)ctx->d_bxof, (const int *)ctx->d_byof));
     }
     // pixel level
     p.w = ctx->W; p.h = ctx->H; p.level = 0;
@@ -369,9 +435,173 @@ static seeds_status enqueue(seeds_ctx *ctx, const uint8_t *img, const int32_t *i
             s++;
         }
     CK(prof_begin(ctx, st, SEEDS_KIND_EMIT));
-    k_emit<<<grid1(ctx->N * nf, 256, 1), 256, 0, st>>>(ctx->d_lab, out, ctx->N * nf);
-    CK(cudaGetLastError());
+    CK(launch_pdl(k_emit, grid1(ctx->N * nf, 256, 1), dim3(256), 0, st, (const uint16_t *)ctx->d_lab, out,
+                  (long long)(ctx->N * nf)));
     CK(prof_end(ctx, st));
+    ctx->last_done = s;
+    ctx->last_final = s & 1;
+    return SEEDS_OK;
+}
+
+static int resolved_mode(const seeds_ctx *c)
+{
+    if (c->mode != SEEDS_MODE_AUTO) return c->mode;
+    return SEEDS_MODE_GRAPH;  // resident mode is opt-in until it is faster
+}
+
+template <typename BinT, int GAMMA, int P>
+static int resident_clusters(int cs, size_t smem)
+{
+    auto k = k_resident<BinT, GAMMA, P>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+static int resident_clusters_for(const seeds_ctx *c, int cs, size_t smem)
+{
+    if (c->bb == 1) return c->gamma ? resident_clusters<uint8_t, 1, 3>(cs, smem) : resident_clusters<uint8_t, 0, 2>(cs, smem);
+    return c->gamma ? resident_clusters<uint16_t, 1, 3>(cs, smem) : resident_clusters<uint16_t, 0, 2>(cs, smem);
+}
+
+static size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+
+// Resident mode (seeds_resident.cuh): partition the rows into CS bands aligned
+// with the top-level block rows (each >= 2 pixel rows), lay out the shared
+// memory and check that a cluster of CS CTAs can be co-scheduled.
+static void setup_resident(seeds_ctx *c)
+{
+    c->cluster = 0;
+    if (c->GX > 16383 || c->GY > 16383 || c->L > 8) return;  // record packing limits
+    const int T = c->L > 0 ? (c->GY >> (c->L - 1)) : c->H;     // row units the bands are made of
+    auto unit_row = [&](int t) { return c->L > 0 ? c->rowstart[(size_t)t << (c->L - 1)] : t; };
+    for (int cs = std::min(16, T); cs >= 1; cs--) {
+        // prefer the smallest cluster with the least rows per band
+        const int per = (T + cs - 1) / cs;
+        const int cs_min = (T + per - 1) / per;
+        if (cs != cs_min) continue;
+        std::vector<int> top(cs + 1), ys(cs + 1);
+        for (int r = 0; r <= cs; r++) {
+            top[r] = (int)((long long)r * T / cs);
+            ys[r] = unit_row(top[r]);
+        }
+        int bmin = 1 << 30, bmax = 0;
+        for (int r = 0; r < cs; r++) {
+            bmin = std::min(bmin, ys[r + 1] - ys[r]);
+            bmax = std::max(bmax, ys[r + 1] - ys[r]);
+        }
+        if (cs > 1 && bmin < 2) continue;
+        ResParams &q = c->rp;
+        q = ResParams{};
+        q.kloc = (c->K + cs - 1) / cs;
+        q.rec_cap = ((c->W + 1) / 2) * ((bmax + 1) / 2) + 32;
+        q.lab_rows = bmax + 4;
+        const size_t tabw = (2 * (size_t)c->B + 2) * 4;
+        size_t off = 0;
+        q.o_lab = (unsigned)off;  off = align16(off + (size_t)q.lab_rows * c->W * 2);
+        q.o_bins = (unsigned)off; off = align16(off + (size_t)bmax * c->W * c->bb);
+        q.o_H = (unsigned)off;    off = align16(off + 2 * (size_t)q.kloc * c->B * 4);
+        q.o_A = (unsigned)off;    off = align16(off + 2 * (size_t)q.kloc * 4);
+        q.o_rec = (unsigned)off;  off = align16(off + 2 * (size_t)q.rec_cap * sizeof(Rec));
+        q.o_misc = (unsigned)off; off = align16(off + 16);
+        q.o_scr = (unsigned)off;  off = align16(off + (size_t)SMALL_ALPHA * 512 * 2);
+        q.o_tab = (unsigned)off;
+        const size_t limit = 227 * 1024;
+        if (off + tabw > limit) continue;
+        q.ntab = (int)std::min<size_t>(16, (limit - off) / tabw);
+        const size_t smem = off + q.ntab * tabw;
+        const int n = resident_clusters_for(c, cs, smem);
+        if (n <= 0) continue;
+        std::vector<int> h(2 * (cs + 1));
+        for (int r = 0; r <= cs; r++) {
+            h[r] = ys[r];
+            h[cs + 1 + r] = top[r];
+        }
+        if (c->d_band) cudaFree(c->d_band);
+        if (cudaMalloc(&c->d_band, h.size() * sizeof(int)) != cudaSuccess ||
+            cudaMemcpy(c->d_band, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        q.band_y = c->d_band;
+        q.band_top = c->d_band + cs + 1;
+        q.big_mask = 0;
+        for (int l = 0; l < c->L; l++)
+            if (max_block_area(c, l) > SMALL_ALPHA) q.big_mask |= 1 << l;
+        c->cluster = cs;
+        c->max_clusters = n;
+        c->res_smem = smem;
+        return;
+    }
+}
+
+template <typename BinT, int GAMMA, int P>
+static cudaError_t launch_resident_t(seeds_ctx *ctx, const ResParams &q, int ncl, cudaStream_t st)
+{
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ctx->cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(ncl * ctx->cluster);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = ctx->res_smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_resident<BinT, GAMMA, P>, q);
+}
+
+static seeds_status run_resident(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
+                                 cudaStream_t st)
+{
+    ResParams q = ctx->rp;
+    q.img = img; q.init = init; q.out = out;
+    q.W = ctx->W; q.H = ctx->H; q.C = ctx->C; q.bpc = ctx->bpc; q.B = ctx->B; q.K = ctx->K; q.nx = ctx->nx;
+    q.L = ctx->L; q.iters = ctx->iters; q.limit = ctx->limit; q.S = ctx->S; q.nf = nf;
+    q.colstart = ctx->d_colstart; q.rowstart = ctx->d_rowstart; q.bxof = ctx->d_bxof; q.byof = ctx->d_byof;
+    q.moves = ctx->d_moves;
+    for (int i = 0; i < 2; i++) {
+        q.Hout[i] = ctx->d_H[i];
+        q.Aout[i] = ctx->d_A[i];
+    }
+    q.H_fs = ctx->H_fs;
+    q.trace = ctx->d_trace;
+    const int ncl = std::max(1, std::min(nf, ctx->max_clusters));
+    CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
+    cudaError_t e;
+    if (ctx->bb == 1)
+        e = ctx->gamma ? launch_resident_t<uint8_t, 1, 3>(ctx, q, ncl, st) : launch_resident_t<uint8_t, 0, 2>(ctx, q, ncl, st);
+    else
+        e = ctx->gamma ? launch_resident_t<uint16_t, 1, 3>(ctx, q, ncl, st)
+                       : launch_resident_t<uint16_t, 0, 2>(ctx, q, ncl, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_resident launch");
+    CK(prof_end(ctx, st));
+    // sub-sweeps run: the schedule is data independent
+    const bool blocks = init == nullptr && ctx->L > 0;
+    int s = 0;
+    const int total = (blocks ? 4 * ctx->L * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
+    s = ctx->limit >= 0 ? std::min(ctx->limit, total) : total;
     ctx->last_done = s;
     ctx->last_final = s & 1;
     return SEEDS_OK;
@@ -382,6 +612,14 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
 {
     seeds_status r = ensure_frames(ctx, nf);
     if (r != SEEDS_OK) return r;
+    if (resolved_mode(ctx) == SEEDS_MODE_RESIDENT) {
+        ctx->ev_used = 0;
+        r = run_resident(ctx, img, init, out, nf, st);
+        if (r != SEEDS_OK) return r;
+        ctx->last_nf = nf;
+        ctx->ran = true;
+        return SEEDS_OK;
+    }
     GraphKey key;
     key.img = img; key.init = init; key.out = out; key.nf = nf; key.limit = ctx->limit; key.prof = ctx->prof;
     if (!ctx->exec || !(key == ctx->key)) {
@@ -451,11 +689,12 @@ seeds_status seeds_create(int width, int height, int channels, int n_superpixels
     up(ctx->d_bxof, ctx->bxof);
     up(ctx->d_byof, ctx->byof);
     // shared-memory opt-in of the block kernels (set outside any graph capture)
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block<32, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block<8, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block<32, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block<8, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block_large<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block_large<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, ctx->dev);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) setup_resident(ctx);
+    if (const char *v = getenv("SEEDS_PIXEL_TILED")) ctx->pixel_tiled = atoi(v) != 0;
     if (e != cudaSuccess) {
         seeds_status st = e == cudaErrorMemoryAllocation ? SEEDS_ENOMEM : SEEDS_ECUDA;
         seeds_destroy(ctx);
@@ -517,7 +756,9 @@ seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *o)
     o->nx = ctx->nx; o->ny = ctx->ny; o->k_actual = ctx->K; o->levels_eff = ctx->L;
     o->grid_x = ctx->GX; o->grid_y = ctx->GY; o->colour_period = ctx->P; o->bins_total = ctx->B;
     o->bin_bytes = ctx->bb; o->subsweeps = ctx->S; o->max_block_area = ctx->amax;
-    o->kernels_per_run = ctx->kernels_per_run;
+    o->exec_mode = resolved_mode(ctx);
+    o->cluster_size = ctx->cluster;
+    o->kernels_per_run = o->exec_mode == SEEDS_MODE_RESIDENT ? 1 : ctx->kernels_per_run;
     o->workspace_bytes_per_frame = (size_t)ctx->N * (ctx->bb + 2) +
                                    (size_t)(((long long)ctx->GX * ctx->GY + 7) / 8 * 8) * 4 +
                                    (size_t)ctx->K * (ctx->B + 1) * 8 + (size_t)ctx->N * sizeof(Rec) * 2;
@@ -583,6 +824,36 @@ seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out,
     return SEEDS_OK;
 }
 
+seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
+{
+    if (!ctx || mode < SEEDS_MODE_AUTO || mode > SEEDS_MODE_RESIDENT) return SEEDS_EINVAL;
+    if (mode == SEEDS_MODE_RESIDENT && ctx->cluster == 0) {
+        snprintf(ctx->err, sizeof ctx->err, "the frame does not fit a co-schedulable cluster (resident mode)");
+        return SEEDS_ESTATE;
+    }
+    ctx->mode = mode;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap)
+{
+    if (!ctx) return SEEDS_EINVAL;
+    const size_t n = (size_t)std::max(1, ctx->cluster) * (ctx->S + 4) * 2;
+    if (enable && !ctx->d_trace) {
+        CK(cudaMalloc(&ctx->d_trace, n * sizeof(long long)));
+        CK(cudaMemset(ctx->d_trace, 0, n * sizeof(long long)));
+    }
+    if (host_out && ctx->d_trace) {
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(host_out, ctx->d_trace, std::min(n, (size_t)cap) * sizeof(long long), cudaMemcpyDeviceToHost));
+    }
+    if (!enable && ctx->d_trace) {
+        cudaFree(ctx->d_trace);
+        ctx->d_trace = nullptr;
+    }
+    return SEEDS_OK;
+}
+
 seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps)
 {
     if (!ctx || max_subsweeps < -1) return SEEDS_EINVAL;
@@ -605,7 +876,7 @@ void seeds_destroy(seeds_ctx *ctx)
     if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
     void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1],
-                    ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage,
+                    ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band,
                     ctx->d_init_stage, ctx->d_out_stage};
     for (void *p : ptrs)
         if (p) cudaFree(p);

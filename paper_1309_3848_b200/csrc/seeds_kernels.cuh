@@ -11,12 +11,17 @@
 // which holds the state after s-2, both the deltas of s-1 (replayed from the
 // previous sub-sweep's records) and its own deltas -- so (Hy, Ay) is the
 // state after s when the kernel ends and the next sub-sweep swaps roles.
-// One kernel per sub-sweep; the kernel boundary is the only ordering point.
+// One kernel per sub-sweep (graph mode) or one cluster barrier per sub-sweep
+// (resident mode); that is the only ordering point.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace seeds {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int SMALL_ALPHA = 16;       // resident mode: blocks up to this many pixels, one thread per block
+constexpr int GRAPH_SMALL_ALPHA = 4;  // graph mode: the same for blocks up to 4 pixels (finest levels)
 
 // A histogram delta: superpixel k loses `count` pixels of bin `bin` to n.
 // (S5.3.3: pixel = one increment and decrement; block =
@@ -33,10 +38,21 @@ __constant__ uint32_t c_removable[8];
 
 __device__ __forceinline__ bool removable(int m) { return (c_removable[m >> 5] >> (m & 31)) & 1u; }
 
+// Programmatic dependent launch: wait until this kernel's predecessor has
+// completed and its writes are visible, then let the next kernel of the graph
+// start launching (its CTAs wait in their own pdl_enter).  Triggering only
+// after the wait keeps at most one kernel ahead resident.  Both are no-ops
+// for a kernel launched without PDL.
+__device__ __forceinline__ void pdl_enter()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+}
+
 struct SweepParams {
     int W, H, B, K;
     int w, h;          // dims of the map the units live on (block map or pixel plane)
-    int level;         // block level (block kernel)
+    int level;         // block level (block kernels)
     int cx, cy;        // colour class offsets: units are (cx + step*i, cy + step*j)
     int uw, uh;        // units per row / rows of this colour class
     const void *bins;  // bin plane (uint8 or uint16), frame stride N
@@ -67,18 +83,19 @@ __device__ __forceinline__ void apply_prev(const SweepParams &p, int f, long lon
     }
 }
 
-// Candidates and ring mask of unit (x, y) with label k on map m (w x h):
-// candidates = labels of the in-map 4-neighbours in order W, E, N, S other
-// than k, first occurrence only (reading Q5).
 __device__ __forceinline__ int lab_at(const uint16_t *m, int w, int h, int x, int y)
 {
     return (x >= 0 && x < w && y >= 0 && y < h) ? (int)m[(long long)y * w + x] : -1;
 }
 
+// Candidates and ring mask of unit (x, y) with label k on map m (w x h).
+// Candidates = labels of the in-map 4-neighbours in order W, E, N, S other
+// than k, first occurrence only (reading Q5): slot d is a candidate iff bit d
+// of `valid` is set.  Fixed slots keep everything in registers.
 struct Neigh {
-    int cand[4];
-    int nc;
-    int mask;
+    int v[4];   // W, E, N, S labels (-1 outside the map)
+    int valid;  // candidate slots
+    int mask;   // ring mask
 };
 
 __device__ __forceinline__ Neigh neighbourhood(const uint16_t *m, int w, int h, int x, int y, int k)
@@ -90,15 +107,14 @@ __device__ __forceinline__ Neigh neighbourhood(const uint16_t *m, int w, int h, 
     Neigh r;
     r.mask = (vN == k) | (vNE == k) << 1 | (vE == k) << 2 | (vSE == k) << 3 | (vS == k) << 4 |
              (vSW == k) << 5 | (vW == k) << 6 | (vNW == k) << 7;
-    r.nc = 0;
-    const int order[4] = {vW, vE, vN, vS};
+    r.v[0] = vW; r.v[1] = vE; r.v[2] = vN; r.v[3] = vS;
+    r.valid = 0;
 #pragma unroll
     for (int d = 0; d < 4; d++) {
-        const int v = order[d];
-        bool fresh = v >= 0 && v != k;
+        bool ok = r.v[d] >= 0 && r.v[d] != k;
 #pragma unroll
-        for (int i = 0; i < d; i++) fresh = fresh && (i >= r.nc || r.cand[i] != v);
-        if (fresh) r.cand[r.nc++] = v;
+        for (int e = 0; e < d; e++) ok = ok && r.v[e] != r.v[d];
+        r.valid |= (int)ok << d;
     }
     return r;
 }
@@ -111,12 +127,31 @@ __device__ __forceinline__ bool gt_prod(unsigned long long a, unsigned long long
     return h1 > h2 || (h1 == h2 && a * b > c * d);
 }
 
-template <int G>
-__device__ __forceinline__ unsigned long long group_sum(unsigned long long v, unsigned gmask)
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v)
 {
 #pragma unroll
-    for (int off = G / 2; off >= 1; off >>= 1) v += __shfl_xor_sync(gmask, v, off);
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
     return v;
+}
+
+// Reserve n consecutive record slots per lane on *cnt (all 32 lanes call);
+// returns this lane's first slot.  Also counts accepted units into *moves.
+__device__ __forceinline__ int reserve_warp(int *cnt, int *moves, int n, bool moved)
+{
+    const int lane = threadIdx.x & 31;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    const unsigned mv = __ballot_sync(FULL, moved);
+    int base = 0;
+    if (lane == 31 && total) base = atomicAdd(cnt, total);
+    if (lane == 0 && mv) atomicAdd(moves, __popc(mv));
+    base = __shfl_sync(FULL, base, 31);
+    return base + incl - n;
 }
 
 // ---------------------------------------------------------------------------
@@ -127,43 +162,57 @@ __device__ __forceinline__ unsigned long long group_sum(unsigned long long v, un
 // the levels.  Histogram atomics are warp-aggregated with
 // __match_any_sync on the (label, bin) key.
 // ---------------------------------------------------------------------------
+struct SeedArgs {
+    const uint8_t *img;
+    int W, C, bpc, L, nx, B, K;
+    long long N, H_fs;
+    const int *bxof, *byof;
+    const int32_t *init;  // warm-start labels or nullptr (grid)
+    void *bins;
+    uint16_t *lab;        // nullptr when the block phase builds the labels later
+    int *H, *A;
+};
+
+// Pixels t0 + threadIdx.x, t0 + T + threadIdx.x, ... of frame f (t0, T warp-uniform).
 template <typename BinT>
-__global__ void __launch_bounds__(256) k_seed(const uint8_t *__restrict__ img, int W, int C, int bpc,
-                                              long long N, int L, int nx, int B,
-                                              const int *__restrict__ bxof, const int *__restrict__ byof,
-                                              const int32_t *__restrict__ init, BinT *__restrict__ bins,
-                                              uint16_t *__restrict__ lab, int *__restrict__ Hout,
-                                              int *__restrict__ Aout, long long H_fs, int K)
+__device__ __forceinline__ void seed_pixels(const SeedArgs &a, int f, long long t0, long long T)
 {
-    const int f = blockIdx.y;
-    const long long stride = (long long)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < N; base += stride) {
+    BinT *bins = static_cast<BinT *>(a.bins);
+    for (long long base = t0; base < a.N; base += T) {
         const long long p = base + threadIdx.x;
-        const bool valid = p < N;
+        const bool valid = p < a.N;
         int key = -1, label = -1;
         if (valid) {
-            const int y = (int)(p / W), x = (int)(p - (long long)y * W);
-            const uint8_t *v = img + ((long long)f * N + p) * C;
+            const int y = (int)(p / a.W), x = (int)(p - (long long)y * a.W);
+            const uint8_t *v = a.img + ((long long)f * a.N + p) * a.C;
             int b = 0;
-            for (int c = 0; c < C; c++) b = b * bpc + (((int)v[c] * bpc) >> 8);
-            bins[(long long)f * N + p] = (BinT)b;
-            if (init) label = init[(long long)f * N + p];
-            else label = (byof[y] >> L) * nx + (bxof[x] >> L);
-            if (lab) lab[(long long)f * N + p] = (uint16_t)label;
-            key = label * B + b;
+            for (int c = 0; c < a.C; c++) b = b * a.bpc + (((int)v[c] * a.bpc) >> 8);
+            bins[(long long)f * a.N + p] = (BinT)b;
+            if (a.init) label = a.init[(long long)f * a.N + p];
+            else label = (a.byof[y] >> a.L) * a.nx + (a.bxof[x] >> a.L);
+            if (a.lab) a.lab[(long long)f * a.N + p] = (uint16_t)label;
+            key = label * a.B + b;
         }
-        unsigned m = __match_any_sync(0xffffffffu, key);
-        if (valid && lane == __ffs(m) - 1) atomicAdd(&Hout[(long long)f * H_fs + key], __popc(m));
-        m = __match_any_sync(0xffffffffu, label);
-        if (valid && lane == __ffs(m) - 1) atomicAdd(&Aout[(long long)f * K + label], __popc(m));
+        unsigned m = __match_any_sync(FULL, key);
+        if (valid && lane == __ffs(m) - 1) atomicAdd(&a.H[(long long)f * a.H_fs + key], __popc(m));
+        m = __match_any_sync(FULL, label);
+        if (valid && lane == __ffs(m) - 1) atomicAdd(&a.A[(long long)f * a.K + label], __popc(m));
     }
+}
+
+template <typename BinT>
+__global__ void __launch_bounds__(256) k_seed(SeedArgs a)
+{
+    pdl_enter();
+    seed_pixels<BinT>(a, blockIdx.y, (long long)blockIdx.x * blockDim.x, (long long)gridDim.x * blockDim.x);
 }
 
 // Top block map M_{L-1}: superpixel (I, J) = 2x2 blocks of the largest size
 // (Fig. blocks).
 __global__ void k_topmap(uint16_t *M, int w, int h, long long fs, int nx)
 {
+    pdl_enter();
     const int f = blockIdx.y;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < w * h; t += gridDim.x * blockDim.x) {
         const int j = t / w, i = t - j * w;
@@ -174,6 +223,7 @@ __global__ void k_topmap(uint16_t *M, int w, int h, long long fs, int nx)
 // Next finer level: every child block takes its parent's label.
 __global__ void k_pushdown(const uint16_t *Mp, uint16_t *Mc, int wc, int hc, long long fs)
 {
+    pdl_enter();
     const int f = blockIdx.y;
     const int wp = wc >> 1;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < wc * hc; t += gridDim.x * blockDim.x) {
@@ -186,6 +236,7 @@ __global__ void k_pushdown(const uint16_t *Mp, uint16_t *Mc, int wc, int hc, lon
 __global__ void k_expand(const uint16_t *M0, uint16_t *lab, int W, long long N, int GX, long long map_fs,
                          const int *bxof, const int *byof)
 {
+    pdl_enter();
     const int f = blockIdx.y;
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N;
          p += (long long)gridDim.x * blockDim.x) {
@@ -197,6 +248,7 @@ __global__ void k_expand(const uint16_t *M0, uint16_t *lab, int W, long long N, 
 // uint16 plane -> int32 labels_out (8 labels per thread per step when aligned).
 __global__ void k_emit(const uint16_t *__restrict__ lab, int32_t *__restrict__ out, long long total)
 {
+    pdl_enter();
     const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
     if ((((uintptr_t)out) & 31) == 0) {
@@ -218,30 +270,20 @@ __global__ void k_emit(const uint16_t *__restrict__ lab, int32_t *__restrict__ o
 // K3 block sub-sweep (level l, colour c): boundary + ring test on the block
 // map, block histogram from the bin plane, Proposition 1
 // cross-multiplied (reading R1), first accepted candidate wins; G is ignored
-// at block level.  A group of G lanes handles one block:
-// the block's bins are aggregated in a per-group shared-memory table (count
-// per bin + list of the non-empty bins), the intersection sums
+// at block level.  With l the block histogram (alpha px):
 //   N_n = sum_b min(h_n[b] alpha, l_b A_n)
 //   N_k = sum_b min((h_k[b] - l_b) alpha, l_b (A_k - alpha))
-// run over the non-empty bins only and are reduced with warp shuffles (K5),
-// and the move is accepted iff N_n (A_k - alpha) > N_k A_n.
+// over the non-empty bins only (the others add 0), and the move k -> n is
+// accepted iff N_n (A_k - alpha) > N_k A_n (exact 128-bit products).
 // ---------------------------------------------------------------------------
-template <int G, typename BinT>
-__global__ void __launch_bounds__(256) k_block(SweepParams p, int gpc)
+
+// Blocks of <= SMALL_ALPHA pixels: one thread per block.  The block's bins go
+// to a per-thread shared-memory scratch column scr[i * stride]; the distinct
+// bins are found by pairwise comparison.  Units t0 + threadIdx.x + i T.
+template <typename BinT>
+__device__ __forceinline__ void block_small_units(const SweepParams &p, int f, long long t0, long long T,
+                                                  uint16_t *scr, int stride)
 {
-    extern __shared__ uint32_t smem[];
-    const int f = blockIdx.y;
-    apply_prev(p, f, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
-
-    const int g = threadIdx.x / G, lane = threadIdx.x % G;
-    uint32_t *cnt = smem + (size_t)g * (2 * p.B + 2);
-    uint32_t *list = cnt + p.B;
-    uint32_t *nlist = list + p.B;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
-    for (int b = lane; b < p.B; b += G) cnt[b] = 0;
-    if (lane == 0) *nlist = 0;
-    __syncwarp(gmask);
-
     uint16_t *M = p.map + f * p.map_fs;
     const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
     const int *Hx = p.Hx + f * p.H_fs;
@@ -250,53 +292,134 @@ __global__ void __launch_bounds__(256) k_block(SweepParams p, int gpc)
     int *Ay = p.Ay + (long long)f * p.K;
     const long long nunits = (long long)p.uw * p.uh;
 
-    for (long long t = (long long)blockIdx.x * gpc + g; t < nunits; t += (long long)gridDim.x * gpc) {
+    for (long long base = t0; base < nunits; base += T) {
+        const long long t = base + threadIdx.x;
+        int acc = -1, k = 0, alpha = 0, nd = 0, bi = 0, bj = 0;
+        if (t < nunits) {
+            const int tj = (int)(t / p.uw), ti = (int)(t - (long long)tj * p.uw);
+            bi = p.cx + 2 * ti;
+            bj = p.cy + 2 * tj;
+            k = M[(long long)bj * p.w + bi];
+            const Neigh nb = neighbourhood(M, p.w, p.h, bi, bj, k);
+            if (nb.valid && removable(nb.mask)) {
+                const int xa = p.colstart[bi << p.level], xb = p.colstart[(bi + 1) << p.level];
+                const int ya = p.rowstart[bj << p.level], yb = p.rowstart[(bj + 1) << p.level];
+                const int rw = xb - xa;
+                alpha = rw * (yb - ya);
+                long long An[4];
+#pragma unroll
+                for (int d = 0; d < 4; d++) An[d] = (nb.valid >> d & 1) ? Ax[nb.v[d]] : 1;
+                const long long Ak = Ax[k];
+                for (int i = 0, y = ya, x = xa; i < alpha; i++) {
+                    scr[i * stride] = (uint16_t)bins[(long long)y * p.W + x];
+                    if (++x == xb) { x = xa; y++; }
+                }
+                unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+                for (int i = 0; i < alpha; i++) {
+                    const int b = scr[i * stride];
+                    bool first = true;
+                    for (int j = 0; j < i; j++) first = first && scr[j * stride] != b;
+                    if (!first) continue;
+                    long long l = 1;
+                    for (int j = i + 1; j < alpha; j++) l += scr[j * stride] == b;
+                    nd++;
+                    const long long u = (long long)(Hx[(long long)k * p.B + b] - l) * alpha, v = l * (Ak - alpha);
+                    Nk += (unsigned long long)(u < v ? u : v);
+#pragma unroll
+                    for (int d = 0; d < 4; d++)
+                        if (nb.valid >> d & 1) {
+                            const long long un = (long long)Hx[(long long)nb.v[d] * p.B + b] * alpha, vn = l * An[d];
+                            Nn[d] += (unsigned long long)(un < vn ? un : vn);
+                        }
+                }
+#pragma unroll
+                for (int d = 0; d < 4; d++)
+                    if (acc < 0 && (nb.valid >> d & 1) &&
+                        gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
+                        acc = nb.v[d];
+            }
+        }
+        int slot = reserve_warp(&p.cnt_out[f], &p.moves_out[f], acc >= 0 ? nd : 0, acc >= 0);
+        if (acc >= 0) {
+            M[(long long)bj * p.w + bi] = (uint16_t)acc;
+            Rec *rec = p.rec_out + f * p.rec_fs;
+            for (int i = 0; i < alpha; i++) {
+                const int b = scr[i * stride];
+                bool first = true;
+                for (int j = 0; j < i; j++) first = first && scr[j * stride] != b;
+                if (!first) continue;
+                int l = 1;
+                for (int j = i + 1; j < alpha; j++) l += scr[j * stride] == b;
+                rec[slot++] = Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)b | ((uint32_t)l << 16)};
+                atomicSub(&Hy[(long long)k * p.B + b], l);
+                atomicAdd(&Hy[(long long)acc * p.B + b], l);
+            }
+            atomicSub(&Ay[k], alpha);
+            atomicAdd(&Ay[acc], alpha);
+        }
+    }
+}
+
+// Larger blocks: one warp per block.  The block histogram is aggregated in the
+// warp's shared-memory table (count per bin, zero on entry and exit) plus a
+// list of the non-empty bins; the sums run over that list and are reduced with
+// warp shuffles (K5).  Units u0, u0 + U, ... (one per warp).
+template <typename BinT>
+__device__ __forceinline__ void block_large_units(const SweepParams &p, int f, long long u0, long long U,
+                                                  uint32_t *cnt, uint32_t *list, uint32_t *nlist)
+{
+    const int lane = threadIdx.x & 31;
+    uint16_t *M = p.map + f * p.map_fs;
+    const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
+    const int *Hx = p.Hx + f * p.H_fs;
+    const int *Ax = p.Ax + (long long)f * p.K;
+    int *Hy = p.Hy + f * p.H_fs;
+    int *Ay = p.Ay + (long long)f * p.K;
+    const long long nunits = (long long)p.uw * p.uh;
+
+    for (long long t = u0; t < nunits; t += U) {
         const int tj = (int)(t / p.uw), ti = (int)(t - (long long)tj * p.uw);
         const int bi = p.cx + 2 * ti, bj = p.cy + 2 * tj;
         const int k = M[(long long)bj * p.w + bi];
         const Neigh nb = neighbourhood(M, p.w, p.h, bi, bj, k);
-        if (nb.nc == 0 || !removable(nb.mask)) continue;
+        if (!nb.valid || !removable(nb.mask)) continue;
 
         const int xa = p.colstart[bi << p.level], xb = p.colstart[(bi + 1) << p.level];
         const int ya = p.rowstart[bj << p.level], yb = p.rowstart[(bj + 1) << p.level];
         const int rw = xb - xa;
         const int alpha = rw * (yb - ya);
-        for (int q = lane; q < alpha; q += G) {
+        long long An[4];
+#pragma unroll
+        for (int d = 0; d < 4; d++) An[d] = (nb.valid >> d & 1) ? Ax[nb.v[d]] : 1;
+        const long long Ak = Ax[k];
+        for (int q = lane; q < alpha; q += 32) {
             const int dy = q / rw;
             const int b = bins[(long long)(ya + dy) * p.W + xa + (q - dy * rw)];
             if (atomicAdd(&cnt[b], 1u) == 0u) list[atomicAdd(nlist, 1u)] = (uint32_t)b;
         }
-        __syncwarp(gmask);
+        __syncwarp();
         const int ns = (int)*nlist;
-
-        const long long Ak = Ax[k];
-        const int *Hk = Hx + (long long)k * p.B;
-        unsigned long long Nk = 0;
-        for (int i = lane; i < ns; i += G) {
+        unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+        for (int i = lane; i < ns; i += 32) {
             const int b = list[i];
             const long long l = cnt[b];
-            const long long u = (long long)(Hk[b] - l) * alpha, v = l * (Ak - alpha);
+            const long long u = (long long)(Hx[(long long)k * p.B + b] - l) * alpha, v = l * (Ak - alpha);
             Nk += (unsigned long long)(u < v ? u : v);
+#pragma unroll
+            for (int d = 0; d < 4; d++)
+                if (nb.valid >> d & 1) {
+                    const long long un = (long long)Hx[(long long)nb.v[d] * p.B + b] * alpha, vn = l * An[d];
+                    Nn[d] += (unsigned long long)(un < vn ? un : vn);
+                }
         }
-        Nk = group_sum<G>(Nk, gmask);
-
+        Nk = warp_sum(Nk);
         int acc = -1;
-        for (int ci = 0; ci < nb.nc; ci++) {
-            const int n = nb.cand[ci];
-            const long long An = Ax[n];
-            const int *Hn = Hx + (long long)n * p.B;
-            unsigned long long Nn = 0;
-            for (int i = lane; i < ns; i += G) {
-                const int b = list[i];
-                const long long l = cnt[b];
-                const long long u = (long long)Hn[b] * alpha, v = l * An;
-                Nn += (unsigned long long)(u < v ? u : v);
-            }
-            Nn = group_sum<G>(Nn, gmask);
-            if (gt_prod(Nn, (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An)) {
-                acc = n;
-                break;
-            }
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            Nn[d] = warp_sum(Nn[d]);
+            if (acc < 0 && (nb.valid >> d & 1) &&
+                gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
+                acc = nb.v[d];
         }
         if (acc >= 0) {
             int base = 0;
@@ -307,9 +430,9 @@ __global__ void __launch_bounds__(256) k_block(SweepParams p, int gpc)
                 atomicSub(&Ay[k], alpha);
                 atomicAdd(&Ay[acc], alpha);
             }
-            base = __shfl_sync(gmask, base, 0, G);
+            base = __shfl_sync(FULL, base, 0);
             Rec *rec = p.rec_out + f * p.rec_fs + base;
-            for (int i = lane; i < ns; i += G) {
+            for (int i = lane; i < ns; i += 32) {
                 const int b = list[i];
                 const int l = (int)cnt[b];
                 rec[i] = Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)b | ((uint32_t)l << 16)};
@@ -317,12 +440,39 @@ __global__ void __launch_bounds__(256) k_block(SweepParams p, int gpc)
                 atomicAdd(&Hy[(long long)acc * p.B + b], l);
             }
         }
-        __syncwarp(gmask);
-        for (int i = lane; i < ns; i += G) cnt[list[i]] = 0;
-        __syncwarp(gmask);
+        __syncwarp();
+        for (int i = lane; i < ns; i += 32) cnt[list[i]] = 0;
+        __syncwarp();
         if (lane == 0) *nlist = 0;
-        __syncwarp(gmask);
+        __syncwarp();
     }
+}
+
+template <typename BinT>
+__global__ void __launch_bounds__(256) k_block_small(SweepParams p)
+{
+    __shared__ uint16_t scr[SMALL_ALPHA * 256];
+    pdl_enter();
+    const int f = blockIdx.y;
+    apply_prev(p, f, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
+    block_small_units<BinT>(p, f, (long long)blockIdx.x * blockDim.x, (long long)gridDim.x * blockDim.x,
+                            scr + threadIdx.x, blockDim.x);
+}
+
+template <typename BinT>
+__global__ void __launch_bounds__(256) k_block_large(SweepParams p)
+{
+    extern __shared__ uint32_t smem[];
+    pdl_enter();
+    const int f = blockIdx.y;
+    apply_prev(p, f, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    uint32_t *cnt = smem + (size_t)wid * (2 * p.B + 2);
+    for (int b = lane; b < p.B; b += 32) cnt[b] = 0;
+    if (lane == 0) cnt[2 * p.B] = 0;
+    __syncwarp();
+    block_large_units<BinT>(p, f, (long long)blockIdx.x * nw + wid, (long long)gridDim.x * nw, cnt, cnt + p.B,
+                            cnt + 2 * p.B);
 }
 
 // ---------------------------------------------------------------------------
@@ -333,49 +483,43 @@ __global__ void __launch_bounds__(256) k_block(SweepParams p, int gpc)
 // and with gamma = 1 the Proposition-2 boundary test:
 //   S = sum_{i in W3(p)} (b_i(n) + 1 - b_i(k)) >= 0, patches clamped (Q15).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int smooth_sum(const uint16_t *L, int W, int H, int x, int y, int k, int n)
+__device__ __noinline__ int smooth_sum(const uint16_t *L, int W, int H, int x, int y, int k, int n)
 {
-    int win[5][5];
-#pragma unroll
-    for (int dy = 0; dy < 5; dy++)
-#pragma unroll
-        for (int dx = 0; dx < 5; dx++) win[dy][dx] = lab_at(L, W, H, x + dx - 2, y + dy - 2);
+    // weight of each 5x5 cell = number of in-image 3x3 patch centres i in W3(p)
+    // with the cell in W3(i); S = |W3(p) in image| + sum_q w_q ([q = n] - [q = k]).
     int S = 0;
-#pragma unroll
-    for (int iy = 1; iy <= 3; iy++)
-#pragma unroll
-        for (int ix = 1; ix <= 3; ix++) {
-            if (win[iy][ix] < 0) continue;  // patch centre outside the image
-            int bn = 0, bk = 0;
-#pragma unroll
-            for (int qy = -1; qy <= 1; qy++)
-#pragma unroll
-                for (int qx = -1; qx <= 1; qx++) {
-                    const int v = win[iy + qy][ix + qx];
-                    bn += v == n;
-                    bk += v == k;
+    for (int iy = y - 1; iy <= y + 1; iy++) {
+        if (iy < 0 || iy >= H) continue;
+        for (int ix = x - 1; ix <= x + 1; ix++) {
+            if (ix < 0 || ix >= W) continue;
+            int d = 1;  // the "+1" of the proposition
+            for (int qy = iy - 1; qy <= iy + 1; qy++) {
+                if (qy < 0 || qy >= H) continue;
+                const uint16_t *row = L + (long long)qy * W;
+                for (int qx = ix - 1; qx <= ix + 1; qx++) {
+                    if (qx < 0 || qx >= W) continue;
+                    const int v = row[qx];
+                    d += (v == n) - (v == k);
                 }
-            S += bn + 1 - bk;
+            }
+            S += d;
         }
+    }
     return S;
 }
 
+// Threads t0 + threadIdx.x, t0 + T + threadIdx.x, ... of the frame (t0 and T
+// warp-uniform, T a multiple of 32).
 template <typename BinT, int GAMMA, int P>
-__global__ void __launch_bounds__(256) k_pixel(SweepParams p)
+__device__ __forceinline__ void pixel_units(const SweepParams &p, int f, long long t0, long long T)
 {
-    const int f = blockIdx.y;
-    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    apply_prev(p, f, tid, (long long)gridDim.x * blockDim.x);
-
     uint16_t *L = p.map + f * p.map_fs;
     const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
     const int *Hx = p.Hx + f * p.H_fs;
     const int *Ax = p.Ax + (long long)f * p.K;
     const long long nunits = (long long)p.uw * p.uh;
-    const int lane = threadIdx.x & 31;
 
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < nunits;
-         base += (long long)gridDim.x * blockDim.x) {
+    for (long long base = t0; base < nunits; base += T) {
         const long long t = base + threadIdx.x;
         int acc = -1, k = 0, j = 0, x = 0, y = 0;
         if (t < nunits) {
@@ -383,32 +527,158 @@ __global__ void __launch_bounds__(256) k_pixel(SweepParams p)
             x = p.cx + P * ti;
             y = p.cy + P * tj;
             k = L[(long long)y * p.W + x];
+            j = bins[(long long)y * p.W + x];
             const Neigh nb = neighbourhood(L, p.W, p.H, x, y, k);
-            if (nb.nc > 0 && removable(nb.mask)) {
-                j = bins[(long long)y * p.W + x];
+            if (nb.valid && removable(nb.mask)) {
                 const long long hk = Hx[(long long)k * p.B + j], Ak = Ax[k];
-                for (int ci = 0; ci < nb.nc; ci++) {
-                    const int n = nb.cand[ci];
-                    const long long hn = Hx[(long long)n * p.B + j], An = Ax[n];
-                    if (hn * (Ak - 1) > (hk - 1) * An) {
-                        if (GAMMA && smooth_sum(L, p.W, p.H, x, y, k, n) < 0) continue;
-                        acc = n;
-                        break;
-                    }
+                long long hn[4], An[4];
+#pragma unroll
+                for (int d = 0; d < 4; d++) {
+                    const bool v = nb.valid >> d & 1;
+                    hn[d] = v ? Hx[(long long)nb.v[d] * p.B + j] : 0;
+                    An[d] = v ? Ax[nb.v[d]] : 1;
                 }
+#pragma unroll
+                for (int d = 0; d < 4; d++)
+                    if (acc < 0 && (nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d] &&
+                        (!GAMMA || smooth_sum(L, p.W, p.H, x, y, k, nb.v[d]) >= 0))
+                        acc = nb.v[d];
             }
         }
-        const unsigned am = __ballot_sync(0xffffffffu, acc >= 0);
-        if (am) {
-            const int leader = __ffs(am) - 1;
-            int slot = 0;
-            if (lane == leader) {
-                slot = atomicAdd(&p.cnt_out[f], __popc(am));
-                atomicAdd(&p.moves_out[f], __popc(am));
+        const int slot = reserve_warp(&p.cnt_out[f], &p.moves_out[f], acc >= 0 ? 1 : 0, acc >= 0);
+        if (acc >= 0) {
+            L[(long long)y * p.W + x] = (uint16_t)acc;
+            p.rec_out[f * p.rec_fs + slot] = Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)j | (1u << 16)};
+            int *Hy = p.Hy + f * p.H_fs;
+            int *Ay = p.Ay + (long long)f * p.K;
+            atomicSub(&Hy[(long long)k * p.B + j], 1);
+            atomicAdd(&Hy[(long long)acc * p.B + j], 1);
+            atomicSub(&Ay[k], 1);
+            atomicAdd(&Ay[acc], 1);
+        }
+    }
+}
+
+// Tiled pixel sub-sweep: a CTA stages a TW x TH label tile plus a halo of R
+// (1 for gamma = 0, 2 for gamma = 1) in shared memory with coalesced loads,
+// each thread loads the bin of its units in the same phase, and the decisions
+// read labels from shared memory; only the histogram gathers and the
+// accepted moves touch global memory.  Labels outside the image are 0xFFFF.
+constexpr int TILE_W = 48, TILE_H = 48;  // multiples of both colour periods (2, 3)
+
+__device__ __forceinline__ int slab_at(const uint16_t *s, int sw, int x, int y)
+{
+    const int v = s[y * sw + x];
+    return v == 0xFFFF ? -1 : v;
+}
+
+template <int R>
+__device__ __forceinline__ Neigh neighbourhood_s(const uint16_t *s, int sw, int x, int y, int k)
+{
+    const int vN = slab_at(s, sw, x, y - 1), vNE = slab_at(s, sw, x + 1, y - 1);
+    const int vE = slab_at(s, sw, x + 1, y), vSE = slab_at(s, sw, x + 1, y + 1);
+    const int vS = slab_at(s, sw, x, y + 1), vSW = slab_at(s, sw, x - 1, y + 1);
+    const int vW = slab_at(s, sw, x - 1, y), vNW = slab_at(s, sw, x - 1, y - 1);
+    Neigh r;
+    r.mask = (vN == k) | (vNE == k) << 1 | (vE == k) << 2 | (vSE == k) << 3 | (vS == k) << 4 |
+             (vSW == k) << 5 | (vW == k) << 6 | (vNW == k) << 7;
+    r.v[0] = vW; r.v[1] = vE; r.v[2] = vN; r.v[3] = vS;
+    r.valid = 0;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        bool ok = r.v[d] >= 0 && r.v[d] != k;
+#pragma unroll
+        for (int e = 0; e < d; e++) ok = ok && r.v[e] != r.v[d];
+        r.valid |= (int)ok << d;
+    }
+    return r;
+}
+
+// S of Proposition 2 from the shared tile (cells outside the image are -1 and
+// never equal k or n; a patch centre outside the image is skipped).
+__device__ __forceinline__ int smooth_sum_s(const uint16_t *s, int sw, int x, int y, int k, int n)
+{
+    int S = 0;
+#pragma unroll
+    for (int iy = -1; iy <= 1; iy++)
+#pragma unroll
+        for (int ix = -1; ix <= 1; ix++) {
+            if (s[(y + iy) * sw + x + ix] == 0xFFFF) continue;
+            int d = 1;
+#pragma unroll
+            for (int qy = -1; qy <= 1; qy++)
+#pragma unroll
+                for (int qx = -1; qx <= 1; qx++) {
+                    const int v = s[(y + iy + qy) * sw + x + ix + qx];
+                    d += (v == n) - (v == k);
+                }
+            S += d;
+        }
+    return S;
+}
+
+template <typename BinT, int GAMMA, int P>
+__global__ void __launch_bounds__(256) k_pixel_tile(SweepParams p, int tiles_x, int ntiles)
+{
+    constexpr int R = GAMMA ? 2 : 1;
+    constexpr int SW = TILE_W + 2 * R, SH = TILE_H + 2 * R;
+    // units of one colour in a tile: (TILE_W / P) x (TILE_H / P) (tiles start at multiples of P)
+    constexpr int UW = TILE_W / P, UH = TILE_H / P, UNITS = UW * UH;
+    constexpr int UPT = (UNITS + 255) / 256;
+    __shared__ uint16_t s[SH * SW];
+    pdl_enter();
+    const int f = blockIdx.y;
+    apply_prev(p, f, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
+    uint16_t *L = p.map + f * p.map_fs;
+    const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
+    const int *Hx = p.Hx + f * p.H_fs;
+    const int *Ax = p.Ax + (long long)f * p.K;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int x0 = (tile % tiles_x) * TILE_W, y0 = (tile / tiles_x) * TILE_H;
+        __syncthreads();  // previous tile's readers are done
+        for (int i = threadIdx.x; i < SH * SW; i += blockDim.x) {
+            const int ty = i / SW, tx = i - ty * SW;
+            const int gx = x0 - R + tx, gy = y0 - R + ty;
+            s[i] = (gx >= 0 && gx < p.W && gy >= 0 && gy < p.H) ? L[(long long)gy * p.W + gx] : (uint16_t)0xFFFF;
+        }
+        int jj[UPT];
+#pragma unroll
+        for (int u = 0; u < UPT; u++) {
+            const int t = threadIdx.x + 256 * u;
+            const int gx = x0 + p.cx + P * (t % UW), gy = y0 + p.cy + P * (t / UW);
+            jj[u] = (t < UNITS && gx < p.W && gy < p.H) ? (int)bins[(long long)gy * p.W + gx] : 0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < UPT; u++) {
+            const int t = threadIdx.x + 256 * u;
+            const int lx = p.cx + P * (t % UW), ly = p.cy + P * (t / UW);
+            const int gx = x0 + lx, gy = y0 + ly;
+            const int sx = lx + R, sy = ly + R;
+            int acc = -1, k = 0;
+            const int j = jj[u];
+            if (t < UNITS && gx < p.W && gy < p.H) {
+                k = s[sy * SW + sx];
+                const Neigh nb = neighbourhood_s<R>(s, SW, sx, sy, k);
+                if (nb.valid && removable(nb.mask)) {
+                    const long long hk = Hx[(long long)k * p.B + j], Ak = Ax[k];
+                    long long hn[4], An[4];
+#pragma unroll
+                    for (int d = 0; d < 4; d++) {
+                        const bool v = nb.valid >> d & 1;
+                        hn[d] = v ? Hx[(long long)nb.v[d] * p.B + j] : 0;
+                        An[d] = v ? Ax[nb.v[d]] : 1;
+                    }
+#pragma unroll
+                    for (int d = 0; d < 4; d++)
+                        if (acc < 0 && (nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d] &&
+                            (!GAMMA || smooth_sum_s(s, SW, sx, sy, k, nb.v[d]) >= 0))
+                            acc = nb.v[d];
+                }
             }
-            slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(am & ((1u << lane) - 1u));
+            const int slot = reserve_warp(&p.cnt_out[f], &p.moves_out[f], acc >= 0 ? 1 : 0, acc >= 0);
             if (acc >= 0) {
-                L[(long long)y * p.W + x] = (uint16_t)acc;
+                L[(long long)gy * p.W + gx] = (uint16_t)acc;
                 p.rec_out[f * p.rec_fs + slot] =
                     Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)j | (1u << 16)};
                 int *Hy = p.Hy + f * p.H_fs;
@@ -420,6 +690,15 @@ __global__ void __launch_bounds__(256) k_pixel(SweepParams p)
             }
         }
     }
+}
+
+template <typename BinT, int GAMMA, int P>
+__global__ void __launch_bounds__(256) k_pixel(SweepParams p)
+{
+    pdl_enter();
+    const int f = blockIdx.y;
+    apply_prev(p, f, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
+    pixel_units<BinT, GAMMA, P>(p, f, (long long)blockIdx.x * blockDim.x, (long long)gridDim.x * blockDim.x);
 }
 
 }  // namespace seeds

@@ -21,7 +21,7 @@ _STATUS = {0: "ok", -1: "invalid argument", -2: "out of memory", -3: "CUDA error
 
 EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "seeds_query",
            "seeds_read_state", "seeds_debug_limit", "seeds_stats", "seeds_sync", "seeds_destroy",
-           "seeds_profile", "seeds_profile_collect",
+           "seeds_profile", "seeds_profile_collect", "seeds_set_mode", "seeds_debug_trace",
            "seeds_status_string", "seeds_last_error"]
 
 
@@ -35,7 +35,7 @@ class Info(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "width", "height", "channels", "nx", "ny", "k_actual", "levels_eff", "grid_x", "grid_y",
         "colour_period", "bins_total", "bin_bytes", "subsweeps", "max_block_area",
-        "kernels_per_run")] + [
+        "kernels_per_run", "exec_mode", "cluster_size")] + [
         ("workspace_bytes_per_frame", ctypes.c_size_t)]
 
 
@@ -62,6 +62,8 @@ def load(path: str = LIB_PATH):
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
         "seeds_profile": ([vp, i], i),
+        "seeds_set_mode": ([vp, i], i),
+        "seeds_debug_trace": ([vp, i, vp, i], i),
         "seeds_profile_collect": ([vp, vp, vp, vp], i),
         "seeds_destroy": ([vp], None),
         "seeds_status_string": ([i], ctypes.c_char_p),
@@ -98,6 +100,8 @@ class Geometry:
     subsweeps: int
     max_block_area: int
     kernels_per_run: int
+    exec_mode: int
+    cluster_size: int
     workspace_bytes_per_frame: int
 
 
@@ -199,18 +203,36 @@ class Seeds:
                                           _stream_ptr(stream)))
         return out
 
-    KINDS = ("seed", "block", "pixel", "emit")
+    KINDS = ("seed", "block", "pixel", "emit", "frame")
+    MODES = {"auto": 0, "graph": 1, "resident": 2}
+
+    def set_mode(self, mode: str):
+        self._check(self._lib.seeds_set_mode(self._ctx, self.MODES[mode]))
+        self._refresh()
+
+    def _refresh(self):
+        info = Info()
+        self._check(self._lib.seeds_query(self._ctx, ctypes.byref(info)))
+        self.info = Geometry(**{f: getattr(info, f) for f in Geometry.__dataclass_fields__})
 
     def profile(self, enable: bool = True):
         self._check(self._lib.seeds_profile(self._ctx, int(enable)))
 
     def profile_collect(self, stream=None):
         """{kind: (total ms, launches)} accumulated over profiled runs."""
-        ms = np.zeros(4, np.float64)
-        n = np.zeros(4, np.int64)
+        ms = np.zeros(5, np.float64)
+        n = np.zeros(5, np.int64)
         self._check(self._lib.seeds_profile_collect(self._ctx, _stream_ptr(stream), ms.ctypes.data,
                                                     n.ctypes.data))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.KINDS)}
+
+    def debug_trace(self, enable: bool = True):
+        """Resident mode: per-CTA clock64 stamps [cta, phase, (work done, barrier passed)]."""
+        cs = max(1, self.info.cluster_size)
+        n = cs * (self.info.subsweeps + 4) * 2
+        out = np.zeros(n, np.int64)
+        self._check(self._lib.seeds_debug_trace(self._ctx, int(enable), out.ctypes.data if enable else None, n))
+        return out.reshape(cs, self.info.subsweeps + 4, 2)
 
     def debug_limit(self, max_subsweeps: int):
         self._check(self._lib.seeds_debug_limit(self._ctx, max_subsweeps))

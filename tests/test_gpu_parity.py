@@ -19,12 +19,21 @@ def torch_cuda():
     return torch
 
 
-def gpu_run(torch, img, p, init=None, limit=-1):
+MODES = ["graph", "resident"]
+
+
+@pytest.fixture(params=MODES)
+def mode(request):
+    return request.param
+
+
+def gpu_run(torch, img, p, init=None, limit=-1, mode="auto"):
     from paper_1309_3848_b200.seeds import Seeds
     imgs = img if img.ndim == 4 else img[None]
     n, H, W, C = imgs.shape
     s = Seeds(W, H, C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
               p["smoothness_prior"], p["iters_per_level"])
+    s.set_mode(mode)
     if limit >= 0:
         s.debug_limit(limit)
     d = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
@@ -40,8 +49,8 @@ def gpu_run(torch, img, p, init=None, limit=-1):
     return out
 
 
-def assert_parity(torch, orc, img, p, init=None, limit=-1):
-    lab, h, a, s = gpu_run(torch, img, p, init=init, limit=limit)
+def assert_parity(torch, orc, img, p, init=None, limit=-1, mode="auto"):
+    lab, h, a, s = gpu_run(torch, img, p, init=init, limit=limit, mode=mode)
     imgs = img if img.ndim == 4 else img[None]
     for f in range(imgs.shape[0]):
         r = orc.run(imgs[f], **p, init_labels=None if init is None else init[f], max_subsweeps=limit)
@@ -57,30 +66,30 @@ def assert_parity(torch, orc, img, p, init=None, limit=-1):
     return lab, s
 
 
-def test_c1_full(torch_cuda, orc):
-    assert_parity(torch_cuda, orc, configs.frames("c1")[0], configs.params("c1"))
+def test_c1_full(torch_cuda, orc, mode):
+    assert_parity(torch_cuda, orc, configs.frames("c1")[0], configs.params("c1"), mode=mode)
 
 
 @pytest.mark.parametrize("gamma", [0, 1])
-def test_c2_full(torch_cuda, orc, gamma):
+def test_c2_full(torch_cuda, orc, gamma, mode):
     p = configs.params("c2")
     p["smoothness_prior"] = gamma
-    assert_parity(torch_cuda, orc, configs.frames("c2")[0], p)
+    assert_parity(torch_cuda, orc, configs.frames("c2")[0], p, mode=mode)
 
 
-def test_c1_every_subsweep(torch_cuda, orc):
+def test_c1_every_subsweep(torch_cuda, orc, mode):
     """Bisection hook: the state after s sub-sweeps matches for every s."""
     img = configs.frames("c1")[0]
     p = configs.params("c1")
     for s in range(0, 35):
-        assert_parity(torch_cuda, orc, img, p, limit=s)
+        assert_parity(torch_cuda, orc, img, p, limit=s, mode=mode)
 
 
-def test_c2_subsweeps(torch_cuda, orc):
+def test_c2_subsweeps(torch_cuda, orc, mode):
     img = configs.frames("c2")[0]
     p = configs.params("c2")
     for s in (1, 4, 17, 63, 64, 65, 80):
-        assert_parity(torch_cuda, orc, img, p, limit=s)
+        assert_parity(torch_cuda, orc, img, p, limit=s, mode=mode)
 
 
 @pytest.mark.parametrize("W,H,K,L,bpc,C,gamma,iters", [
@@ -98,41 +107,41 @@ def test_c2_subsweeps(torch_cuda, orc):
     (64, 64, 4, 5, 16, 2, 1, 2),    # deep levels (clamped), B = 256
     (200, 150, 2000, 3, 5, 3, 1, 2),  # many tiny superpixels, L clamped
 ])
-def test_shapes_and_degenerate_cases(torch_cuda, orc, W, H, K, L, bpc, C, gamma, iters):
+def test_shapes_and_degenerate_cases(torch_cuda, orc, W, H, K, L, bpc, C, gamma, iters, mode):
     img = mosaic.mosaic(W, H, max(1, min(20, W * H // 30)), 9.0, seed=W * 1000 + H, C=C, grad=20.0)
     p = dict(n_superpixels=K, n_levels=L, bins_per_channel=bpc, smoothness_prior=gamma,
              iters_per_level=iters)
-    assert_parity(torch_cuda, orc, img, p)
+    assert_parity(torch_cuda, orc, img, p, mode=mode)
 
 
-def test_constant_image(torch_cuda, orc):
+def test_constant_image(torch_cuda, orc, mode):
     img = np.full((61, 47, 3), 99, np.uint8)
     p = dict(n_superpixels=12, n_levels=2, bins_per_channel=5, smoothness_prior=1, iters_per_level=3)
-    lab, s = assert_parity(torch_cuda, orc, img, p)
+    lab, s = assert_parity(torch_cuda, orc, img, p, mode=mode)
     assert s.stats(0).sum() == 0
 
 
-def test_batch_independent_frames(torch_cuda, orc):
+def test_batch_independent_frames(torch_cuda, orc, mode):
     """c3-shaped batch (K=400): every frame equals its own oracle run."""
     imgs = configs.frames("c3", n=6)
-    assert_parity(torch_cuda, orc, imgs, configs.params("c3"))
+    assert_parity(torch_cuda, orc, imgs, configs.params("c3"), mode=mode)
 
 
-def test_warm_start(torch_cuda, orc):
+def test_warm_start(torch_cuda, orc, mode):
     """Warm start (reading O9): labels of frame t seed frame t+1."""
     f, _ = mosaic.moving_mosaic(3, 160, 96, 15, 8.0, seed=42)
     p = dict(n_superpixels=40, n_levels=3, bins_per_channel=5, smoothness_prior=0, iters_per_level=3)
     r0 = orc.run(f[0], **p)
     init = np.stack([r0.labels, r0.labels])
-    assert_parity(torch_cuda, orc, f[1:], p, init=init)
+    assert_parity(torch_cuda, orc, f[1:], p, init=init, mode=mode)
 
 
-def test_c3_sampled_full_batch(torch_cuda, orc):
+def test_c3_sampled_full_batch(torch_cuda, orc, mode):
     """The full 256-frame c3 batch in one launch; frames 0, 85, 170, 255 checked
     against the oracle, every frame checked for histogram/size invariants."""
     imgs = configs.frames("c3")
     p = configs.params("c3")
-    lab, h, a, s = gpu_run(torch_cuda, imgs, p)
+    lab, h, a, s = gpu_run(torch_cuda, imgs, p, mode=mode)
     N = imgs.shape[1] * imgs.shape[2]
     assert (a.sum(1) == N).all()
     assert (h.sum(2) == a).all()
@@ -142,13 +151,14 @@ def test_c3_sampled_full_batch(torch_cuda, orc):
         np.testing.assert_array_equal(h[f], r.hist)
 
 
-def test_repeat_launch_is_deterministic(torch_cuda):
+def test_repeat_launch_is_deterministic(torch_cuda, mode):
     """Graph replays give identical output (no order dependence on the GPU)."""
     from paper_1309_3848_b200.seeds import Seeds
     img = configs.frames("c2")[0]
     p = configs.params("c2")
     s = Seeds(img.shape[1], img.shape[0], 3, *[p[k] for k in (
         "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    s.set_mode(mode)
     d = torch_cuda.from_numpy(img).cuda()
     out = torch_cuda.empty(img.shape[:2], dtype=torch_cuda.int32, device="cuda")
     ref = s.iterate(d, out).clone()
@@ -166,3 +176,16 @@ def test_host_entry_point(torch_cuda, orc):
     out = np.empty(img.shape[:2], np.int32)
     s.batch_host(np.ascontiguousarray(img), out)
     np.testing.assert_array_equal(out, orc.run(img, **p).labels)
+
+
+def test_modes_resolved(torch_cuda):
+    """A c2 frame fits a co-schedulable cluster (resident mode available) and
+    both modes report their launch counts (seeds_query)."""
+    from paper_1309_3848_b200.seeds import Seeds
+    s = Seeds(481, 321, 3, 200, 4, 5, 1, 4)
+    print("cluster size", s.info.cluster_size, "mode", s.info.exec_mode)
+    assert 1 <= s.info.cluster_size <= 16
+    s.set_mode("resident")
+    assert s.info.exec_mode == 2 and s.info.kernels_per_run == 1
+    s.set_mode("graph")
+    assert s.info.exec_mode == 1 and s.info.kernels_per_run == 107
