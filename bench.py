@@ -181,7 +181,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="auto", choices=["auto", "graph", "resident"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "graph", "resident", "grid"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--json-out", default=None)
@@ -312,7 +312,7 @@ def main():
                                    f"L={info.levels_eff}, I={p['iters_per_level']}, "
                                    f"B={info.bins_total}, gamma={p['smoothness_prior']}",
                        "frames_per_step_per_rank": nf,
-                       "exec_mode": {1: "graph", 2: "resident"}[info.exec_mode],
+                       "exec_mode": {1: "graph", 2: "resident", 3: "grid"}[info.exec_mode],
                        "cluster_size": info.cluster_size,
                        "parallelism": "replicas" if scaling == "weak" else f"frames/{world}",
                        "l2": "512 MiB buffer rewritten between timed steps (outside events)"},

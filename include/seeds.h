@@ -71,8 +71,10 @@ typedef struct {
     int subsweeps;       /* 4 L_eff I + P^2 I sub-sweeps per cold frame */
     int max_block_area;  /* largest top-level block, pixels */
     int kernels_per_run; /* kernel launches of one cold run in the resolved mode */
-    int exec_mode;       /* resolved execution mode (SEEDS_MODE_GRAPH or _RESIDENT) */
+    int exec_mode;       /* resolved execution mode of a one-frame run (SEEDS_MODE_GRAPH, _RESIDENT, _GRID) */
     int cluster_size;    /* CTAs per cluster of the resident kernel (0: frame does not fit) */
+    int grid_ctas;       /* CTAs of the grid-mode launch for one frame (0: no tile plan fits) */
+    int grid_tiles;      /* tiles of one frame in grid mode */
     size_t workspace_bytes_per_frame;
 } seeds_info;
 
@@ -147,11 +149,13 @@ seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int3
  * bisect a divergence against the oracle's max_subsweeps. */
 seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps);
 
-/* seeds_debug_trace -- resident mode only: enable (1) per-CTA clock64 stamps of
- * every sub-sweep of frame 0 (work finished / barrier passed), copy them to
- * host_out[min(cap, cluster_size*(subsweeps+4)*2)] (int64, layout
- * [cta][phase][2]), or disable (0) and free the buffer.  Synchronises the
- * device when host_out is given.  Diagnostic; not part of the hot path. */
+/* seeds_debug_trace -- resident / grid mode only: enable (1) per-CTA clock64
+ * stamps of every sub-sweep (slot 0 work finished, 1 barrier passed; grid mode
+ * also 2 replayed, 3 staged, 4 filtered, 5 decided), copy them to
+ * host_out[min(cap, ctas*(subsweeps+4)*8)] (int64, layout [cta][phase][8],
+ * ctas = max(#SM, cluster_size)), or disable (0) and free the buffer.
+ * Synchronises the device when host_out is given.  Diagnostic; not part of
+ * the hot path. */
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap);
 
 /* seeds_stats -- accepted moves per sub-sweep of frame `frame` of the last
@@ -170,7 +174,7 @@ enum {
     SEEDS_KIND_COUNT = 5
 };
 
-/* Execution modes (seeds_set_mode).  Both give bit-identical results.
+/* Execution modes (seeds_set_mode).  All give bit-identical results.
  *  GRAPH:    one kernel per sub-sweep, the run captured as a CUDA graph with
  *            programmatic dependent launch; every kernel spans all frames of
  *            the batch, state in HBM/L2 (any frame size).
@@ -178,12 +182,16 @@ enum {
  *            keeps labels, bins and histograms in (distributed) shared memory
  *            and separates sub-sweeps by cluster barriers; clusters loop over
  *            the frames of the batch (frames that fit a cluster, e.g. 481x321).
- *  AUTO:     GRAPH (RESIDENT is selected explicitly). */
-enum { SEEDS_MODE_AUTO = 0, SEEDS_MODE_GRAPH = 1, SEEDS_MODE_RESIDENT = 2 };
+ *  GRID:     one cooperative launch over every SM for the whole run: the batch
+ *            is cut into tiles of top-level blocks owned by fixed CTAs, state
+ *            in L2, one grid barrier per sub-sweep (frames up to 32000 px wide
+ *            whose tile plan fits shared memory).
+ *  AUTO:     GRID when its tile plan fits, else GRAPH. */
+enum { SEEDS_MODE_AUTO = 0, SEEDS_MODE_GRAPH = 1, SEEDS_MODE_RESIDENT = 2, SEEDS_MODE_GRID = 3 };
 
 /* seeds_set_mode -- pick the execution mode for later runs.  SEEDS_EINVAL for
  * an unknown mode; SEEDS_ESTATE if RESIDENT is requested but the frame does
- * not fit a co-schedulable cluster. */
+ * not fit a co-schedulable cluster, or GRID but no tile plan fits. */
 seeds_status seeds_set_mode(seeds_ctx *ctx, int mode);
 
 /* seeds_profile -- enable (1) or disable (0) per-kernel device timing: later

@@ -3,6 +3,8 @@
 // Integer geometry, workspaces, the sub-sweep schedule and its CUDA-graph
 // capture.  Every step of the hot path runs in the kernels of
 // seeds_kernels.cuh; this file only allocates, launches and copies.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,6 +17,7 @@
 #include "../../include/seeds.h"
 #include "seeds_kernels.cuh"
 #include "seeds_resident.cuh"
+#include "seeds_grid.cuh"
 
 using namespace seeds;
 
@@ -27,9 +30,11 @@ struct GraphKey {
     int nf = -1;
     int limit = -2;
     bool prof = false;
+    int mode = -1;
     bool operator==(const GraphKey &o) const
     {
-        return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof;
+        return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof &&
+               mode == o.mode;
     }
 };
 
@@ -87,7 +92,24 @@ struct seeds_ctx {
     int ntab = 0;
     ResParams rp{};           // resident layout (pointers filled per run)
     int *d_band = nullptr;    // band_y (CS+1) then band_top (CS+1)
+    uint32_t *d_kmap = nullptr;  // resident: home CTA | local row << 8 per superpixel
     long long *d_trace = nullptr;  // resident-kernel phase clocks (seeds_debug_trace)
+    // grid mode (seeds_grid.cuh): padded label planes, records, barrier counter, tile plan
+    uint16_t *d_labp = nullptr;
+    long long labp_fs = 0;
+    int lpitch = 0;
+    unsigned *d_sync = nullptr;
+    GRec *d_grec = nullptr;
+    size_t grec_bytes = 0;
+    GridTile *d_tiles = nullptr;
+    void *d_binsp = nullptr;     // padded bin planes for TMA staging (grid mode, bins not resident)
+    size_t binsp_bytes = 0;
+    size_t tiles_cap = 0;
+    int grid_nf = -1;      // batch size the plan is for
+    bool grid_ok = false;
+    int grid_G = 0;
+    size_t grid_smem = 0;
+    GridParams gp{};
     int n_sm = 148;
     bool pixel_tiled = true;  // SEEDS_PIXEL_TILED=0 selects the untiled pixel kernel
 };
@@ -263,6 +285,13 @@ static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
         CK(cudaMalloc(&ctx->d_A[i], F * ctx->K * 4));
         CK(cudaMalloc(&ctx->d_rec[i], F * ctx->rec_fs * sizeof(Rec)));
     }
+    release((void *&)ctx->d_labp);
+    ctx->lpitch = (ctx->W + 4 + 7) / 8 * 8;
+    ctx->labp_fs = (long long)(ctx->H + 4) * ctx->lpitch;
+    CK(cudaMalloc(&ctx->d_labp, F * ctx->labp_fs * 2));
+    CK(cudaMemset(ctx->d_labp, 0xFF, F * ctx->labp_fs * 2));  // sentinel border (never written)
+    if (!ctx->d_sync) CK(cudaMalloc(&ctx->d_sync, 16));
+    ctx->grid_nf = -1;
     CK(cudaMalloc(&ctx->d_cnt, (size_t)(ctx->S + 1) * F * 4));
     CK(cudaMalloc(&ctx->d_moves, (size_t)(ctx->S + 1) * F * 4));
     ctx->cap_frames = nf;
@@ -443,10 +472,346 @@ static seeds_status enqueue(seeds_ctx *ctx, const uint8_t *img, const int32_t *i
     return SEEDS_OK;
 }
 
-static int resolved_mode(const seeds_ctx *c)
+static bool plan_grid(seeds_ctx *c, int nf);
+static size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+
+// Execution mode of a run of nf frames: AUTO takes the grid mode whenever its
+// tile plan fits, else the graph mode.
+static int resolved_mode(seeds_ctx *c, int nf)
 {
-    if (c->mode != SEEDS_MODE_AUTO) return c->mode;
-    return SEEDS_MODE_GRAPH;  // resident mode is opt-in until it is faster
+    if (c->mode == SEEDS_MODE_GRAPH || c->mode == SEEDS_MODE_RESIDENT) return c->mode;
+    return plan_grid(c, nf) ? SEEDS_MODE_GRID : SEEDS_MODE_GRAPH;
+}
+
+// ---------------------------------------------------------------------------
+// Grid mode (seeds_grid.cuh): tile plan for a batch of nf frames.  Tiles are
+// rectangles of a x b top-level blocks (pixels when L = 0); the plan takes the
+// (a, b) with the least pixels on the busiest CTA (tiles go round-robin to
+// min(#SM, #tiles) CTAs), then the least halo.  Shared memory per CTA: the
+// staged labels of one tile (+ 2-pixel halo), the bins of all its tiles when
+// they fit (else of one tile, restaged every sub-sweep), the unit queue, the
+// warp tables of the large-block path and the block geometry.
+// ---------------------------------------------------------------------------
+template <typename BinT, int GAMMA, int P>
+static int grid_occupancy(size_t smem)
+{
+    auto k = k_grid<BinT, GAMMA, P>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, GRID_THREADS, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+static int grid_occupancy_for(const seeds_ctx *c, size_t smem)
+{
+    if (c->bb == 1) return c->gamma ? grid_occupancy<uint8_t, 1, 3>(smem) : grid_occupancy<uint8_t, 0, 2>(smem);
+    return c->gamma ? grid_occupancy<uint16_t, 1, 3>(smem) : grid_occupancy<uint16_t, 0, 2>(smem);
+}
+
+static std::vector<int> size_candidates(int n)
+{
+    std::vector<int> v;
+    for (int a = 1; a <= n; a = a < 64 ? a + 1 : a + a / 16) v.push_back(a);
+    if (v.back() != n) v.push_back(n);
+    return v;
+}
+
+static size_t align128(size_t v) { return (v + 127) & ~(size_t)127; }
+
+// TMA descriptors of the grid plan: the padded label planes (u16, x y frame,
+// box bw x bh) and, when the bins are staged, the padded bin planes.
+static bool encode_tmaps(seeds_ctx *c, GridParams &q)
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess || !fn) {
+            cudaGetLastError();
+            return false;
+        }
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint32_t es[3] = {1, 1, 1};
+    {
+        const cuuint64_t dims[3] = {(cuuint64_t)c->lpitch, (cuuint64_t)(c->H + 4), (cuuint64_t)c->cap_frames};
+        const cuuint64_t strides[2] = {(cuuint64_t)c->lpitch * 2, (cuuint64_t)c->labp_fs * 2};
+        const cuuint32_t box[3] = {(cuuint32_t)q.bw, (cuuint32_t)q.bh, 1};
+        if (enc(&q.tm_lab, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, c->d_labp, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    if (!q.bins_res) {
+        const cuuint64_t dims[3] = {(cuuint64_t)q.bpitch, (cuuint64_t)c->H, (cuuint64_t)c->cap_frames};
+        const cuuint64_t strides[2] = {(cuuint64_t)q.bpitch * c->bb, (cuuint64_t)q.binsp_fs * c->bb};
+        const cuuint32_t box[3] = {(cuuint32_t)q.bbw, (cuuint32_t)(q.bh - 4), 1};
+        if (enc(&q.tm_bins, c->bb == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                c->d_binsp, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    return true;
+}
+
+static bool plan_grid(seeds_ctx *c, int nf)
+{
+    if (c->cap_frames < nf && ensure_frames(c, nf) != SEEDS_OK) return false;  // the TMA maps need the planes
+    if (c->grid_nf == nf) return c->grid_ok;
+    c->grid_nf = nf;
+    c->grid_ok = false;
+    if (c->W > 32000 || c->H > 32000) return false;
+    const int Lm = c->L > 0 ? c->L - 1 : 0;
+    const int TX = c->L > 0 ? c->GX >> Lm : c->W, TY = c->L > 0 ? c->GY >> Lm : c->H;
+    auto ux = [&](int i) { return c->L > 0 ? c->colstart[(size_t)i << Lm] : i; };
+    auto uy = [&](int j) { return c->L > 0 ? c->rowstart[(size_t)j << Lm] : j; };
+    int muw = 0, muh = 0;
+    for (int i = 0; i < TX; i++) muw = std::max(muw, ux(i + 1) - ux(i));
+    for (int j = 0; j < TY; j++) muh = std::max(muh, uy(j + 1) - uy(j));
+    const size_t limit = 227 * 1024;
+    const size_t tabw = (2 * (size_t)c->B + 2) * 4;
+    bool need_tab = false;
+    GridParams &q = c->gp;
+    q = GridParams{};
+    for (int l = 0; l < c->L; l++) {
+        const int am = max_block_area(c, l);
+        q.bkind[l] = am <= 4 ? BK_T4 : am <= 32 ? BK_T16 : BK_WARP;
+        int gs = 0;
+        while ((1 << gs) < am && gs < 5) gs++;
+        q.gshift[l] = gs;
+        need_tab = need_tab || q.bkind[l] == BK_WARP;
+    }
+    const size_t fixed = 64 + 16 + align16((size_t)(c->GX + c->GY + 2) * 4) + (need_tab ? tabw : 0);
+    double best = 1e300;
+    int ba = 0, bb_ = 0;
+    for (int a : size_candidates(TX))
+        for (int b : size_candidates(TY)) {
+            const long long T = (long long)nf * ((TX + a - 1) / a) * ((TY + b - 1) / b);
+            const long long G = std::min<long long>(c->n_sm, T);
+            const long long tw = (long long)a * muw, th = (long long)b * muh;
+            if ((tw + 4 + 14) / 8 * 8 > 256 || th + 4 > 256) continue;  // TMA box limits (aligned start)
+            const size_t stage = 2 * align128((size_t)((tw + 4 + 14) / 8 * 8) * (th + 4) * 2);
+            const size_t minimal = stage + 2 * align128((size_t)(tw + 32) * th * c->bb) + align16((size_t)tw * th * 4) + fixed;
+            if (minimal > limit) continue;
+            const long long per = (T + G - 1) / G;
+            const double score = (double)per * tw * th + 4.0 * per * (tw + th + 4);
+            if (score < best) {
+                best = score;
+                ba = a;
+                bb_ = b;
+            }
+        }
+    if (!ba) return false;
+    // tiles of one frame, then their per-tile capacities
+    const int ntx = (TX + ba - 1) / ba, nty = (TY + bb_ - 1) / bb_;
+    std::vector<GridTile> ft;
+    std::vector<long long> tpx, tq, tr;
+    for (int ty = 0; ty < nty; ty++)
+        for (int tx = 0; tx < ntx; tx++) {
+            GridTile t{};
+            const int i0 = tx * ba, i1 = std::min(TX, (tx + 1) * ba), j0 = ty * bb_, j1 = std::min(TY, (ty + 1) * bb_);
+            t.X0 = ux(i0); t.X1 = ux(i1); t.Y0 = uy(j0); t.Y1 = uy(j1);
+            t.BX0 = i0 << Lm; t.BX1 = i1 << Lm; t.BY0 = j0 << Lm; t.BY1 = j1 << Lm;
+            const long long w = t.X1 - t.X0, h = t.Y1 - t.Y0;
+            long long qc = ((w + c->P - 1) / c->P) * ((h + c->P - 1) / c->P), rc = qc;
+            for (int l = 0; l < c->L; l++) {
+                const int bx0 = t.BX0 >> l, bx1 = t.BX1 >> l, by0 = t.BY0 >> l, by1 = t.BY1 >> l;
+                for (int cy = 0; cy < 2; cy++)
+                    for (int cx = 0; cx < 2; cx++) {
+                        long long units = 0, sum = 0;
+                        for (int bj = by0; bj < by1; bj++) {
+                            if ((bj & 1) != cy) continue;
+                            const int bh = c->rowstart[(size_t)(bj + 1) << l] - c->rowstart[(size_t)bj << l];
+                            for (int bi = bx0; bi < bx1; bi++) {
+                                if ((bi & 1) != cx) continue;
+                                const int bw = c->colstart[(size_t)(bi + 1) << l] - c->colstart[(size_t)bi << l];
+                                units++;
+                                sum += std::min(bw * bh, c->B);
+                            }
+                        }
+                        qc = std::max(qc, units);
+                        rc = std::max(rc, sum);
+                    }
+            }
+            ft.push_back(t);
+            tpx.push_back(w * h);
+            tq.push_back(qc);
+            tr.push_back(rc);
+        }
+    const long long T = (long long)nf * ft.size();
+    const int G = (int)std::min<long long>(c->n_sm, T);
+    std::vector<long long> cpx(G, 0), crec(G, 0);
+    long long qcap = 0;
+    int max_tw = 0, max_th = 0;
+    for (size_t i = 0; i < ft.size(); i++) {
+        max_tw = std::max(max_tw, ft[i].X1 - ft[i].X0);
+        max_th = std::max(max_th, ft[i].Y1 - ft[i].Y0);
+        qcap = std::max(qcap, tq[i]);
+    }
+    // TMA boxes start at a 16-byte aligned column at or left of the tile's halo
+    q.bw = (max_tw + 4 + 7 + 7) / 8 * 8;
+    q.bh = max_th + 4;
+    q.bbw = c->bb == 1 ? (max_tw + 15 + 15) / 16 * 16 : (max_tw + 7 + 7) / 8 * 8;
+    q.stage_bytes = (int)align128((size_t)q.bw * q.bh * 2);
+    q.bins_bytes = (int)align128((size_t)q.bbw * max_th * c->bb);
+    q.tx_bytes = q.bw * q.bh * 2;  // + the bin box when the bins are staged (set with bins_res)
+    q.tiles_per_cta = (int)((T + G - 1) / G);
+    std::vector<GridTile> tiles((size_t)T);
+    for (long long t = 0; t < T; t++) {
+        const size_t i = (size_t)(t % (long long)ft.size());
+        GridTile g = ft[i];
+        g.f = (int)(t / (long long)ft.size());
+        const int cta = (int)(t % G);
+        g.boff = (int)cpx[cta];
+        cpx[cta] += tpx[i];
+        crec[cta] += tr[i];
+        tiles[(size_t)t] = g;
+    }
+    const long long max_cpx = *std::max_element(cpx.begin(), cpx.end());
+    const long long rec_cap = *std::max_element(crec.begin(), crec.end()) + 32;
+    // shared-memory layout: records in shared memory saves the replay an L2
+    // round trip, so it is preferred over shared-memory-resident bins
+    for (int opt = 0; opt < 4; opt++) {
+        const int rs = opt < 2, res = !(opt & 1);
+        size_t off = 0;
+        q.o_stage = (unsigned)off; off = align128(off + 2 * (size_t)q.stage_bytes);
+        q.o_bins = (unsigned)off;  off = align128(off + (res ? (size_t)max_cpx * c->bb : 2 * (size_t)q.bins_bytes));
+        q.o_rec = (unsigned)off;   off = align16(off + (rs ? 2 * (size_t)rec_cap * sizeof(GRec) : 0));
+        q.o_queue = (unsigned)off; off = align16(off + (size_t)(qcap + 32) * 4);
+        q.o_misc = (unsigned)off;  off = align16(off + 64);
+        q.o_mbar = (unsigned)off;  off = align16(off + 16);
+        q.o_tiles = (unsigned)off; off = align16(off + (size_t)q.tiles_per_cta * sizeof(GridTile));
+        q.o_geo = (unsigned)off;   off = align16(off + (size_t)(c->GX + c->GY + 2) * 4);
+        q.o_tab = (unsigned)off;
+        if (off + (need_tab ? tabw : 0) > limit) continue;
+        q.ntab = need_tab ? (int)std::min<size_t>(GRID_THREADS / 32, (limit - off) / tabw) : 0;
+        const size_t smem = off + q.ntab * tabw;
+        const int occ = grid_occupancy_for(c, smem);
+        if (occ < 1) continue;
+        q.bins_res = res;
+        q.rec_smem = rs;
+        q.tx_bytes = q.bw * q.bh * 2 + (res ? 0 : q.bbw * (q.bh - 4) * c->bb);
+        q.q_cap = (int)qcap + 32;
+        q.GX = c->GX;
+        q.GY = c->GY;
+        q.rec_cap = rec_cap;
+        q.ntiles = (int)T;
+        // device buffers: tiles, records
+        if (c->tiles_cap < tiles.size()) {
+            if (c->d_tiles) cudaFree(c->d_tiles);
+            c->d_tiles = nullptr;
+            c->tiles_cap = 0;
+            if (cudaMalloc(&c->d_tiles, tiles.size() * sizeof(GridTile)) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            c->tiles_cap = tiles.size();
+        }
+        if (cudaMemcpy(c->d_tiles, tiles.data(), tiles.size() * sizeof(GridTile), cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        const size_t rb = rs ? 16 : (size_t)G * 2 * rec_cap * sizeof(GRec);
+        if (c->grec_bytes < rb) {
+            if (c->d_grec) cudaFree(c->d_grec);
+            c->d_grec = nullptr;
+            c->grec_bytes = 0;
+            if (cudaMalloc(&c->d_grec, rb) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            c->grec_bytes = rb;
+        }
+        q.tiles = c->d_tiles;
+        q.rec = c->d_grec;
+        if (!res) {  // padded bin planes for the TMA
+            q.bpitch = c->bb == 1 ? (c->W + 15) / 16 * 16 : (c->W + 7) / 8 * 8;
+            q.binsp_fs = (long long)q.bpitch * c->H;
+            const size_t bytes = (size_t)c->cap_frames * q.binsp_fs * c->bb;
+            if (c->binsp_bytes < bytes) {
+                if (c->d_binsp) cudaFree(c->d_binsp);
+                c->d_binsp = nullptr;
+                c->binsp_bytes = 0;
+                if (cudaMalloc(&c->d_binsp, bytes) != cudaSuccess) {
+                    cudaGetLastError();
+                    return false;
+                }
+                c->binsp_bytes = bytes;
+            }
+            q.binsp = c->d_binsp;
+        }
+        if (!encode_tmaps(c, q)) return false;
+        c->grid_G = G;
+        c->grid_smem = smem;
+        c->grid_ok = true;
+        return true;
+    }
+    return false;
+}
+
+template <typename BinT, int GAMMA, int P>
+static cudaError_t launch_grid_t(seeds_ctx *ctx, const GridParams &q, cudaStream_t st)
+{
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3(ctx->grid_G);
+    cfg.blockDim = dim3(GRID_THREADS);
+    cfg.dynamicSmemBytes = ctx->grid_smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_grid<BinT, GAMMA, P>, q);
+}
+
+// Enqueue one grid-mode run: zero the histograms, move counters and the barrier
+// counter, then the single persistent launch.
+static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
+                                 cudaStream_t st)
+{
+    for (int i = 0; i < 2; i++) {
+        CK(cudaMemsetAsync(ctx->d_H[i], 0, (size_t)nf * ctx->H_fs * 4, st));
+        CK(cudaMemsetAsync(ctx->d_A[i], 0, (size_t)nf * ctx->K * 4, st));
+    }
+    CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)(ctx->S + 1) * nf * 4, st));
+    CK(cudaMemsetAsync(ctx->d_sync, 0, 16, st));
+    GridParams q = ctx->gp;
+    q.img = img; q.init = init; q.out = out;
+    q.W = ctx->W; q.H = ctx->H; q.C = ctx->C; q.bpc = ctx->bpc; q.B = ctx->B; q.K = ctx->K; q.nx = ctx->nx;
+    q.L = ctx->L; q.iters = ctx->iters; q.limit = ctx->limit; q.S = ctx->S; q.nf = nf;
+    q.colstart = ctx->d_colstart; q.rowstart = ctx->d_rowstart; q.bxof = ctx->d_bxof; q.byof = ctx->d_byof;
+    q.lab = ctx->d_labp; q.lab_fs = ctx->labp_fs; q.lpitch = ctx->lpitch;
+    q.bins = ctx->d_bins; q.N = ctx->N;
+    for (int i = 0; i < 2; i++) {
+        q.Hb[i] = ctx->d_H[i];
+        q.Ab[i] = ctx->d_A[i];
+    }
+    q.H_fs = ctx->H_fs;
+    q.moves = ctx->d_moves;
+    q.sync = ctx->d_sync;
+    q.trace = ctx->d_trace;
+    ctx->ev_used = 0;
+    CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
+    cudaError_t e;
+    if (ctx->bb == 1)
+        e = ctx->gamma ? launch_grid_t<uint8_t, 1, 3>(ctx, q, st) : launch_grid_t<uint8_t, 0, 2>(ctx, q, st);
+    else
+        e = ctx->gamma ? launch_grid_t<uint16_t, 1, 3>(ctx, q, st) : launch_grid_t<uint16_t, 0, 2>(ctx, q, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid launch");
+    CK(prof_end(ctx, st));
+    const bool blocks = init == nullptr && ctx->L > 0;
+    const int total = (blocks ? 4 * ctx->L * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
+    ctx->last_done = ctx->limit >= 0 ? std::min(ctx->limit, total) : total;
+    ctx->last_final = ctx->last_done & 1;
+    return SEEDS_OK;
 }
 
 template <typename BinT, int GAMMA, int P>
@@ -465,7 +830,7 @@ static int resident_clusters(int cs, size_t smem)
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(512);
+    cfg.blockDim = dim3(RES_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -483,15 +848,14 @@ static int resident_clusters_for(const seeds_ctx *c, int cs, size_t smem)
     return c->gamma ? resident_clusters<uint16_t, 1, 3>(cs, smem) : resident_clusters<uint16_t, 0, 2>(cs, smem);
 }
 
-static size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
-
 // Resident mode (seeds_resident.cuh): partition the rows into CS bands aligned
-// with the top-level block rows (each >= 2 pixel rows), lay out the shared
-// memory and check that a cluster of CS CTAs can be co-scheduled.
+// with the top-level block rows (each >= 2 pixel rows), give every superpixel
+// a home CTA (the band holding the centre row of its grid cell), lay out the
+// shared memory and check that a cluster of CS CTAs can be co-scheduled.
 static void setup_resident(seeds_ctx *c)
 {
     c->cluster = 0;
-    if (c->GX > 16383 || c->GY > 16383 || c->L > 8) return;  // record packing limits
+    if (c->GX > 16383 || c->GY > 16383 || c->L > 8 || c->K > 8192) return;  // record / table limits
     const int T = c->L > 0 ? (c->GY >> (c->L - 1)) : c->H;     // row units the bands are made of
     auto unit_row = [&](int t) { return c->L > 0 ? c->rowstart[(size_t)t << (c->L - 1)] : t; };
     for (int cs = std::min(16, T); cs >= 1; cs--) {
@@ -510,24 +874,72 @@ static void setup_resident(seeds_ctx *c)
             bmax = std::max(bmax, ys[r + 1] - ys[r]);
         }
         if (cs > 1 && bmin < 2) continue;
+        // home CTA of each superpixel
+        std::vector<uint32_t> kmap(c->K);
+        std::vector<int> nloc(cs, 0);
+        for (int k = 0; k < c->K; k++) {
+            const int gy = k / c->nx;
+            const int yc = (c->rowstart[(size_t)gy << c->L] + c->rowstart[(size_t)(gy + 1) << c->L]) / 2;
+            int r = 0;
+            while (r + 1 < cs && ys[r + 1] <= yc) r++;
+            kmap[k] = (uint32_t)r | (uint32_t)(nloc[r]++) << 8;
+        }
         ResParams &q = c->rp;
         q = ResParams{};
-        q.kloc = (c->K + cs - 1) / cs;
-        q.rec_cap = ((c->W + 1) / 2) * ((bmax + 1) / 2) + 32;
+        q.kloc = *std::max_element(nloc.begin(), nloc.end());
+        // queue capacity: the most units of one colour class in a band (pixel
+        // level and every block level); record capacity: the most histogram
+        // deltas one sub-sweep of a band can emit (one per pixel unit, or per
+        // distinct bin of each block: at most min(alpha, B))
+        long long qcap = (long long)((c->W + c->P - 1) / c->P) * ((bmax + c->P - 1) / c->P);
+        long long rcap = qcap;
+        for (int l = 0; l < c->L; l++) {
+            const int GXl = c->GX >> l;
+            for (int r = 0; r < cs; r++) {
+                const int j0 = top[r] << (c->L - 1 - l), j1 = top[r + 1] << (c->L - 1 - l);
+                qcap = std::max(qcap, (long long)((GXl + 1) / 2) * ((j1 - j0 + 1) / 2));
+                for (int cy = 0; cy < 2; cy++)
+                    for (int cx = 0; cx < 2; cx++) {
+                        long long sum = 0;
+                        for (int bj = j0; bj < j1; bj++) {
+                            if ((bj & 1) != cy) continue;
+                            const int h = c->rowstart[(size_t)(bj + 1) << l] - c->rowstart[(size_t)bj << l];
+                            for (int bi = cx; bi < GXl; bi += 2) {
+                                const int w = c->colstart[(size_t)(bi + 1) << l] - c->colstart[(size_t)bi << l];
+                                sum += std::min(w * h, c->B);
+                            }
+                        }
+                        rcap = std::max(rcap, sum);
+                    }
+            }
+        }
+        q.q_cap = (int)qcap + 32;
+        q.rec_cap = (int)rcap + 32;
+        q.pitch = c->W + 2 * RES_PAD;
         q.lab_rows = bmax + 4;
+        q.GX = c->GX;
+        q.GY = c->GY;
+        bool need_tab = false;
+        for (int l = 0; l < c->L; l++) {
+            const int am = max_block_area(c, l);
+            q.bkind[l] = am <= 4 ? BK_T4 : am <= 16 ? BK_T16 : BK_WARP;
+            need_tab = need_tab || q.bkind[l] == BK_WARP;
+        }
         const size_t tabw = (2 * (size_t)c->B + 2) * 4;
         size_t off = 0;
-        q.o_lab = (unsigned)off;  off = align16(off + (size_t)q.lab_rows * c->W * 2);
-        q.o_bins = (unsigned)off; off = align16(off + (size_t)bmax * c->W * c->bb);
-        q.o_H = (unsigned)off;    off = align16(off + 2 * (size_t)q.kloc * c->B * 4);
-        q.o_A = (unsigned)off;    off = align16(off + 2 * (size_t)q.kloc * 4);
-        q.o_rec = (unsigned)off;  off = align16(off + 2 * (size_t)q.rec_cap * sizeof(Rec));
-        q.o_misc = (unsigned)off; off = align16(off + 16);
-        q.o_scr = (unsigned)off;  off = align16(off + (size_t)SMALL_ALPHA * 512 * 2);
+        q.o_lab = (unsigned)off;   off = align16(off + (size_t)q.lab_rows * q.pitch * 2);
+        q.o_bins = (unsigned)off;  off = align16(off + (size_t)bmax * c->W * c->bb);
+        q.o_H = (unsigned)off;     off = align16(off + 2 * (size_t)q.kloc * c->B * 4);
+        q.o_A = (unsigned)off;     off = align16(off + 2 * (size_t)q.kloc * 4);
+        q.o_rec = (unsigned)off;   off = align16(off + 2 * (size_t)q.rec_cap * sizeof(Rec));
+        q.o_misc = (unsigned)off;  off = align16(off + 16);
+        q.o_kaddr = (unsigned)off; off = align16(off + 2 * (size_t)c->K * 4);
+        q.o_geo = (unsigned)off;   off = align16(off + (size_t)(c->GX + c->GY + 2) * 4);
+        q.o_queue = (unsigned)off; off = align16(off + (size_t)q.q_cap * 4);
         q.o_tab = (unsigned)off;
         const size_t limit = 227 * 1024;
-        if (off + tabw > limit) continue;
-        q.ntab = (int)std::min<size_t>(16, (limit - off) / tabw);
+        if (off + (need_tab ? tabw : 0) > limit) continue;
+        q.ntab = need_tab ? (int)std::min<size_t>(RES_THREADS / 32, (limit - off) / tabw) : 0;
         const size_t smem = off + q.ntab * tabw;
         const int n = resident_clusters_for(c, cs, smem);
         if (n <= 0) continue;
@@ -537,16 +949,20 @@ static void setup_resident(seeds_ctx *c)
             h[cs + 1 + r] = top[r];
         }
         if (c->d_band) cudaFree(c->d_band);
+        c->d_band = nullptr;
+        if (c->d_kmap) cudaFree(c->d_kmap);
+        c->d_kmap = nullptr;
         if (cudaMalloc(&c->d_band, h.size() * sizeof(int)) != cudaSuccess ||
-            cudaMemcpy(c->d_band, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaMemcpy(c->d_band, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMalloc(&c->d_kmap, kmap.size() * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMemcpy(c->d_kmap, kmap.data(), kmap.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) !=
+                cudaSuccess) {
             cudaGetLastError();
             return;
         }
         q.band_y = c->d_band;
         q.band_top = c->d_band + cs + 1;
-        q.big_mask = 0;
-        for (int l = 0; l < c->L; l++)
-            if (max_block_area(c, l) > SMALL_ALPHA) q.big_mask |= 1 << l;
+        q.kmap = c->d_kmap;
         c->cluster = cs;
         c->max_clusters = n;
         c->res_smem = smem;
@@ -564,7 +980,7 @@ static cudaError_t launch_resident_t(seeds_ctx *ctx, const ResParams &q, int ncl
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(ncl * ctx->cluster);
-    cfg.blockDim = dim3(512);
+    cfg.blockDim = dim3(RES_THREADS);
     cfg.dynamicSmemBytes = ctx->res_smem;
     cfg.stream = st;
     cfg.attrs = attr;
@@ -612,7 +1028,8 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
 {
     seeds_status r = ensure_frames(ctx, nf);
     if (r != SEEDS_OK) return r;
-    if (resolved_mode(ctx) == SEEDS_MODE_RESIDENT) {
+    const int mode = resolved_mode(ctx, nf);
+    if (mode == SEEDS_MODE_RESIDENT) {
         ctx->ev_used = 0;
         r = run_resident(ctx, img, init, out, nf, st);
         if (r != SEEDS_OK) return r;
@@ -622,14 +1039,16 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     }
     GraphKey key;
     key.img = img; key.init = init; key.out = out; key.nf = nf; key.limit = ctx->limit; key.prof = ctx->prof;
+    key.mode = mode;
     if (!ctx->exec || !(key == ctx->key)) {
         if (ctx->exec) {
             cudaGraphExecDestroy(ctx->exec);
             ctx->exec = nullptr;
         }
         CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-        seeds_status er = ctx->bb == 1 ? enqueue<uint8_t>(ctx, img, init, out, nf, ctx->cap_stream)
-                                       : enqueue<uint16_t>(ctx, img, init, out, nf, ctx->cap_stream);
+        seeds_status er = mode == SEEDS_MODE_GRID ? enqueue_grid(ctx, img, init, out, nf, ctx->cap_stream)
+                          : ctx->bb == 1          ? enqueue<uint8_t>(ctx, img, init, out, nf, ctx->cap_stream)
+                                                  : enqueue<uint16_t>(ctx, img, init, out, nf, ctx->cap_stream);
         cudaGraph_t graph = nullptr;
         cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
         if (er != SEEDS_OK) {
@@ -756,9 +1175,15 @@ seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *o)
     o->nx = ctx->nx; o->ny = ctx->ny; o->k_actual = ctx->K; o->levels_eff = ctx->L;
     o->grid_x = ctx->GX; o->grid_y = ctx->GY; o->colour_period = ctx->P; o->bins_total = ctx->B;
     o->bin_bytes = ctx->bb; o->subsweeps = ctx->S; o->max_block_area = ctx->amax;
-    o->exec_mode = resolved_mode(ctx);
+    o->exec_mode = resolved_mode(const_cast<seeds_ctx *>(ctx), 1);
     o->cluster_size = ctx->cluster;
-    o->kernels_per_run = o->exec_mode == SEEDS_MODE_RESIDENT ? 1 : ctx->kernels_per_run;
+    {
+        seeds_ctx *m = const_cast<seeds_ctx *>(ctx);
+        const bool ok = plan_grid(m, 1);
+        o->grid_ctas = ok ? m->grid_G : 0;
+        o->grid_tiles = ok ? m->gp.ntiles : 0;
+    }
+    o->kernels_per_run = o->exec_mode == SEEDS_MODE_GRAPH ? ctx->kernels_per_run : 1;
     o->workspace_bytes_per_frame = (size_t)ctx->N * (ctx->bb + 2) +
                                    (size_t)(((long long)ctx->GX * ctx->GY + 7) / 8 * 8) * 4 +
                                    (size_t)ctx->K * (ctx->B + 1) * 8 + (size_t)ctx->N * sizeof(Rec) * 2;
@@ -826,9 +1251,13 @@ seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out,
 
 seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 {
-    if (!ctx || mode < SEEDS_MODE_AUTO || mode > SEEDS_MODE_RESIDENT) return SEEDS_EINVAL;
+    if (!ctx || mode < SEEDS_MODE_AUTO || mode > SEEDS_MODE_GRID) return SEEDS_EINVAL;
     if (mode == SEEDS_MODE_RESIDENT && ctx->cluster == 0) {
         snprintf(ctx->err, sizeof ctx->err, "the frame does not fit a co-schedulable cluster (resident mode)");
+        return SEEDS_ESTATE;
+    }
+    if (mode == SEEDS_MODE_GRID && !plan_grid(ctx, 1)) {
+        snprintf(ctx->err, sizeof ctx->err, "no grid-mode tile plan fits shared memory");
         return SEEDS_ESTATE;
     }
     ctx->mode = mode;
@@ -838,7 +1267,7 @@ seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap)
 {
     if (!ctx) return SEEDS_EINVAL;
-    const size_t n = (size_t)std::max(1, ctx->cluster) * (ctx->S + 4) * 2;
+    const size_t n = (size_t)std::max(ctx->n_sm, ctx->cluster) * (ctx->S + 4) * 8;
     if (enable && !ctx->d_trace) {
         CK(cudaMalloc(&ctx->d_trace, n * sizeof(long long)));
         CK(cudaMemset(ctx->d_trace, 0, n * sizeof(long long)));
@@ -876,7 +1305,8 @@ void seeds_destroy(seeds_ctx *ctx)
     if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
     void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1],
-                    ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band,
+                    ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band, ctx->d_kmap,
+                    ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp,
                     ctx->d_init_stage, ctx->d_out_stage};
     for (void *p : ptrs)
         if (p) cudaFree(p);

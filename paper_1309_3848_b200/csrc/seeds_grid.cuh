@@ -1,0 +1,776 @@
+// seeds_grid.cuh -- grid mode: one persistent launch over every SM for the
+// whole refinement of a batch, one software grid barrier per sub-sweep
+// (DESIGN.md section 6).
+//
+//  * Tiles.  The frames are cut into rectangles of top-level blocks (so every
+//    block of every level lies in exactly one tile); tile t belongs to CTA
+//    t mod gridDim.x for the whole run.  The host sizes the tiles so that the
+//    CTAs get equal pixel counts.
+//  * State in L2.  Pixel labels live in a global plane with a 2-pixel sentinel
+//    border (0xFFFF equals no superpixel, so no label read needs a bounds
+//    test); block levels work on that plane too (a level-l block carries one
+//    label: its top-left pixel's; its ring is read at the adjacent pixels; a
+//    block move writes its pixels).  H and A are double buffered exactly as in
+//    the graph path: sub-sweep s reads buffer s&1 and adds into the other the
+//    previous sub-sweep's deltas (replayed from this CTA's own records) and its
+//    own.  Every read of mutable state bypasses L1 (ld.global.cg).
+//  * Per sub-sweep and tile: stage the tile's labels plus a 2-pixel halo into
+//    shared memory (the bins of the CTA's tiles stay in shared memory for the
+//    whole run when they fit), run the cheap boundary and ring tests
+//     one thread per unit and push the survivors to a queue,
+//    then run the colour / smoothness tests densely over the queue: one thread
+//    per pixel or small block, one warp per large block (K5).
+//  * Same-colour units never read each other's labels (reading O7), so a
+//    tile staged while other CTAs write moves of the same sub-sweep sees the
+//    same values either way; the grid barrier (release / acquire at GPU scope)
+//    orders everything else.
+#pragma once
+#include <cuda.h>  // CUtensorMap (encoded by the host; no driver calls here)
+
+#include "seeds_kernels.cuh"
+
+namespace seeds {
+
+constexpr int GRID_THREADS = 512;
+
+struct GridTile {
+    int f;               // frame
+    int X0, X1, Y0, Y1;  // pixel rectangle
+    int BX0, BX1, BY0, BY1;  // level-0 block index rectangle (multiples of 2^(L-1))
+    int boff;            // offset of the tile's bins in the CTA's shared bins (resident bins)
+    int pad;
+};
+
+// A histogram delta of frame f (grid mode): k | n << 16, bin | count << 16.
+struct GRec {
+    uint32_t kn, bc, f, pad;
+};
+
+struct GridParams {
+    CUtensorMap tm_lab;   // TMA: padded label planes (x, y, frame), box bw x bh x 1
+    CUtensorMap tm_bins;  // TMA: padded bin planes (x, y, frame), box bbw x bh x 1 (staged bins only)
+    const uint8_t *img;
+    const int32_t *init;  // warm-start labels or nullptr
+    int32_t *out;
+    int W, H, C, bpc, B, K, nx, L, iters, limit, S, nf;
+    const int *colstart, *rowstart, *bxof, *byof;
+    const GridTile *tiles;
+    int ntiles;
+    uint16_t *lab;         // padded label planes: pixel (x, y) of frame f at f*lab_fs + (y+2)*lpitch + x+2
+    long long lab_fs;
+    int lpitch;
+    void *bins;            // bin planes (W x H per frame) when the bins do not stay in shared memory
+    long long N;
+    int *Hb[2], *Ab[2];
+    long long H_fs;
+    int *moves;            // (S + 1) x nf accepted units per sub-sweep
+    unsigned *sync;        // grid barrier counter (zero at launch)
+    long long *trace;      // debug: per CTA, per phase (clock64 at work end, after barrier), or nullptr
+    GRec *rec;             // per CTA: 2 lists of rec_cap records
+    long long rec_cap;
+    int bkind[16];         // per level: BK_T4 (thread per block), BK_T16 (G-lane segments), BK_WARP
+    int gshift[16];        // per level: log2 G of the segment path
+    void *binsp;           // padded bin planes (pitch bpitch) when the bins are staged
+    long long binsp_fs;
+    int bpitch;
+    unsigned o_stage, o_bins, o_queue, o_tab, o_misc, o_geo, o_rec, o_tiles, o_mbar;
+    int stage_bytes, bins_bytes;  // one stage buffer of labels / of bins (two of each), 128-byte multiples
+    int tx_bytes;                 // bytes one tile's TMA loads deliver (label box + bin box)
+    int bw, bbw, bh;              // TMA boxes: label box bw x bh, bin box bbw x (bh - 4)
+    int tiles_per_cta, q_cap, ntab, GX, GY, bins_res, rec_smem;
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned &target)
+{
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        unsigned v;
+        long long spins = 0;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (++spins > (1LL << 26)) __trap();  // a CTA that never arrives: fail loudly instead of hanging
+        } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned n)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity)
+{
+    uint32_t done = 0;
+    long long spins = 0;
+    do {
+        if (++spins > (1LL << 26)) __trap();  // a lost TMA completion: fail loudly instead of hanging
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// 3-D TMA tile load (x, y, frame) into shared memory, completion on mbarrier b
+__device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *tm, int x, int y, int z, uint64_t *b)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(b))
+        : "memory");
+}
+
+template <typename BinT>
+struct GridCta {
+    const GridParams &q;
+    uint16_t *stage0;  // two TMA stage buffers: a tile's labels + 2-pixel halo, pitch bw
+    BinT *sbins;       // bins: every owned tile (bins_res) or two TMA stage buffers
+    uint32_t *rem;     // removable-ring LUT (8 words, reading Q8)
+    GridTile *tiles;   // this CTA's tiles
+    uint64_t *mbar;    // two mbarriers (one per stage buffer)
+    uint16_t *stage;   // the current tile's staged labels
+    uint32_t *queue;   // surviving units of the current tile and sub-sweep
+    uint32_t *tabs;    // ntab warp tables of 2B + 2 words
+    int *misc;         // [0], [1]: record counts of the two lists, [2]: queue length
+    int *cs, *rs;      // level-0 block column / row starts (GX + 1, GY + 1)
+    // current tile
+    int f, X0, X1, Y0, Y1, sp, tbp;
+    int sx0, bx0;      // first staged column: labels (padded plane) and bins, 16-byte aligned for the TMA
+    const BinT *tb;    // bins of the current tile, row pitch tbp
+    uint16_t *glab;    // global label plane of frame f, (0, 0) at pixel (-2, -2)
+    const int *Hf0, *Hf1, *Af0, *Af1;  // the frame's two histogram / size buffers
+
+    __device__ GridCta(const GridParams &qq, unsigned char *smem) : q(qq)
+    {
+        stage0 = reinterpret_cast<uint16_t *>(smem + q.o_stage);
+        sbins = reinterpret_cast<BinT *>(smem + q.o_bins);
+        rem = reinterpret_cast<uint32_t *>(smem + q.o_misc + 16);
+        tiles = reinterpret_cast<GridTile *>(smem + q.o_tiles);
+        mbar = reinterpret_cast<uint64_t *>(smem + q.o_mbar);
+        queue = reinterpret_cast<uint32_t *>(smem + q.o_queue);
+        tabs = reinterpret_cast<uint32_t *>(smem + q.o_tab);
+        misc = reinterpret_cast<int *>(smem + q.o_misc);
+        cs = reinterpret_cast<int *>(smem + q.o_geo);
+        rs = cs + q.GX + 1;
+    }
+    __device__ __forceinline__ void select(const GridTile &t, int slot)
+    {
+        f = t.f;
+        X0 = t.X0; X1 = t.X1; Y0 = t.Y0; Y1 = t.Y1;
+        sp = q.bw;
+        sx0 = X0 & ~7;
+        stage = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(stage0) + slot * q.stage_bytes);
+        if (q.bins_res) {
+            tb = sbins + t.boff;
+            tbp = X1 - X0;
+            bx0 = X0;
+        } else {
+            tb = reinterpret_cast<const BinT *>(reinterpret_cast<const unsigned char *>(sbins) + slot * q.bins_bytes);
+            tbp = q.bbw;
+            bx0 = X0 & ~(16 / (int)sizeof(BinT) - 1);
+        }
+        glab = q.lab + (long long)f * q.lab_fs;
+        Hf0 = q.Hb[0] + (long long)f * q.H_fs;
+        Hf1 = q.Hb[1] + (long long)f * q.H_fs;
+        Af0 = q.Ab[0] + (long long)f * q.K;
+        Af1 = q.Ab[1] + (long long)f * q.K;
+    }
+    __device__ __forceinline__ const uint16_t *cell(int x, int y) const
+    {
+        return stage + (y - Y0 + 2) * sp + (x + 2 - sx0);
+    }
+    __device__ __forceinline__ int bin(int x, int y) const { return tb[(y - Y0) * tbp + (x - bx0)]; }
+    __device__ __forceinline__ bool removable_s(int m) const { return (rem[m >> 5] >> (m & 31)) & 1u; }
+    // TMA: stage tile t into buffer `slot` (thread 0 only)
+    __device__ __forceinline__ void issue(const GridTile &t, int slot) const
+    {
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy label writes before the TMA reads
+        mbar_expect(&mbar[slot], (unsigned)q.tx_bytes);
+        // box starts must be 16-byte aligned in x (the TMA faults otherwise)
+        tma_load3(reinterpret_cast<unsigned char *>(stage0) + slot * q.stage_bytes, &q.tm_lab, t.X0 & ~7, t.Y0, t.f,
+                  &mbar[slot]);
+        if (!q.bins_res)
+            tma_load3(reinterpret_cast<unsigned char *>(sbins) + slot * q.bins_bytes, &q.tm_bins,
+                      t.X0 & ~(16 / (int)sizeof(BinT) - 1), t.Y0, t.f, &mbar[slot]);
+    }
+    __device__ __forceinline__ int ldA(int buf, int k) const { return __ldcg((buf ? Af1 : Af0) + k); }
+    __device__ __forceinline__ int ldH(int buf, int k, int b) const
+    {
+        return __ldcg((buf ? Hf1 : Hf0) + (long long)k * q.B + b);
+    }
+    __device__ __forceinline__ void set(int x, int y, int v) const
+    {
+        glab[(long long)(y + 2) * q.lpitch + x + 2] = (uint16_t)v;
+    }
+};
+
+__device__ __forceinline__ void gdelta(const GridParams &q, int buf, int f, int k, int n, int b, int count)
+{
+    int *H = (buf ? q.Hb[1] : q.Hb[0]) + (long long)f * q.H_fs;
+    int *A = (buf ? q.Ab[1] : q.Ab[0]) + (long long)f * q.K;
+    atomicAdd(H + (long long)k * q.B + b, -count);
+    atomicAdd(H + (long long)n * q.B + b, count);
+    atomicAdd(A + k, -count);
+    atomicAdd(A + n, count);
+}
+
+// Block colour test (Prop. 1, R1) of a block of alpha <= 4 pixels by one
+// thread, every gather issued before the first use (see block_thread).
+template <typename Ctx>
+__device__ __forceinline__ int block_t4(const Ctx &c, int ob, int k, const Neigh &nb, int xa, int ya, int rw,
+                                        int alpha, int (&bv)[4], int (&cnt)[4])
+{
+    {
+        int x = 0, y = 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            bv[i] = i < alpha ? c.bin(xa + x, ya + y) : -1 - i;
+            if (++x == rw) { x = 0; y++; }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        bool first = i < alpha;
+#pragma unroll
+        for (int j = 0; j < i; j++) first = first && bv[j] != bv[i];
+        int n = 1;
+#pragma unroll
+        for (int j = i + 1; j < 4; j++) n += bv[j] == bv[i];
+        cnt[i] = first ? n : 0;
+    }
+    int nn[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) nn[d] = (nb.valid >> d & 1) ? nb.v[d] : k;
+    const long long Ak = c.ldA(ob, k);
+    long long An[4], hk[4], hn[4][4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) An[d] = c.ldA(ob, nn[d]);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int b = bv[i] < 0 ? 0 : bv[i];
+        hk[i] = c.ldH(ob, k, b);
+#pragma unroll
+        for (int d = 0; d < 4; d++) hn[i][d] = c.ldH(ob, nn[d], b);
+    }
+    unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+    const long long al = alpha;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        if (!cnt[i]) continue;
+        const long long lb = cnt[i];
+        const long long u = (hk[i] - lb) * al, v = lb * (Ak - al);
+        Nk += (unsigned long long)(u < v ? u : v);
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const long long un = hn[i][d] * al, vn = lb * An[d];
+            Nn[d] += (unsigned long long)(un < vn ? un : vn);
+        }
+    }
+    int acc = -1;
+#pragma unroll
+    for (int d = 0; d < 4; d++)
+        if (acc < 0 && (nb.valid >> d & 1) && gt_prod(Nn[d], (unsigned long long)(Ak - al), Nk, (unsigned long long)An[d]))
+            acc = nb.v[d];
+    return acc;
+}
+
+template <typename BinT, int GAMMA, int P>
+__global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant__ GridParams q)
+{
+    extern __shared__ __align__(128) uint32_t smem[];
+    GridCta<BinT> c(q, reinterpret_cast<unsigned char *>(smem));
+    constexpr int NT = GRID_THREADS, NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int W = q.W, B = q.B;
+    const int TW = 2 * B + 2;  // warp table words
+    unsigned target = 0;
+    GRec *const rec0 = q.rec_smem ? reinterpret_cast<GRec *>(reinterpret_cast<unsigned char *>(smem) + q.o_rec)
+                                  : q.rec + (long long)blockIdx.x * 2 * q.rec_cap;
+    GRec *const rec1 = rec0 + q.rec_cap;
+    auto rec_list = [&](int b) { return b ? rec1 : rec0; };
+
+    for (int i = tid; i < q.ntab * TW; i += NT) c.tabs[i] = 0;
+    for (int i = tid; i <= q.GX; i += NT) c.cs[i] = q.colstart[i];
+    for (int i = tid; i <= q.GY; i += NT) c.rs[i] = q.rowstart[i];
+    if (tid < 4) c.misc[tid] = 0;
+    if (tid < 8) c.rem[tid] = c_removable[tid];
+    const int ntl = blockIdx.x < q.ntiles ? (q.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // tiles of this CTA
+    for (int i = tid; i < ntl; i += NT) c.tiles[i] = q.tiles[blockIdx.x + (long long)i * gridDim.x];
+    if (tid == 0) {
+        mbar_init(&c.mbar[0], 1);
+        mbar_init(&c.mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    unsigned phase0 = 0, phase1 = 0;  // parity of the next completion of each stage buffer
+    __syncthreads();
+
+    // ---- seed: bins (reading Q1), labels (grid, or warm
+    // start, reading O9) and the histogram counts (Eq. 6) into both buffers,
+    // warp-aggregated on the (label, bin) key
+    for (int ti = 0; ti < ntl; ti++) {
+        const GridTile t = c.tiles[ti];
+        const int tw = t.X1 - t.X0;
+        BinT *tb = q.bins_res ? c.sbins + t.boff : static_cast<BinT *>(q.binsp) + (long long)t.f * q.binsp_fs;
+        uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
+        int *H0 = q.Hb[0] + (long long)t.f * q.H_fs, *H1 = q.Hb[1] + (long long)t.f * q.H_fs;
+        int *A0 = q.Ab[0] + (long long)t.f * q.K, *A1 = q.Ab[1] + (long long)t.f * q.K;
+        const long long fN = (long long)t.f * q.N;
+        for (int y = t.Y0 + wid; y < t.Y1; y += NW) {
+            const int gy = (q.byof[y] >> q.L) * q.nx;
+            for (int x0 = t.X0; x0 < t.X1; x0 += 32) {
+                const int x = x0 + lane;
+                int key = -1, k = -1, b = 0;
+                if (x < t.X1) {
+                    const uint8_t *v = q.img + (fN + (long long)y * W + x) * q.C;
+                    for (int ch = 0; ch < q.C; ch++) b = b * q.bpc + (((int)v[ch] * q.bpc) >> 8);
+                    if (q.bins_res) tb[(y - t.Y0) * tw + x - t.X0] = (BinT)b;
+                    else tb[(long long)y * q.bpitch + x] = (BinT)b;
+                    k = q.init ? q.init[fN + (long long)y * W + x] : gy + (q.bxof[x] >> q.L);
+                    gl[(long long)(y + 2) * q.lpitch + x + 2] = (uint16_t)k;
+                    key = k * B + b;
+                }
+                unsigned m = __match_any_sync(FULL, key);
+                if (x < t.X1 && lane == __ffs(m) - 1) {
+                    atomicAdd(H0 + key, __popc(m));
+                    atomicAdd(H1 + key, __popc(m));
+                }
+                m = __match_any_sync(FULL, k);
+                if (x < t.X1 && lane == __ffs(m) - 1) {
+                    atomicAdd(A0 + k, __popc(m));
+                    atomicAdd(A1 + k, __popc(m));
+                }
+            }
+        }
+    }
+    grid_barrier(q.sync, target);
+
+    int s = 0;
+    // debug trace [cta][phase][8]: 0 work done, 1 barrier passed, 2 replayed,
+    // 3 last tile staged, 4 last tile filtered, 5 last tile decided
+    auto stamp = [&](int phase, int which) {
+        if (q.trace && tid == 0) q.trace[((long long)blockIdx.x * (q.S + 4) + phase) * 8 + which] = clock64();
+    };
+    stamp(0, 1);
+    auto count_moves = [&](bool moved) {
+        const unsigned mv = __ballot_sync(FULL, moved);
+        if (lane == 0 && mv) atomicAdd(&q.moves[(long long)(s + 1) * q.nf + c.f], __popc(mv));
+    };
+    // Start of sub-sweep s: replay this CTA's deltas of sub-sweep s-1 into
+    // buffer yb and reset the list that sub-sweep s fills.
+    auto begin_subsweep = [&](int yb) {
+        if (tid == 0 && ntl > 0) c.issue(c.tiles[0], 0);  // overlaps the replay
+        const int nrec = c.misc[yb];
+        const GRec *r = rec_list(yb);
+        for (int e = tid; e < nrec; e += NT) {
+            const GRec x = r[e];
+            gdelta(q, yb, (int)x.f, x.kn & 0xFFFF, x.kn >> 16, x.bc & 0xFFFF, x.bc >> 16);
+        }
+        if (tid == 0) c.misc[yb ^ 1] = 0;  // list yb^1 was last read before the barrier
+        stamp(s + 1, 2);
+    };
+    // Tile pipeline: the CTA's tiles are staged by TMA (labels + 2-pixel halo,
+    // and the bins when they do not stay in shared memory) into two alternating
+    // buffers; tile i + 1 is requested before tile i is processed.
+    auto stage_wait = [&](int ti) {
+        if (ti & 1) {
+            mbar_wait(&c.mbar[1], phase1);
+            phase1 ^= 1;
+        } else {
+            mbar_wait(&c.mbar[0], phase0);
+            phase0 ^= 1;
+        }
+        c.select(c.tiles[ti], ti & 1);
+        stamp(s + 1, 3);
+    };
+    auto end_tile = [&]() {
+        __syncthreads();
+        stamp(s + 1, 5);
+        if (tid == 0) c.misc[2] = 0;
+    };
+    auto end_subsweep = [&]() {
+        stamp(s + 1, 0);
+        grid_barrier(q.sync, target);
+        stamp(s + 1, 1);
+        s++;
+    };
+    // A move k -> n of `count` pixels of bin b: record + histogram deltas.
+    auto emit = [&](GRec *r, int slot, int k, int n, int b, int count, int yb) {
+        r[slot] = GRec{(uint32_t)k | ((uint32_t)n << 16), (uint32_t)b | ((uint32_t)count << 16), (uint32_t)c.f, 0u};
+        gdelta(q, yb, c.f, k, n, b, count);
+    };
+
+    const bool blocks = q.init == nullptr && q.L > 0;
+    // ---- block levels, largest first ---------------------
+    if (blocks) {
+        for (int l = q.L - 1; l >= 0; l--) {
+            const int kind = q.bkind[l];
+            const int gs = q.gshift[l], G = 1 << gs;
+            for (int it = 0; it < q.iters; it++)
+                for (int col = 0; col < 4; col++) {
+                    if (q.limit >= 0 && s >= q.limit) break;
+                    const int cx = col & 1, cy = col >> 1;
+                    const int ob = s & 1, yb_ = ob ^ 1;
+                    begin_subsweep(yb_);
+                    for (int ti = 0; ti < ntl; ti++) {
+                        if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1);
+                        stage_wait(ti);
+                        const GridTile t = c.tiles[ti];
+                        const int bx0 = t.BX0 >> l, bx1 = t.BX1 >> l, by0 = t.BY0 >> l, by1 = t.BY1 >> l;
+                        const int ifirst = bx0 + ((bx0 & 1) != cx), jfirst = by0 + ((by0 & 1) != cy);
+                        const int uw = ifirst < bx1 ? (bx1 - ifirst + 1) / 2 : 0;
+                        const int uh = jfirst < by1 ? (by1 - jfirst + 1) / 2 : 0;
+                        const int nunits = uw * uh;
+                        const float inv_uw = 1.0f / (float)max(uw, 1);
+                        auto rect = [&](int u, int &bi, int &bj, int &xa, int &xb, int &ya, int &yb) {
+                            const int tj = div_small(u, uw, inv_uw);
+                            bi = ifirst + 2 * (u - tj * uw);
+                            bj = jfirst + 2 * tj;
+                            xa = c.cs[bi << l]; xb = c.cs[(bi + 1) << l];
+                            ya = c.rs[bj << l]; yb = c.rs[(bj + 1) << l];
+                        };
+                        // lanes per unit of the decision pass; survivors of the
+                        // boundary + ring test go through a queue only when the
+                        // units do not fit one pass
+                        const int per_unit = kind == BK_T4 ? 1 : kind == BK_WARP ? 32 : G;
+                        const bool direct = (long long)nunits * per_unit <= NT;
+                        int nq = nunits;
+                        if (!direct) {
+                            for (int base = wid * 32; base < nunits; base += NT) {
+                                const int u = base + lane;
+                                bool take = false;
+                                if (u < nunits) {
+                                    int bi, bj, xa, xb, ya, yb;
+                                    rect(u, bi, bj, xa, xb, ya, yb);
+                                    const Neigh nb = ring_at(c.cell(xa, ya), c.sp, xb - xa, (yb - ya) * c.sp);
+                                    take = nb.valid && c.removable_s(nb.mask);
+                                }
+                                push_warp(c.queue, &c.misc[2], take, (uint32_t)u);
+                            }
+                            __syncthreads();
+                            nq = c.misc[2];
+                        }
+                        stamp(s + 1, 4);
+                        if (kind == BK_T4) {
+                            // one thread per block (<= 4 px), all gathers in flight together
+                            for (int base = wid * 32; base < nq; base += NT) {
+                                const int e = base + lane;
+                                int acc = -1, k = 0, xa = 0, xb = 0, ya = 0, yb = 0, nd = 0;
+                                int bv[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
+                                if (e < nq) {
+                                    int bi, bj;
+                                    rect(direct ? e : (int)c.queue[e], bi, bj, xa, xb, ya, yb);
+                                    const uint16_t *a = c.cell(xa, ya);
+                                    k = a[0];
+                                    const Neigh nb = ring_at(a, c.sp, xb - xa, (yb - ya) * c.sp);
+                                    if (nb.valid && c.removable_s(nb.mask)) {
+                                        const int rw = xb - xa, alpha = rw * (yb - ya);
+                                        acc = block_t4(c, ob, k, nb, xa, ya, rw, alpha, bv, cnt);
+                                        if (acc >= 0) nd = (cnt[0] != 0) + (cnt[1] != 0) + (cnt[2] != 0) + (cnt[3] != 0);
+                                    }
+                                }
+                                count_moves(acc >= 0);
+                                int slot = append_warp(&c.misc[ob], nd);
+                                if (acc >= 0) {
+                                    GRec *r = rec_list(ob);
+#pragma unroll
+                                    for (int i = 0; i < 4; i++)
+                                        if (cnt[i]) emit(r, slot++, k, acc, bv[i], cnt[i], yb_);
+                                    for (int y = ya; y < yb; y++)
+                                        for (int x = xa; x < xb; x++) c.set(x, y, acc);
+                                }
+                            }
+                        } else if (kind != BK_WARP) {
+                            // G lanes per block (<= 32 px): lane i holds pixel i, equal
+                            // bins merged by __match_any_sync, segmented reduction (K5)
+                            const int segs = 32 >> gs, seg = lane >> gs, si = lane & (G - 1);
+                            for (int base = wid * segs; base < nq; base += NW * segs) {
+                                const int e = base + seg;
+                                int acc = -1, k = 0, xa = 0, xb = 0, ya = 0, yb = 0, rw = 1, alpha = 0;
+                                Neigh nb;
+                                nb.valid = 0;
+                                nb.mask = 0;
+                                if (e < nq) {
+                                    int bi, bj;
+                                    rect(direct ? e : (int)c.queue[e], bi, bj, xa, xb, ya, yb);
+                                    const uint16_t *a = c.cell(xa, ya);
+                                    k = a[0];
+                                    nb = ring_at(a, c.sp, xb - xa, (yb - ya) * c.sp);
+                                    rw = xb - xa;
+                                    alpha = rw * (yb - ya);
+                                }
+                                const bool ok = nb.valid && c.removable_s(nb.mask);
+                                int b = -1;
+                                if (ok && si < alpha) {
+                                    const int dy = div_small(si, rw, 1.0f / (float)rw);
+                                    b = c.bin(xa + si - dy * rw, ya + dy);
+                                }
+                                const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : (seg << 16) | b);
+                                const bool leader = b >= 0 && lane == __ffs(m) - 1;
+                                const long long lb = __popc(m);
+                                unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+                                long long Ak = 1, An[4] = {1, 1, 1, 1};
+                                if (ok) {
+                                    const int bb = b < 0 ? 0 : b;
+                                    Ak = c.ldA(ob, k);
+                                    const long long hk = c.ldH(ob, k, bb);
+                                    long long hn[4];
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) {
+                                        const int n = (nb.valid >> d & 1) ? nb.v[d] : k;
+                                        An[d] = c.ldA(ob, n);
+                                        hn[d] = c.ldH(ob, n, bb);
+                                    }
+                                    if (leader) {
+                                        const long long al = alpha;
+                                        const long long uu = (hk - lb) * al, vv = lb * (Ak - al);
+                                        Nk = (unsigned long long)(uu < vv ? uu : vv);
+#pragma unroll
+                                        for (int d = 0; d < 4; d++) {
+                                            const long long un = hn[d] * al, vn = lb * An[d];
+                                            Nn[d] = (nb.valid >> d & 1) ? (unsigned long long)(un < vn ? un : vn) : 0ull;
+                                        }
+                                    }
+                                }
+                                for (int o = G >> 1; o >= 1; o >>= 1) {
+                                    Nk += __shfl_xor_sync(FULL, Nk, o);
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) Nn[d] += __shfl_xor_sync(FULL, Nn[d], o);
+                                }
+                                if (ok) {
+#pragma unroll
+                                    for (int d = 0; d < 4; d++)
+                                        if (acc < 0 && (nb.valid >> d & 1) &&
+                                            gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
+                                            acc = nb.v[d];
+                                }
+                                count_moves(acc >= 0 && si == 0);
+                                const int slot = append_warp(&c.misc[ob], acc >= 0 && leader ? 1 : 0);
+                                if (acc >= 0) {
+                                    if (leader) emit(rec_list(ob), slot, k, acc, b, (int)lb, yb_);
+                                    if (si < alpha) {
+                                        const int dy = div_small(si, rw, 1.0f / (float)rw);
+                                        c.set(xa + si - dy * rw, ya + dy, acc);
+                                    }
+                                }
+                            }
+                        } else if (wid < q.ntab) {
+                            // one warp per block; per-warp bin table + list of non-empty bins (K5)
+                            uint32_t *cnt = c.tabs + (size_t)wid * TW, *list = cnt + B, *nlist = cnt + 2 * B;
+                            const int nwu = q.ntab < NW ? q.ntab : NW;
+                            for (int e = wid; e < nq; e += nwu) {
+                                int bi, bj, xa, xb, ya, yb;
+                                rect(direct ? e : (int)c.queue[e], bi, bj, xa, xb, ya, yb);
+                                const uint16_t *a = c.cell(xa, ya);
+                                const int k = a[0];
+                                const Neigh nb = ring_at(a, c.sp, xb - xa, (yb - ya) * c.sp);
+                                if (!nb.valid || !c.removable_s(nb.mask)) continue;
+                                const int rw = xb - xa, alpha = rw * (yb - ya);
+                                const float inv = 1.0f / (float)rw;
+                                // candidate sizes first: their loads overlap the histogram build
+                                const long long Ak = c.ldA(ob, k);
+                                long long An[4];
+#pragma unroll
+                                for (int d = 0; d < 4; d++) An[d] = c.ldA(ob, (nb.valid >> d & 1) ? nb.v[d] : k);
+                                for (int i0 = 0; i0 < alpha; i0 += 32) {
+                                    const int i = i0 + lane;
+                                    int b = -1;
+                                    if (i < alpha) {
+                                        const int dy = div_small(i, rw, inv);
+                                        b = c.bin(xa + i - dy * rw, ya + dy);
+                                    }
+                                    const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : b);
+                                    if (b >= 0 && lane == __ffs(m) - 1 &&
+                                        atomicAdd(&cnt[b], (unsigned)__popc(m)) == 0u)
+                                        list[atomicAdd(nlist, 1u)] = (uint32_t)b;
+                                }
+                                __syncwarp();
+                                const int ns = (int)*nlist;
+                                unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+                                for (int i = lane; i < ns; i += 32) {
+                                    const int b = list[i];
+                                    const long long lc = cnt[b];
+                                    const long long hk = c.ldH(ob, k, b);
+                                    long long hn[4];
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) hn[d] = c.ldH(ob, (nb.valid >> d & 1) ? nb.v[d] : k, b);
+                                    const long long u = (hk - lc) * alpha, v = lc * (Ak - alpha);
+                                    Nk += (unsigned long long)(u < v ? u : v);
+#pragma unroll
+                                    for (int d = 0; d < 4; d++)
+                                        if (nb.valid >> d & 1) {
+                                            const long long un = hn[d] * alpha, vn = lc * An[d];
+                                            Nn[d] += (unsigned long long)(un < vn ? un : vn);
+                                        }
+                                }
+                                // five independent butterfly reductions, interleaved
+#pragma unroll
+                                for (int o = 16; o >= 1; o >>= 1) {
+                                    Nk += __shfl_xor_sync(FULL, Nk, o);
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) Nn[d] += __shfl_xor_sync(FULL, Nn[d], o);
+                                }
+                                int acc = -1;
+#pragma unroll
+                                for (int d = 0; d < 4; d++)
+                                    if (acc < 0 && (nb.valid >> d & 1) &&
+                                        gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
+                                        acc = nb.v[d];
+                                if (acc >= 0) {
+                                    int base = 0;
+                                    if (lane == 0) {
+                                        base = atomicAdd(&c.misc[ob], ns);
+                                        atomicAdd(&q.moves[(long long)(s + 1) * q.nf + c.f], 1);
+                                    }
+                                    base = __shfl_sync(FULL, base, 0);
+                                    GRec *r = rec_list(ob);
+                                    for (int i = lane; i < ns; i += 32) {
+                                        const int b = list[i];
+                                        emit(r, base + i, k, acc, b, (int)cnt[b], yb_);
+                                    }
+                                    for (int i = lane; i < alpha; i += 32) {
+                                        const int dy = div_small(i, rw, inv);
+                                        c.set(xa + i - dy * rw, ya + dy, acc);
+                                    }
+                                }
+                                __syncwarp();
+                                for (int i = lane; i < ns; i += 32) cnt[list[i]] = 0;
+                                __syncwarp();
+                                if (lane == 0) *nlist = 0;
+                                __syncwarp();
+                            }
+                        }
+                        end_tile();
+                    }
+                    end_subsweep();
+                }
+        }
+    }
+
+    // ---- pixel level, P x P colouring (Q11) --------------
+    for (int it = 0; it < q.iters; it++)
+        for (int col = 0; col < P * P; col++) {
+            if (q.limit >= 0 && s >= q.limit) break;
+            const int cx = col % P, cy = col / P;
+            const int ob = s & 1, yb_ = ob ^ 1;
+            begin_subsweep(yb_);
+            for (int ti = 0; ti < ntl; ti++) {
+                if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1);
+                stage_wait(ti);
+                const GridTile t = c.tiles[ti];
+                const int xfirst = t.X0 + (((cx - t.X0) % P) + P) % P;
+                const int yfirst = t.Y0 + (((cy - t.Y0) % P) + P) % P;
+                const int uw = xfirst < t.X1 ? (t.X1 - xfirst + P - 1) / P : 0;
+                const int uh = yfirst < t.Y1 ? (t.Y1 - yfirst + P - 1) / P : 0;
+                const int nunits = uw * uh;
+                const float inv_uw = 1.0f / (float)max(uw, 1);
+                auto unit_xy = [&](int u, int &x, int &y) {
+                    const int tj = div_small(u, uw, inv_uw);
+                    x = xfirst + P * (u - tj * uw);
+                    y = yfirst + P * tj;
+                };
+                const bool direct = nunits <= NT;
+                int nq = nunits;
+                if (!direct) {
+                    // filter: boundary + ring test, survivors (x | y << 16, tile-relative) to the queue
+                    for (int base = wid * 32; base < nunits; base += NT) {
+                        const int u = base + lane;
+                        bool take = false;
+                        uint32_t v = 0;
+                        if (u < nunits) {
+                            int x, y;
+                            unit_xy(u, x, y);
+                            const Neigh nb = ring_at(c.cell(x, y), c.sp, 1, c.sp);
+                            take = nb.valid && c.removable_s(nb.mask);
+                            v = (uint32_t)(x - t.X0) | (uint32_t)(y - t.Y0) << 16;
+                        }
+                        push_warp(c.queue, &c.misc[2], take, v);
+                    }
+                    __syncthreads();
+                    nq = c.misc[2];
+                }
+                stamp(s + 1, 4);
+                for (int base = wid * 32; base < nq; base += NT) {
+                    const int e = base + lane;
+                    int acc = -1, k = 0, j = 0, x = 0, y = 0;
+                    if (e < nq) {
+                        if (direct) {
+                            unit_xy(e, x, y);
+                        } else {
+                            const uint32_t v = c.queue[e];
+                            x = t.X0 + (int)(v & 0xFFFF);
+                            y = t.Y0 + (int)(v >> 16);
+                        }
+                        const uint16_t *a = c.cell(x, y);
+                        const int sp = c.sp;
+                        k = a[0];
+                        const Neigh nb = ring_at(a, sp, 1, sp);
+                        if (nb.valid && c.removable_s(nb.mask)) {
+                            j = c.bin(x, y);
+                            // all gathers in flight together (invalid slots re-read k's row)
+                            const long long hk = c.ldH(ob, k, j), Ak = c.ldA(ob, k);
+                            long long hn[4], An[4];
+#pragma unroll
+                            for (int d = 0; d < 4; d++) {
+                                const int n = (nb.valid >> d & 1) ? nb.v[d] : k;
+                                hn[d] = c.ldH(ob, n, j);
+                                An[d] = c.ldA(ob, n);
+                            }
+                            int pass = 0;  // candidates passing the colour test (Prop. 1, one look-up)
+#pragma unroll
+                            for (int d = 0; d < 4; d++)
+                                pass |= (int)((nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d]) << d;
+                            if (!GAMMA) {
+                                if (pass) acc = nb.v[__ffs(pass) - 1];
+                            } else if (pass) {
+                                uint16_t w[25];
+#pragma unroll
+                                for (int dy = -2; dy <= 2; dy++)
+#pragma unroll
+                                    for (int dx = -2; dx <= 2; dx++) w[(dy + 2) * 5 + dx + 2] = a[dy * sp + dx];
+                                const uint32_t vx = (x > 0 ? 1u : 0u) | 2u | (x + 1 < W ? 4u : 0u);
+                                const uint32_t vy = (y > 0 ? 1u : 0u) | 2u | (y + 1 < q.H ? 4u : 0u);
+                                uint32_t centres = 0;
+#pragma unroll
+                                for (int iy = 0; iy < 3; iy++)
+                                    if (vy >> iy & 1) centres |= vx << (3 * iy);
+                                const int base_s = __popc(centres) - box_sum(win_mask(w, k), centres);
+#pragma unroll
+                                for (int d = 0; d < 4; d++)
+                                    if (acc < 0 && (pass >> d & 1) && base_s + box_sum(win_mask(w, nb.v[d]), centres) >= 0)
+                                        acc = nb.v[d];
+                            }
+                        }
+                    }
+                    count_moves(acc >= 0);
+                    const int slot = append_warp(&c.misc[ob], acc >= 0 ? 1 : 0);
+                    if (acc >= 0) {
+                        emit(rec_list(ob), slot, k, acc, j, 1, yb_);
+                        c.set(x, y, acc);
+                    }
+                }
+                end_tile();
+            }
+            end_subsweep();
+        }
+
+    // ---- outputs: int32 labels of the owned tiles --------------------------
+    for (int ti = 0; ti < ntl; ti++) {
+        const GridTile t = c.tiles[ti];
+        const uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
+        int32_t *o = q.out + (long long)t.f * q.N;
+        for (int y = t.Y0 + wid; y < t.Y1; y += NW)
+            for (int x = t.X0 + lane; x < t.X1; x += 32)
+                o[(long long)y * W + x] = __ldcg(gl + (long long)(y + 2) * q.lpitch + x + 2);
+    }
+}
+
+}  // namespace seeds

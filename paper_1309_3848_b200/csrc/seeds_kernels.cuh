@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(256) k_block_small(SweepParams p)
 template <typename BinT>
 __global__ void __launch_bounds__(256) k_block_large(SweepParams p)
 {
-    extern __shared__ uint32_t smem[];
+    extern __shared__ __align__(128) uint32_t smem[];
     pdl_enter();
     const int f = blockIdx.y;
     apply_prev(p, f, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
@@ -699,6 +699,167 @@ __global__ void __launch_bounds__(256) k_pixel(SweepParams p)
     const int f = blockIdx.y;
     apply_prev(p, f, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
     pixel_units<BinT, GAMMA, P>(p, f, (long long)blockIdx.x * blockDim.x, (long long)gridDim.x * blockDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// Helpers shared by the persistent kernels (grid mode, seeds_grid.cuh, and
+// resident mode, seeds_resident.cuh): their label planes carry a sentinel
+// border, so label reads need no bounds test.
+// ---------------------------------------------------------------------------
+
+// per-level block strategies of the persistent kernels
+enum { BK_T4 = 0, BK_T16 = 1, BK_WARP = 2 };
+
+// q = t / d for small non-negative t, d (< 2^22) with a float reciprocal and
+// an exact correction.
+__device__ __forceinline__ int div_small(int t, int d, float inv)
+{
+    int q = __float2int_rz((float)t * inv);
+    q -= q * d > t;
+    q += (q + 1) * d <= t;
+    return q;
+}
+
+constexpr uint16_t SENT = 0xFFFF;
+
+// Ring mask + candidates (W, E, N, S, first occurrence, reading Q5) from the
+// 8 ring labels; SENT (outside the image) is never a candidate nor equal to k.
+__device__ __forceinline__ Neigh neigh8(int k, int vN, int vNE, int vE, int vSE, int vS, int vSW, int vW, int vNW)
+{
+    Neigh r;
+    r.mask = (vN == k) | (vNE == k) << 1 | (vE == k) << 2 | (vSE == k) << 3 | (vS == k) << 4 | (vSW == k) << 5 |
+             (vW == k) << 6 | (vNW == k) << 7;
+    r.v[0] = vW; r.v[1] = vE; r.v[2] = vN; r.v[3] = vS;
+    r.valid = 0;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        bool ok = r.v[d] != SENT && r.v[d] != k;
+#pragma unroll
+        for (int e = 0; e < d; e++) ok = ok && r.v[e] != r.v[d];
+        r.valid |= (int)ok << d;
+    }
+    return r;
+}
+
+// Ring of a pixel (a = its cell) or of a block whose rectangle spans dxb
+// columns and dyb rows (times the pitch) from its top-left cell a.
+__device__ __forceinline__ Neigh ring_at(const uint16_t *a, int pitch, int dxb, int dyb)
+{
+    return neigh8(a[0], a[-pitch], a[dxb - pitch], a[dxb], a[dxb + dyb], a[dyb], a[dyb - 1], a[-1], a[-pitch - 1]);
+}
+
+// Warp-aggregated append of n entries to a CTA-local list; returns the first slot.
+__device__ __forceinline__ int append_warp(int *count, int n)
+{
+    const int lane = threadIdx.x & 31;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    int base = 0;
+    if (lane == 31 && total) base = atomicAdd(count, total);
+    base = __shfl_sync(FULL, base, 31);
+    return base + incl - n;
+}
+
+// Push `v` into the queue if `take` (all 32 lanes call).
+__device__ __forceinline__ void push_warp(uint32_t *queue, int *count, bool take, uint32_t v)
+{
+    const unsigned b = __ballot_sync(FULL, take);
+    if (!b) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(count, __popc(b));
+    base = __shfl_sync(FULL, base, 0);
+    if (take) queue[base + __popc(b & ((1u << lane) - 1))] = v;
+}
+
+// Proposition 2 on the 5x5 label window of p, as bit masks:
+// bit (dy + 2) * 5 + (dx + 2).  S(n) = sum over the in-image patch centres i
+// of W3(p) of (1 + |W3(i) n n| - |W3(i) n k|), |.| counting cells of that
+// label; cells outside the image are SENT and match nothing (reading Q15).
+constexpr uint32_t BOX3 = 0x1CE7u;  // 3x3 box at the window's top-left corner
+
+__device__ __forceinline__ uint32_t win_mask(const uint16_t (&w)[25], int v)
+{
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 25; i++) m |= (uint32_t)(w[i] == v) << i;
+    return m;
+}
+
+__device__ __forceinline__ int box_sum(uint32_t m, uint32_t centres)
+{
+    int s = 0;
+#pragma unroll
+    for (int iy = 0; iy < 3; iy++)
+#pragma unroll
+        for (int ix = 0; ix < 3; ix++)
+            if (centres >> (iy * 3 + ix) & 1) s += __popc(m & (BOX3 << (iy * 5 + ix)));
+    return s;
+}
+
+// Block colour test (Prop. 1, R1) of one block of alpha <= TA pixels by one
+// thread: the block histogram l_b from the bins held in registers (distinct
+// bins by pairwise comparison), then
+//   N_n = sum_b min(H[n][b] alpha, l_b A_n), N_k = sum_b min((H[k][b] - l_b) alpha, l_b (A_k - alpha))
+// and the first candidate with N_n (A_k - alpha) > N_k A_n wins.
+template <int TA, typename Ctx>
+__device__ __forceinline__ int block_thread(const Ctx &c, int ob, int k, const Neigh &nb, int xa, int ya,
+                                            int rw, int alpha, int (&bv)[TA], int (&cnt)[TA])
+{
+    {
+        int x = 0, y = 0;
+#pragma unroll
+        for (int i = 0; i < TA; i++) {
+            bv[i] = i < alpha ? c.bin(xa + x, ya + y) : -1 - i;
+            if (++x == rw) { x = 0; y++; }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < TA; i++) {
+        bool first = i < alpha;
+#pragma unroll
+        for (int j = 0; j < i; j++) first = first && bv[j] != bv[i];
+        int n = 1;
+#pragma unroll
+        for (int j = i + 1; j < TA; j++) n += bv[j] == bv[i];
+        cnt[i] = first ? n : 0;
+    }
+    const long long Ak = c.ldA(ob, k);
+    long long An[4] = {1, 1, 1, 1};
+#pragma unroll
+    for (int d = 0; d < 4; d++)
+        if (nb.valid >> d & 1) An[d] = c.ldA(ob, nb.v[d]);
+    unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+    const long long al = alpha;
+#pragma unroll
+    for (int i = 0; i < TA; i++) {
+        if (!cnt[i]) continue;
+        const long long lb = cnt[i];
+        const long long h = c.ldH(ob, k, bv[i]);
+        long long g[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int d = 0; d < 4; d++)
+            if (nb.valid >> d & 1) g[d] = c.ldH(ob, nb.v[d], bv[i]);
+        const long long u = (h - lb) * al, v = lb * (Ak - al);
+        Nk += (unsigned long long)(u < v ? u : v);
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const long long un = g[d] * al, vn = lb * An[d];
+            Nn[d] += (unsigned long long)(un < vn ? un : vn);
+        }
+    }
+    int acc = -1;
+#pragma unroll
+    for (int d = 0; d < 4; d++)
+        if (acc < 0 && (nb.valid >> d & 1) &&
+            gt_prod(Nn[d], (unsigned long long)(Ak - al), Nk, (unsigned long long)An[d]))
+            acc = nb.v[d];
+    return acc;
 }
 
 }  // namespace seeds

@@ -5,29 +5,38 @@
 //  * Row bands.  CTA r of the cluster owns image rows [y0_r, y1_r), aligned with
 //    the top-level block rows so that every block of every level lies inside
 //    one band.  It keeps the labels of its band plus a halo of 2 rows above
-//    and below (the Prop.-2 window radius), and the bins of its band.
+//    and below (the Prop.-2 window radius) in a plane padded by 2 sentinel
+//    columns on each side, so that no label read needs a bounds test: outside
+//    the image the label is 0xFFFF, which equals no superpixel (K <= 65535).
 //  * Labels only.  Block levels work on the pixel label plane: a level-l
 //    block carries one label, so its label is that of any of its pixels and
-//    its 8 neighbours are read at the pixels adjacent to its rectangle (all
-//    within one row of it).  A block move writes its pixels; no block maps,
-//    no push-down, no expansion.
+//    its 8 neighbours are read at the pixels adjacent to its rectangle.  A
+//    block move writes its pixels; no block maps, no push-down, no expansion.
 //  * Histograms in distributed shared memory.  Superpixel k's row H[k][*] and
-//    A[k] live in CTA (k mod CS); gathers and updates are DSMEM loads and
-//    atomics.  The snapshot is double buffered exactly as in the graph path:
-//    sub-sweep s reads buffer s&1 and adds the previous sub-sweep's deltas
-//    (replayed from this CTA's own move records) and its own into the other.
+//    A[k] live in the CTA whose band holds the centre row of k's grid cell, so
+//    most gathers of a band are CTA-local; a per-frame table gives every k's
+//    cluster-window address.  The snapshot is double buffered as in the graph
+//    path: sub-sweep s reads buffer s&1 and adds the previous sub-sweep's
+//    deltas (replayed from this CTA's own records) and its own into the other.
+//  * Filter, compact, decide.  A sub-sweep first runs the cheap boundary and
+//    ring tests over every unit of the colour class, one
+//    thread per unit, and pushes the survivors into a shared-memory queue;
+//    the colour / smoothness tests then run densely over the queue: one thread
+//    per pixel or small block, one warp per large block (K5).
 //  * A label written within 2 rows of a band edge is also written into the
 //    neighbour CTA's halo copy.  Same-colour units never read each other
 //    (reading O7), so halo copies are exact at every sub-sweep boundary.
-//  * One cluster barrier per sub-sweep (barrier.cluster arrive.release /
-//    wait.acquire) orders every label write and DSMEM atomic.
+//  * One cluster barrier per sub-sweep orders every label write and DSMEM
+//    reduction.  Cluster barriers invalidate L1, so everything read after the
+//    seed (block geometry included) lives in shared memory.
 // HBM traffic: the image in, int32 labels (and the final histograms) out.
 #pragma once
-#include <cooperative_groups.h>
-
 #include "seeds_kernels.cuh"
 
 namespace seeds {
+
+constexpr int RES_THREADS = 512;
+constexpr int RES_PAD = 2;  // sentinel columns on each side of a label row
 
 struct ResParams {
     const uint8_t *img;
@@ -35,24 +44,25 @@ struct ResParams {
     int32_t *out;
     int W, H, C, bpc, B, K, nx, L, iters, limit, S, nf;
     const int *colstart, *rowstart, *bxof, *byof;
-    const int *band_y;    // CS + 1 row boundaries of the bands
-    const int *band_top;  // CS + 1 top-level block row boundaries of the bands (L > 0)
-    int big_mask;         // bit l: level l has blocks larger than SMALL_ALPHA (warp per block)
-    int *moves;           // (S + 1) x nf accepted units per sub-sweep
-    long long *trace;     // debug: per CTA, per phase (clock64 at work end, after barrier), or nullptr
+    const int *band_y;     // CS + 1 row boundaries of the bands
+    const int *band_top;   // CS + 1 top-level block row boundaries of the bands (L > 0)
+    const uint32_t *kmap;  // K entries: owner CTA | local row << 8
+    int bkind[16];         // per level: BK_T4 (blocks <= 4 px), BK_T16 (<= 16 px), BK_WARP
+    int *moves;            // (S + 1) x nf accepted units per sub-sweep
+    long long *trace;      // debug: per CTA, per phase (clock64 at work end, after barrier), or nullptr
     int *Hout[2], *Aout[2];  // final histograms go to buffer (sub-sweeps run) & 1
     long long H_fs;
     // shared-memory layout (byte offsets) and capacities
-    unsigned o_lab, o_bins, o_H, o_A, o_rec, o_tab, o_misc, o_scr;
-    int lab_rows, kloc, rec_cap, ntab;
+    unsigned o_lab, o_bins, o_H, o_A, o_rec, o_tab, o_misc, o_kaddr, o_geo, o_queue;
+    int pitch, lab_rows, kloc, rec_cap, q_cap, ntab, GX, GY;
 };
 
-namespace cgx = cooperative_groups;
-
-// Distributed shared memory access with explicit cluster-window addresses:
-// mapa gives the address of the same offset in CTA `rank`'s shared memory;
-// updates are fire-and-forget reductions at cluster scope (ordered by the
-// cluster barrier's release/acquire), loads are ld.shared::cluster.
+// Distributed shared memory with explicit cluster-window addresses: mapa gives
+// the address of the same offset in CTA `rank`'s shared memory; reductions are
+// fire-and-forget at cluster scope and loads are ld.shared::cluster, both
+// ordered against the next sub-sweep by the cluster barrier.  The loads are
+// volatile (never merged or hoisted across a barrier) but carry no memory
+// clobber, so several of them are in flight together.
 __device__ __forceinline__ uint32_t cl_addr(const void *local, int rank)
 {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(local);
@@ -63,7 +73,7 @@ __device__ __forceinline__ uint32_t cl_addr(const void *local, int rank)
 __device__ __forceinline__ int cl_ld(uint32_t addr)
 {
     int v;
-    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ void cl_red(uint32_t addr, int v)
@@ -74,28 +84,48 @@ __device__ __forceinline__ void cl_st16(uint32_t addr, uint16_t v)
 {
     asm volatile("st.shared::cluster.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
 }
+__device__ __forceinline__ void cluster_barrier()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ int cluster_rank()
+{
+    int r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ int cluster_size()
+{
+    int r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
 
 template <typename BinT>
 struct ResCta {
     const ResParams &q;
-    cgx::cluster_group cl;
-    int CS, rank, y0, y1, yprev0, ynext0;
-    uint16_t *lab;     // (lab_rows) x W, row 0 = image row y0 - 2
+    int CS, rank, y0, y1, yprev0, ynext0, pitch;
+    uint16_t *lab;     // lab_rows x pitch; row 0 = image row y0 - 2, column 0 = x - 2
     BinT *bins;        // (y1 - y0) x W
-    int *Hs, *As;      // 2 buffers: [buf][kloc][B], [buf][kloc]
-    Rec *rec;          // 2 x rec_cap
+    int *Hs, *As;      // [buf][kloc][B], [buf][kloc]
+    Rec *rec;          // 2 x rec_cap histogram deltas (k | n << 16, bin | count << 16)
     uint32_t *tabs;    // ntab warp tables of 2B + 2 words
-    uint16_t *scr;     // SMALL_ALPHA x blockDim scratch columns (small blocks)
-    int *misc;         // [0], [1]: record counts of the two buffers
+    int *misc;         // [0], [1]: record counts of the two lists, [2]: queue length
+    uint32_t *haddr;   // K: cluster address of H[k][0] in buffer 0
+    uint32_t *aaddr;   // K: cluster address of A[k] in buffer 0
+    int *cs, *rs;      // level-0 block column / row starts (GX + 1, GY + 1)
+    uint32_t *queue;   // q_cap surviving units of the current sub-sweep
+    uint32_t hbuf, abuf;  // byte strides of one buffer
 
-    __device__ ResCta(const ResParams &qq, unsigned char *smem) : q(qq), cl(cgx::this_cluster())
+    __device__ ResCta(const ResParams &qq, unsigned char *smem) : q(qq)
     {
-        CS = (int)cl.num_blocks();
-        rank = (int)cl.block_rank();
+        CS = cluster_size();
+        rank = cluster_rank();
         y0 = q.band_y[rank];
         y1 = q.band_y[rank + 1];
         yprev0 = rank > 0 ? q.band_y[rank - 1] : 0;
         ynext0 = rank + 1 < CS ? q.band_y[rank + 1] : 0;
+        pitch = q.pitch;
         lab = reinterpret_cast<uint16_t *>(smem + q.o_lab);
         bins = reinterpret_cast<BinT *>(smem + q.o_bins);
         Hs = reinterpret_cast<int *>(smem + q.o_H);
@@ -103,346 +133,281 @@ struct ResCta {
         rec = reinterpret_cast<Rec *>(smem + q.o_rec);
         tabs = reinterpret_cast<uint32_t *>(smem + q.o_tab);
         misc = reinterpret_cast<int *>(smem + q.o_misc);
-        scr = reinterpret_cast<uint16_t *>(smem + q.o_scr);
+        haddr = reinterpret_cast<uint32_t *>(smem + q.o_kaddr);
+        aaddr = haddr + q.K;
+        cs = reinterpret_cast<int *>(smem + q.o_geo);
+        rs = cs + q.GX + 1;
+        queue = reinterpret_cast<uint32_t *>(smem + q.o_queue);
+        hbuf = (uint32_t)q.kloc * q.B * 4;
+        abuf = (uint32_t)q.kloc * 4;
     }
 
-    __device__ __forceinline__ int get(int x, int y) const
+    // label cell of image pixel (x, y), y within [y0 - 2, y1 + 2), x within [-2, W + 2)
+    __device__ __forceinline__ const uint16_t *cell(int x, int y) const
     {
-        if (x < 0 || x >= q.W || y < 0 || y >= q.H) return -1;
-        return lab[(y - y0 + 2) * q.W + x];
+        return lab + (y - y0 + 2) * pitch + x + RES_PAD;
     }
     // write a label; mirror it into a neighbour's halo when within 2 rows of an edge
     __device__ __forceinline__ void set(int x, int y, int v)
     {
-        lab[(y - y0 + 2) * q.W + x] = (uint16_t)v;
-        if (y < y0 + 2 && rank > 0) cl_st16(cl_addr(lab + (y - yprev0 + 2) * q.W + x, rank - 1), (uint16_t)v);
-        if (y >= y1 - 2 && rank + 1 < CS) cl_st16(cl_addr(lab + (y - ynext0 + 2) * q.W + x, rank + 1), (uint16_t)v);
+        uint16_t *c = lab + (y - y0 + 2) * pitch + x + RES_PAD;
+        *c = (uint16_t)v;
+        if (y < y0 + 2 && rank > 0)
+            cl_st16(cl_addr(lab + (y - yprev0 + 2) * pitch + x + RES_PAD, rank - 1), (uint16_t)v);
+        if (y >= y1 - 2 && rank + 1 < CS)
+            cl_st16(cl_addr(lab + (y - ynext0 + 2) * pitch + x + RES_PAD, rank + 1), (uint16_t)v);
     }
     __device__ __forceinline__ int bin(int x, int y) const { return bins[(y - y0) * q.W + x]; }
-    // cluster-window address of H[k][0] / A[k] in buffer b (owner: CTA k mod CS)
-    __device__ __forceinline__ uint32_t hrow(int b, int k) const
+    __device__ __forceinline__ uint32_t hrow(int buf, int k) const { return haddr[k] + (uint32_t)buf * hbuf; }
+    __device__ __forceinline__ uint32_t acell(int buf, int k) const { return aaddr[k] + (uint32_t)buf * abuf; }
+    __device__ __forceinline__ int ldA(int buf, int k) const { return cl_ld(acell(buf, k)); }
+    __device__ __forceinline__ int ldH(int buf, int k, int b) const { return cl_ld(hrow(buf, k) + 4 * b); }
+    // histogram delta of a move k -> n: `count` pixels of bin b
+    __device__ __forceinline__ void delta(int buf, int k, int n, int b, int count) const
     {
-        return cl_addr(Hs + ((size_t)b * q.kloc + k / CS) * q.B, k % CS);
-    }
-    __device__ __forceinline__ uint32_t acell(int b, int k) const
-    {
-        return cl_addr(As + (size_t)b * q.kloc + k / CS, k % CS);
-    }
-
-    // ring mask + candidates from the 8 label samples (N, NE, E, SE, S, SW, W, NW)
-    __device__ __forceinline__ Neigh neigh8(int k, int vN, int vNE, int vE, int vSE, int vS, int vSW, int vW,
-                                            int vNW) const
-    {
-        Neigh r;
-        r.mask = (vN == k) | (vNE == k) << 1 | (vE == k) << 2 | (vSE == k) << 3 | (vS == k) << 4 |
-                 (vSW == k) << 5 | (vW == k) << 6 | (vNW == k) << 7;
-        r.v[0] = vW; r.v[1] = vE; r.v[2] = vN; r.v[3] = vS;
-        r.valid = 0;
-#pragma unroll
-        for (int d = 0; d < 4; d++) {
-            bool ok = r.v[d] >= 0 && r.v[d] != k;
-#pragma unroll
-            for (int e = 0; e < d; e++) ok = ok && r.v[e] != r.v[d];
-            r.valid |= (int)ok << d;
-        }
-        return r;
-    }
-
-    // Prop. 2 sum S over the clamped 3x3 patches around (x, y)
-    __device__ __forceinline__ int smooth(int x, int y, int k, int n) const
-    {
-        int S = 0;
-        for (int iy = y - 1; iy <= y + 1; iy++)
-            for (int ix = x - 1; ix <= x + 1; ix++) {
-                if (get(ix, iy) < 0) continue;
-                int d = 1;
-#pragma unroll
-                for (int qy = -1; qy <= 1; qy++)
-#pragma unroll
-                    for (int qx = -1; qx <= 1; qx++) {
-                        const int v = get(ix + qx, iy + qy);
-                        d += (v == n) - (v == k);
-                    }
-                S += d;
-            }
-        return S;
+        cl_red(hrow(buf, k) + 4 * b, -count);
+        cl_red(hrow(buf, n) + 4 * b, count);
+        cl_red(acell(buf, k), -count);
+        cl_red(acell(buf, n), count);
     }
 };
 
-// Warp-aggregated append of n records to this CTA's list b; returns the first slot.
-__device__ __forceinline__ int append_warp(int *count, int n)
-{
-    const int lane = threadIdx.x & 31;
-    int incl = n;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(FULL, incl, 31);
-    int base = 0;
-    if (lane == 31 && total) base = atomicAdd(count, total);
-    base = __shfl_sync(FULL, base, 31);
-    return base + incl - n;
-}
-
-// Decide one block unit (thread per block, alpha <= SMALL_ALPHA): returns the
-// accepted neighbour label or -1.  Bins are read from the band's shared copy;
-// the distinct bins are found by pairwise comparison.
-template <typename BinT>
-__device__ __forceinline__ int decide_block_small(ResCta<BinT> &c, int ob, int k, const Neigh &nb, int xa, int xb,
-                                                  int ya, int yb, uint16_t *scr, int stride, int &nd)
-{
-    int alpha = 0;
-    for (int y = ya; y < yb; y++)
-        for (int x = xa; x < xb; x++) scr[(alpha++) * stride] = (uint16_t)c.bin(x, y);
-    const long long Ak = cl_ld(c.acell(ob, k));
-    long long An[4];
-    uint32_t hn[4];
-#pragma unroll
-    for (int d = 0; d < 4; d++) {
-        const bool v = nb.valid >> d & 1;
-        An[d] = v ? cl_ld(c.acell(ob, nb.v[d])) : 1;
-        hn[d] = v ? c.hrow(ob, nb.v[d]) : 0;
-    }
-    const uint32_t hk = c.hrow(ob, k);
-    unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
-    nd = 0;
-    for (int i = 0; i < alpha; i++) {
-        const int b = scr[i * stride];
-        bool first = true;
-        for (int j = 0; j < i; j++) first = first && scr[j * stride] != b;
-        if (!first) continue;
-        long long l = 1;
-        for (int j = i + 1; j < alpha; j++) l += scr[j * stride] == b;
-        nd++;
-        const long long u = (long long)(cl_ld(hk + 4 * b) - l) * alpha, v = l * (Ak - alpha);
-        Nk += (unsigned long long)(u < v ? u : v);
-#pragma unroll
-        for (int d = 0; d < 4; d++)
-            if (nb.valid >> d & 1) {
-                const long long un = (long long)cl_ld(hn[d] + 4 * b) * alpha, vn = l * An[d];
-                Nn[d] += (unsigned long long)(un < vn ? un : vn);
-            }
-    }
-    int acc = -1;
-#pragma unroll
-    for (int d = 0; d < 4; d++)
-        if (acc < 0 && (nb.valid >> d & 1) &&
-            gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
-            acc = nb.v[d];
-    return acc;
-}
-
 template <typename BinT, int GAMMA, int P>
-__global__ void __launch_bounds__(512, 1) k_resident(ResParams q)
+__global__ void __launch_bounds__(RES_THREADS, 1) k_resident(ResParams q)
 {
-    extern __shared__ __align__(16) uint32_t smem[];
+    extern __shared__ __align__(128) uint32_t smem[];
     ResCta<BinT> c(q, reinterpret_cast<unsigned char *>(smem));
-    const int nthr = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
+    constexpr int NT = RES_THREADS;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NW = NT / 32;
     const int ncl = gridDim.x / c.CS, cid = blockIdx.x / c.CS;
-    const int W = q.W, B = q.B;
+    const int W = q.W, B = q.B, pitch = c.pitch;
     const int band = c.y1 - c.y0;
     const int TW = 2 * B + 2;  // warp table words
 
-    for (int i = tid; i < q.ntab * TW; i += nthr) c.tabs[i] = 0;
+    for (int i = tid; i < q.ntab * TW; i += NT) c.tabs[i] = 0;
+    for (int i = tid; i <= q.GX; i += NT) c.cs[i] = q.colstart[i];
+    for (int i = tid; i <= q.GY; i += NT) c.rs[i] = q.rowstart[i];
+    // cluster-window addresses of every superpixel's histogram row and size
+    for (int k = tid; k < q.K; k += NT) {
+        const uint32_t m = q.kmap[k];
+        const int own = m & 0xFF, loc = m >> 8;
+        c.haddr[k] = cl_addr(c.Hs + (size_t)loc * B, own);
+        c.aaddr[k] = cl_addr(c.As + loc, own);
+    }
 
     for (int f = cid; f < q.nf; f += ncl) {
         const bool blocks = q.init == nullptr && q.L > 0;
         const long long fN = (long long)f * W * q.H;
         int *moves_f = q.moves + f;
         // ---- seed: zero own histogram rows and counters --------------------
-        for (int i = tid; i < 2 * q.kloc * B; i += nthr) c.Hs[i] = 0;
-        for (int i = tid; i < 2 * q.kloc; i += nthr) c.As[i] = 0;
-        if (tid < 2) c.misc[tid] = 0;
+        for (int i = tid; i < 2 * q.kloc * B; i += NT) c.Hs[i] = 0;
+        for (int i = tid; i < 2 * q.kloc; i += NT) c.As[i] = 0;
+        if (tid < 4) c.misc[tid] = 0;
         if (c.rank == 0)
-            for (int i = tid; i <= q.S; i += nthr) moves_f[(long long)i * q.nf] = 0;
-        c.cl.sync();
-        // labels of the band + halo (grid, or warm start, O9)
-        for (int i = tid; i < (band + 4) * W; i += nthr) {
-            const int ly = i / W, x = i - ly * W, y = c.y0 - 2 + ly;
-            int v = 0xFFFF;
-            if (y >= 0 && y < q.H)
-                v = q.init ? q.init[fN + (long long)y * W + x] : (q.byof[y] >> q.L) * q.nx + (q.bxof[x] >> q.L);
-            c.lab[i] = (uint16_t)v;
-        }
-        // bins of the band (reading Q1) and the histogram counts (Eq. 6), DSMEM
-        // atomics warp-aggregated on the (label, bin) key
-        for (int base = wid * 32; base < band * W; base += nthr) {
-            const int i = base + lane;
-            int key = -1, k = -1, b = 0;
-            if (i < band * W) {
-                const int ly = i / W, x = i - ly * W, y = c.y0 + ly;
-                const uint8_t *v = q.img + (fN + (long long)y * W + x) * q.C;
-                for (int ch = 0; ch < q.C; ch++) b = b * q.bpc + (((int)v[ch] * q.bpc) >> 8);
-                c.bins[i] = (BinT)b;
-                k = q.init ? q.init[fN + (long long)y * W + x] : (q.byof[y] >> q.L) * q.nx + (q.bxof[x] >> q.L);
-                key = k * B + b;
+            for (int i = tid; i <= q.S; i += NT) moves_f[(long long)i * q.nf] = 0;
+        // labels of the band + halo + sentinel columns (grid, PAPER.md:460-469,
+        // or warm start, reading O9)
+        for (int ly = wid; ly < band + 4; ly += NW) {
+            const int y = c.y0 - 2 + ly;
+            const bool in = y >= 0 && y < q.H;
+            const int gy = in ? (q.byof[y] >> q.L) * q.nx : 0;
+            for (int xx = lane; xx < pitch; xx += 32) {
+                const int x = xx - RES_PAD;
+                int v = SENT;
+                if (in && x >= 0 && x < W)
+                    v = q.init ? q.init[fN + (long long)y * W + x] : gy + (q.bxof[x] >> q.L);
+                c.lab[ly * pitch + xx] = (uint16_t)v;
             }
-            unsigned m = __match_any_sync(FULL, key);
-            if (i < band * W && lane == __ffs(m) - 1) cl_red(c.hrow(0, k) + 4 * b, __popc(m));
-            m = __match_any_sync(FULL, k);
-            if (i < band * W && lane == __ffs(m) - 1) cl_red(c.acell(0, k), __popc(m));
         }
-        c.cl.sync();
-        for (int i = tid; i < q.kloc * B; i += nthr) c.Hs[q.kloc * B + i] = c.Hs[i];
-        for (int i = tid; i < q.kloc; i += nthr) c.As[q.kloc + i] = c.As[i];
-        c.cl.sync();
+        __syncthreads();
+        cluster_barrier();  // histogram rows zeroed cluster-wide before the counts
+        // bins of the band (reading Q1) and the histogram counts (Eq. 6), DSMEM
+        // reductions warp-aggregated on the (label, bin) key
+        for (int ly = wid; ly < band; ly += NW) {
+            const int y = c.y0 + ly;
+            for (int x0 = 0; x0 < W; x0 += 32) {
+                const int x = x0 + lane;
+                int key = -1, k = -1, b = 0;
+                if (x < W) {
+                    const uint8_t *v = q.img + (fN + (long long)y * W + x) * q.C;
+                    for (int ch = 0; ch < q.C; ch++) b = b * q.bpc + (((int)v[ch] * q.bpc) >> 8);
+                    c.bins[ly * W + x] = (BinT)b;
+                    k = *c.cell(x, y);
+                    key = k * B + b;
+                }
+                unsigned m = __match_any_sync(FULL, key);
+                if (x < W && lane == __ffs(m) - 1) cl_red(c.hrow(0, k) + 4 * b, __popc(m));
+                m = __match_any_sync(FULL, k);
+                if (x < W && lane == __ffs(m) - 1) cl_red(c.acell(0, k), __popc(m));
+            }
+        }
+        cluster_barrier();
+        for (int i = tid; i < q.kloc * B; i += NT) c.Hs[q.kloc * B + i] = c.Hs[i];
+        for (int i = tid; i < q.kloc; i += NT) c.As[q.kloc + i] = c.As[i];
+        cluster_barrier();
 
         int s = 0;
         // debug timing (first frame only): [rank][phase][0] = work done, [1] = barrier passed
         auto stamp = [&](int phase, int which) {
             if (q.trace && f == 0 && tid == 0)
-                q.trace[((long long)c.rank * (q.S + 4) + phase) * 2 + which] = clock64();
+                q.trace[((long long)c.rank * (q.S + 4) + phase) * 8 + which] = clock64();
         };
         stamp(0, 1);
-        // replay this CTA's records of sub-sweep s-1 into buffer yb: pixel
-        // records one per thread, block records one warp per record (lanes over
-        // the block's pixels, equal bins aggregated with __match_any_sync)
-        auto replay = [&](int yb, bool prev_block) {
-            const int pb = (s + 1) & 1;
+
+        // Start of sub-sweep s: replay this CTA's deltas of sub-sweep s-1 into
+        // buffer yb and reset the list that sub-sweep s fills.
+        auto begin_subsweep = [&](int yb) {
+            const int pb = yb;  // sub-sweep s-1 wrote list (s-1)&1 = yb
             const int nrec = c.misc[pb];
             const Rec *r = c.rec + (size_t)pb * q.rec_cap;
-            if (!prev_block) {
-                for (int e = tid; e < nrec; e += nthr) {
-                    const Rec x = r[e];
-                    const int k = x.kn & 0xFFFF, n = x.kn >> 16, b = x.bc & 0xFFFF;
-                    cl_red(c.hrow(yb, k) + 4 * b, -1);
-                    cl_red(c.hrow(yb, n) + 4 * b, 1);
-                    cl_red(c.acell(yb, k), -1);
-                    cl_red(c.acell(yb, n), 1);
-                }
-                return;
-            }
-            for (int e = wid; e < nrec; e += nw) {
+            for (int e = tid; e < nrec; e += NT) {
                 const Rec x = r[e];
-                const int k = x.kn & 0xFFFF, n = x.kn >> 16;
-                const int bi = x.bc & 0x3FFF, bj = (x.bc >> 14) & 0x3FFF, l = (x.bc >> 28) & 0x7;
-                const int xa = q.colstart[bi << l], xb = q.colstart[(bi + 1) << l];
-                const int ya = q.rowstart[bj << l], y2 = q.rowstart[(bj + 1) << l];
-                const int rw = xb - xa, alpha = rw * (y2 - ya);
-                const uint32_t hk = c.hrow(yb, k), hn = c.hrow(yb, n);
-                for (int base = 0; base < alpha; base += 32) {
-                    const int i = base + lane;
-                    const int b = i < alpha ? c.bin(xa + i % rw, ya + i / rw) : -1;
-                    const unsigned m = __match_any_sync(FULL, b);
-                    if (b >= 0 && lane == __ffs(m) - 1) {
-                        cl_red(hk + 4 * b, -__popc(m));
-                        cl_red(hn + 4 * b, __popc(m));
-                    }
-                }
-                if (lane == 0) {
-                    cl_red(c.acell(yb, k), -alpha);
-                    cl_red(c.acell(yb, n), alpha);
-                }
+                c.delta(yb, x.kn & 0xFFFF, x.kn >> 16, x.bc & 0xFFFF, x.bc >> 16);
             }
+            // list ob = yb ^ 1 was last read (replayed) before the barrier
+            if (tid == 0) c.misc[yb ^ 1] = 0;
         };
-        bool prev_block = false;
+        auto end_subsweep = [&]() {
+            __syncthreads();
+            if (tid == 0) c.misc[2] = 0;  // the queue of the next sub-sweep
+            stamp(s + 1, 0);
+            cluster_barrier();
+            stamp(s + 1, 1);
+            s++;
+        };
+        auto count_moves = [&](bool moved) {
+            const unsigned mv = __ballot_sync(FULL, moved);
+            if (lane == 0 && mv) atomicAdd(&moves_f[(long long)(s + 1) * q.nf], __popc(mv));
+        };
 
         // ---- block levels, largest first -----------------
         if (blocks) {
             for (int l = q.L - 1; l >= 0; l--) {
-                const int GXl = (q.nx << q.L) >> l;
+                const int GXl = q.GX >> l;
                 const int jb0 = q.band_top[c.rank] << (q.L - 1 - l), jb1 = q.band_top[c.rank + 1] << (q.L - 1 - l);
-                const bool big = (q.big_mask >> l) & 1;
+                const int kind = q.bkind[l];
                 for (int it = 0; it < q.iters; it++)
                     for (int col = 0; col < 4; col++) {
                         if (q.limit >= 0 && s >= q.limit) break;
                         const int cx = col & 1, cy = col >> 1;
                         const int ob = s & 1, yb_ = ob ^ 1;
-                        replay(yb_, prev_block);
-                        prev_block = true;
-                        if (tid == 0) c.misc[ob] = 0;
-                        __syncthreads();
+                        begin_subsweep(yb_);
                         const int uw = (GXl - cx + 1) / 2;
+                        const float inv_uw = 1.0f / (float)uw;
                         const int jfirst = jb0 + ((jb0 & 1) != cy ? 1 : 0);
                         const int uh = jfirst < jb1 ? (jb1 - jfirst + 1) / 2 : 0;
                         const int nunits = uw * uh;
-                        if (!big) {
-                            for (int base = wid * 32; base < nunits; base += nthr) {
-                                const int t = base + lane;
-                                int acc = -1, k = 0, xa = 0, xb = 0, ya = 0, yb = 0, bi = 0, bj = 0, nd = 0;
-                                uint16_t *scr = c.scr + tid;
-                                if (t < nunits) {
-                                    bi = cx + 2 * (t % uw);
-                                    bj = jfirst + 2 * (t / uw);
-                                    xa = q.colstart[bi << l]; xb = q.colstart[(bi + 1) << l];
-                                    ya = q.rowstart[bj << l]; yb = q.rowstart[(bj + 1) << l];
-                                    k = c.get(xa, ya);
-                                    const Neigh nb = c.neigh8(k, c.get(xa, ya - 1), c.get(xb, ya - 1), c.get(xb, ya),
-                                                              c.get(xb, yb), c.get(xa, yb), c.get(xa - 1, yb),
-                                                              c.get(xa - 1, ya), c.get(xa - 1, ya - 1));
-                                    if (nb.valid && removable(nb.mask))
-                                        acc = decide_block_small<BinT>(c, ob, k, nb, xa, xb, ya, yb, scr, nthr, nd);
-                                }
-                                const int slot = append_warp(&c.misc[ob], acc >= 0 ? 1 : 0);
-                                const unsigned mv = __ballot_sync(FULL, acc >= 0);
-                                if (lane == 0 && mv) atomicAdd(&moves_f[(long long)(s + 1) * q.nf], __popc(mv));
-                                if (acc >= 0) {
-                                    c.rec[(size_t)ob * q.rec_cap + slot] =
-                                        Rec{(uint32_t)k | ((uint32_t)acc << 16),
-                                            (uint32_t)bi | ((uint32_t)bj << 14) | ((uint32_t)l << 28) | 0x80000000u};
-                                    const uint32_t hk = c.hrow(yb_, k), hn = c.hrow(yb_, acc);
+                        // unit t -> block (bi, bj) -> rectangle
+                        auto rect = [&](int t, int &bi, int &bj, int &xa, int &xb, int &ya, int &yb) {
+                            const int tj = div_small(t, uw, inv_uw);
+                            bi = cx + 2 * (t - tj * uw);
+                            bj = jfirst + 2 * tj;
+                            xa = c.cs[bi << l]; xb = c.cs[(bi + 1) << l];
+                            ya = c.rs[bj << l]; yb = c.rs[(bj + 1) << l];
+                        };
+                        // filter: boundary + ring test, survivors to the queue
+                        for (int base = wid * 32; base < nunits; base += NT) {
+                            const int t = base + lane;
+                            bool take = false;
+                            if (t < nunits) {
+                                int bi, bj, xa, xb, ya, yb;
+                                rect(t, bi, bj, xa, xb, ya, yb);
+                                const Neigh nb = ring_at(c.cell(xa, ya), pitch, xb - xa, (yb - ya) * pitch);
+                                take = nb.valid && removable(nb.mask);
+                            }
+                            push_warp(c.queue, &c.misc[2], take, (uint32_t)t);
+                        }
+                        __syncthreads();
+                        const int nq = c.misc[2];
+                        if (kind != BK_WARP) {
+                            // one thread per block
+                            for (int base = wid * 32; base < nq; base += NT) {
+                                const int e = base + lane;
+                                int acc = -1, k = 0, bi = 0, bj = 0, xa = 0, xb = 0, ya = 0, yb = 0, nd = 0;
+                                int bv[16], cnt[16];
+                                if (e < nq) {
+                                    rect((int)c.queue[e], bi, bj, xa, xb, ya, yb);
+                                    const uint16_t *a = c.cell(xa, ya);
+                                    k = a[0];
+                                    const Neigh nb = ring_at(a, pitch, xb - xa, (yb - ya) * pitch);
                                     const int alpha = (xb - xa) * (yb - ya);
-                                    for (int i = 0; i < alpha; i++) {
-                                        const int b = scr[i * nthr];
-                                        bool first = true;
-                                        for (int j = 0; j < i; j++) first = first && scr[j * nthr] != b;
-                                        if (!first) continue;
-                                        int l = 1;
-                                        for (int j = i + 1; j < alpha; j++) l += scr[j * nthr] == b;
-                                        cl_red(hk + 4 * b, -l);
-                                        cl_red(hn + 4 * b, l);
+                                    if (kind == BK_T4) {
+                                        int bv4[4], cnt4[4];
+                                        acc = block_thread<4>(c, ob, k, nb, xa, ya, xb - xa, alpha, bv4, cnt4);
+#pragma unroll
+                                        for (int i = 0; i < 4; i++) { bv[i] = bv4[i]; cnt[i] = cnt4[i]; }
+#pragma unroll
+                                        for (int i = 4; i < 16; i++) cnt[i] = 0;
+                                    } else {
+                                        acc = block_thread<16>(c, ob, k, nb, xa, ya, xb - xa, alpha, bv, cnt);
                                     }
+                                    if (acc >= 0) {
+#pragma unroll
+                                        for (int i = 0; i < 16; i++) nd += cnt[i] != 0;
+                                    }
+                                }
+                                count_moves(acc >= 0);
+                                int slot = append_warp(&c.misc[ob], nd);
+                                if (acc >= 0) {
+                                    Rec *r = c.rec + (size_t)ob * q.rec_cap;
+#pragma unroll
+                                    for (int i = 0; i < 16; i++)
+                                        if (cnt[i]) {
+                                            r[slot++] = Rec{(uint32_t)k | ((uint32_t)acc << 16),
+                                                            (uint32_t)bv[i] | ((uint32_t)cnt[i] << 16)};
+                                            c.delta(yb_, k, acc, bv[i], cnt[i]);
+                                        }
                                     for (int y = ya; y < yb; y++)
                                         for (int x = xa; x < xb; x++) c.set(x, y, acc);
-                                    cl_red(c.acell(yb_, k), -alpha);
-                                    cl_red(c.acell(yb_, acc), alpha);
                                 }
                             }
                         } else if (wid < q.ntab) {
                             // one warp per block; per-warp bin table + list of non-empty bins (K5)
                             uint32_t *cnt = c.tabs + (size_t)wid * TW, *list = cnt + B, *nlist = cnt + 2 * B;
-                            const int nwu = q.ntab < nw ? q.ntab : nw;
-                            for (int t = wid; t < nunits; t += nwu) {
-                                const int bi = cx + 2 * (t % uw), bj = jfirst + 2 * (t / uw);
-                                const int xa = q.colstart[bi << l], xb = q.colstart[(bi + 1) << l];
-                                const int ya = q.rowstart[bj << l], yb = q.rowstart[(bj + 1) << l];
-                                const int k = c.get(xa, ya);
-                                const Neigh nb = c.neigh8(k, c.get(xa, ya - 1), c.get(xb, ya - 1), c.get(xb, ya),
-                                                          c.get(xb, yb), c.get(xa, yb), c.get(xa - 1, yb),
-                                                          c.get(xa - 1, ya), c.get(xa - 1, ya - 1));
-                                if (!nb.valid || !removable(nb.mask)) continue;
+                            const int nwu = q.ntab < NW ? q.ntab : NW;
+                            for (int e = wid; e < nq; e += nwu) {
+                                int bi, bj, xa, xb, ya, yb;
+                                rect((int)c.queue[e], bi, bj, xa, xb, ya, yb);
+                                const uint16_t *a = c.cell(xa, ya);
+                                const int k = a[0];
+                                const Neigh nb = ring_at(a, pitch, xb - xa, (yb - ya) * pitch);
                                 const int rw = xb - xa, alpha = rw * (yb - ya);
-                                for (int base = 0; base < alpha; base += 32) {
-                                    const int i = base + lane;
-                                    const int b = i < alpha ? c.bin(xa + i % rw, ya + i / rw) : -1;
-                                    const unsigned m = __match_any_sync(FULL, b);
-                                    if (b >= 0 && lane == __ffs(m) - 1 && atomicAdd(&cnt[b], (unsigned)__popc(m)) == 0u)
+                                const float inv = 1.0f / (float)rw;
+                                for (int i0 = 0; i0 < alpha; i0 += 32) {
+                                    const int i = i0 + lane;
+                                    int b = -1;
+                                    if (i < alpha) {
+                                        const int dy = div_small(i, rw, inv);
+                                        b = c.bin(xa + i - dy * rw, ya + dy);
+                                    }
+                                    const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : b);
+                                    if (b >= 0 && lane == __ffs(m) - 1 &&
+                                        atomicAdd(&cnt[b], (unsigned)__popc(m)) == 0u)
                                         list[atomicAdd(nlist, 1u)] = (uint32_t)b;
                                 }
                                 __syncwarp();
                                 const int ns = (int)*nlist;
                                 const long long Ak = cl_ld(c.acell(ob, k));
-                                long long An[4];
-                                uint32_t hn[4];
+                                long long An[4] = {1, 1, 1, 1};
 #pragma unroll
-                                for (int d = 0; d < 4; d++) {
-                                    const bool v = nb.valid >> d & 1;
-                                    An[d] = v ? cl_ld(c.acell(ob, nb.v[d])) : 1;
-                                    hn[d] = v ? c.hrow(ob, nb.v[d]) : 0;
-                                }
-                                const uint32_t hk = c.hrow(ob, k);
+                                for (int d = 0; d < 4; d++)
+                                    if (nb.valid >> d & 1) An[d] = cl_ld(c.acell(ob, nb.v[d]));
                                 unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
                                 for (int i = lane; i < ns; i += 32) {
                                     const int b = list[i];
                                     const long long lc = cnt[b];
-                                    const long long u = (long long)(cl_ld(hk + 4 * b) - lc) * alpha, v = lc * (Ak - alpha);
+                                    const long long hk = cl_ld(c.hrow(ob, k) + 4 * b);
+                                    long long hn[4] = {0, 0, 0, 0};
+#pragma unroll
+                                    for (int d = 0; d < 4; d++)
+                                        if (nb.valid >> d & 1) hn[d] = cl_ld(c.hrow(ob, nb.v[d]) + 4 * b);
+                                    const long long u = (hk - lc) * alpha, v = lc * (Ak - alpha);
                                     Nk += (unsigned long long)(u < v ? u : v);
 #pragma unroll
                                     for (int d = 0; d < 4; d++)
                                         if (nb.valid >> d & 1) {
-                                            const long long un = (long long)cl_ld(hn[d] + 4 * b) * alpha, vn = lc * An[d];
+                                            const long long un = hn[d] * alpha, vn = lc * An[d];
                                             Nn[d] += (unsigned long long)(un < vn ? un : vn);
                                         }
                                 }
@@ -456,23 +421,23 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResParams q)
                                         acc = nb.v[d];
                                 }
                                 if (acc >= 0) {
+                                    int base = 0;
                                     if (lane == 0) {
-                                        const int slot = atomicAdd(&c.misc[ob], 1);
-                                        c.rec[(size_t)ob * q.rec_cap + slot] =
-                                            Rec{(uint32_t)k | ((uint32_t)acc << 16),
-                                                (uint32_t)bi | ((uint32_t)bj << 14) | ((uint32_t)l << 28) | 0x80000000u};
+                                        base = atomicAdd(&c.misc[ob], ns);
                                         atomicAdd(&moves_f[(long long)(s + 1) * q.nf], 1);
-                                        cl_red(c.acell(yb_, k), -alpha);
-                                        cl_red(c.acell(yb_, acc), alpha);
                                     }
-                                    const uint32_t hky = c.hrow(yb_, k), hny = c.hrow(yb_, acc);
+                                    base = __shfl_sync(FULL, base, 0);
+                                    Rec *r = c.rec + (size_t)ob * q.rec_cap + base;
                                     for (int i = lane; i < ns; i += 32) {
                                         const int b = list[i];
                                         const int lc = (int)cnt[b];
-                                        cl_red(hky + 4 * b, -lc);
-                                        cl_red(hny + 4 * b, lc);
+                                        r[i] = Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)b | ((uint32_t)lc << 16)};
+                                        c.delta(yb_, k, acc, b, lc);
                                     }
-                                    for (int i = lane; i < alpha; i += 32) c.set(xa + i % rw, ya + i / rw, acc);
+                                    for (int i = lane; i < alpha; i += 32) {
+                                        const int dy = div_small(i, rw, inv);
+                                        c.set(xa + i - dy * rw, ya + dy, acc);
+                                    }
                                 }
                                 __syncwarp();
                                 for (int i = lane; i < ns; i += 32) cnt[list[i]] = 0;
@@ -481,11 +446,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResParams q)
                                 __syncwarp();
                             }
                         }
-                        __syncthreads();
-                        stamp(s + 1, 0);
-                        c.cl.sync();
-                        stamp(s + 1, 1);
-                        s++;
+                        end_subsweep();
                     }
             }
         }
@@ -496,77 +457,105 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResParams q)
                 if (q.limit >= 0 && s >= q.limit) break;
                 const int cx = col % P, cy = col / P;
                 const int ob = s & 1, yb_ = ob ^ 1;
-                replay(yb_, prev_block);
-                prev_block = false;
-                if (tid == 0) c.misc[ob] = 0;
-                __syncthreads();
+                begin_subsweep(yb_);
                 const int uw = (W - cx + P - 1) / P;
+                const float inv_uw = 1.0f / (float)uw;
                 const int yfirst = c.y0 + (((cy - c.y0) % P) + P) % P;
                 const int uh = yfirst < c.y1 ? (c.y1 - yfirst + P - 1) / P : 0;
                 const int nunits = uw * uh;
-                for (int base = wid * 32; base < nunits; base += nthr) {
+                // filter: boundary + ring test, survivors (x | row << 16) to the queue
+                for (int base = wid * 32; base < nunits; base += NT) {
                     const int t = base + lane;
-                    int acc = -1, k = 0, j = 0, x = 0, y = 0;
+                    bool take = false;
+                    uint32_t v = 0;
                     if (t < nunits) {
-                        x = cx + P * (t % uw);
-                        y = yfirst + P * (t / uw);
-                        k = c.get(x, y);
+                        const int tj = div_small(t, uw, inv_uw);
+                        const int x = cx + P * (t - tj * uw), y = yfirst + P * tj;
+                        const Neigh nb = ring_at(c.cell(x, y), pitch, 1, pitch);
+                        take = nb.valid && removable(nb.mask);
+                        v = (uint32_t)x | (uint32_t)(y - c.y0) << 16;
+                    }
+                    push_warp(c.queue, &c.misc[2], take, v);
+                }
+                __syncthreads();
+                const int nq = c.misc[2];
+                for (int base = wid * 32; base < nq; base += NT) {
+                    const int e = base + lane;
+                    int acc = -1, k = 0, j = 0, x = 0, y = 0;
+                    if (e < nq) {
+                        const uint32_t v = c.queue[e];
+                        x = v & 0xFFFF;
+                        y = c.y0 + (int)(v >> 16);
+                        const uint16_t *a = c.cell(x, y);
+                        k = a[0];
+                        const Neigh nb = ring_at(a, pitch, 1, pitch);
                         j = c.bin(x, y);
-                        const Neigh nb = c.neigh8(k, c.get(x, y - 1), c.get(x + 1, y - 1), c.get(x + 1, y),
-                                                  c.get(x + 1, y + 1), c.get(x, y + 1), c.get(x - 1, y + 1),
-                                                  c.get(x - 1, y), c.get(x - 1, y - 1));
-                        if (nb.valid && removable(nb.mask)) {
-                            const long long hk = cl_ld(c.hrow(ob, k) + 4 * j), Ak = cl_ld(c.acell(ob, k));
-                            long long hn[4], An[4];
+                        const long long hk = cl_ld(c.hrow(ob, k) + 4 * j), Ak = cl_ld(c.acell(ob, k));
+                        long long hn[4] = {0, 0, 0, 0}, An[4] = {1, 1, 1, 1};
 #pragma unroll
-                            for (int d = 0; d < 4; d++) {
-                                const bool v = nb.valid >> d & 1;
-                                hn[d] = v ? cl_ld(c.hrow(ob, nb.v[d]) + 4 * j) : 0;
-                                An[d] = v ? cl_ld(c.acell(ob, nb.v[d])) : 1;
+                        for (int d = 0; d < 4; d++)
+                            if (nb.valid >> d & 1) {
+                                hn[d] = cl_ld(c.hrow(ob, nb.v[d]) + 4 * j);
+                                An[d] = cl_ld(c.acell(ob, nb.v[d]));
                             }
+                        int pass = 0;  // candidates passing the colour test (Prop. 1, one look-up)
+#pragma unroll
+                        for (int d = 0; d < 4; d++)
+                            pass |= (int)((nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d]) << d;
+                        if (!GAMMA) {
+                            if (pass) acc = nb.v[__ffs(pass) - 1];
+                        } else if (pass) {
+                            uint16_t w[25];
+#pragma unroll
+                            for (int dy = -2; dy <= 2; dy++)
+#pragma unroll
+                                for (int dx = -2; dx <= 2; dx++) w[(dy + 2) * 5 + dx + 2] = a[dy * pitch + dx];
+                            // in-image patch centres of W3(p)
+                            const uint32_t vx = (x > 0 ? 1u : 0u) | 2u | (x + 1 < W ? 4u : 0u);
+                            const uint32_t vy = (y > 0 ? 1u : 0u) | 2u | (y + 1 < q.H ? 4u : 0u);
+                            uint32_t centres = 0;
+#pragma unroll
+                            for (int iy = 0; iy < 3; iy++)
+                                if (vy >> iy & 1) centres |= vx << (3 * iy);
+                            const int base_s = __popc(centres) - box_sum(win_mask(w, k), centres);
 #pragma unroll
                             for (int d = 0; d < 4; d++)
-                                if (acc < 0 && (nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d] &&
-                                    (!GAMMA || c.smooth(x, y, k, nb.v[d]) >= 0))
+                                if (acc < 0 && (pass >> d & 1) && base_s + box_sum(win_mask(w, nb.v[d]), centres) >= 0)
                                     acc = nb.v[d];
                         }
                     }
+                    count_moves(acc >= 0);
                     const int slot = append_warp(&c.misc[ob], acc >= 0 ? 1 : 0);
-                    const unsigned mv = __ballot_sync(FULL, acc >= 0);
-                    if (lane == 0 && mv) atomicAdd(&moves_f[(long long)(s + 1) * q.nf], __popc(mv));
                     if (acc >= 0) {
                         c.rec[(size_t)ob * q.rec_cap + slot] =
                             Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)j | (1u << 16)};
-                        cl_red(c.hrow(yb_, k) + 4 * j, -1);
-                        cl_red(c.hrow(yb_, acc) + 4 * j, 1);
-                        cl_red(c.acell(yb_, k), -1);
-                        cl_red(c.acell(yb_, acc), 1);
+                        c.delta(yb_, k, acc, j, 1);
                         c.set(x, y, acc);
                     }
                 }
-                __syncthreads();
-                stamp(s + 1, 0);
-                c.cl.sync();
-                stamp(s + 1, 1);
-                s++;
+                end_subsweep();
             }
 
         // ---- outputs: labels of the band, final histograms of the owned rows ----
-        for (int i = tid; i < band * W; i += nthr) q.out[fN + (long long)c.y0 * W + i] = c.lab[2 * W + i];
+        for (int ly = wid; ly < band; ly += NW) {
+            int32_t *o = q.out + fN + (long long)(c.y0 + ly) * W;
+            const uint16_t *src = c.lab + (ly + 2) * pitch + RES_PAD;
+            for (int x = lane; x < W; x += 32) o[x] = src[x];
+        }
         {
             const int fb = s & 1;
             int *Ho = q.Hout[fb] + (long long)f * q.H_fs;
             int *Ao = q.Aout[fb] + (long long)f * q.K;
-            for (int i = tid; i < q.kloc * B; i += nthr) {
-                const int kl = i / B, b = i - kl * B, k = kl * c.CS + c.rank;
-                if (k < q.K) Ho[(long long)k * B + b] = c.Hs[(size_t)fb * q.kloc * B + i];
-            }
-            for (int kl = tid; kl < q.kloc; kl += nthr) {
-                const int k = kl * c.CS + c.rank;
-                if (k < q.K) Ao[k] = c.As[(size_t)fb * q.kloc + kl];
+            for (int k = wid; k < q.K; k += NW) {
+                const uint32_t m = q.kmap[k];
+                if ((int)(m & 0xFF) != c.rank) continue;
+                const int loc = m >> 8;
+                for (int b = lane; b < B; b += 32)
+                    Ho[(long long)k * B + b] = c.Hs[(size_t)fb * q.kloc * B + (size_t)loc * B + b];
+                if (lane == 0) Ao[k] = c.As[(size_t)fb * q.kloc + loc];
             }
         }
-        c.cl.sync();  // the next frame reuses the shared state
+        cluster_barrier();  // the next frame reuses the shared state
     }
 }
 

@@ -35,7 +35,7 @@ class Info(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "width", "height", "channels", "nx", "ny", "k_actual", "levels_eff", "grid_x", "grid_y",
         "colour_period", "bins_total", "bin_bytes", "subsweeps", "max_block_area",
-        "kernels_per_run", "exec_mode", "cluster_size")] + [
+        "kernels_per_run", "exec_mode", "cluster_size", "grid_ctas", "grid_tiles")] + [
         ("workspace_bytes_per_frame", ctypes.c_size_t)]
 
 
@@ -102,6 +102,8 @@ class Geometry:
     kernels_per_run: int
     exec_mode: int
     cluster_size: int
+    grid_ctas: int
+    grid_tiles: int
     workspace_bytes_per_frame: int
 
 
@@ -204,7 +206,7 @@ class Seeds:
         return out
 
     KINDS = ("seed", "block", "pixel", "emit", "frame")
-    MODES = {"auto": 0, "graph": 1, "resident": 2}
+    MODES = {"auto": 0, "graph": 1, "resident": 2, "grid": 3}
 
     def set_mode(self, mode: str):
         self._check(self._lib.seeds_set_mode(self._ctx, self.MODES[mode]))
@@ -226,13 +228,16 @@ class Seeds:
                                                     n.ctypes.data))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.KINDS)}
 
-    def debug_trace(self, enable: bool = True):
-        """Resident mode: per-CTA clock64 stamps [cta, phase, (work done, barrier passed)]."""
-        cs = max(1, self.info.cluster_size)
-        n = cs * (self.info.subsweeps + 4) * 2
+    def debug_trace(self, enable: bool = True, n_sm: int | None = None):
+        """Resident / grid mode: per-CTA clock64 stamps [cta, phase, slot] (include/seeds.h)."""
+        if n_sm is None:
+            import torch
+            n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        cs = max(n_sm, self.info.cluster_size)
+        n = cs * (self.info.subsweeps + 4) * 8
         out = np.zeros(n, np.int64)
         self._check(self._lib.seeds_debug_trace(self._ctx, int(enable), out.ctypes.data if enable else None, n))
-        return out.reshape(cs, self.info.subsweeps + 4, 2)
+        return out.reshape(cs, self.info.subsweeps + 4, 8)
 
     def debug_limit(self, max_subsweeps: int):
         self._check(self._lib.seeds_debug_limit(self._ctx, max_subsweeps))

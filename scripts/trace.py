@@ -1,0 +1,51 @@
+"""Per-CTA clock64 trace of one resident / grid run: work and barrier cycles
+per sub-sweep (max / min over CTAs), summarised per phase group."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1309_3848_b200 import configs  # noqa: E402
+from paper_1309_3848_b200.seeds import Seeds  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+mode = sys.argv[2] if len(sys.argv) > 2 else "resident"
+img = configs.frames(cfg, n=1)[0]
+p = configs.params(cfg)
+s = Seeds(img.shape[1], img.shape[0], img.shape[2], *[p[k] for k in (
+    "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+s.set_mode(mode)
+s.debug_trace(True)
+d = torch.from_numpy(img).cuda()
+for _ in range(3):
+    out = s.iterate(d)
+torch.cuda.synchronize()
+tr = s.debug_trace(True)
+S = s.info.subsweeps
+L, I, P = s.info.levels_eff, p["iters_per_level"], s.info.colour_period
+ncta = tr.shape[0]
+active = tr[:, S, 1] != 0
+tr = tr[active].astype(np.float64)
+print(f"{cfg} {mode}: CTAs {ncta} (active {int(active.sum())}), S {S}")
+prev1 = tr[:, 0:S, 1]
+cur = tr[:, 1:S + 1, :]
+work = cur[:, :, 0] - prev1          # (cta, S)
+bar = cur[:, :, 1] - cur[:, :, 0]
+parts = {"replay": cur[:, :, 2] - prev1, "stage": cur[:, :, 3] - cur[:, :, 2],
+         "filter": cur[:, :, 4] - cur[:, :, 3], "decide": cur[:, :, 5] - cur[:, :, 4],
+         "tail": cur[:, :, 0] - cur[:, :, 5]}
+have_parts = mode == "grid"
+groups = [(f"level {l}", 4 * I) for l in range(L - 1, -1, -1)] + [("pixel", P * P * I)]
+i = 0
+for name, n in groups:
+    sl = slice(i, i + n)
+    w = work[:, sl]
+    line = (f"{name:>8}: work max {w.max(0).mean():7.0f} mean {w.mean():7.0f} min {w.min(0).mean():7.0f} | "
+            f"barrier min {bar[:, sl].min(0).mean():6.0f} max {bar[:, sl].max(0).mean():6.0f} | "
+            f"work+barrier {(w + bar[:, sl]).mean():7.0f}")
+    if have_parts:
+        line += " | " + " ".join(f"{k} {v[:, sl].mean():5.0f}/{v[:, sl].max(0).mean():5.0f}" for k, v in parts.items())
+    print(line)
+    i += n

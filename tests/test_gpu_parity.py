@@ -19,7 +19,7 @@ def torch_cuda():
     return torch
 
 
-MODES = ["graph", "resident"]
+MODES = ["graph", "resident", "grid"]
 
 
 @pytest.fixture(params=MODES)
@@ -179,13 +179,16 @@ def test_host_entry_point(torch_cuda, orc):
 
 
 def test_modes_resolved(torch_cuda):
-    """A c2 frame fits a co-schedulable cluster (resident mode available) and
-    both modes report their launch counts (seeds_query)."""
+    """A c2 frame fits a co-schedulable cluster (resident mode) and a grid tile
+    plan (grid mode, the AUTO choice); every mode reports its launch count."""
     from paper_1309_3848_b200.seeds import Seeds
     s = Seeds(481, 321, 3, 200, 4, 5, 1, 4)
     print("cluster size", s.info.cluster_size, "mode", s.info.exec_mode)
     assert 1 <= s.info.cluster_size <= 16
+    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 1
     s.set_mode("resident")
     assert s.info.exec_mode == 2 and s.info.kernels_per_run == 1
     s.set_mode("graph")
     assert s.info.exec_mode == 1 and s.info.kernels_per_run == 107
+    s.set_mode("grid")
+    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 1
