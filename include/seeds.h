@@ -151,8 +151,8 @@ seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps);
 
 /* seeds_debug_trace -- resident / grid mode only: enable (1) per-CTA clock64
  * stamps of every sub-sweep (slot 0 work finished, 1 barrier passed; grid mode
- * also 2 replayed, 3 staged, 4 filtered, 5 decided), copy them to
- * host_out[min(cap, ctas*(subsweeps+4)*8)] (int64, layout [cta][phase][8],
+ * also 2 replayed, 3 staged, 4 filtered, 5 decided; 8.. detail builds), copy
+ * them to host_out[min(cap, ctas*(subsweeps+4)*16)] (int64, layout [cta][phase][16],
  * ctas = max(#SM, cluster_size)), or disable (0) and free the buffer.
  * Synchronises the device when host_out is given.  Diagnostic; not part of
  * the hot path. */

@@ -524,6 +524,18 @@ static std::vector<int> size_candidates(int n)
 
 static size_t align128(size_t v) { return (v + 127) & ~(size_t)127; }
 
+// An environment switch set to 0 (for A/B measurements of optional paths).
+static bool getenv_off(const char *name)
+{
+    const char *v = getenv(name);
+    return v && atoi(v) == 0;
+}
+static bool getenv_on(const char *name)
+{
+    const char *v = getenv(name);
+    return v && atoi(v) != 0;
+}
+
 // TMA descriptors of the grid plan: the padded label planes (u16, x y frame,
 // box bw x bh) and, when the bins are staged, the padded bin planes.
 static bool encode_tmaps(seeds_ctx *c, GridParams &q)
@@ -578,6 +590,8 @@ static bool plan_grid(seeds_ctx *c, int nf)
     const size_t tabw = (2 * (size_t)c->B + 2) * 4;
     bool need_tab = false;
     GridParams &q = c->gp;
+    int nsm = c->n_sm;  // SEEDS_GRID_CTAS caps the CTAs (experiments)
+    if (const char *v = getenv("SEEDS_GRID_CTAS")) nsm = std::max(1, std::min(nsm, atoi(v)));
     q = GridParams{};
     for (int l = 0; l < c->L; l++) {
         const int am = max_block_area(c, l);
@@ -587,13 +601,13 @@ static bool plan_grid(seeds_ctx *c, int nf)
         q.gshift[l] = gs;
         need_tab = need_tab || q.bkind[l] == BK_WARP;
     }
-    const size_t fixed = 64 + 16 + align16((size_t)(c->GX + c->GY + 2) * 4) + (need_tab ? tabw : 0);
+    const size_t fixed = 128 + 16 + align16((size_t)(c->GX + c->GY + 2) * 4) + (need_tab ? tabw : 0);
     double best = 1e300;
     int ba = 0, bb_ = 0;
     for (int a : size_candidates(TX))
         for (int b : size_candidates(TY)) {
             const long long T = (long long)nf * ((TX + a - 1) / a) * ((TY + b - 1) / b);
-            const long long G = std::min<long long>(c->n_sm, T);
+            const long long G = std::min<long long>(nsm, T);
             const long long tw = (long long)a * muw, th = (long long)b * muh;
             if ((tw + 4 + 14) / 8 * 8 > 256 || th + 4 > 256) continue;  // TMA box limits (aligned start)
             const size_t stage = 2 * align128((size_t)((tw + 4 + 14) / 8 * 8) * (th + 4) * 2);
@@ -645,7 +659,7 @@ static bool plan_grid(seeds_ctx *c, int nf)
             tr.push_back(rc);
         }
     const long long T = (long long)nf * ft.size();
-    const int G = (int)std::min<long long>(c->n_sm, T);
+    const int G = (int)std::min<long long>(nsm, T);
     std::vector<long long> cpx(G, 0), crec(G, 0);
     long long qcap = 0;
     int max_tw = 0, max_th = 0;
@@ -684,10 +698,28 @@ static bool plan_grid(seeds_ctx *c, int nf)
         q.o_bins = (unsigned)off;  off = align128(off + (res ? (size_t)max_cpx * c->bb : 2 * (size_t)q.bins_bytes));
         q.o_rec = (unsigned)off;   off = align16(off + (rs ? 2 * (size_t)rec_cap * sizeof(GRec) : 0));
         q.o_queue = (unsigned)off; off = align16(off + (size_t)(qcap + 32) * 4);
-        q.o_misc = (unsigned)off;  off = align16(off + 64);
+        q.o_misc = (unsigned)off;  off = align16(off + 128);
         q.o_mbar = (unsigned)off;  off = align16(off + 16);
         q.o_tiles = (unsigned)off; off = align16(off + (size_t)q.tiles_per_cta * sizeof(GridTile));
         q.o_geo = (unsigned)off;   off = align16(off + (size_t)(c->GX + c->GY + 2) * 4);
+        // histogram cache (single-tile CTAs): A, slot table, row list, rows
+        q.cache = 0;
+        q.hc_rows = 0;
+        if (q.tiles_per_cta == 1 && c->K <= 16384 && getenv_on("SEEDS_GRID_CACHE")) {
+            const size_t base = align16(off + (size_t)c->K * 4) + align16(c->K) + align16(255 * 2);
+            const size_t tab = need_tab ? tabw : 0;
+            if (base + tab < limit) {
+                const int rows = (int)std::min<size_t>(255, (limit - base - tab) / ((size_t)c->B * 4));
+                if (rows >= 16) {
+                    q.cache = 1;
+                    q.hc_rows = rows > 64 ? 64 : rows;
+                    q.o_ac = (unsigned)off;    off = align16(off + (size_t)c->K * 4);
+                    q.o_kslot = (unsigned)off; off = align16(off + (size_t)c->K);
+                    q.o_klist = (unsigned)off; off = align16(off + 255 * 2);
+                    q.o_hc = (unsigned)off;    off = align16(off + (size_t)q.hc_rows * c->B * 4);
+                }
+            }
+        }
         q.o_tab = (unsigned)off;
         if (off + (need_tab ? tabw : 0) > limit) continue;
         q.ntab = need_tab ? (int)std::min<size_t>(GRID_THREADS / 32, (limit - off) / tabw) : 0;
@@ -1267,7 +1299,7 @@ seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap)
 {
     if (!ctx) return SEEDS_EINVAL;
-    const size_t n = (size_t)std::max(ctx->n_sm, ctx->cluster) * (ctx->S + 4) * 8;
+    const size_t n = (size_t)std::max(ctx->n_sm, ctx->cluster) * (ctx->S + 4) * 16;
     if (enable && !ctx->d_trace) {
         CK(cudaMalloc(&ctx->d_trace, n * sizeof(long long)));
         CK(cudaMemset(ctx->d_trace, 0, n * sizeof(long long)));

@@ -73,12 +73,43 @@ struct GridParams {
     void *binsp;           // padded bin planes (pitch bpitch) when the bins are staged
     long long binsp_fs;
     int bpitch;
-    unsigned o_stage, o_bins, o_queue, o_tab, o_misc, o_geo, o_rec, o_tiles, o_mbar;
+    unsigned o_stage, o_bins, o_queue, o_tab, o_misc, o_geo, o_rec, o_tiles, o_mbar, o_params;
     int stage_bytes, bins_bytes;  // one stage buffer of labels / of bins (two of each), 128-byte multiples
     int tx_bytes;                 // bytes one tile's TMA loads deliver (label box + bin box)
     int bw, bbw, bh;              // TMA boxes: label box bw x bh, bin box bbw x (bh - 4)
     int tiles_per_cta, q_cap, ntab, GX, GY, bins_res, rec_smem;
+    // histogram cache (CTAs with a single tile): A of the frame and the H rows of
+    // the superpixels present in the tile + halo, loaded right after each barrier
+    int cache;             // 1: enabled
+    int hc_rows;           // capacity in rows
+    unsigned o_hc, o_ac, o_kslot, o_klist;
 };
+
+// Split grid barrier: arrive (CTA barrier, then thread 0 publishes the CTA's
+// writes with a GPU-scope fence and counts in) ... wait (thread 0 polls for
+// every CTA's arrival, acquire, then a CTA barrier).  Local work that touches
+// no state another CTA writes may run between the two.
+__device__ __forceinline__ void grid_arrive(unsigned *ctr, unsigned &target)
+{
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+    }
+}
+__device__ __forceinline__ void grid_wait(unsigned *ctr, unsigned target)
+{
+    if (threadIdx.x == 0) {
+        unsigned v;
+        long long spins = 0;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (++spins > (1LL << 26)) __trap();  // a CTA that never arrives: fail loudly instead of hanging
+        } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
+}
 
 __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned &target)
 {
@@ -137,10 +168,14 @@ struct GridCta {
     uint32_t *rem;     // removable-ring LUT (8 words, reading Q8)
     GridTile *tiles;   // this CTA's tiles
     uint64_t *mbar;    // two mbarriers (one per stage buffer)
+    int *hc, *ac;      // histogram cache: cached H rows (hc_rows x B) and A (K)
+    uint8_t *kslot;    // K: cache row of superpixel k, 0xFF = not cached
+    uint16_t *klist;   // hc_rows: superpixel of each cache row
     uint16_t *stage;   // the current tile's staged labels
     uint32_t *queue;   // surviving units of the current tile and sub-sweep
     uint32_t *tabs;    // ntab warp tables of 2B + 2 words
-    int *misc;         // [0], [1]: record counts of the two lists, [2]: queue length
+    int *misc;         // [0], [1]: record counts of the two lists, [2]: queue length, [3]: cached rows,
+                       // [4..7]: detail timing; the ring LUT follows at +64 bytes
     int *cs, *rs;      // level-0 block column / row starts (GX + 1, GY + 1)
     // current tile
     int f, X0, X1, Y0, Y1, sp, tbp;
@@ -149,13 +184,20 @@ struct GridCta {
     uint16_t *glab;    // global label plane of frame f, (0, 0) at pixel (-2, -2)
     const int *Hf0, *Hf1, *Af0, *Af1;  // the frame's two histogram / size buffers
 
-    __device__ GridCta(const GridParams &qq, unsigned char *smem) : q(qq)
+    const CUtensorMap *tm_lab, *tm_bins;  // in the kernel's parameter space
+
+    __device__ GridCta(const GridParams &qq, unsigned char *smem, const CUtensorMap *tl, const CUtensorMap *tb_)
+        : q(qq), tm_lab(tl), tm_bins(tb_)
     {
         stage0 = reinterpret_cast<uint16_t *>(smem + q.o_stage);
         sbins = reinterpret_cast<BinT *>(smem + q.o_bins);
-        rem = reinterpret_cast<uint32_t *>(smem + q.o_misc + 16);
+        rem = reinterpret_cast<uint32_t *>(smem + q.o_misc + 64);
         tiles = reinterpret_cast<GridTile *>(smem + q.o_tiles);
         mbar = reinterpret_cast<uint64_t *>(smem + q.o_mbar);
+        hc = reinterpret_cast<int *>(smem + q.o_hc);
+        ac = reinterpret_cast<int *>(smem + q.o_ac);
+        kslot = reinterpret_cast<uint8_t *>(smem + q.o_kslot);
+        klist = reinterpret_cast<uint16_t *>(smem + q.o_klist);
         queue = reinterpret_cast<uint32_t *>(smem + q.o_queue);
         tabs = reinterpret_cast<uint32_t *>(smem + q.o_tab);
         misc = reinterpret_cast<int *>(smem + q.o_misc);
@@ -196,15 +238,25 @@ struct GridCta {
         asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy label writes before the TMA reads
         mbar_expect(&mbar[slot], (unsigned)q.tx_bytes);
         // box starts must be 16-byte aligned in x (the TMA faults otherwise)
-        tma_load3(reinterpret_cast<unsigned char *>(stage0) + slot * q.stage_bytes, &q.tm_lab, t.X0 & ~7, t.Y0, t.f,
+        tma_load3(reinterpret_cast<unsigned char *>(stage0) + slot * q.stage_bytes, tm_lab, t.X0 & ~7, t.Y0, t.f,
                   &mbar[slot]);
         if (!q.bins_res)
-            tma_load3(reinterpret_cast<unsigned char *>(sbins) + slot * q.bins_bytes, &q.tm_bins,
+            tma_load3(reinterpret_cast<unsigned char *>(sbins) + slot * q.bins_bytes, tm_bins,
                       t.X0 & ~(16 / (int)sizeof(BinT) - 1), t.Y0, t.f, &mbar[slot]);
     }
-    __device__ __forceinline__ int ldA(int buf, int k) const { return __ldcg((buf ? Af1 : Af0) + k); }
+    // Histogram reads of a decision (always buffer ob of the sub-sweep, which
+    // is the one the cache holds)
+    __device__ __forceinline__ int ldA(int buf, int k) const
+    {
+        if (q.cache) return ac[k];
+        return __ldcg((buf ? Af1 : Af0) + k);
+    }
     __device__ __forceinline__ int ldH(int buf, int k, int b) const
     {
+        if (q.cache) {
+            const int r = kslot[k];
+            if (r != 0xFF) return hc[r * q.B + b];
+        }
         return __ldcg((buf ? Hf1 : Hf0) + (long long)k * q.B + b);
     }
     __device__ __forceinline__ void set(int x, int y, int v) const
@@ -284,10 +336,11 @@ __device__ __forceinline__ int block_t4(const Ctx &c, int ob, int k, const Neigh
 }
 
 template <typename BinT, int GAMMA, int P>
-__global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant__ GridParams q)
+__global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant__ GridParams qp)
 {
     extern __shared__ __align__(128) uint32_t smem[];
-    GridCta<BinT> c(q, reinterpret_cast<unsigned char *>(smem));
+    const GridParams &q = qp;
+    GridCta<BinT> c(q, reinterpret_cast<unsigned char *>(smem), &qp.tm_lab, &qp.tm_bins);
     constexpr int NT = GRID_THREADS, NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int W = q.W, B = q.B;
@@ -313,6 +366,45 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
     unsigned phase0 = 0, phase1 = 0;  // parity of the next completion of each stage buffer
     __syncthreads();
 
+    // Labels present in the (single) tile + halo -> the cache rows of the next
+    // sub-sweep (run while waiting at the grid barrier; a label entering the
+    // halo later is read from global memory).
+    auto build_cache_list = [&](bool from_stage) {
+        for (int k = tid; k < q.K; k += NT) c.kslot[k] = 0;
+        __syncthreads();
+        const GridTile &t = c.tiles[0];
+        const int rows = t.Y1 - t.Y0 + 4, cols = t.X1 - t.X0 + 4, n = rows * cols;
+        const float inv = 1.0f / (float)cols;
+        for (int i = tid; i < n; i += NT) {
+            const int r = div_small(i, cols, inv), x = t.X0 - 2 + (i - r * cols), y = t.Y0 - 2 + r;
+            int v = SENT;
+            if (from_stage) {
+                v = *c.cell(x, y);
+            } else if (x >= 0 && x < W && y >= 0 && y < q.H) {
+                v = q.init ? q.init[(long long)t.f * q.N + (long long)y * W + x]
+                           : (q.byof[y] >> q.L) * q.nx + (q.bxof[x] >> q.L);
+            }
+            if (v != SENT) c.kslot[v] = 1;
+        }
+        __syncthreads();
+        if (tid == 0) c.misc[3] = 0;
+        __syncthreads();
+        for (int k = tid; k < q.K; k += NT) {
+            if (!c.kslot[k]) {
+                c.kslot[k] = 0xFF;
+                continue;
+            }
+            const int r = atomicAdd(&c.misc[3], 1);
+            if (r < q.hc_rows) {
+                c.kslot[k] = (uint8_t)r;
+                c.klist[r] = (uint16_t)k;
+            } else {
+                c.kslot[k] = 0xFF;
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && c.misc[3] > q.hc_rows) c.misc[3] = q.hc_rows;
+    };
     // ---- seed: bins (reading Q1), labels (grid, or warm
     // start, reading O9) and the histogram counts (Eq. 6) into both buffers,
     // warp-aggregated on the (label, bin) key
@@ -351,13 +443,15 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
             }
         }
     }
-    grid_barrier(q.sync, target);
+    grid_arrive(q.sync, target);
+    if (q.cache && ntl > 0) build_cache_list(false);
+    grid_wait(q.sync, target);
 
     int s = 0;
     // debug trace [cta][phase][8]: 0 work done, 1 barrier passed, 2 replayed,
     // 3 last tile staged, 4 last tile filtered, 5 last tile decided
     auto stamp = [&](int phase, int which) {
-        if (q.trace && tid == 0) q.trace[((long long)blockIdx.x * (q.S + 4) + phase) * 8 + which] = clock64();
+        if (q.trace && tid == 0) q.trace[((long long)blockIdx.x * (q.S + 4) + phase) * 16 + which] = clk64();
     };
     stamp(0, 1);
     auto count_moves = [&](bool moved) {
@@ -368,6 +462,18 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
     // buffer yb and reset the list that sub-sweep s fills.
     auto begin_subsweep = [&](int yb) {
         if (tid == 0 && ntl > 0) c.issue(c.tiles[0], 0);  // overlaps the replay
+        if (q.cache) {
+            // histogram cache of buffer ob = yb ^ 1 (the snapshot of this sub-sweep)
+            c.select(c.tiles[0], 0);
+            const int *Hx = (yb ^ 1) ? c.Hf1 : c.Hf0, *Ax = (yb ^ 1) ? c.Af1 : c.Af0;
+            const int nk = c.misc[3], tot = nk * B;
+            const float invB = 1.0f / (float)B;
+            for (int i = tid; i < tot; i += NT) {
+                const int r = div_small(i, B, invB);
+                c.hc[i] = __ldcg(Hx + (long long)c.klist[r] * B + (i - r * B));
+            }
+            for (int k = tid; k < q.K; k += NT) c.ac[k] = __ldcg(Ax + k);
+        }
         const int nrec = c.misc[yb];
         const GRec *r = rec_list(yb);
         for (int e = tid; e < nrec; e += NT) {
@@ -389,6 +495,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
             phase0 ^= 1;
         }
         c.select(c.tiles[ti], ti & 1);
+        if (q.cache) __syncthreads();  // the cache fill of the other threads
         stamp(s + 1, 3);
     };
     auto end_tile = [&]() {
@@ -398,7 +505,9 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
     };
     auto end_subsweep = [&]() {
         stamp(s + 1, 0);
-        grid_barrier(q.sync, target);
+        grid_arrive(q.sync, target);
+        if (q.cache) build_cache_list(true);
+        grid_wait(q.sync, target);
         stamp(s + 1, 1);
         s++;
     };
@@ -698,10 +807,20 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
                     nq = c.misc[2];
                 }
                 stamp(s + 1, 4);
+#ifdef SEEDS_DETAIL
+                unsigned *dmax = reinterpret_cast<unsigned *>(c.misc + 4);
+                if (tid < 7) dmax[tid] = 0;
+                __syncthreads();
+                const long long dt0 = clk64();
+                long long dt1 = dt0, dt2 = dt0, dta = dt0, dtb = dt0, dtp = dt0, dtu = dt0;
+#endif
                 for (int base = wid * 32; base < nq; base += NT) {
                     const int e = base + lane;
                     int acc = -1, k = 0, j = 0, x = 0, y = 0;
                     if (e < nq) {
+#ifdef SEEDS_DETAIL
+                        dtp = clk64();
+#endif
                         if (direct) {
                             unit_xy(e, x, y);
                         } else {
@@ -711,10 +830,21 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
                         }
                         const uint16_t *a = c.cell(x, y);
                         const int sp = c.sp;
+#ifdef SEEDS_DETAIL
+                        dtu = clk64();
+                        k = (int)(dtu & 0);
+#endif
                         k = a[0];
                         const Neigh nb = ring_at(a, sp, 1, sp);
+#ifdef SEEDS_DETAIL
+                        dta = clk64();
+                        if (nb.valid) k = (k + (int)(dta & 0)) ;
+#endif
                         if (nb.valid && c.removable_s(nb.mask)) {
                             j = c.bin(x, y);
+#ifdef SEEDS_DETAIL
+                            dtb = clk64();
+#endif
                             // all gathers in flight together (invalid slots re-read k's row)
                             const long long hk = c.ldH(ob, k, j), Ak = c.ldA(ob, k);
                             long long hn[4], An[4];
@@ -728,6 +858,9 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
 #pragma unroll
                             for (int d = 0; d < 4; d++)
                                 pass |= (int)((nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d]) << d;
+#ifdef SEEDS_DETAIL
+                            dt1 = clk64();
+#endif
                             if (!GAMMA) {
                                 if (pass) acc = nb.v[__ffs(pass) - 1];
                             } else if (pass) {
@@ -750,6 +883,9 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
                             }
                         }
                     }
+#ifdef SEEDS_DETAIL
+                    dt2 = clk64();
+#endif
                     count_moves(acc >= 0);
                     const int slot = append_warp(&c.misc[ob], acc >= 0 ? 1 : 0);
                     if (acc >= 0) {
@@ -757,6 +893,22 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
                         c.set(x, y, acc);
                     }
                 }
+#ifdef SEEDS_DETAIL
+                {
+                    const long long dt3 = clk64();
+                    atomicMax(&dmax[0], (unsigned)(dt1 - dt0));
+                    atomicMax(&dmax[1], (unsigned)(dt2 - dt0));
+                    atomicMax(&dmax[2], (unsigned)(dt3 - dt0));
+                    atomicMax(&dmax[3], (unsigned)(dta - dt0));
+                    atomicMax(&dmax[4], (unsigned)(dtb - dt0));
+                    atomicMax(&dmax[5], (unsigned)(dtp - dt0));
+                    atomicMax(&dmax[6], (unsigned)(dtu - dt0));
+                    __syncthreads();
+                    if (q.trace && tid == 0)
+                        for (int i = 0; i < 7; i++)
+                            q.trace[((long long)blockIdx.x * (q.S + 4) + s + 1) * 16 + 8 + i] = dmax[i];
+                }
+#endif
                 end_tile();
             }
             end_subsweep();

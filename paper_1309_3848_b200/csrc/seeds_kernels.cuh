@@ -707,6 +707,14 @@ __global__ void __launch_bounds__(256) k_pixel(SweepParams p)
 // border, so label reads need no bounds test.
 // ---------------------------------------------------------------------------
 
+// SM clock read that memory operations are not moved across (debug traces).
+__device__ __forceinline__ long long clk64()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    return t;
+}
+
 // per-level block strategies of the persistent kernels
 enum { BK_T4 = 0, BK_T16 = 1, BK_WARP = 2 };
 

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_resident(ResParams q)
         // debug timing (first frame only): [rank][phase][0] = work done, [1] = barrier passed
         auto stamp = [&](int phase, int which) {
             if (q.trace && f == 0 && tid == 0)
-                q.trace[((long long)c.rank * (q.S + 4) + phase) * 8 + which] = clock64();
+                q.trace[((long long)c.rank * (q.S + 4) + phase) * 16 + which] = clk64();
         };
         stamp(0, 1);
 

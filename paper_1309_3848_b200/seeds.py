@@ -234,10 +234,10 @@ class Seeds:
             import torch
             n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
         cs = max(n_sm, self.info.cluster_size)
-        n = cs * (self.info.subsweeps + 4) * 8
+        n = cs * (self.info.subsweeps + 4) * 16
         out = np.zeros(n, np.int64)
         self._check(self._lib.seeds_debug_trace(self._ctx, int(enable), out.ctypes.data if enable else None, n))
-        return out.reshape(cs, self.info.subsweeps + 4, 8)
+        return out.reshape(cs, self.info.subsweeps + 4, 16)
 
     def debug_limit(self, max_subsweeps: int):
         self._check(self._lib.seeds_debug_limit(self._ctx, max_subsweeps))

@@ -5,6 +5,12 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 
+__device__ __forceinline__ long long clk()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    return t;
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
 {
     unsigned v;
@@ -147,6 +153,29 @@ __global__ void k_cluster(int iters, long long *out)
     if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
 }
 
+
+// After a barrier, every CTA loads `per` ints per thread: mode 0 from a small
+// array shared by all CTAs (hot lines), mode 1 from a CTA-private region.
+__global__ void k_hot(unsigned *ctr, unsigned *flags, int *data, int iters, int mode, long long *out)
+{
+    __shared__ int sm[2048];
+    unsigned epoch = 0;
+    grid_barrier<0>(ctr, flags, epoch);
+    long long tload = 0;
+    for (int i = 0; i < iters; i++) {
+        grid_barrier<0>(ctr, flags, epoch);
+        const long long t0 = clk();
+        const int base = mode == 0 ? 0 : blockIdx.x * 2048;
+        int v0 = __ldcg(data + base + (threadIdx.x * 4) % 256);
+        int v1 = __ldcg(data + base + (threadIdx.x * 4 + 1) % 256);
+        int v2 = __ldcg(data + base + 256 + threadIdx.x);
+        sm[threadIdx.x] = v0 + v1 + v2;
+        __syncthreads();
+        tload += clk() - t0;
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = tload / iters;
+}
+
 template <int V>
 void run(int nsm, unsigned *ctr, unsigned *flags, int *data, long long *out, int mode, int nthr = 512)
 {
@@ -202,16 +231,21 @@ int main()
     long long *out, h[4];
     cudaMalloc(&ctr, 32 * 4 * 32);
     cudaMalloc(&flags, 256 * 4);
-    cudaMalloc(&data, (nsm * 512 + 8192) * 4);
-    cudaMemset(data, 0, (nsm * 512 + 8192) * 4);
+    cudaMalloc(&data, (nsm * 2048 + 8192) * 4);
+    cudaMemset(data, 0, (nsm * 2048 + 8192) * 4);
     cudaMalloc(&out, 256 * 8);
-    for (int n : {8, 16, 32, 74, 148}) {
-        run<0>(n, ctr, flags, data, out, 0);
-        run<10>(n, ctr, flags, data, out, 0);
+    for (int mode = 0; mode < 2; mode++) {
+        cudaMemset(ctr, 0, 32 * 4 * 32);
+        const int iters = 200;
+        void *args[] = {&ctr, &flags, &data, (void *)&iters, &mode, &out};
+        cudaLaunchCooperativeKernel((void *)k_hot, nsm, 512, args, 0, 0);
+        cudaDeviceSynchronize();
+        long long hh[256];
+        cudaMemcpy(hh, out, nsm * 8, cudaMemcpyDeviceToHost);
+        long long mx = 0, sum = 0;
+        for (int i = 0; i < nsm; i++) { mx = hh[i] > mx ? hh[i] : mx; sum += hh[i]; }
+        printf("post-barrier loads, %s: max %lld mean %lld cycles\n", mode ? "CTA-private" : "shared hot", mx, sum / nsm);
     }
-    run<0>(148, ctr, flags, data, out, 0, 128);
-    run<0>(148, ctr, flags, data, out, 0, 1024);
-    run<9>(148, ctr, flags, data, out, 0, 128);
     int hb[4096];
     for (int i = 0; i < 4096; i++) hb[i] = (i + 33 * 7) % 4096;
     cudaMemcpy(data, hb, sizeof hb, cudaMemcpyHostToDevice);

@@ -36,6 +36,9 @@ bar = cur[:, :, 1] - cur[:, :, 0]
 parts = {"replay": cur[:, :, 2] - prev1, "stage": cur[:, :, 3] - cur[:, :, 2],
          "filter": cur[:, :, 4] - cur[:, :, 3], "decide": cur[:, :, 5] - cur[:, :, 4],
          "tail": cur[:, :, 0] - cur[:, :, 5]}
+if (cur[:, :, 8] != 0).any():
+    parts.update({"d.pre": cur[:, :, 13], "d.xy": cur[:, :, 14], "d.ring": cur[:, :, 11], "d.bin": cur[:, :, 12], "d.gath": cur[:, :, 8], "d.dec": cur[:, :, 9],
+                  "d.emit": cur[:, :, 10]})
 have_parts = mode == "grid"
 groups = [(f"level {l}", 4 * I) for l in range(L - 1, -1, -1)] + [("pixel", P * P * I)]
 i = 0
