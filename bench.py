@@ -5,15 +5,21 @@
 One step = one whole refinement (seed, every block and pixel sub-sweep, emit)
 of one batch of synthetic frames already resident in HBM.  Default workload:
 c2 = one 481x321 RGB Voronoi-mosaic frame, K=200, 4 block levels, I=4, 125
-bins, gamma=1 (BASELINE.json configs[1]).  A c2 frame does not shard, so N
-GPUs run N independent replicas ("scaling": "weak"); --config c3 runs the
-256-frame batch sharded by frame ("strong").
+bins, gamma=1 (BASELINE.json configs[1]).  The other configs:
+  c1  160x120 single frame (the oracle's small case)
+  c3  256 independent 481x321 frames, K=400 -- sharded by frame over ranks
+  c4  64 frames of 1920x1080 video, K=1000, L=5, gamma=0, as 8 clips of 8:
+      frame 0 of a clip cold, frames 1..7 warm-started from the previous
+      frame's labels (reading Q14/O9) -- clips sharded over ranks
+  c5  one 8192x8192 frame, K=20000, L=6 (-> 5), 512 bins
+A c2 (c1, c5) frame is not partitioned: N GPUs run N independent replicas
+("scaling": "weak").  c3 and c4 shard a fixed job ("strong").
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--mode auto|grid|graph|resident]
   python bench.py --impl reference ...   # the CPU oracle, timed as it stands
 
 L2: a 512 MiB buffer (> 126 MB L2) is rewritten between timed steps, outside
-the CUDA-event brackets of each step; the inputs themselves fit in L2.
+the CUDA-event brackets of each step.
 """
 from __future__ import annotations
 
@@ -33,6 +39,7 @@ from paper_1309_3848_b200 import configs  # noqa: E402
 
 METRIC = "Mpixels/s SEEDS refinement (481x321 frames/s, 200 SP); % of B200 HBM peak"
 UNIT = "Mpixels/s"
+MODE_NAMES = {1: "graph", 2: "resident", 3: "grid"}
 
 
 def peaks():
@@ -44,21 +51,27 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def algorithmic_bytes(info, C, nf, N):
-    """Per-launch algorithmic bytes of each kernel class (DESIGN.md section 6)."""
-    bb, P, L = info.bin_bytes, info.colour_period, info.levels_eff
-    return {
-        "seed": nf * N * (C + bb + (0 if L > 0 else 2)),   # image in, bins (+ labels) out
-        "block": nf * N * bb / 4.0,                         # bin plane once per 4 sub-sweeps
-        "pixel": nf * N * (2 + bb) / float(P * P),          # labels + bins once per P^2 sub-sweeps
-        "emit": nf * N * (2 + 4),                           # uint16 in, int32 out
-    }
-
-
-def frame_bytes(info, C, N, iters):
-    """Algorithmic bytes of one cold frame: N [C + bb + 4 + I L bb + I (2 + bb)]."""
+def frame_bytes(info, C, N, iters, warm=False):
+    """Algorithmic bytes of one frame: image in, bin plane out,
+    int32 labels out, per block iteration one pass over the bin plane, per
+    pixel iteration one pass over labels + bins.  Cold: N [C + bb + 4 + I L bb
+    + I (2 + bb)]; warm (no block levels, int32 labels in): N [C + bb + 8 + I (2 + bb)]."""
     bb, L = info.bin_bytes, info.levels_eff
+    if warm:
+        return N * (C + bb + 8 + iters * (2 + bb))
     return N * (C + bb + 4 + iters * L * bb + iters * (2 + bb))
+
+
+def algorithmic_bytes(info, C, nf, N, iters):
+    """Per-launch algorithmic bytes of each kernel class (DESIGN.md section 6)."""
+    bb, P = info.bin_bytes, info.colour_period
+    return {
+        "seed": nf * N * (C + bb + (0 if info.levels_eff > 0 else 2)),
+        "block": nf * N * bb / 4.0,
+        "pixel": nf * N * (2 + bb) / float(P * P),
+        "emit": nf * N * (2 + 4),
+        "frame": nf * frame_bytes(info, C, N, iters),
+    }
 
 
 class Clocks:
@@ -109,37 +122,109 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def workload(name, rank, world):
-    c = configs.CONFIGS[name]
+class Workload:
+    """The frames one rank refines per step, on the device and from the host."""
+
+    def __init__(self, name, rank, world):
+        import numpy as np
+        self.name = name
+        c = self.c = configs.CONFIGS[name]
+        self.p = configs.params(name)
+        self.W, self.H, self.C = c["W"], c["H"], c["C"]
+        self.N = self.W * self.H
+        if name == "c3":
+            per = c["frames"] // world
+            self.groups = [configs.frames(name)[rank * per:(rank + 1) * per]]
+            self.warm = [False]
+            self.scaling = "strong"
+            self.parallelism = f"frames/{world}"
+        elif name == "c4":
+            clips = configs.clips(name)
+            mine = clips[rank::world]  # clips round-robin to ranks
+            self.groups = [np.ascontiguousarray(mine[:, t]) for t in range(c["clip"])]
+            self.warm = [t > 0 for t in range(c["clip"])]
+            self.scaling = "strong"
+            self.parallelism = f"clips/{world}"
+        else:
+            self.groups = [configs.frames(name, n=1)]
+            self.warm = [False]
+            self.scaling = "weak"
+            self.parallelism = "replicas"
+        self.nf = self.groups[0].shape[0]
+        self.frames_per_step = self.nf * len(self.groups)
+
+    def describe(self, info):
+        c, p = self.c, self.p
+        extra = ""
+        if self.name == "c4":
+            extra = f", {len(self.groups)}-frame clips x {self.nf} per rank (frame 0 cold, 1..7 warm)"
+        return (f"{self.name}: {self.frames_per_step} x {self.W}x{self.H} RGB Voronoi mosaic per rank, "
+                f"K={p['n_superpixels']} (K_act={info.k_actual}), L={info.levels_eff}, "
+                f"I={p['iters_per_level']}, B={info.bins_total}, gamma={p['smoothness_prior']}{extra}")
+
+    def setup(self, torch):
+        self.d_in = [torch.from_numpy(g).cuda() for g in self.groups]
+        self.d_out = [torch.empty((self.nf, self.H, self.W), dtype=torch.int32, device="cuda")
+                      for _ in self.groups]
+        self.h_in = [torch.from_numpy(g).pin_memory() for g in self.groups]
+        self.h_out = [torch.empty((self.nf, self.H, self.W), dtype=torch.int32).pin_memory()
+                      for _ in self.groups]
+
+    def step(self, s, stream):
+        for i, d in enumerate(self.d_in):
+            init = self.d_out[i - 1] if self.warm[i] else None
+            s.batch(d, init_labels=init, labels_out=self.d_out[i], stream=stream)
+
+    def host_step(self, s, stream):
+        """Through the host-memory C-ABI entry point: copies in, runs, copies out."""
+        for i, h in enumerate(self.h_in):
+            init = self.h_out[i - 1].numpy() if self.warm[i] else None
+            s.batch_host(h.numpy(), self.h_out[i].numpy(), init_labels=init, stream=stream)
+
+    def h2d_bytes(self):
+        return sum(g.nbytes for g in self.groups) + sum(self.nf * self.N * 4 for w in self.warm if w)
+
+    def d2h_bytes(self):
+        return len(self.groups) * self.nf * self.N * 4
+
+    def algorithmic_bytes(self, info):
+        return sum(self.nf * frame_bytes(info, self.C, self.N, self.p["iters_per_level"], warm=w)
+                   for w in self.warm)
+
+
+def reference_sample(name):
+    """A bounded sample of config `name` for the CPU oracle: (frames, params, note)."""
+    import numpy as np
+    p = configs.params(name)
     if name == "c3":
-        per = c["frames"] // world
-        lo = rank * per
-        imgs = configs.frames(name)[lo:lo + per]
-        scaling = "strong"
-    else:
-        imgs = configs.frames(name, n=1)
-        scaling = "weak"
-    return c, imgs, scaling
+        return configs.frames(name, n=2), p, "2 frames of c3 (481x321, K=400)"
+    if name == "c4":
+        return configs.clips(name)[0, :1], p, "frame 0 of clip 0 of c4 (1920x1080, K=1000, cold)"
+    if name == "c5":
+        # a 1024x1024 crop with the same superpixel size and bins (K scaled by area)
+        f = configs.frames(name, n=1)[:, :1024, :1024]
+        q = dict(p)
+        q["n_superpixels"] = max(1, p["n_superpixels"] * 1024 * 1024 // (8192 * 8192))
+        return np.ascontiguousarray(f), q, "1024x1024 crop of c5, K scaled to 312 (same superpixel size, 512 bins)"
+    return configs.frames(name, n=1), p, f"1 frame of {name}"
 
 
 def cpu_baseline(name, budget_s=10.0):
     """The oracle as it stands (one thread, COL schedule) on a bounded sample."""
     import oracle
-    c = configs.CONFIGS[name]
-    p = configs.params(name)
-    imgs = configs.frames(name, n=1 if name != "c3" else 4)
+    imgs, p, note = reference_sample(name)
     oracle.build()
-    n, t0 = 0, time.perf_counter()
+    n, px, t0 = 0, 0, time.perf_counter()
     while True:
-        oracle.run(imgs[n % len(imgs)], **p)
+        img = imgs[n % len(imgs)]
+        oracle.run(img, **p)
         n += 1
+        px += img.shape[0] * img.shape[1]
         el = time.perf_counter() - t0
         if el >= budget_s or n >= 200:
             break
-    px = n * c["W"] * c["H"]
     return {"value": px / el / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n} {c['W']}x{c['H']} frames of {name}, single thread, COL schedule, "
-                      f"{el:.1f} s"}
+            "sample": f"{n} runs of {note}, single thread, COL schedule, {el:.1f} s"}
 
 
 def run_reference(args):
@@ -148,27 +233,26 @@ def run_reference(args):
         return 0
     import oracle
     name = args.config
-    c = configs.CONFIGS[name]
-    p = configs.params(name)
-    imgs = configs.frames(name, n=1 if name != "c3" else 2)
+    imgs, p, note = reference_sample(name)
     oracle.build()
     for i in range(args.warmup):
         oracle.run(imgs[i % len(imgs)], **p)
-    t = []
+    t, px = [], 0
     for i in range(args.steps):
+        img = imgs[i % len(imgs)]
         t0 = time.perf_counter()
-        oracle.run(imgs[i % len(imgs)], **p)
+        oracle.run(img, **p)
         t.append(time.perf_counter() - t0)
+        px += img.shape[0] * img.shape[1]
     tot = sum(t)
-    px = args.steps * c["W"] * c["H"]
     v = px / tot / 1e6
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "config": {"workload": f"{name}: {c['W']}x{c['H']} RGB mosaic, "
-                                                        f"1 frame/step, oracle COL schedule"},
+            "data": "synthetic",
+            "config": {"workload": f"{name}: {note} per step, oracle COL schedule"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} frames of {name}, one frame per step"},
+                             "sample": f"{args.steps} steps, each {note}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -179,7 +263,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="auto", choices=["auto", "graph", "resident", "grid"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -189,7 +273,6 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
     import torch
 
     rank = int(os.environ.get("RANK", "0"))
@@ -204,25 +287,21 @@ def main():
     from paper_1309_3848_b200.seeds import Seeds
 
     name = args.config
-    c, imgs, scaling = workload(name, rank, world)
-    nf, H, W, C = imgs.shape
-    N = H * W
-    p = configs.params(name)
-    s = Seeds(W, H, C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
+    wl = Workload(name, rank, world)
+    p = wl.p
+    s = Seeds(wl.W, wl.H, wl.C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
               p["smoothness_prior"], p["iters_per_level"])
     s.set_mode(args.mode)
     info = s.info
     stream = torch.cuda.current_stream()
-    d_img = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
-    d_out = torch.empty((nf, H, W), dtype=torch.int32, device="cuda")
+    wl.setup(torch)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
-    def step():
-        s.batch(d_img, labels_out=d_out, stream=stream)
-
-    for i in range(max(3, args.warmup)):
-        step()
+    for _ in range(max(3, args.warmup)):
+        wl.step(s, stream)
     torch.cuda.synchronize()
+    info = s.info
+    mode_name = MODE_NAMES.get(info.exec_mode, str(info.exec_mode))
 
     # ---- timed region: K steps, CUDA events on the launching stream -------
     clocks = Clocks(local)
@@ -235,63 +314,63 @@ def main():
     for i in range(args.steps):
         flush.fill_(i & 0xFF)  # evict L2 between steps (outside the events)
         ev[i][0].record(stream)
-        step()
+        wl.step(s, stream)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     clk = clocks.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    tot_ms = sum(step_ms)
+    tot_ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms_max = float(t.item())
-    px_all = nf * N * world * args.steps
+    px_all = wl.frames_per_step * wl.N * world * args.steps
     value = px_all / (tot_ms_max / 1e3) / 1e6
-    launches = info.kernels_per_run * args.steps
+    runs_per_step = len(wl.groups)
+    launches = info.kernels_per_run * runs_per_step * args.steps
 
     # ---- per-kernel timing pass (event pairs inside the graph) ------------
     s.profile(True)
     kp = min(args.steps, 20)
+    prof = None
     for i in range(kp):
         flush.fill_(i & 0xFF)
-        step()
+        wl.step(s, stream)
         prof = s.profile_collect(stream=stream)
     s.profile(False)
     torch.cuda.synchronize()
-    ab = algorithmic_bytes(info, C, nf, N)
-    ab["frame"] = frame_bytes(info, C, N, p["iters_per_level"]) * nf
+    ab = algorithmic_bytes(info, wl.C, wl.nf, wl.N, p["iters_per_level"])
+    ab["frame"] = wl.algorithmic_bytes(info) / runs_per_step  # per launch (a warm run has no block levels)
     kinds = {k: {"ms_total": v[0] / kp, "launches": v[1] // kp,
                  "avg_launch_us": 1e3 * v[0] / max(1, v[1]),
                  "gbps": (ab[k] / (v[0] / max(1, v[1]) / 1e3) / 1e9) if v[1] else None}
-             for k, v in prof.items()}
+             for k, v in prof.items() if v[1]}
     dom = max(kinds, key=lambda k: kinds[k]["ms_total"])
     hbm, hbm_src = peaks()
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(name, {}).get(dom)
+        traffic = tr.get(f"{name}/{mode_name}", {}).get(dom)
     except Exception:
         pass
     achieved = kinds[dom]["gbps"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm if achieved else None, "traffic": traffic,
                 "kernel": dom, "peak_source": hbm_src,
-                "algorithmic_bytes_per_launch": ab[dom]}
+                "algorithmic_bytes_per_launch": ab[dom],
+                "note": "latency-bound: one grid barrier per sub-sweep dominates a single frame"
+                        if wl.frames_per_step * wl.N < 4_000_000 else "per-launch algorithmic bytes / launch time"}
 
     # ---- end to end through the host-memory C-ABI entry point --------------
-    h_img = torch.from_numpy(np.ascontiguousarray(imgs)).pin_memory()
-    h_out = torch.empty((nf, H, W), dtype=torch.int32).pin_memory()
-    h_img_np, h_out_np = h_img.numpy(), h_out.numpy()
     for _ in range(3):
-        s.batch_host(h_img_np, h_out_np, stream=stream)
+        wl.host_step(s, stream)
     e2e_ms = 0.0
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        s.batch_host(h_img_np, h_out_np, stream=stream)
+        wl.host_step(s, stream)
         b.record(stream)
         b.synchronize()
         e2e_ms += a.elapsed_time(b)
@@ -299,29 +378,27 @@ def main():
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = px_all / (float(t.item()) / 1e3) / 1e6
-    assert (h_out == d_out.cpu()).all(), "host and device entry points disagree"
+    for h, d in zip(wl.h_out, wl.d_out):
+        assert torch.equal(h, d.cpu()), "host and device entry points disagree"
 
     if rank == 0:
-        fb = frame_bytes(info, C, N, p["iters_per_level"])
+        fb = wl.algorithmic_bytes(info)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms_max / args.steps, "higher_is_better": True,
-            "scaling": scaling, "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"{name}: {nf} x {W}x{H} RGB Voronoi mosaic per rank, "
-                                   f"K={p['n_superpixels']} (K_act={info.k_actual}), "
-                                   f"L={info.levels_eff}, I={p['iters_per_level']}, "
-                                   f"B={info.bins_total}, gamma={p['smoothness_prior']}",
-                       "frames_per_step_per_rank": nf,
-                       "exec_mode": {1: "graph", 2: "resident", 3: "grid"}[info.exec_mode],
-                       "cluster_size": info.cluster_size,
-                       "parallelism": "replicas" if scaling == "weak" else f"frames/{world}",
+            "scaling": wl.scaling, "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": wl.describe(info),
+                       "frames_per_step_per_rank": wl.frames_per_step,
+                       "exec_mode": mode_name,
+                       "grid_ctas": info.grid_ctas, "grid_tiles_per_frame": info.grid_tiles,
+                       "parallelism": wl.parallelism,
                        "l2": "512 MiB buffer rewritten between timed steps (outside events)"},
-            "frames_per_s": nf * world * args.steps / (tot_ms_max / 1e3),
-            "e2e_hbm_frac": (fb * nf * args.steps / (tot_ms_max / 1e3) / 1e9) / hbm,
+            "frames_per_s": wl.frames_per_step * world * args.steps / (tot_ms_max / 1e3),
+            "e2e_hbm_frac": (fb * args.steps / (tot_ms_max / 1e3) / 1e9) / hbm,
             "roofline": roofline,
             "kernels": kinds,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(nf * N * C),
-                    "d2h_bytes_per_step": int(nf * N * 4)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wl.h2d_bytes()),
+                    "d2h_bytes_per_step": int(wl.d2h_bytes())},
             "gpu_launches": launches,
             "clocks": clk,
         }

@@ -7,6 +7,10 @@ Readings Q4 (n_levels counts block levels), Q12 (I = 4 where unstated) and Q13
 """
 from __future__ import annotations
 
+import os
+
+import numpy as np
+
 from . import mosaic
 
 CONFIGS = {
@@ -29,11 +33,48 @@ def params(cfg: str) -> dict:
                 smoothness_prior=c["gamma"], iters_per_level=c["iters"])
 
 
+CACHE_DIR = os.environ.get("SEEDS_INPUT_CACHE", "/tmp/seeds_inputs")
+
+
 def frames(cfg: str, n: int | None = None):
-    """(n, H, W, C) uint8 frames of config ``cfg``."""
+    """(n, H, W, C) uint8 frames of config ``cfg``.  Large inputs are cached as
+    .npy under CACHE_DIR (a speed-up only: a missing or unreadable cache file
+    is regenerated from the seed)."""
+    c = CONFIGS[cfg]
+    n_ = c["frames"] if n is None else n
+    if c["W"] * c["H"] * n_ >= 4_000_000:
+        path = os.path.join(CACHE_DIR, f"{cfg}_{c['index']}_{n_}.npy")
+        try:
+            out = np.load(path)
+            if out.shape == (n_, c["H"], c["W"], c["C"]) and out.dtype == np.uint8:
+                return out
+        except Exception:
+            pass
+        out = _frames(cfg, n_)
+        try:
+            os.makedirs(CACHE_DIR, exist_ok=True)
+            tmp = f"{path}.{os.getpid()}.npy"
+            np.save(tmp, out)
+            os.replace(tmp, path)
+        except Exception:
+            pass
+        return out
+    return _frames(cfg, n_)
+
+
+def clips(cfg: str = "c4"):
+    """The video of ``cfg`` as (n_clips, clip_len, H, W, C): clip c is frames
+    [c * clip_len, (c + 1) * clip_len) (reading Q14: clips of 8 frames; frame 0
+    of a clip starts cold, the others from the previous frame's labels)."""
+    c = CONFIGS[cfg]
+    f = frames(cfg)
+    L = c["clip"]
+    return f.reshape(c["frames"] // L, L, c["H"], c["W"], c["C"])
+
+
+def _frames(cfg: str, n: int):
     c = CONFIGS[cfg]
     seed = 1000 * c["index"]
-    n = c["frames"] if n is None else n
     if cfg == "c3":
         return mosaic.mosaic_batch(n, c["W"], c["H"], c["R"][0], c["R"][1], c["sigma"][0],
                                    c["sigma"][1], seed=seed, grad=c["grad"], C=c["C"])
@@ -41,7 +82,6 @@ def frames(cfg: str, n: int | None = None):
         f, _ = mosaic.moving_mosaic(n, c["W"], c["H"], c["R"], c["sigma"], seed=seed,
                                     grad=c["grad"], C=c["C"])
         return f
-    import numpy as np
     out = np.empty((n, c["H"], c["W"], c["C"]), np.uint8)
     for i in range(n):
         out[i] = mosaic.mosaic(c["W"], c["H"], c["R"], c["sigma"], seed=seed + i, C=c["C"],

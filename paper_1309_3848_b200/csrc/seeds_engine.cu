@@ -67,8 +67,15 @@ struct seeds_ctx {
     int32_t *d_init_stage = nullptr, *d_out_stage = nullptr;
     // graph
     cudaStream_t cap_stream = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    GraphKey key;
+    // instantiated runs, keyed by their pointers / sizes (least recently used dropped)
+    struct GraphEntry {
+        GraphKey key;
+        cudaGraphExec_t exec;
+        int done;  // sub-sweeps the run performs (data independent)
+        unsigned long long used;
+    };
+    std::vector<GraphEntry> graphs;
+    unsigned long long tick = 0;
     // state of the last run
     int limit = -1;
     int last_nf = 0;
@@ -249,15 +256,17 @@ static void build_removable(uint32_t lut[8])
     }
 }
 
+static void drop_graphs(seeds_ctx *c)
+{
+    for (auto &g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+}
+
 static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
 {
     if (nf <= ctx->cap_frames) return SEEDS_OK;
     CK(cudaDeviceSynchronize());
-    if (ctx->exec) {  // the cached graph points at the buffers freed below
-        cudaGraphExecDestroy(ctx->exec);
-        ctx->exec = nullptr;
-        ctx->key = GraphKey();
-    }
+    drop_graphs(ctx);  // the cached graphs point at the buffers freed below
     auto release = [](void *&p) {
         if (p) cudaFree(p);
         p = nullptr;
@@ -576,6 +585,8 @@ static bool plan_grid(seeds_ctx *c, int nf)
 {
     if (c->cap_frames < nf && ensure_frames(c, nf) != SEEDS_OK) return false;  // the TMA maps need the planes
     if (c->grid_nf == nf) return c->grid_ok;
+    cudaDeviceSynchronize();  // a running launch may still read the old plan's tiles / records
+    drop_graphs(c);           // graphs captured with the old plan read its tiles / records
     c->grid_nf = nf;
     c->grid_ok = false;
     if (c->W > 32000 || c->H > 32000) return false;
@@ -1072,10 +1083,21 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     GraphKey key;
     key.img = img; key.init = init; key.out = out; key.nf = nf; key.limit = ctx->limit; key.prof = ctx->prof;
     key.mode = mode;
-    if (!ctx->exec || !(key == ctx->key)) {
-        if (ctx->exec) {
-            cudaGraphExecDestroy(ctx->exec);
-            ctx->exec = nullptr;
+    seeds_ctx::GraphEntry *hit = nullptr;
+    for (auto &g : ctx->graphs)
+        if (g.key == key) hit = &g;
+    if (hit && ctx->prof) {  // profiled runs re-capture (the event pairs are per capture)
+        cudaGraphExecDestroy(hit->exec);
+        ctx->graphs.erase(ctx->graphs.begin() + (hit - ctx->graphs.data()));
+        hit = nullptr;
+    }
+    if (!hit) {
+        if (ctx->graphs.size() >= 16) {
+            size_t lru = 0;
+            for (size_t i = 1; i < ctx->graphs.size(); i++)
+                if (ctx->graphs[i].used < ctx->graphs[lru].used) lru = i;
+            cudaGraphExecDestroy(ctx->graphs[lru].exec);
+            ctx->graphs.erase(ctx->graphs.begin() + lru);
         }
         CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
         seeds_status er = mode == SEEDS_MODE_GRID ? enqueue_grid(ctx, img, init, out, nf, ctx->cap_stream)
@@ -1088,12 +1110,17 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
             return er;
         }
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
-        e = cudaGraphInstantiate(&ctx->exec, graph, 0);
+        cudaGraphExec_t exec = nullptr;
+        e = cudaGraphInstantiate(&exec, graph, 0);
         cudaGraphDestroy(graph);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
-        ctx->key = key;
+        ctx->graphs.push_back({key, exec, ctx->last_done, 0});
+        hit = &ctx->graphs.back();
     }
-    CK(cudaGraphLaunch(ctx->exec, st));
+    hit->used = ++ctx->tick;
+    ctx->last_done = hit->done;
+    ctx->last_final = hit->done & 1;
+    CK(cudaGraphLaunch(hit->exec, st));
     ctx->last_nf = nf;
     ctx->ran = true;
     return SEEDS_OK;
@@ -1334,7 +1361,7 @@ void seeds_destroy(seeds_ctx *ctx)
 {
     if (!ctx) return;
     cudaDeviceSynchronize();
-    if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
+    drop_graphs(ctx);
     void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1],
                     ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band, ctx->d_kmap,
