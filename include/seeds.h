@@ -153,7 +153,7 @@ seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps);
  * stamps of every sub-sweep (slot 0 work finished, 1 barrier passed; grid mode
  * also 2 replayed, 3 staged, 4 filtered, 5 decided; 8.. detail builds), copy
  * them to host_out[min(cap, ctas*(subsweeps+4)*16)] (int64, layout [cta][phase][16],
- * ctas = max(#SM, cluster_size)), or disable (0) and free the buffer.
+ * ctas = max(4 #SM, cluster_size)), or disable (0) and free the buffer.
  * Synchronises the device when host_out is given.  Diagnostic; not part of
  * the hot path. */
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap);

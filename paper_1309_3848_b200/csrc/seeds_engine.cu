@@ -115,6 +115,7 @@ struct seeds_ctx {
     int grid_nf = -1;      // batch size the plan is for
     bool grid_ok = false;
     int grid_G = 0;
+    int grid_nt = 512;     // threads per CTA of the plan
     size_t grid_smem = 0;
     GridParams gp{};
     int n_sm = 148;
@@ -501,26 +502,34 @@ static int resolved_mode(seeds_ctx *c, int nf)
 // they fit (else of one tile, restaged every sub-sweep), the unit queue, the
 // warp tables of the large-block path and the block geometry.
 // ---------------------------------------------------------------------------
-template <typename BinT, int GAMMA, int P>
+template <typename BinT, int GAMMA, int P, int NT>
 static int grid_occupancy(size_t smem)
 {
-    auto k = k_grid<BinT, GAMMA, P>;
+    auto k = k_grid<BinT, GAMMA, P, NT>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, GRID_THREADS, smem) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     return n;
 }
 
-static int grid_occupancy_for(const seeds_ctx *c, size_t smem)
+template <int NT>
+static int grid_occupancy_nt(const seeds_ctx *c, size_t smem)
 {
-    if (c->bb == 1) return c->gamma ? grid_occupancy<uint8_t, 1, 3>(smem) : grid_occupancy<uint8_t, 0, 2>(smem);
-    return c->gamma ? grid_occupancy<uint16_t, 1, 3>(smem) : grid_occupancy<uint16_t, 0, 2>(smem);
+    if (c->bb == 1)
+        return c->gamma ? grid_occupancy<uint8_t, 1, 3, NT>(smem) : grid_occupancy<uint8_t, 0, 2, NT>(smem);
+    return c->gamma ? grid_occupancy<uint16_t, 1, 3, NT>(smem) : grid_occupancy<uint16_t, 0, 2, NT>(smem);
+}
+
+static int grid_occupancy_for(const seeds_ctx *c, size_t smem, int nt)
+{
+    return nt == GRID_THREADS ? grid_occupancy_nt<GRID_THREADS>(c, smem)
+                              : grid_occupancy_nt<GRID_THREADS_SMALL>(c, smem);
 }
 
 static std::vector<int> size_candidates(int n)
@@ -581,6 +590,11 @@ static bool encode_tmaps(seeds_ctx *c, GridParams &q)
     return true;
 }
 
+static bool plan_try(seeds_ctx *c, int nf, int nt);
+
+// Plan for nf frames: one 512-thread CTA per SM, unless that leaves CTAs with
+// several tiles -- then four 128-thread CTAs per SM (each with its own tiles
+// and TMA pipeline) when such a plan fits.
 static bool plan_grid(seeds_ctx *c, int nf)
 {
     if (c->cap_frames < nf && ensure_frames(c, nf) != SEEDS_OK) return false;  // the TMA maps need the planes
@@ -590,6 +604,16 @@ static bool plan_grid(seeds_ctx *c, int nf)
     c->grid_nf = nf;
     c->grid_ok = false;
     if (c->W > 32000 || c->H > 32000) return false;
+    const char *v = getenv("SEEDS_GRID_NT");
+    const int force = v ? atoi(v) : 0;
+    if (force == GRID_THREADS || force == GRID_THREADS_SMALL) return c->grid_ok = plan_try(c, nf, force);
+    if (!plan_try(c, nf, GRID_THREADS)) return false;
+    if (c->gp.tiles_per_cta >= 2 && !plan_try(c, nf, GRID_THREADS_SMALL)) plan_try(c, nf, GRID_THREADS);
+    return c->grid_ok = true;
+}
+
+static bool plan_try(seeds_ctx *c, int nf, int nt)
+{
     const int Lm = c->L > 0 ? c->L - 1 : 0;
     const int TX = c->L > 0 ? c->GX >> Lm : c->W, TY = c->L > 0 ? c->GY >> Lm : c->H;
     auto ux = [&](int i) { return c->L > 0 ? c->colstart[(size_t)i << Lm] : i; };
@@ -597,11 +621,12 @@ static bool plan_grid(seeds_ctx *c, int nf)
     int muw = 0, muh = 0;
     for (int i = 0; i < TX; i++) muw = std::max(muw, ux(i + 1) - ux(i));
     for (int j = 0; j < TY; j++) muh = std::max(muh, uy(j + 1) - uy(j));
-    const size_t limit = 227 * 1024;
+    const int cps = GRID_THREADS / nt;  // CTAs per SM
+    const size_t limit = cps == 1 ? 227 * 1024 : (228 * 1024) / cps - 1024;
     const size_t tabw = (2 * (size_t)c->B + 2) * 4;
     bool need_tab = false;
     GridParams &q = c->gp;
-    int nsm = c->n_sm;  // SEEDS_GRID_CTAS caps the CTAs (experiments)
+    int nsm = c->n_sm * cps;  // SEEDS_GRID_CTAS caps the CTAs (experiments)
     if (const char *v = getenv("SEEDS_GRID_CTAS")) nsm = std::max(1, std::min(nsm, atoi(v)));
     q = GridParams{};
     for (int l = 0; l < c->L; l++) {
@@ -612,7 +637,7 @@ static bool plan_grid(seeds_ctx *c, int nf)
         q.gshift[l] = gs;
         need_tab = need_tab || q.bkind[l] == BK_WARP;
     }
-    const size_t fixed = 128 + 16 + align16((size_t)(c->GX + c->GY + 2) * 4) + (need_tab ? tabw : 0);
+    const size_t fixed = 128 + 16 + (need_tab ? tabw : 0);
     double best = 1e300;
     int ba = 0, bb_ = 0;
     for (int a : size_candidates(TX))
@@ -712,7 +737,6 @@ static bool plan_grid(seeds_ctx *c, int nf)
         q.o_misc = (unsigned)off;  off = align16(off + 128);
         q.o_mbar = (unsigned)off;  off = align16(off + 16);
         q.o_tiles = (unsigned)off; off = align16(off + (size_t)q.tiles_per_cta * sizeof(GridTile));
-        q.o_geo = (unsigned)off;   off = align16(off + (size_t)(c->GX + c->GY + 2) * 4);
         // histogram cache (single-tile CTAs): A, slot table, row list, rows
         q.cache = 0;
         q.hc_rows = 0;
@@ -733,16 +757,18 @@ static bool plan_grid(seeds_ctx *c, int nf)
         }
         q.o_tab = (unsigned)off;
         if (off + (need_tab ? tabw : 0) > limit) continue;
-        q.ntab = need_tab ? (int)std::min<size_t>(GRID_THREADS / 32, (limit - off) / tabw) : 0;
+        q.ntab = need_tab ? (int)std::min<size_t>(nt / 32, (limit - off) / tabw) : 0;
         const size_t smem = off + q.ntab * tabw;
-        const int occ = grid_occupancy_for(c, smem);
-        if (occ < 1) continue;
+        const int occ = grid_occupancy_for(c, smem, nt);
+        if (occ < cps) continue;
         q.bins_res = res;
         q.rec_smem = rs;
         q.tx_bytes = q.bw * q.bh * 2 + (res ? 0 : q.bbw * (q.bh - 4) * c->bb);
         q.q_cap = (int)qcap + 32;
         q.GX = c->GX;
         q.GY = c->GY;
+        q.invGX = 1.0f / (float)c->GX;
+        q.invGY = 1.0f / (float)c->GY;
         q.rec_cap = rec_cap;
         q.ntiles = (int)T;
         // device buffers: tiles, records
@@ -793,13 +819,13 @@ static bool plan_grid(seeds_ctx *c, int nf)
         if (!encode_tmaps(c, q)) return false;
         c->grid_G = G;
         c->grid_smem = smem;
-        c->grid_ok = true;
+        c->grid_nt = nt;
         return true;
     }
     return false;
 }
 
-template <typename BinT, int GAMMA, int P>
+template <typename BinT, int GAMMA, int P, int NT>
 static cudaError_t launch_grid_t(seeds_ctx *ctx, const GridParams &q, cudaStream_t st)
 {
     cudaLaunchConfig_t cfg = {};
@@ -807,12 +833,12 @@ static cudaError_t launch_grid_t(seeds_ctx *ctx, const GridParams &q, cudaStream
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.gridDim = dim3(ctx->grid_G);
-    cfg.blockDim = dim3(GRID_THREADS);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = ctx->grid_smem;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_grid<BinT, GAMMA, P>, q);
+    return cudaLaunchKernelEx(&cfg, k_grid<BinT, GAMMA, P, NT>, q);
 }
 
 // Enqueue one grid-mode run: zero the histograms, move counters and the barrier
@@ -844,10 +870,16 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     ctx->ev_used = 0;
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
     cudaError_t e;
-    if (ctx->bb == 1)
-        e = ctx->gamma ? launch_grid_t<uint8_t, 1, 3>(ctx, q, st) : launch_grid_t<uint8_t, 0, 2>(ctx, q, st);
+    if (ctx->grid_nt == GRID_THREADS)
+        e = ctx->bb == 1 ? (ctx->gamma ? launch_grid_t<uint8_t, 1, 3, GRID_THREADS>(ctx, q, st)
+                                       : launch_grid_t<uint8_t, 0, 2, GRID_THREADS>(ctx, q, st))
+                         : (ctx->gamma ? launch_grid_t<uint16_t, 1, 3, GRID_THREADS>(ctx, q, st)
+                                       : launch_grid_t<uint16_t, 0, 2, GRID_THREADS>(ctx, q, st));
     else
-        e = ctx->gamma ? launch_grid_t<uint16_t, 1, 3>(ctx, q, st) : launch_grid_t<uint16_t, 0, 2>(ctx, q, st);
+        e = ctx->bb == 1 ? (ctx->gamma ? launch_grid_t<uint8_t, 1, 3, GRID_THREADS_SMALL>(ctx, q, st)
+                                       : launch_grid_t<uint8_t, 0, 2, GRID_THREADS_SMALL>(ctx, q, st))
+                         : (ctx->gamma ? launch_grid_t<uint16_t, 1, 3, GRID_THREADS_SMALL>(ctx, q, st)
+                                       : launch_grid_t<uint16_t, 0, 2, GRID_THREADS_SMALL>(ctx, q, st));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid launch");
     CK(prof_end(ctx, st));
     const bool blocks = init == nullptr && ctx->L > 0;
@@ -1326,7 +1358,7 @@ seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap)
 {
     if (!ctx) return SEEDS_EINVAL;
-    const size_t n = (size_t)std::max(ctx->n_sm, ctx->cluster) * (ctx->S + 4) * 16;
+    const size_t n = (size_t)std::max(4 * ctx->n_sm, ctx->cluster) * (ctx->S + 4) * 16;
     if (enable && !ctx->d_trace) {
         CK(cudaMalloc(&ctx->d_trace, n * sizeof(long long)));
         CK(cudaMemset(ctx->d_trace, 0, n * sizeof(long long)));

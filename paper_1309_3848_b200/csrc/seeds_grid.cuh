@@ -31,7 +31,12 @@
 
 namespace seeds {
 
+// Threads per CTA: 512 (one CTA per SM; plans whose CTAs own one tile, where
+// the run is latency-bound) or 128 (four CTAs per SM; plans whose CTAs own
+// several tiles, so that four independent tile pipelines hide each other's
+// latencies).
 constexpr int GRID_THREADS = 512;
+constexpr int GRID_THREADS_SMALL = 128;
 
 struct GridTile {
     int f;               // frame
@@ -78,6 +83,7 @@ struct GridParams {
     int tx_bytes;                 // bytes one tile's TMA loads deliver (label box + bin box)
     int bw, bbw, bh;              // TMA boxes: label box bw x bh, bin box bbw x (bh - 4)
     int tiles_per_cta, q_cap, ntab, GX, GY, bins_res, rec_smem;
+    float invGX, invGY;
     // histogram cache (CTAs with a single tile): A of the frame and the H rows of
     // the superpixels present in the tile + halo, loaded right after each barrier
     int cache;             // 1: enabled
@@ -176,7 +182,6 @@ struct GridCta {
     uint32_t *tabs;    // ntab warp tables of 2B + 2 words
     int *misc;         // [0], [1]: record counts of the two lists, [2]: queue length, [3]: cached rows,
                        // [4..7]: detail timing; the ring LUT follows at +64 bytes
-    int *cs, *rs;      // level-0 block column / row starts (GX + 1, GY + 1)
     // current tile
     int f, X0, X1, Y0, Y1, sp, tbp;
     int sx0, bx0;      // first staged column: labels (padded plane) and bins, 16-byte aligned for the TMA
@@ -201,8 +206,6 @@ struct GridCta {
         queue = reinterpret_cast<uint32_t *>(smem + q.o_queue);
         tabs = reinterpret_cast<uint32_t *>(smem + q.o_tab);
         misc = reinterpret_cast<int *>(smem + q.o_misc);
-        cs = reinterpret_cast<int *>(smem + q.o_geo);
-        rs = cs + q.GX + 1;
     }
     __device__ __forceinline__ void select(const GridTile &t, int slot)
     {
@@ -231,6 +234,9 @@ struct GridCta {
         return stage + (y - Y0 + 2) * sp + (x + 2 - sx0);
     }
     __device__ __forceinline__ int bin(int x, int y) const { return tb[(y - Y0) * tbp + (x - bx0)]; }
+    // level-0 block column / row starts: colstart[i] = floor(i W / GX) (reading O2)
+    __device__ __forceinline__ int colx(int i) const { return div_small(i * q.W, q.GX, q.invGX); }
+    __device__ __forceinline__ int rowy(int j) const { return div_small(j * q.H, q.GY, q.invGY); }
     __device__ __forceinline__ bool removable_s(int m) const { return (rem[m >> 5] >> (m & 31)) & 1u; }
     // TMA: stage tile t into buffer `slot` (thread 0 only)
     __device__ __forceinline__ void issue(const GridTile &t, int slot) const
@@ -335,13 +341,13 @@ __device__ __forceinline__ int block_t4(const Ctx &c, int ob, int k, const Neigh
     return acc;
 }
 
-template <typename BinT, int GAMMA, int P>
-__global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant__ GridParams qp)
+template <typename BinT, int GAMMA, int P, int NT>
+__global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_constant__ GridParams qp)
 {
     extern __shared__ __align__(128) uint32_t smem[];
     const GridParams &q = qp;
     GridCta<BinT> c(q, reinterpret_cast<unsigned char *>(smem), &qp.tm_lab, &qp.tm_bins);
-    constexpr int NT = GRID_THREADS, NW = NT / 32;
+    constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int W = q.W, B = q.B;
     const int TW = 2 * B + 2;  // warp table words
@@ -352,8 +358,6 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
     auto rec_list = [&](int b) { return b ? rec1 : rec0; };
 
     for (int i = tid; i < q.ntab * TW; i += NT) c.tabs[i] = 0;
-    for (int i = tid; i <= q.GX; i += NT) c.cs[i] = q.colstart[i];
-    for (int i = tid; i <= q.GY; i += NT) c.rs[i] = q.rowstart[i];
     if (tid < 4) c.misc[tid] = 0;
     if (tid < 8) c.rem[tid] = c_removable[tid];
     const int ntl = blockIdx.x < q.ntiles ? (q.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // tiles of this CTA
@@ -543,8 +547,8 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(const __grid_constant_
                             const int tj = div_small(u, uw, inv_uw);
                             bi = ifirst + 2 * (u - tj * uw);
                             bj = jfirst + 2 * tj;
-                            xa = c.cs[bi << l]; xb = c.cs[(bi + 1) << l];
-                            ya = c.rs[bj << l]; yb = c.rs[(bj + 1) << l];
+                            xa = c.colx(bi << l); xb = c.colx((bi + 1) << l);
+                            ya = c.rowy(bj << l); yb = c.rowy((bj + 1) << l);
                         };
                         // lanes per unit of the decision pass; survivors of the
                         // boundary + ring test go through a queue only when the

@@ -233,7 +233,7 @@ class Seeds:
         if n_sm is None:
             import torch
             n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-        cs = max(n_sm, self.info.cluster_size)
+        cs = max(4 * n_sm, self.info.cluster_size)
         n = cs * (self.info.subsweeps + 4) * 16
         out = np.zeros(n, np.int64)
         self._check(self._lib.seeds_debug_trace(self._ctx, int(enable), out.ctypes.data if enable else None, n))
