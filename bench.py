@@ -12,8 +12,11 @@ bins, gamma=1 (BASELINE.json configs[1]).  The other configs:
       frame 0 of a clip cold, frames 1..7 warm-started from the previous
       frame's labels (reading Q14/O9) -- clips sharded over ranks
   c5  one 8192x8192 frame, K=20000, L=6 (-> 5), 512 bins
-A c2 (c1, c5) frame is not partitioned: N GPUs run N independent replicas
-("scaling": "weak").  c3 and c4 shard a fixed job ("strong").
+A c2 (c1) frame is not partitioned: N GPUs run N independent replicas
+("scaling": "weak").  c3 and c4 shard a fixed job ("strong"); c5 at N > 1 (or
+with --bands) is refined as N row bands, one per rank, exchanging sparse
+histogram-delta records (all-gather) and two-row label halos (send/recv) over
+torch.distributed after every sub-sweep ("strong", include/seeds.h row-band mode).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--mode auto|grid|graph|resident]
   python bench.py --impl reference ...   # the CPU oracle, timed as it stands
@@ -122,6 +125,71 @@ class Clocks:
                 "samples": len(sm)}
 
 
+class BandWorkload:
+    """c5 as row bands: this rank refines band `rank` of `world` of the frame."""
+
+    def __init__(self, name, rank, world):
+        self.name = name
+        c = self.c = configs.CONFIGS[name]
+        self.p = configs.params(name)
+        self.W, self.H, self.C = c["W"], c["H"], c["C"]
+        self.N = self.W * self.H
+        self.img = configs.frames(name, n=1)[0]
+        self.rank, self.world = rank, world
+        self.frames_per_step = 1
+        self.scaling = "strong"
+        self.parallelism = f"row bands/{world}"
+        self.nf = 1
+        self.groups = [None]  # one run per step
+
+    def make_context(self):
+        from paper_1309_3848_b200.seeds import SeedsBand
+        p = self.p
+        return SeedsBand(self.W, self.H, self.C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
+                         p["smoothness_prior"], p["iters_per_level"], self.rank, self.world)
+
+    def describe(self, info):
+        p = self.p
+        return (f"{self.name}: one {self.W}x{self.H} RGB Voronoi mosaic as {self.world} row bands (this rank: rows "
+                f"{self.s.row0}..{self.s.row1}), K={p['n_superpixels']} (K_act={info.k_actual}), "
+                f"L={info.levels_eff}, I={p['iters_per_level']}, B={info.bins_total}, gamma={p['smoothness_prior']}")
+
+    def setup(self, torch, s):
+        from paper_1309_3848_b200.bands import DistExchange
+        self.s = s
+        self.ex = DistExchange()
+        self.d_in = torch.from_numpy(self.img).cuda()
+        self.d_out = torch.zeros((self.H, self.W), dtype=torch.int32, device="cuda")
+        self.h_in = torch.from_numpy(self.img).pin_memory()
+        self.h_out = torch.zeros((self.H, self.W), dtype=torch.int32).pin_memory()
+        self.d_tmp_in = torch.empty_like(self.d_in)
+        self.d_tmp_out = torch.zeros_like(self.d_out)
+
+    def step(self, s, stream):
+        from paper_1309_3848_b200 import bands
+        bands.dist_run(s, self.d_in, self.d_out, exchange=self.ex, stream=stream)
+
+    def host_step(self, s, stream):
+        from paper_1309_3848_b200 import bands
+        self.d_tmp_in.copy_(self.h_in, non_blocking=True)
+        bands.dist_run(s, self.d_tmp_in, self.d_tmp_out, exchange=self.ex, stream=stream)
+        self.h_out[s.row0:s.row1].copy_(self.d_tmp_out[s.row0:s.row1], non_blocking=True)
+        stream.synchronize()
+
+    def check(self, torch):
+        s = self.s
+        assert torch.equal(self.h_out[s.row0:s.row1], self.d_out[s.row0:s.row1].cpu())
+
+    def h2d_bytes(self):
+        return self.img.nbytes
+
+    def d2h_bytes(self):
+        return (self.s.row1 - self.s.row0) * self.W * 4
+
+    def algorithmic_bytes(self, info):
+        return frame_bytes(info, self.C, self.N, self.p["iters_per_level"]) * (self.s.row1 - self.s.row0) / self.H
+
+
 class Workload:
     """The frames one rank refines per step, on the device and from the host."""
 
@@ -162,7 +230,17 @@ class Workload:
                 f"K={p['n_superpixels']} (K_act={info.k_actual}), L={info.levels_eff}, "
                 f"I={p['iters_per_level']}, B={info.bins_total}, gamma={p['smoothness_prior']}{extra}")
 
-    def setup(self, torch):
+    def make_context(self):
+        from paper_1309_3848_b200.seeds import Seeds
+        p = self.p
+        return Seeds(self.W, self.H, self.C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
+                     p["smoothness_prior"], p["iters_per_level"])
+
+    def check(self, torch):
+        for h, d in zip(self.h_out, self.d_out):
+            assert torch.equal(h, d.cpu()), "host and device entry points disagree"
+
+    def setup(self, torch, s=None):
         self.d_in = [torch.from_numpy(g).cuda() for g in self.groups]
         self.d_out = [torch.empty((self.nf, self.H, self.W), dtype=torch.int32, device="cuda")
                       for _ in self.groups]
@@ -269,6 +347,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--bands", action="store_true", help="c5: row-band mode even on one rank")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -287,21 +366,27 @@ def main():
     from paper_1309_3848_b200.seeds import Seeds
 
     name = args.config
-    wl = Workload(name, rank, world)
+    banded = name == "c5" and (world > 1 or args.bands)
+    if banded and not dist:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+    wl = BandWorkload(name, rank, world) if banded else Workload(name, rank, world)
     p = wl.p
-    s = Seeds(wl.W, wl.H, wl.C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
-              p["smoothness_prior"], p["iters_per_level"])
-    s.set_mode(args.mode)
+    s = wl.make_context()
+    if not banded:
+        s.set_mode(args.mode)
     info = s.info
     stream = torch.cuda.current_stream()
-    wl.setup(torch)
+    wl.setup(torch, s)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     for _ in range(max(3, args.warmup)):
         wl.step(s, stream)
     torch.cuda.synchronize()
     info = s.info
-    mode_name = MODE_NAMES.get(info.exec_mode, str(info.exec_mode))
+    mode_name = "grid-bands" if banded else MODE_NAMES.get(info.exec_mode, str(info.exec_mode))
 
     # ---- timed region: K steps, CUDA events on the launching stream -------
     clocks = Clocks(local)
@@ -325,20 +410,26 @@ def main():
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms_max = float(t.item())
-    px_all = wl.frames_per_step * wl.N * world * args.steps
+    # pixels refined by the whole job per step: a banded c5 frame is one frame over all ranks
+    px_all = (wl.N if banded else wl.frames_per_step * wl.N * world) * args.steps
     value = px_all / (tot_ms_max / 1e3) / 1e6
     runs_per_step = len(wl.groups)
     launches = info.kernels_per_run * runs_per_step * args.steps
+    if banded:  # seed + per sub-sweep (apply records + grid launch) + emit
+        launches = (2 + 2 * s.subsweeps) * args.steps
 
     # ---- per-kernel timing pass (event pairs inside the graph) ------------
-    s.profile(True)
     kp = min(args.steps, 20)
-    prof = None
-    for i in range(kp):
-        flush.fill_(i & 0xFF)
-        wl.step(s, stream)
-        prof = s.profile_collect(stream=stream)
-    s.profile(False)
+    if banded:  # one grid launch per sub-sweep; the whole step is the unit
+        prof = {"frame": (tot_ms_max / args.steps * kp, kp)}
+    else:
+        s.profile(True)
+        prof = None
+        for i in range(kp):
+            flush.fill_(i & 0xFF)
+            wl.step(s, stream)
+            prof = s.profile_collect(stream=stream)
+        s.profile(False)
     torch.cuda.synchronize()
     ab = algorithmic_bytes(info, wl.C, wl.nf, wl.N, p["iters_per_level"])
     ab["frame"] = wl.algorithmic_bytes(info) / runs_per_step  # per launch (a warm run has no block levels)
@@ -378,8 +469,7 @@ def main():
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = px_all / (float(t.item()) / 1e3) / 1e6
-    for h, d in zip(wl.h_out, wl.d_out):
-        assert torch.equal(h, d.cpu()), "host and device entry points disagree"
+    wl.check(torch)
 
     if rank == 0:
         fb = wl.algorithmic_bytes(info)
@@ -392,6 +482,7 @@ def main():
                        "exec_mode": mode_name,
                        "grid_ctas": info.grid_ctas, "grid_tiles_per_frame": info.grid_tiles,
                        "parallelism": wl.parallelism,
+                       "exchange": "NCCL all-gather of delta records + halo send/recv per sub-sweep" if banded else None,
                        "l2": "512 MiB buffer rewritten between timed steps (outside events)"},
             "frames_per_s": wl.frames_per_step * world * args.steps / (tot_ms_max / 1e3),
             "e2e_hbm_frac": (fb * args.steps / (tot_ms_max / 1e3) / 1e9) / hbm,

@@ -52,7 +52,7 @@ typedef enum {
     SEEDS_EINVAL = -1, /* an argument is out of its documented range */
     SEEDS_ENOMEM = -2, /* a device or pinned-host allocation failed */
     SEEDS_ECUDA = -3,  /* a CUDA runtime error; seeds_last_error() has the text */
-    SEEDS_ENCCL = -4,  /* reserved for the row-band multi-GPU mode */
+    SEEDS_ENCCL = -4,  /* reserved (the row-band exchange is done by the caller) */
     SEEDS_ESTATE = -5, /* call out of order (e.g. read_state before any run) */
     SEEDS_ERANGE = -6  /* the problem exceeds an integer width (see seeds_create) */
 } seeds_status;
@@ -204,6 +204,72 @@ seeds_status seeds_profile(seeds_ctx *ctx, int enable);
  * total milliseconds and launches_out[SEEDS_KIND_COUNT] launch counts (host
  * pointers, either may be NULL).  Call once after every profiled run. */
 seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out, long long *launches_out);
+
+/* ---------------------------------------------------------------------------
+ * Row-band mode: one very large frame refined by n_bands cooperating contexts
+ * (one per GPU / rank), BASELINE.json configs[4] and SURVEY.md section 8(e).
+ * Band b owns the pixel rows of superpixel rows [b*ny/n, (b+1)*ny/n) (whole
+ * superpixel rows, so every block of every level lies in one band).  Every
+ * band keeps a full replica of the histograms and the full label plane, but
+ * decides only its own rows.  The caller drives the schedule:
+ *
+ *   seeds_band_seed(ctx, image, init)            every rank, the whole frame
+ *   for s in 0 .. subsweeps-1:
+ *     seeds_band_subsweep(ctx, s, all_records_of_s-1, n, my_records, my_n)
+ *     exchange: all-gather the records (the concatenation of every band's
+ *       records, in any order); send seeds_band_halo(get) top rows to band
+ *       b-1 and bottom rows to band b+1, seeds_band_halo(put) what arrives
+ *   seeds_band_finish(ctx, all_records_of_last, n, labels_out)  this band's rows
+ *
+ * The records are the sparse histogram deltas of a sub-sweep (opaque,
+ * record_bytes each); applying every band's records keeps every replica equal
+ * to the one-GPU state, so any n_bands gives bit-identical results
+ * (tests/test_bands.py).  Sub-sweep s of the snapshot schedule (reading O7)
+ * reads the histograms after sub-sweep s-1 and the labels within 2 rows of
+ * the band, which is what the exchange provides.
+ * ------------------------------------------------------------------------- */
+
+/* seeds_create_banded -- as seeds_create, plus band (0 <= band < n_bands) and
+ * n_bands (1 .. ny, the superpixel rows).  SEEDS_EINVAL also for a band of
+ * fewer than 2 pixel rows; SEEDS_ERANGE if no grid-mode tile plan fits. */
+seeds_status seeds_create_banded(int width, int height, int channels, int n_superpixels, int n_levels,
+                                 int bins_per_channel, int smoothness_prior, int iters_per_level, int band,
+                                 int n_bands, seeds_ctx **out);
+
+/* seeds_band_info -- the band's pixel rows [*row0, *row1), the most records one
+ * sub-sweep of the band can emit (*record_capacity) and their size in bytes.
+ * Any pointer may be NULL. */
+seeds_status seeds_band_info(const seeds_ctx *ctx, int *row0, int *row1, long long *record_capacity,
+                             int *record_bytes);
+
+/* seeds_band_seed -- quantise and label the WHOLE frame and count its
+ * histograms (every band does the same, so the replicas start equal).
+ *   image_u8     device, height*width*channels bytes (the whole frame)
+ *   init_labels  NULL (cold: grid) or device height*width int32 (warm start:
+ *                no block levels, reading O9) */
+seeds_status seeds_band_seed(seeds_ctx *ctx, const uint8_t *image_u8, const int32_t *init_labels, void *stream);
+
+/* seeds_band_subsweep -- apply records_in (device, *n_in records: every band's
+ * records of sub-sweep s-1; NULL for s = 0) to the histograms, then run
+ * sub-sweep s (0 <= s < subsweeps of the seeded run) on this band's rows,
+ * writing its records to records_out (device, capacity from seeds_band_info)
+ * and their count to *n_out (device int32).  SEEDS_ESTATE before a seed or for
+ * s out of range. */
+seeds_status seeds_band_subsweep(seeds_ctx *ctx, int s, const void *records_in, const int32_t *n_in,
+                                 void *records_out, int32_t *n_out, void *stream);
+
+/* seeds_band_halo -- put = 0: copy this band's first two rows to top and its
+ * last two rows to bottom (device, 2*width uint16 each; either may be NULL).
+ * put = 1: write top into the two rows above the band and bottom into the two
+ * rows below it (ignored at the image border). */
+seeds_status seeds_band_halo(seeds_ctx *ctx, int put, uint16_t *top, uint16_t *bottom, void *stream);
+
+/* seeds_band_finish -- apply records_in (every band's records of the last
+ * sub-sweep; may be NULL) and write this band's rows of the int32 labels into
+ * labels_out (device, height*width; other rows untouched).  seeds_read_state
+ * then returns this band's replica of the histograms (equal on every band). */
+seeds_status seeds_band_finish(seeds_ctx *ctx, const void *records_in, const int32_t *n_in, int32_t *labels_out,
+                               void *stream);
 
 /* seeds_sync -- wait for `stream` and report any pending CUDA error. */
 seeds_status seeds_sync(seeds_ctx *ctx, void *stream);

@@ -116,6 +116,17 @@ struct seeds_ctx {
     bool grid_ok = false;
     int grid_G = 0;
     int grid_nt = 512;     // threads per CTA of the plan
+    // row-band mode (seeds_create_banded): band `band` of `band_n`, top-unit rows
+    // [band_u0, band_u1) = pixel rows [band_y0, band_y1); record list + count
+    bool banded = false;
+    int band = 0, band_n = 1, band_u0 = 0, band_u1 = 0, band_y0 = 0, band_y1 = 0;
+    GRec *d_brec = nullptr;
+    int *d_bcount = nullptr;
+    long long brec_cap = 0;
+    int band_total = 0;    // sub-sweeps of the seeded run (cold or warm)
+    bool band_seeded = false;
+    bool band_warm = false;
+    const int32_t *band_init = nullptr;
     size_t grid_smem = 0;
     GridParams gp{};
     int n_sm = 148;
@@ -618,6 +629,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     const int TX = c->L > 0 ? c->GX >> Lm : c->W, TY = c->L > 0 ? c->GY >> Lm : c->H;
     auto ux = [&](int i) { return c->L > 0 ? c->colstart[(size_t)i << Lm] : i; };
     auto uy = [&](int j) { return c->L > 0 ? c->rowstart[(size_t)j << Lm] : j; };
+    const int UY0 = c->banded ? c->band_u0 : 0, TYb = c->banded ? c->band_u1 - c->band_u0 : TY;
     int muw = 0, muh = 0;
     for (int i = 0; i < TX; i++) muw = std::max(muw, ux(i + 1) - ux(i));
     for (int j = 0; j < TY; j++) muh = std::max(muh, uy(j + 1) - uy(j));
@@ -641,8 +653,8 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     double best = 1e300;
     int ba = 0, bb_ = 0;
     for (int a : size_candidates(TX))
-        for (int b : size_candidates(TY)) {
-            const long long T = (long long)nf * ((TX + a - 1) / a) * ((TY + b - 1) / b);
+        for (int b : size_candidates(TYb)) {
+            const long long T = (long long)nf * ((TX + a - 1) / a) * ((TYb + b - 1) / b);
             const long long G = std::min<long long>(nsm, T);
             const long long tw = (long long)a * muw, th = (long long)b * muh;
             if ((tw + 4 + 14) / 8 * 8 > 256 || th + 4 > 256) continue;  // TMA box limits (aligned start)
@@ -659,13 +671,14 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         }
     if (!ba) return false;
     // tiles of one frame, then their per-tile capacities
-    const int ntx = (TX + ba - 1) / ba, nty = (TY + bb_ - 1) / bb_;
+    const int ntx = (TX + ba - 1) / ba, nty = (TYb + bb_ - 1) / bb_;
     std::vector<GridTile> ft;
     std::vector<long long> tpx, tq, tr;
     for (int ty = 0; ty < nty; ty++)
         for (int tx = 0; tx < ntx; tx++) {
             GridTile t{};
-            const int i0 = tx * ba, i1 = std::min(TX, (tx + 1) * ba), j0 = ty * bb_, j1 = std::min(TY, (ty + 1) * bb_);
+            const int i0 = tx * ba, i1 = std::min(TX, (tx + 1) * ba);
+            const int j0 = UY0 + ty * bb_, j1 = UY0 + std::min(TYb, (ty + 1) * bb_);
             t.X0 = ux(i0); t.X1 = ux(i1); t.Y0 = uy(j0); t.Y1 = uy(j1);
             t.BX0 = i0 << Lm; t.BX1 = i1 << Lm; t.BY0 = j0 << Lm; t.BY1 = j1 << Lm;
             const long long w = t.X1 - t.X0, h = t.Y1 - t.Y0;
@@ -729,6 +742,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     // round trip, so it is preferred over shared-memory-resident bins
     for (int opt = 0; opt < 4; opt++) {
         const int rs = opt < 2, res = !(opt & 1);
+        if (c->banded && (rs || res)) continue;  // band mode: bins from k_band_seed, records to the host
         size_t off = 0;
         q.o_stage = (unsigned)off; off = align128(off + 2 * (size_t)q.stage_bytes);
         q.o_bins = (unsigned)off;  off = align128(off + (res ? (size_t)max_cpx * c->bb : 2 * (size_t)q.bins_bytes));
@@ -1397,12 +1411,184 @@ void seeds_destroy(seeds_ctx *ctx)
     void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1],
                     ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band, ctx->d_kmap,
-                    ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp,
+                    ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp, ctx->d_bcount,
                     ctx->d_init_stage, ctx->d_out_stage};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     delete ctx;
+}
+
+// ---------------------------------------------------------------------------
+// Row-band mode (include/seeds.h)
+// ---------------------------------------------------------------------------
+seeds_status seeds_create_banded(int width, int height, int channels, int n_superpixels, int n_levels,
+                                 int bins_per_channel, int smoothness_prior, int iters_per_level, int band,
+                                 int n_bands, seeds_ctx **out)
+{
+    if (!out || n_bands < 1 || band < 0 || band >= n_bands) return SEEDS_EINVAL;
+    seeds_ctx *ctx = nullptr;
+    seeds_status st = seeds_create(width, height, channels, n_superpixels, n_levels, bins_per_channel,
+                                   smoothness_prior, iters_per_level, &ctx);
+    if (st != SEEDS_OK) return st;
+    if (n_bands > ctx->ny) {
+        seeds_destroy(ctx);
+        return SEEDS_EINVAL;
+    }
+    // bands are runs of whole superpixel rows, so every block of every level
+    // lies in one band
+    const int j0 = (int)((long long)band * ctx->ny / n_bands), j1 = (int)((long long)(band + 1) * ctx->ny / n_bands);
+    ctx->banded = true;
+    ctx->band = band;
+    ctx->band_n = n_bands;
+    ctx->band_y0 = ctx->rowstart[(size_t)j0 << ctx->L];
+    ctx->band_y1 = ctx->rowstart[(size_t)j1 << ctx->L];
+    ctx->band_u0 = ctx->L > 0 ? 2 * j0 : ctx->band_y0;
+    ctx->band_u1 = ctx->L > 0 ? 2 * j1 : ctx->band_y1;
+    if (ctx->band_y1 - ctx->band_y0 < 2) {
+        seeds_destroy(ctx);
+        return SEEDS_EINVAL;
+    }
+    ctx->mode = SEEDS_MODE_GRID;
+    ctx->brec_cap = (long long)(ctx->band_y1 - ctx->band_y0) * ctx->W + 32;
+    cudaError_t e = cudaMalloc(&ctx->d_bcount, 16);
+    if (e != cudaSuccess) {
+        seeds_destroy(ctx);
+        return e == cudaErrorMemoryAllocation ? SEEDS_ENOMEM : SEEDS_ECUDA;
+    }
+    if (!plan_grid(ctx, 1)) {
+        snprintf(ctx->err, sizeof ctx->err, "no grid-mode tile plan fits the band");
+        seeds_destroy(ctx);
+        return SEEDS_ERANGE;
+    }
+    *out = ctx;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_band_info(const seeds_ctx *ctx, int *row0, int *row1, long long *record_capacity,
+                             int *record_bytes)
+{
+    if (!ctx || !ctx->banded) return SEEDS_EINVAL;
+    if (row0) *row0 = ctx->band_y0;
+    if (row1) *row1 = ctx->band_y1;
+    if (record_capacity) *record_capacity = ctx->brec_cap;
+    if (record_bytes) *record_bytes = (int)sizeof(GRec);
+    return SEEDS_OK;
+}
+
+seeds_status seeds_band_seed(seeds_ctx *ctx, const uint8_t *image_u8, const int32_t *init_labels, void *stream)
+{
+    if (!ctx || !ctx->banded || !image_u8) return SEEDS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!plan_grid(ctx, 1)) return SEEDS_ESTATE;
+    CK(cudaMemsetAsync(ctx->d_H[0], 0, (size_t)ctx->H_fs * 4, st));
+    CK(cudaMemsetAsync(ctx->d_A[0], 0, (size_t)ctx->K * 4, st));
+    CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)(ctx->S + 1) * 4, st));
+    const GridParams &q = ctx->gp;
+    const dim3 g(grid1(ctx->N, 256, 1));
+    if (ctx->bb == 1)
+        k_band_seed<uint8_t><<<g, 256, 0, st>>>(image_u8, init_labels, ctx->W, ctx->H, ctx->C, ctx->bpc, ctx->L,
+                                                ctx->nx, ctx->B, ctx->K, ctx->d_bxof, ctx->d_byof, ctx->d_labp,
+                                                ctx->lpitch, (uint8_t *)q.binsp, q.bpitch, ctx->d_H[0], ctx->d_A[0]);
+    else
+        k_band_seed<uint16_t><<<g, 256, 0, st>>>(image_u8, init_labels, ctx->W, ctx->H, ctx->C, ctx->bpc, ctx->L,
+                                                 ctx->nx, ctx->B, ctx->K, ctx->d_bxof, ctx->d_byof, ctx->d_labp,
+                                                 ctx->lpitch, (uint16_t *)q.binsp, q.bpitch, ctx->d_H[0], ctx->d_A[0]);
+    CK(cudaGetLastError());
+    ctx->band_total = (init_labels ? 0 : 4 * ctx->L * ctx->iters) + ctx->P * ctx->P * ctx->iters;
+    ctx->band_seeded = true;
+    ctx->last_nf = 1;
+    ctx->last_final = 0;
+    ctx->last_done = 0;
+    ctx->ran = true;
+    ctx->band_warm = init_labels != nullptr;
+    ctx->band_init = init_labels;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_band_subsweep(seeds_ctx *ctx, int s, const void *records_in, const int32_t *n_in,
+                                 void *records_out, int32_t *n_out, void *stream)
+{
+    if (!ctx || !ctx->banded || !records_out || !n_out) return SEEDS_EINVAL;
+    if (!ctx->band_seeded || s < 0 || s >= ctx->band_total) return SEEDS_ESTATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (records_in && n_in) {
+        k_apply_records<<<ctx->n_sm, 256, 0, st>>>((const GRec *)records_in, n_in, ctx->B, ctx->d_H[0], ctx->d_A[0]);
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemsetAsync(n_out, 0, 4, st));
+    CK(cudaMemsetAsync(ctx->d_sync, 0, 16, st));
+    GridParams q = ctx->gp;
+    q.img = nullptr; q.out = nullptr;
+    q.init = ctx->band_init;  // only tested against NULL: a warm run has no block levels
+    q.W = ctx->W; q.H = ctx->H; q.C = ctx->C; q.bpc = ctx->bpc; q.B = ctx->B; q.K = ctx->K; q.nx = ctx->nx;
+    q.L = ctx->L; q.iters = ctx->iters; q.limit = -1; q.S = ctx->S; q.nf = 1;
+    q.colstart = ctx->d_colstart; q.rowstart = ctx->d_rowstart; q.bxof = ctx->d_bxof; q.byof = ctx->d_byof;
+    q.lab = ctx->d_labp; q.lab_fs = ctx->labp_fs; q.lpitch = ctx->lpitch;
+    q.bins = ctx->d_bins; q.N = ctx->N;
+    for (int i = 0; i < 2; i++) {
+        q.Hb[i] = ctx->d_H[0];
+        q.Ab[i] = ctx->d_A[0];
+    }
+    q.H_fs = ctx->H_fs;
+    q.moves = ctx->d_moves;
+    q.sync = ctx->d_sync;
+    q.trace = nullptr;
+    q.band = 1;
+    q.s0 = s;
+    q.s1 = s + 1;
+    q.rec_out = (GRec *)records_out;
+    q.rec_count = n_out;
+    cudaError_t e;
+    if (ctx->grid_nt == GRID_THREADS)
+        e = ctx->bb == 1 ? (ctx->gamma ? launch_grid_t<uint8_t, 1, 3, GRID_THREADS>(ctx, q, st)
+                                       : launch_grid_t<uint8_t, 0, 2, GRID_THREADS>(ctx, q, st))
+                         : (ctx->gamma ? launch_grid_t<uint16_t, 1, 3, GRID_THREADS>(ctx, q, st)
+                                       : launch_grid_t<uint16_t, 0, 2, GRID_THREADS>(ctx, q, st));
+    else
+        e = ctx->bb == 1 ? (ctx->gamma ? launch_grid_t<uint8_t, 1, 3, GRID_THREADS_SMALL>(ctx, q, st)
+                                       : launch_grid_t<uint8_t, 0, 2, GRID_THREADS_SMALL>(ctx, q, st))
+                         : (ctx->gamma ? launch_grid_t<uint16_t, 1, 3, GRID_THREADS_SMALL>(ctx, q, st)
+                                       : launch_grid_t<uint16_t, 0, 2, GRID_THREADS_SMALL>(ctx, q, st));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid (band) launch");
+    ctx->last_done = s + 1;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_band_halo(seeds_ctx *ctx, int put, uint16_t *top, uint16_t *bottom, void *stream)
+{
+    if (!ctx || !ctx->banded) return SEEDS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t pitch = (size_t)ctx->lpitch * 2, row = (size_t)ctx->W * 2;
+    auto at = [&](int y) { return ctx->d_labp + (size_t)(y + 2) * ctx->lpitch + 2; };
+    if (!put) {  // this band's first and last two rows
+        if (top) CK(cudaMemcpy2DAsync(top, row, at(ctx->band_y0), pitch, row, 2, cudaMemcpyDeviceToDevice, st));
+        if (bottom)
+            CK(cudaMemcpy2DAsync(bottom, row, at(ctx->band_y1 - 2), pitch, row, 2, cudaMemcpyDeviceToDevice, st));
+    } else {  // the neighbours' rows into this band's halo (none beyond the image)
+        if (top && ctx->band > 0)
+            CK(cudaMemcpy2DAsync(at(ctx->band_y0 - 2), pitch, top, row, row, 2, cudaMemcpyDeviceToDevice, st));
+        if (bottom && ctx->band + 1 < ctx->band_n)
+            CK(cudaMemcpy2DAsync(at(ctx->band_y1), pitch, bottom, row, row, 2, cudaMemcpyDeviceToDevice, st));
+    }
+    return SEEDS_OK;
+}
+
+seeds_status seeds_band_finish(seeds_ctx *ctx, const void *records_in, const int32_t *n_in, int32_t *labels_out,
+                               void *stream)
+{
+    if (!ctx || !ctx->banded || !labels_out) return SEEDS_EINVAL;
+    if (!ctx->band_seeded) return SEEDS_ESTATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (records_in && n_in) {  // the last sub-sweep's records
+        k_apply_records<<<ctx->n_sm, 256, 0, st>>>((const GRec *)records_in, n_in, ctx->B, ctx->d_H[0], ctx->d_A[0]);
+        CK(cudaGetLastError());
+    }
+    const long long n = (long long)(ctx->band_y1 - ctx->band_y0) * ctx->W;
+    k_band_emit<<<grid1(n, 256, 1), 256, 0, st>>>(ctx->d_labp, ctx->lpitch, ctx->W, ctx->band_y0, ctx->band_y1,
+                                                  labels_out);
+    CK(cudaGetLastError());
+    return SEEDS_OK;
 }
 
 const char *seeds_status_string(seeds_status s)

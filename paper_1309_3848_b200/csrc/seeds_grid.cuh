@@ -83,6 +83,14 @@ struct GridParams {
     int tx_bytes;                 // bytes one tile's TMA loads deliver (label box + bin box)
     int bw, bbw, bh;              // TMA boxes: label box bw x bh, bin box bbw x (bh - 4)
     int tiles_per_cta, q_cap, ntab, GX, GY, bins_res, rec_smem;
+    // row-band mode (one band of a multi-rank run): the
+    // launch runs sub-sweeps [s0, s1) of its own tiles against a single
+    // histogram buffer (0) that the host keeps current between launches,
+    // appends its delta records to rec_out / rec_count and applies none;
+    // the seed is done by k_band_seed.
+    int band, s0, s1;
+    GRec *rec_out;
+    int *rec_count;
     float invGX, invGY;
     // histogram cache (CTAs with a single tile): A of the frame and the H rows of
     // the superpixels present in the tile + halo, loaded right after each barrier
@@ -352,9 +360,10 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     const int W = q.W, B = q.B;
     const int TW = 2 * B + 2;  // warp table words
     unsigned target = 0;
-    GRec *const rec0 = q.rec_smem ? reinterpret_cast<GRec *>(reinterpret_cast<unsigned char *>(smem) + q.o_rec)
+    GRec *const rec0 = q.band ? q.rec_out : q.rec_smem ? reinterpret_cast<GRec *>(reinterpret_cast<unsigned char *>(smem) + q.o_rec)
                                   : q.rec + (long long)blockIdx.x * 2 * q.rec_cap;
-    GRec *const rec1 = rec0 + q.rec_cap;
+    GRec *const rec1 = q.band ? q.rec_out : rec0 + q.rec_cap;
+    auto rcount = [&](int b) { return q.band ? q.rec_count : &c.misc[b]; };
     auto rec_list = [&](int b) { return b ? rec1 : rec0; };
 
     for (int i = tid; i < q.ntab * TW; i += NT) c.tabs[i] = 0;
@@ -412,7 +421,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     // ---- seed: bins (reading Q1), labels (grid, or warm
     // start, reading O9) and the histogram counts (Eq. 6) into both buffers,
     // warp-aggregated on the (label, bin) key
-    for (int ti = 0; ti < ntl; ti++) {
+    for (int ti = 0; ti < (q.band ? 0 : ntl); ti++) {
         const GridTile t = c.tiles[ti];
         const int tw = t.X1 - t.X0;
         BinT *tb = q.bins_res ? c.sbins + t.boff : static_cast<BinT *>(q.binsp) + (long long)t.f * q.binsp_fs;
@@ -447,9 +456,11 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
             }
         }
     }
-    grid_arrive(q.sync, target);
-    if (q.cache && ntl > 0) build_cache_list(false);
-    grid_wait(q.sync, target);
+    if (!q.band) {
+        grid_arrive(q.sync, target);
+        if (q.cache && ntl > 0) build_cache_list(false);
+        grid_wait(q.sync, target);
+    }
 
     int s = 0;
     // debug trace [cta][phase][8]: 0 work done, 1 barrier passed, 2 replayed,
@@ -478,13 +489,13 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
             }
             for (int k = tid; k < q.K; k += NT) c.ac[k] = __ldcg(Ax + k);
         }
-        const int nrec = c.misc[yb];
+        const int nrec = q.band ? 0 : c.misc[yb];
         const GRec *r = rec_list(yb);
         for (int e = tid; e < nrec; e += NT) {
             const GRec x = r[e];
             gdelta(q, yb, (int)x.f, x.kn & 0xFFFF, x.kn >> 16, x.bc & 0xFFFF, x.bc >> 16);
         }
-        if (tid == 0) c.misc[yb ^ 1] = 0;  // list yb^1 was last read before the barrier
+        if (tid == 0 && !q.band) c.misc[yb ^ 1] = 0;  // list yb^1 was last read before the barrier
         stamp(s + 1, 2);
     };
     // Tile pipeline: the CTA's tiles are staged by TMA (labels + 2-pixel halo,
@@ -518,7 +529,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     // A move k -> n of `count` pixels of bin b: record + histogram deltas.
     auto emit = [&](GRec *r, int slot, int k, int n, int b, int count, int yb) {
         r[slot] = GRec{(uint32_t)k | ((uint32_t)n << 16), (uint32_t)b | ((uint32_t)count << 16), (uint32_t)c.f, 0u};
-        gdelta(q, yb, c.f, k, n, b, count);
+        if (!q.band) gdelta(q, yb, c.f, k, n, b, count);
     };
 
     const bool blocks = q.init == nullptr && q.L > 0;
@@ -530,8 +541,13 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
             for (int it = 0; it < q.iters; it++)
                 for (int col = 0; col < 4; col++) {
                     if (q.limit >= 0 && s >= q.limit) break;
+                    if (s < q.s0) {  // band mode: sub-sweeps of earlier launches
+                        s++;
+                        continue;
+                    }
+                    if (q.s1 >= 0 && s >= q.s1) break;
                     const int cx = col & 1, cy = col >> 1;
-                    const int ob = s & 1, yb_ = ob ^ 1;
+                    const int ob = q.band ? 0 : s & 1, yb_ = ob ^ 1;
                     begin_subsweep(yb_);
                     for (int ti = 0; ti < ntl; ti++) {
                         if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1);
@@ -591,7 +607,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                                     }
                                 }
                                 count_moves(acc >= 0);
-                                int slot = append_warp(&c.misc[ob], nd);
+                                int slot = append_warp(rcount(ob), nd);
                                 if (acc >= 0) {
                                     GRec *r = rec_list(ob);
 #pragma unroll
@@ -666,7 +682,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                                             acc = nb.v[d];
                                 }
                                 count_moves(acc >= 0 && si == 0);
-                                const int slot = append_warp(&c.misc[ob], acc >= 0 && leader ? 1 : 0);
+                                const int slot = append_warp(rcount(ob), acc >= 0 && leader ? 1 : 0);
                                 if (acc >= 0) {
                                     if (leader) emit(rec_list(ob), slot, k, acc, b, (int)lb, yb_);
                                     if (si < alpha) {
@@ -740,7 +756,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                                 if (acc >= 0) {
                                     int base = 0;
                                     if (lane == 0) {
-                                        base = atomicAdd(&c.misc[ob], ns);
+                                        base = atomicAdd(rcount(ob), ns);
                                         atomicAdd(&q.moves[(long long)(s + 1) * q.nf + c.f], 1);
                                     }
                                     base = __shfl_sync(FULL, base, 0);
@@ -772,8 +788,13 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     for (int it = 0; it < q.iters; it++)
         for (int col = 0; col < P * P; col++) {
             if (q.limit >= 0 && s >= q.limit) break;
+            if (s < q.s0) {
+                s++;
+                continue;
+            }
+            if (q.s1 >= 0 && s >= q.s1) break;
             const int cx = col % P, cy = col / P;
-            const int ob = s & 1, yb_ = ob ^ 1;
+            const int ob = q.band ? 0 : s & 1, yb_ = ob ^ 1;
             begin_subsweep(yb_);
             for (int ti = 0; ti < ntl; ti++) {
                 if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1);
@@ -891,7 +912,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                     dt2 = clk64();
 #endif
                     count_moves(acc >= 0);
-                    const int slot = append_warp(&c.misc[ob], acc >= 0 ? 1 : 0);
+                    const int slot = append_warp(rcount(ob), acc >= 0 ? 1 : 0);
                     if (acc >= 0) {
                         emit(rec_list(ob), slot, k, acc, j, 1, yb_);
                         c.set(x, y, acc);
@@ -919,6 +940,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
         }
 
     // ---- outputs: int32 labels of the owned tiles --------------------------
+    if (q.band) return;  // band mode: seeds_band_finish emits the band's rows
     for (int ti = 0; ti < ntl; ti++) {
         const GridTile t = c.tiles[ti];
         const uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
@@ -926,6 +948,62 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
         for (int y = t.Y0 + wid; y < t.Y1; y += NW)
             for (int x = t.X0 + lane; x < t.X1; x += 32)
                 o[(long long)y * W + x] = __ldcg(gl + (long long)(y + 2) * q.lpitch + x + 2);
+    }
+}
+
+// Band mode seed (every rank seeds the whole frame, the image being
+// replicated): bins into the padded bin plane, grid or warm-start labels into
+// the padded label plane, and the histogram counts (Eq. 6) of every pixel into
+// buffer 0 -- one thread per pixel, atomics warp-aggregated on (label, bin).
+template <typename BinT>
+__global__ void __launch_bounds__(256) k_band_seed(const uint8_t *img, const int32_t *init, int W, int H, int C,
+                                                   int bpc, int L, int nx, int B, int K, const int *bxof,
+                                                   const int *byof, uint16_t *lab, int lpitch, BinT *binsp,
+                                                   int bpitch, int *Hb, int *Ab)
+{
+    const long long N = (long long)W * H;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < N; base += (long long)gridDim.x * blockDim.x) {
+        const long long p = base + threadIdx.x;
+        const int lane = threadIdx.x & 31;
+        int key = -1, k = -1;
+        if (p < N) {
+            const int y = (int)(p / W), x = (int)(p - (long long)y * W);
+            int b = 0;
+            for (int ch = 0; ch < C; ch++) b = b * bpc + (((int)img[p * C + ch] * bpc) >> 8);
+            binsp[(long long)y * bpitch + x] = (BinT)b;
+            k = init ? init[p] : (byof[y] >> L) * nx + (bxof[x] >> L);
+            lab[(long long)(y + 2) * lpitch + x + 2] = (uint16_t)k;
+            key = k * B + b;
+        }
+        unsigned m = __match_any_sync(FULL, key);
+        if (p < N && lane == __ffs(m) - 1) atomicAdd(Hb + key, __popc(m));
+        m = __match_any_sync(FULL, k);
+        if (p < N && lane == __ffs(m) - 1) atomicAdd(Ab + k, __popc(m));
+    }
+}
+
+// Band mode: int32 labels of pixel rows [y0, y1) from the padded label plane.
+__global__ void __launch_bounds__(256) k_band_emit(const uint16_t *lab, int lpitch, int W, int y0, int y1, int32_t *out)
+{
+    const long long n = (long long)(y1 - y0) * W;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int y = y0 + (int)(i / W), x = (int)(i - (long long)(y - y0) * W);
+        out[(long long)y * W + x] = lab[(long long)(y + 2) * lpitch + x + 2];
+    }
+}
+
+// Band mode: apply every rank's delta records of the previous sub-sweep to this
+// rank's histogram replica (buffer 0), in any order (integer sums commute).
+__global__ void __launch_bounds__(256) k_apply_records(const GRec *r, const int *n, int B, int *Hb, int *Ab)
+{
+    const int cnt = *n;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
+        const GRec x = r[e];
+        const int k = x.kn & 0xFFFF, nn = x.kn >> 16, b = x.bc & 0xFFFF, c = x.bc >> 16;
+        atomicSub(Hb + (long long)k * B + b, c);
+        atomicAdd(Hb + (long long)nn * B + b, c);
+        atomicSub(Ab + k, c);
+        atomicAdd(Ab + nn, c);
     }
 }
 

@@ -22,7 +22,8 @@ _STATUS = {0: "ok", -1: "invalid argument", -2: "out of memory", -3: "CUDA error
 EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "seeds_query",
            "seeds_read_state", "seeds_debug_limit", "seeds_stats", "seeds_sync", "seeds_destroy",
            "seeds_profile", "seeds_profile_collect", "seeds_set_mode", "seeds_debug_trace",
-           "seeds_status_string", "seeds_last_error"]
+           "seeds_status_string", "seeds_last_error", "seeds_create_banded", "seeds_band_info",
+           "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish"]
 
 
 class SeedsError(RuntimeError):
@@ -66,6 +67,12 @@ def load(path: str = LIB_PATH):
         "seeds_debug_trace": ([vp, i, vp, i], i),
         "seeds_profile_collect": ([vp, vp, vp, vp], i),
         "seeds_destroy": ([vp], None),
+        "seeds_create_banded": ([i] * 10 + [ctypes.POINTER(vp)], i),
+        "seeds_band_info": ([vp, vp, vp, vp, vp], i),
+        "seeds_band_seed": ([vp, vp, vp, vp], i),
+        "seeds_band_subsweep": ([vp, i, vp, vp, vp, vp, vp], i),
+        "seeds_band_halo": ([vp, i, vp, vp, vp], i),
+        "seeds_band_finish": ([vp, vp, vp, vp, vp], i),
         "seeds_status_string": ([i], ctypes.c_char_p),
         "seeds_last_error": ([vp], ctypes.c_char_p),
     }
@@ -244,3 +251,52 @@ class Seeds:
 
     def sync(self, stream=None):
         self._check(self._lib.seeds_sync(self._ctx, _stream_ptr(stream)))
+
+
+class SeedsBand(Seeds):
+    """One band of a row-band run (seeds_create_banded ... seeds_band_finish).
+    The schedule and the exchange between bands are driven by ``bands.py``."""
+
+    def __init__(self, width: int, height: int, channels: int, n_superpixels: int, n_levels: int,
+                 bins_per_channel: int, smoothness_prior: int, iters_per_level: int, band: int,
+                 n_bands: int):
+        self._lib = load()
+        self._ctx = ctypes.c_void_p()
+        st = self._lib.seeds_create_banded(width, height, channels, n_superpixels, n_levels,
+                                           bins_per_channel, int(smoothness_prior), iters_per_level,
+                                           band, n_bands, ctypes.byref(self._ctx))
+        if st != 0:
+            raise SeedsError(st)
+        self.width, self.height, self.channels = width, height, channels
+        self.band, self.n_bands = band, n_bands
+        self.iters = iters_per_level
+        self._refresh()
+        r0, r1, cap, rb = ctypes.c_int(), ctypes.c_int(), ctypes.c_longlong(), ctypes.c_int()
+        self._check(self._lib.seeds_band_info(self._ctx, ctypes.byref(r0), ctypes.byref(r1),
+                                              ctypes.byref(cap), ctypes.byref(rb)))
+        self.row0, self.row1, self.record_capacity, self.record_bytes = r0.value, r1.value, cap.value, rb.value
+        self.subsweeps = 0
+
+    def seed(self, image, init_labels=None, stream=None):
+        self._frames(image)
+        self._check(self._lib.seeds_band_seed(self._ctx, image.data_ptr(),
+                                              None if init_labels is None else init_labels.data_ptr(),
+                                              _stream_ptr(stream)))
+        P = self.info.colour_period
+        self.subsweeps = (0 if init_labels is not None else 4 * self.info.levels_eff * self.iters) + P * P * self.iters
+
+    def subsweep(self, s: int, records_in, n_in, records_out, n_out, stream=None):
+        self._check(self._lib.seeds_band_subsweep(
+            self._ctx, s, None if records_in is None else records_in.data_ptr(),
+            None if n_in is None else n_in.data_ptr(), records_out.data_ptr(), n_out.data_ptr(),
+            _stream_ptr(stream)))
+
+    def halo(self, put: bool, top, bottom, stream=None):
+        self._check(self._lib.seeds_band_halo(self._ctx, int(put), None if top is None else top.data_ptr(),
+                                              None if bottom is None else bottom.data_ptr(),
+                                              _stream_ptr(stream)))
+
+    def finish(self, records_in, n_in, labels_out, stream=None):
+        self._check(self._lib.seeds_band_finish(
+            self._ctx, None if records_in is None else records_in.data_ptr(),
+            None if n_in is None else n_in.data_ptr(), labels_out.data_ptr(), _stream_ptr(stream)))
