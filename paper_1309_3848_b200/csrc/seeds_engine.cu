@@ -777,6 +777,9 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         if (occ < cps) continue;
         q.bins_res = res;
         q.rec_smem = rs;
+        q.band = 0;  // whole-run launch: every sub-sweep (seeds_band_subsweep overrides these)
+        q.s0 = 0;
+        q.s1 = -1;
         q.tx_bytes = q.bw * q.bh * 2 + (res ? 0 : q.bbw * (q.bh - 4) * c->bb);
         q.q_cap = (int)qcap + 32;
         q.GX = c->GX;
