@@ -751,24 +751,6 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.o_misc = (unsigned)off;  off = align16(off + 128);
         q.o_mbar = (unsigned)off;  off = align16(off + 16);
         q.o_tiles = (unsigned)off; off = align16(off + (size_t)q.tiles_per_cta * sizeof(GridTile));
-        // histogram cache (single-tile CTAs): A, slot table, row list, rows
-        q.cache = 0;
-        q.hc_rows = 0;
-        if (q.tiles_per_cta == 1 && c->K <= 16384 && getenv_on("SEEDS_GRID_CACHE")) {
-            const size_t base = align16(off + (size_t)c->K * 4) + align16(c->K) + align16(255 * 2);
-            const size_t tab = need_tab ? tabw : 0;
-            if (base + tab < limit) {
-                const int rows = (int)std::min<size_t>(255, (limit - base - tab) / ((size_t)c->B * 4));
-                if (rows >= 16) {
-                    q.cache = 1;
-                    q.hc_rows = rows > 64 ? 64 : rows;
-                    q.o_ac = (unsigned)off;    off = align16(off + (size_t)c->K * 4);
-                    q.o_kslot = (unsigned)off; off = align16(off + (size_t)c->K);
-                    q.o_klist = (unsigned)off; off = align16(off + 255 * 2);
-                    q.o_hc = (unsigned)off;    off = align16(off + (size_t)q.hc_rows * c->B * 4);
-                }
-            }
-        }
         q.o_tab = (unsigned)off;
         if (off + (need_tab ? tabw : 0) > limit) continue;
         q.ntab = need_tab ? (int)std::min<size_t>(nt / 32, (limit - off) / tabw) : 0;

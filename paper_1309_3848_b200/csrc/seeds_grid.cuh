@@ -92,11 +92,6 @@ struct GridParams {
     GRec *rec_out;
     int *rec_count;
     float invGX, invGY;
-    // histogram cache (CTAs with a single tile): A of the frame and the H rows of
-    // the superpixels present in the tile + halo, loaded right after each barrier
-    int cache;             // 1: enabled
-    int hc_rows;           // capacity in rows
-    unsigned o_hc, o_ac, o_kslot, o_klist;
 };
 
 // Split grid barrier: arrive (CTA barrier, then thread 0 publishes the CTA's
@@ -182,9 +177,6 @@ struct GridCta {
     uint32_t *rem;     // removable-ring LUT (8 words, reading Q8)
     GridTile *tiles;   // this CTA's tiles
     uint64_t *mbar;    // two mbarriers (one per stage buffer)
-    int *hc, *ac;      // histogram cache: cached H rows (hc_rows x B) and A (K)
-    uint8_t *kslot;    // K: cache row of superpixel k, 0xFF = not cached
-    uint16_t *klist;   // hc_rows: superpixel of each cache row
     uint16_t *stage;   // the current tile's staged labels
     uint32_t *queue;   // surviving units of the current tile and sub-sweep
     uint32_t *tabs;    // ntab warp tables of 2B + 2 words
@@ -207,10 +199,6 @@ struct GridCta {
         rem = reinterpret_cast<uint32_t *>(smem + q.o_misc + 64);
         tiles = reinterpret_cast<GridTile *>(smem + q.o_tiles);
         mbar = reinterpret_cast<uint64_t *>(smem + q.o_mbar);
-        hc = reinterpret_cast<int *>(smem + q.o_hc);
-        ac = reinterpret_cast<int *>(smem + q.o_ac);
-        kslot = reinterpret_cast<uint8_t *>(smem + q.o_kslot);
-        klist = reinterpret_cast<uint16_t *>(smem + q.o_klist);
         queue = reinterpret_cast<uint32_t *>(smem + q.o_queue);
         tabs = reinterpret_cast<uint32_t *>(smem + q.o_tab);
         misc = reinterpret_cast<int *>(smem + q.o_misc);
@@ -258,19 +246,10 @@ struct GridCta {
             tma_load3(reinterpret_cast<unsigned char *>(sbins) + slot * q.bins_bytes, tm_bins,
                       t.X0 & ~(16 / (int)sizeof(BinT) - 1), t.Y0, t.f, &mbar[slot]);
     }
-    // Histogram reads of a decision (always buffer ob of the sub-sweep, which
-    // is the one the cache holds)
-    __device__ __forceinline__ int ldA(int buf, int k) const
-    {
-        if (q.cache) return ac[k];
-        return __ldcg((buf ? Af1 : Af0) + k);
-    }
+    // Histogram reads of a decision (the snapshot buffer ob of the sub-sweep)
+    __device__ __forceinline__ int ldA(int buf, int k) const { return __ldcg((buf ? Af1 : Af0) + k); }
     __device__ __forceinline__ int ldH(int buf, int k, int b) const
     {
-        if (q.cache) {
-            const int r = kslot[k];
-            if (r != 0xFF) return hc[r * q.B + b];
-        }
         return __ldcg((buf ? Hf1 : Hf0) + (long long)k * q.B + b);
     }
     __device__ __forceinline__ void set(int x, int y, int v) const
@@ -379,45 +358,6 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     unsigned phase0 = 0, phase1 = 0;  // parity of the next completion of each stage buffer
     __syncthreads();
 
-    // Labels present in the (single) tile + halo -> the cache rows of the next
-    // sub-sweep (run while waiting at the grid barrier; a label entering the
-    // halo later is read from global memory).
-    auto build_cache_list = [&](bool from_stage) {
-        for (int k = tid; k < q.K; k += NT) c.kslot[k] = 0;
-        __syncthreads();
-        const GridTile &t = c.tiles[0];
-        const int rows = t.Y1 - t.Y0 + 4, cols = t.X1 - t.X0 + 4, n = rows * cols;
-        const float inv = 1.0f / (float)cols;
-        for (int i = tid; i < n; i += NT) {
-            const int r = div_small(i, cols, inv), x = t.X0 - 2 + (i - r * cols), y = t.Y0 - 2 + r;
-            int v = SENT;
-            if (from_stage) {
-                v = *c.cell(x, y);
-            } else if (x >= 0 && x < W && y >= 0 && y < q.H) {
-                v = q.init ? q.init[(long long)t.f * q.N + (long long)y * W + x]
-                           : (q.byof[y] >> q.L) * q.nx + (q.bxof[x] >> q.L);
-            }
-            if (v != SENT) c.kslot[v] = 1;
-        }
-        __syncthreads();
-        if (tid == 0) c.misc[3] = 0;
-        __syncthreads();
-        for (int k = tid; k < q.K; k += NT) {
-            if (!c.kslot[k]) {
-                c.kslot[k] = 0xFF;
-                continue;
-            }
-            const int r = atomicAdd(&c.misc[3], 1);
-            if (r < q.hc_rows) {
-                c.kslot[k] = (uint8_t)r;
-                c.klist[r] = (uint16_t)k;
-            } else {
-                c.kslot[k] = 0xFF;
-            }
-        }
-        __syncthreads();
-        if (tid == 0 && c.misc[3] > q.hc_rows) c.misc[3] = q.hc_rows;
-    };
     // ---- seed: bins (reading Q1), labels (grid, or warm
     // start, reading O9) and the histogram counts (Eq. 6) into both buffers,
     // warp-aggregated on the (label, bin) key
@@ -456,11 +396,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
             }
         }
     }
-    if (!q.band) {
-        grid_arrive(q.sync, target);
-        if (q.cache && ntl > 0) build_cache_list(false);
-        grid_wait(q.sync, target);
-    }
+    if (!q.band) grid_barrier(q.sync, target);
 
     int s = 0;
     // debug trace [cta][phase][8]: 0 work done, 1 barrier passed, 2 replayed,
@@ -477,18 +413,6 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     // buffer yb and reset the list that sub-sweep s fills.
     auto begin_subsweep = [&](int yb) {
         if (tid == 0 && ntl > 0) c.issue(c.tiles[0], 0);  // overlaps the replay
-        if (q.cache) {
-            // histogram cache of buffer ob = yb ^ 1 (the snapshot of this sub-sweep)
-            c.select(c.tiles[0], 0);
-            const int *Hx = (yb ^ 1) ? c.Hf1 : c.Hf0, *Ax = (yb ^ 1) ? c.Af1 : c.Af0;
-            const int nk = c.misc[3], tot = nk * B;
-            const float invB = 1.0f / (float)B;
-            for (int i = tid; i < tot; i += NT) {
-                const int r = div_small(i, B, invB);
-                c.hc[i] = __ldcg(Hx + (long long)c.klist[r] * B + (i - r * B));
-            }
-            for (int k = tid; k < q.K; k += NT) c.ac[k] = __ldcg(Ax + k);
-        }
         const int nrec = q.band ? 0 : c.misc[yb];
         const GRec *r = rec_list(yb);
         for (int e = tid; e < nrec; e += NT) {
@@ -510,7 +434,6 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
             phase0 ^= 1;
         }
         c.select(c.tiles[ti], ti & 1);
-        if (q.cache) __syncthreads();  // the cache fill of the other threads
         stamp(s + 1, 3);
     };
     auto end_tile = [&]() {
@@ -520,9 +443,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     };
     auto end_subsweep = [&]() {
         stamp(s + 1, 0);
-        grid_arrive(q.sync, target);
-        if (q.cache) build_cache_list(true);
-        grid_wait(q.sync, target);
+        grid_barrier(q.sync, target);
         stamp(s + 1, 1);
         s++;
     };
