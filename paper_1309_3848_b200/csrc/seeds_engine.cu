@@ -633,7 +633,11 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     int muw = 0, muh = 0;
     for (int i = 0; i < TX; i++) muw = std::max(muw, ux(i + 1) - ux(i));
     for (int j = 0; j < TY; j++) muh = std::max(muh, uy(j + 1) - uy(j));
-    const int cps = GRID_THREADS / nt;  // CTAs per SM
+    // CTAs per SM: 1 x 512 or 4 x 128 threads, 128 registers each.  (8 x 128
+    // at 64 registers made c4 20% faster but spills; a spilled register that
+    // is live across the grid barrier's fence (CCTL.IVALL) is not safe, and c3
+    // came out wrong.)
+    const int cps = GRID_THREADS / nt;
     const size_t limit = cps == 1 ? 227 * 1024 : (228 * 1024) / cps - 1024;
     const size_t tabw = (2 * (size_t)c->B + 2) * 4;
     bool need_tab = false;

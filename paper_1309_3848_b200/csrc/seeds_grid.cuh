@@ -401,8 +401,25 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     int s = 0;
     // debug trace [cta][phase][8]: 0 work done, 1 barrier passed, 2 replayed,
     // 3 last tile staged, 4 last tile filtered, 5 last tile decided
+    // slots 6, 7, 15: per sub-sweep sums over the CTA's tiles of the staging
+    // wait, the filter and the decide phases
+    long long t_last = 0, acc_w = 0, acc_f = 0, acc_d = 0;
     auto stamp = [&](int phase, int which) {
-        if (q.trace && tid == 0) q.trace[((long long)blockIdx.x * (q.S + 4) + phase) * 16 + which] = clk64();
+        if (!q.trace || tid != 0) return;
+        const long long now = clk64();
+        long long *row = q.trace + ((long long)blockIdx.x * (q.S + 4) + phase) * 16;
+        row[which] = now;
+        if (which == 2) t_last = now;
+        if (which == 3) acc_w += now - t_last;
+        if (which == 4) acc_f += now - t_last;
+        if (which == 5) acc_d += now - t_last;
+        if (which >= 3 && which <= 5) t_last = now;
+        if (which == 0) {
+            row[6] = acc_w;
+            row[7] = acc_f;
+            row[15] = acc_d;
+            acc_w = acc_f = acc_d = 0;
+        }
     };
     stamp(0, 1);
     auto count_moves = [&](bool moved) {

@@ -13,6 +13,9 @@ from paper_1309_3848_b200.seeds import Seeds  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 mode = sys.argv[2] if len(sys.argv) > 2 else "resident"
 img = configs.frames(cfg, n=1)[0]
+if len(sys.argv) > 3:  # crop HxW
+    hh, ww = (int(v) for v in sys.argv[3].split("x"))
+    img = np.ascontiguousarray(img[:hh, :ww])
 p = configs.params(cfg)
 s = Seeds(img.shape[1], img.shape[0], img.shape[2], *[p[k] for k in (
     "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
@@ -36,6 +39,8 @@ bar = cur[:, :, 1] - cur[:, :, 0]
 parts = {"replay": cur[:, :, 2] - prev1, "stage": cur[:, :, 3] - cur[:, :, 2],
          "filter": cur[:, :, 4] - cur[:, :, 3], "decide": cur[:, :, 5] - cur[:, :, 4],
          "tail": cur[:, :, 0] - cur[:, :, 5]}
+if (cur[:, :, 6] != 0).any():
+    parts.update({"sum.wait": cur[:, :, 6], "sum.filter": cur[:, :, 7], "sum.decide": cur[:, :, 15]})
 if (cur[:, :, 8] != 0).any():
     parts.update({"d.pre": cur[:, :, 13], "d.xy": cur[:, :, 14], "d.ring": cur[:, :, 11], "d.bin": cur[:, :, 12], "d.gath": cur[:, :, 8], "d.dec": cur[:, :, 9],
                   "d.emit": cur[:, :, 10]})
