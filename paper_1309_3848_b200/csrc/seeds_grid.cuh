@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                             dt1 = clk64();
 #endif
                             if (!GAMMA) {
-                                if (pass) acc = nb.v[__ffs(pass) - 1];
+                                if (pass) acc = (pass & 1) ? nb.v[0] : (pass & 2) ? nb.v[1] : (pass & 4) ? nb.v[2] : nb.v[3];
                             } else if (pass) {
                                 uint16_t w[25];
 #pragma unroll

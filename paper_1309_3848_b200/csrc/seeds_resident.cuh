@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_resident(ResParams q)
                         for (int d = 0; d < 4; d++)
                             pass |= (int)((nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d]) << d;
                         if (!GAMMA) {
-                            if (pass) acc = nb.v[__ffs(pass) - 1];
+                            if (pass) acc = (pass & 1) ? nb.v[0] : (pass & 2) ? nb.v[1] : (pass & 4) ? nb.v[2] : nb.v[3];
                         } else if (pass) {
                             uint16_t w[25];
 #pragma unroll

@@ -55,3 +55,23 @@ def test_product_path_has_no_oracle_import():
                 src = open(os.path.join(dp, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
                 assert "seeds_oracle" not in src, f
+
+
+def test_persistent_kernels_use_no_local_memory():
+    """The grid and resident kernels keep every value in registers or shared
+    memory: a grid barrier's GPU-scope fence invalidates L1 (CCTL.IVALL), so a
+    spilled register live across it is not something to rely on (ptxas -v of
+    the in-tree build, paper_1309_3848_b200/ptxas_info.txt)."""
+    from paper_1309_3848_b200 import build
+    build.build()
+    info = open(os.path.join(ROOT, "paper_1309_3848_b200", "ptxas_info.txt")).read()
+    blocks = re.split(r"Compiling entry function '", info)[1:]
+    seen = 0
+    for b in blocks:
+        name = b.split("'", 1)[0]
+        if "k_grid" not in name and "k_resident" not in name:
+            continue
+        seen += 1
+        m = re.search(r"(\d+) bytes stack frame, (\d+) bytes spill stores, (\d+) bytes spill loads", b)
+        assert m and m.groups() == ("0", "0", "0"), (name, m.group(0) if m else None)
+    assert seen >= 8
