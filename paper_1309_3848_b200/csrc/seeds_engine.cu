@@ -46,6 +46,7 @@ struct seeds_ctx {
     // derived (reading O2)
     int nx, ny, K, L, GX, GY, B, bb, P, amax, S;
     long long N;
+    long long Afs = 0;  // frame stride of A: K rounded up to 4 (16-byte aligned, grid-mode bulk copies)
     int dev;
     // level-0 block geometry
     std::vector<int> colstart, rowstart, bxof, byof;
@@ -175,6 +176,7 @@ static void derive_geometry(seeds_ctx *c)
     c->P = c->gamma ? 3 : 2;
     c->S = 4 * c->L * c->iters + c->P * c->P * c->iters;
     c->N = (long long)c->W * c->H;
+    c->Afs = (c->K + 3) / 4 * 4;
     c->colstart.resize(c->GX + 1);
     c->rowstart.resize(c->GY + 1);
     for (int i = 0; i <= c->GX; i++) c->colstart[i] = (int)((long long)i * c->W / c->GX);
@@ -303,7 +305,7 @@ static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
     for (int i = 0; i < 2; i++) {
         CK(cudaMalloc(&ctx->d_M[i], F * ctx->map_fs * 2));
         CK(cudaMalloc(&ctx->d_H[i], F * ctx->H_fs * 4));
-        CK(cudaMalloc(&ctx->d_A[i], F * ctx->K * 4));
+        CK(cudaMalloc(&ctx->d_A[i], F * ctx->Afs * 4));
         CK(cudaMalloc(&ctx->d_rec[i], F * ctx->rec_fs * sizeof(Rec)));
     }
     release((void *&)ctx->d_labp);
@@ -406,25 +408,25 @@ static seeds_status enqueue(seeds_ctx *ctx, const uint8_t *img, const int32_t *i
     CK(cudaMemsetAsync(ctx->d_cnt, 0, (size_t)bufsz * 4, st));
     CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)bufsz * 4, st));
     CK(cudaMemsetAsync(ctx->d_H[0], 0, (size_t)nf * ctx->H_fs * 4, st));
-    CK(cudaMemsetAsync(ctx->d_A[0], 0, (size_t)nf * ctx->K * 4, st));
+    CK(cudaMemsetAsync(ctx->d_A[0], 0, (size_t)nf * ctx->Afs * 4, st));
     const bool blocks = !warm && ctx->L > 0;
     ctx->ev_used = 0;
     CK(prof_begin(ctx, st, SEEDS_KIND_SEED));
     {
         const dim3 g = grid1(ctx->N, 256, nf);
-        SeedArgs a{img, ctx->W, ctx->C, ctx->bpc, ctx->L, ctx->nx, ctx->B, ctx->K, ctx->N, ctx->H_fs,
+        SeedArgs a{img, ctx->W, ctx->C, ctx->bpc, ctx->L, ctx->nx, ctx->B, ctx->K, ctx->N, ctx->H_fs, ctx->Afs,
                    ctx->d_bxof, ctx->d_byof, init, ctx->d_bins, blocks ? nullptr : ctx->d_lab,
                    ctx->d_H[0], ctx->d_A[0]};
         CK(launch_pdl(k_seed<BinT>, g, dim3(256), 0, st, a));
     }
     CK(prof_end(ctx, st));
     CK(cudaMemcpyAsync(ctx->d_H[1], ctx->d_H[0], (size_t)nf * ctx->H_fs * 4, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(ctx->d_A[1], ctx->d_A[0], (size_t)nf * ctx->K * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->d_A[1], ctx->d_A[0], (size_t)nf * ctx->Afs * 4, cudaMemcpyDeviceToDevice, st));
 
     SweepParams p{};
     p.W = ctx->W; p.H = ctx->H; p.B = ctx->B; p.K = ctx->K;
     p.bins = ctx->d_bins;
-    p.N = ctx->N; p.H_fs = ctx->H_fs; p.rec_fs = ctx->rec_fs;
+    p.N = ctx->N; p.H_fs = ctx->H_fs; p.rec_fs = ctx->rec_fs; p.A_fs = ctx->Afs;
     p.colstart = ctx->d_colstart; p.rowstart = ctx->d_rowstart;
     int s = 0;
     const int limit = ctx->limit;
@@ -755,6 +757,14 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.o_misc = (unsigned)off;  off = align16(off + 128);
         q.o_mbar = (unsigned)off;  off = align16(off + 16);
         q.o_tiles = (unsigned)off; off = align16(off + (size_t)q.tiles_per_cta * sizeof(GridTile));
+        // A cache (two copies of K_pad ints) when it leaves room for the tables
+        q.acache = 0;
+        if (!getenv_off("SEEDS_GRID_ACACHE") &&
+            align16(off + 2 * (size_t)c->Afs * 4) + (need_tab ? tabw : 0) <= limit) {
+            q.acache = 1;
+            q.o_acache = (unsigned)off;
+            off = align16(off + 2 * (size_t)c->Afs * 4);
+        }
         q.o_tab = (unsigned)off;
         if (off + (need_tab ? tabw : 0) > limit) continue;
         q.ntab = need_tab ? (int)std::min<size_t>(nt / 32, (limit - off) / tabw) : 0;
@@ -766,7 +776,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.band = 0;  // whole-run launch: every sub-sweep (seeds_band_subsweep overrides these)
         q.s0 = 0;
         q.s1 = -1;
-        q.tx_bytes = q.bw * q.bh * 2 + (res ? 0 : q.bbw * (q.bh - 4) * c->bb);
+        q.tx_bytes = q.bw * q.bh * 2 + (res ? 0 : q.bbw * (q.bh - 4) * c->bb) + (q.acache ? (int)c->Afs * 4 : 0);
         q.q_cap = (int)qcap + 32;
         q.GX = c->GX;
         q.GY = c->GY;
@@ -851,7 +861,7 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
 {
     for (int i = 0; i < 2; i++) {
         CK(cudaMemsetAsync(ctx->d_H[i], 0, (size_t)nf * ctx->H_fs * 4, st));
-        CK(cudaMemsetAsync(ctx->d_A[i], 0, (size_t)nf * ctx->K * 4, st));
+        CK(cudaMemsetAsync(ctx->d_A[i], 0, (size_t)nf * ctx->Afs * 4, st));
     }
     CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)(ctx->S + 1) * nf * 4, st));
     CK(cudaMemsetAsync(ctx->d_sync, 0, 16, st));
@@ -867,6 +877,7 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
         q.Ab[i] = ctx->d_A[i];
     }
     q.H_fs = ctx->H_fs;
+    q.A_fs = ctx->Afs;
     q.moves = ctx->d_moves;
     q.sync = ctx->d_sync;
     q.trace = ctx->d_trace;
@@ -1080,6 +1091,7 @@ static seeds_status run_resident(seeds_ctx *ctx, const uint8_t *img, const int32
         q.Aout[i] = ctx->d_A[i];
     }
     q.H_fs = ctx->H_fs;
+    q.A_fs = ctx->Afs;
     q.trace = ctx->d_trace;
     const int ncl = std::max(1, std::min(nf, ctx->max_clusters));
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
@@ -1294,7 +1306,7 @@ seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int3
         CK(cudaMemcpyAsync(hist_out, ctx->d_H[b] + (size_t)frame * ctx->H_fs, (size_t)ctx->H_fs * 4,
                            cudaMemcpyDeviceToDevice, st));
     if (sizes_out)
-        CK(cudaMemcpyAsync(sizes_out, ctx->d_A[b] + (size_t)frame * ctx->K, (size_t)ctx->K * 4,
+        CK(cudaMemcpyAsync(sizes_out, ctx->d_A[b] + (size_t)frame * ctx->Afs, (size_t)ctx->K * 4,
                            cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     return SEEDS_OK;
@@ -1520,6 +1532,7 @@ seeds_status seeds_band_subsweep(seeds_ctx *ctx, int s, const void *records_in, 
         q.Ab[i] = ctx->d_A[0];
     }
     q.H_fs = ctx->H_fs;
+    q.A_fs = ctx->Afs;
     q.moves = ctx->d_moves;
     q.sync = ctx->d_sync;
     q.trace = nullptr;

@@ -67,7 +67,7 @@ struct GridParams {
     void *bins;            // bin planes (W x H per frame) when the bins do not stay in shared memory
     long long N;
     int *Hb[2], *Ab[2];
-    long long H_fs;
+    long long H_fs, A_fs;  // frame strides (A_fs = K rounded up to 4: 16-byte aligned frames)
     int *moves;            // (S + 1) x nf accepted units per sub-sweep
     unsigned *sync;        // grid barrier counter (zero at launch)
     long long *trace;      // debug: per CTA, per phase (clock64 at work end, after barrier), or nullptr
@@ -89,6 +89,10 @@ struct GridParams {
     // appends its delta records to rec_out / rec_count and applies none;
     // the seed is done by k_band_seed.
     int band, s0, s1;
+    // A cache: each tile's staging also bulk-copies the sizes A of its frame
+    // (snapshot buffer) into shared memory, so decisions read A there
+    int acache;
+    unsigned o_acache;
     GRec *rec_out;
     int *rec_count;
     float invGX, invGY;
@@ -159,6 +163,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity)
             : "memory");
     } while (!done);
 }
+// 1-D bulk copy global -> shared (bytes a multiple of 16), completion on mbarrier b
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *b)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
 // 3-D TMA tile load (x, y, frame) into shared memory, completion on mbarrier b
 __device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *tm, int x, int y, int z, uint64_t *b)
 {
@@ -177,6 +189,8 @@ struct GridCta {
     uint32_t *rem;     // removable-ring LUT (8 words, reading Q8)
     GridTile *tiles;   // this CTA's tiles
     uint64_t *mbar;    // two mbarriers (one per stage buffer)
+    int *sAc;          // A of the snapshot, one copy per stage buffer (acache)
+    const int *sA;     // the current tile's copy
     uint16_t *stage;   // the current tile's staged labels
     uint32_t *queue;   // surviving units of the current tile and sub-sweep
     uint32_t *tabs;    // ntab warp tables of 2B + 2 words
@@ -199,6 +213,7 @@ struct GridCta {
         rem = reinterpret_cast<uint32_t *>(smem + q.o_misc + 64);
         tiles = reinterpret_cast<GridTile *>(smem + q.o_tiles);
         mbar = reinterpret_cast<uint64_t *>(smem + q.o_mbar);
+        sAc = reinterpret_cast<int *>(smem + q.o_acache);
         queue = reinterpret_cast<uint32_t *>(smem + q.o_queue);
         tabs = reinterpret_cast<uint32_t *>(smem + q.o_tab);
         misc = reinterpret_cast<int *>(smem + q.o_misc);
@@ -209,6 +224,7 @@ struct GridCta {
         X0 = t.X0; X1 = t.X1; Y0 = t.Y0; Y1 = t.Y1;
         sp = q.bw;
         sx0 = X0 & ~7;
+        sA = sAc + (size_t)slot * q.A_fs;
         stage = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(stage0) + slot * q.stage_bytes);
         if (q.bins_res) {
             tb = sbins + t.boff;
@@ -222,8 +238,8 @@ struct GridCta {
         glab = q.lab + (long long)f * q.lab_fs;
         Hf0 = q.Hb[0] + (long long)f * q.H_fs;
         Hf1 = q.Hb[1] + (long long)f * q.H_fs;
-        Af0 = q.Ab[0] + (long long)f * q.K;
-        Af1 = q.Ab[1] + (long long)f * q.K;
+        Af0 = q.Ab[0] + (long long)f * q.A_fs;
+        Af1 = q.Ab[1] + (long long)f * q.A_fs;
     }
     __device__ __forceinline__ const uint16_t *cell(int x, int y) const
     {
@@ -235,10 +251,13 @@ struct GridCta {
     __device__ __forceinline__ int rowy(int j) const { return div_small(j * q.H, q.GY, q.invGY); }
     __device__ __forceinline__ bool removable_s(int m) const { return (rem[m >> 5] >> (m & 31)) & 1u; }
     // TMA: stage tile t into buffer `slot` (thread 0 only)
-    __device__ __forceinline__ void issue(const GridTile &t, int slot) const
+    __device__ __forceinline__ void issue(const GridTile &t, int slot, int ob) const
     {
         asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy label writes before the TMA reads
         mbar_expect(&mbar[slot], (unsigned)q.tx_bytes);
+        if (q.acache)  // the sizes A of the tile's frame in the snapshot buffer (one bulk copy)
+            bulk_load(sAc + (size_t)slot * q.A_fs, (ob ? q.Ab[1] : q.Ab[0]) + (long long)t.f * q.A_fs,
+                      (unsigned)(q.A_fs * 4), &mbar[slot]);
         // box starts must be 16-byte aligned in x (the TMA faults otherwise)
         tma_load3(reinterpret_cast<unsigned char *>(stage0) + slot * q.stage_bytes, tm_lab, t.X0 & ~7, t.Y0, t.f,
                   &mbar[slot]);
@@ -247,7 +266,11 @@ struct GridCta {
                       t.X0 & ~(16 / (int)sizeof(BinT) - 1), t.Y0, t.f, &mbar[slot]);
     }
     // Histogram reads of a decision (the snapshot buffer ob of the sub-sweep)
-    __device__ __forceinline__ int ldA(int buf, int k) const { return __ldcg((buf ? Af1 : Af0) + k); }
+    __device__ __forceinline__ int ldA(int buf, int k) const
+    {
+        if (q.acache) return sA[k];
+        return __ldcg((buf ? Af1 : Af0) + k);
+    }
     __device__ __forceinline__ int ldH(int buf, int k, int b) const
     {
         return __ldcg((buf ? Hf1 : Hf0) + (long long)k * q.B + b);
@@ -261,7 +284,7 @@ struct GridCta {
 __device__ __forceinline__ void gdelta(const GridParams &q, int buf, int f, int k, int n, int b, int count)
 {
     int *H = (buf ? q.Hb[1] : q.Hb[0]) + (long long)f * q.H_fs;
-    int *A = (buf ? q.Ab[1] : q.Ab[0]) + (long long)f * q.K;
+    int *A = (buf ? q.Ab[1] : q.Ab[0]) + (long long)f * q.A_fs;
     atomicAdd(H + (long long)k * q.B + b, -count);
     atomicAdd(H + (long long)n * q.B + b, count);
     atomicAdd(A + k, -count);
@@ -367,7 +390,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
         BinT *tb = q.bins_res ? c.sbins + t.boff : static_cast<BinT *>(q.binsp) + (long long)t.f * q.binsp_fs;
         uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
         int *H0 = q.Hb[0] + (long long)t.f * q.H_fs, *H1 = q.Hb[1] + (long long)t.f * q.H_fs;
-        int *A0 = q.Ab[0] + (long long)t.f * q.K, *A1 = q.Ab[1] + (long long)t.f * q.K;
+        int *A0 = q.Ab[0] + (long long)t.f * q.A_fs, *A1 = q.Ab[1] + (long long)t.f * q.A_fs;
         const long long fN = (long long)t.f * q.N;
         for (int y = t.Y0 + wid; y < t.Y1; y += NW) {
             const int gy = (q.byof[y] >> q.L) * q.nx;
@@ -429,7 +452,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
     // Start of sub-sweep s: replay this CTA's deltas of sub-sweep s-1 into
     // buffer yb and reset the list that sub-sweep s fills.
     auto begin_subsweep = [&](int yb) {
-        if (tid == 0 && ntl > 0) c.issue(c.tiles[0], 0);  // overlaps the replay
+        if (tid == 0 && ntl > 0) c.issue(c.tiles[0], 0, (yb ^ 1));  // overlaps the replay
         const int nrec = q.band ? 0 : c.misc[yb];
         const GRec *r = rec_list(yb);
         for (int e = tid; e < nrec; e += NT) {
@@ -437,6 +460,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
             gdelta(q, yb, (int)x.f, x.kn & 0xFFFF, x.kn >> 16, x.bc & 0xFFFF, x.bc >> 16);
         }
         if (tid == 0 && !q.band) c.misc[yb ^ 1] = 0;  // list yb^1 was last read before the barrier
+        __syncthreads();  // the reset precedes every append of this sub-sweep
         stamp(s + 1, 2);
     };
     // Tile pipeline: the CTA's tiles are staged by TMA (labels + 2-pixel halo,
@@ -453,10 +477,13 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
         c.select(c.tiles[ti], ti & 1);
         stamp(s + 1, 3);
     };
+    // Every thread read the queue length before its decisions, so the reset can
+    // precede the barrier; after it, warps may run ahead into the next
+    // (prefetched) tile and push into the queue.
     auto end_tile = [&]() {
+        if (tid == 0) c.misc[2] = 0;
         __syncthreads();
         stamp(s + 1, 5);
-        if (tid == 0) c.misc[2] = 0;
     };
     auto end_subsweep = [&]() {
         stamp(s + 1, 0);
@@ -488,7 +515,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                     const int ob = q.band ? 0 : s & 1, yb_ = ob ^ 1;
                     begin_subsweep(yb_);
                     for (int ti = 0; ti < ntl; ti++) {
-                        if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1);
+                        if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1, ob);
                         stage_wait(ti);
                         const GridTile t = c.tiles[ti];
                         const int bx0 = t.BX0 >> l, bx1 = t.BX1 >> l, by0 = t.BY0 >> l, by1 = t.BY1 >> l;
@@ -735,7 +762,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
             const int ob = q.band ? 0 : s & 1, yb_ = ob ^ 1;
             begin_subsweep(yb_);
             for (int ti = 0; ti < ntl; ti++) {
-                if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1);
+                if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1, ob);
                 stage_wait(ti);
                 const GridTile t = c.tiles[ti];
                 const int xfirst = t.X0 + (((cx - t.X0) % P) + P) % P;

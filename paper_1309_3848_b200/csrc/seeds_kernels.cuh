@@ -58,6 +58,7 @@ struct SweepParams {
     const void *bins;  // bin plane (uint8 or uint16), frame stride N
     uint16_t *map;     // labels of the units (in-place writes), frame stride map_fs
     long long N, map_fs, H_fs;
+    long long A_fs;    // frame stride of the sizes A (K rounded up to 4)
     const int *colstart, *rowstart;  // level-0 block starts (GX+1 / GY+1 entries)
     const int *Hx, *Ax;  // snapshot
     int *Hy, *Ay;        // next state
@@ -72,7 +73,7 @@ __device__ __forceinline__ void apply_prev(const SweepParams &p, int f, long lon
     const int n = p.cnt_prev[f];
     const Rec *r = p.rec_prev + f * p.rec_fs;
     int *Hy = p.Hy + f * p.H_fs;
-    int *Ay = p.Ay + (long long)f * p.K;
+    int *Ay = p.Ay + (long long)f * p.A_fs;
     for (long long e = tid; e < n; e += nthr) {
         const Rec q = r[e];
         const int k = q.kn & 0xFFFF, nn = q.kn >> 16, b = q.bc & 0xFFFF, c = q.bc >> 16;
@@ -165,7 +166,7 @@ __device__ __forceinline__ int reserve_warp(int *cnt, int *moves, int n, bool mo
 struct SeedArgs {
     const uint8_t *img;
     int W, C, bpc, L, nx, B, K;
-    long long N, H_fs;
+    long long N, H_fs, A_fs;
     const int *bxof, *byof;
     const int32_t *init;  // warm-start labels or nullptr (grid)
     void *bins;
@@ -197,7 +198,7 @@ __device__ __forceinline__ void seed_pixels(const SeedArgs &a, int f, long long 
         unsigned m = __match_any_sync(FULL, key);
         if (valid && lane == __ffs(m) - 1) atomicAdd(&a.H[(long long)f * a.H_fs + key], __popc(m));
         m = __match_any_sync(FULL, label);
-        if (valid && lane == __ffs(m) - 1) atomicAdd(&a.A[(long long)f * a.K + label], __popc(m));
+        if (valid && lane == __ffs(m) - 1) atomicAdd(&a.A[(long long)f * a.A_fs + label], __popc(m));
     }
 }
 
@@ -287,9 +288,9 @@ __device__ __forceinline__ void block_small_units(const SweepParams &p, int f, l
     uint16_t *M = p.map + f * p.map_fs;
     const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
     const int *Hx = p.Hx + f * p.H_fs;
-    const int *Ax = p.Ax + (long long)f * p.K;
+    const int *Ax = p.Ax + (long long)f * p.A_fs;
     int *Hy = p.Hy + f * p.H_fs;
-    int *Ay = p.Ay + (long long)f * p.K;
+    int *Ay = p.Ay + (long long)f * p.A_fs;
     const long long nunits = (long long)p.uw * p.uh;
 
     for (long long base = t0; base < nunits; base += T) {
@@ -372,9 +373,9 @@ __device__ __forceinline__ void block_large_units(const SweepParams &p, int f, l
     uint16_t *M = p.map + f * p.map_fs;
     const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
     const int *Hx = p.Hx + f * p.H_fs;
-    const int *Ax = p.Ax + (long long)f * p.K;
+    const int *Ax = p.Ax + (long long)f * p.A_fs;
     int *Hy = p.Hy + f * p.H_fs;
-    int *Ay = p.Ay + (long long)f * p.K;
+    int *Ay = p.Ay + (long long)f * p.A_fs;
     const long long nunits = (long long)p.uw * p.uh;
 
     for (long long t = u0; t < nunits; t += U) {
@@ -516,7 +517,7 @@ __device__ __forceinline__ void pixel_units(const SweepParams &p, int f, long lo
     uint16_t *L = p.map + f * p.map_fs;
     const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
     const int *Hx = p.Hx + f * p.H_fs;
-    const int *Ax = p.Ax + (long long)f * p.K;
+    const int *Ax = p.Ax + (long long)f * p.A_fs;
     const long long nunits = (long long)p.uw * p.uh;
 
     for (long long base = t0; base < nunits; base += T) {
@@ -550,7 +551,7 @@ __device__ __forceinline__ void pixel_units(const SweepParams &p, int f, long lo
             L[(long long)y * p.W + x] = (uint16_t)acc;
             p.rec_out[f * p.rec_fs + slot] = Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)j | (1u << 16)};
             int *Hy = p.Hy + f * p.H_fs;
-            int *Ay = p.Ay + (long long)f * p.K;
+            int *Ay = p.Ay + (long long)f * p.A_fs;
             atomicSub(&Hy[(long long)k * p.B + j], 1);
             atomicAdd(&Hy[(long long)acc * p.B + j], 1);
             atomicSub(&Ay[k], 1);
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(256) k_pixel_tile(SweepParams p, int tiles_x, 
     uint16_t *L = p.map + f * p.map_fs;
     const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
     const int *Hx = p.Hx + f * p.H_fs;
-    const int *Ax = p.Ax + (long long)f * p.K;
+    const int *Ax = p.Ax + (long long)f * p.A_fs;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int x0 = (tile % tiles_x) * TILE_W, y0 = (tile / tiles_x) * TILE_H;
         __syncthreads();  // previous tile's readers are done
@@ -682,7 +683,7 @@ __global__ void __launch_bounds__(256) k_pixel_tile(SweepParams p, int tiles_x, 
                 p.rec_out[f * p.rec_fs + slot] =
                     Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)j | (1u << 16)};
                 int *Hy = p.Hy + f * p.H_fs;
-                int *Ay = p.Ay + (long long)f * p.K;
+                int *Ay = p.Ay + (long long)f * p.A_fs;
                 atomicSub(&Hy[(long long)k * p.B + j], 1);
                 atomicAdd(&Hy[(long long)acc * p.B + j], 1);
                 atomicSub(&Ay[k], 1);

@@ -51,7 +51,7 @@ struct ResParams {
     int *moves;            // (S + 1) x nf accepted units per sub-sweep
     long long *trace;      // debug: per CTA, per phase (clock64 at work end, after barrier), or nullptr
     int *Hout[2], *Aout[2];  // final histograms go to buffer (sub-sweeps run) & 1
-    long long H_fs;
+    long long H_fs, A_fs;
     // shared-memory layout (byte offsets) and capacities
     unsigned o_lab, o_bins, o_H, o_A, o_rec, o_tab, o_misc, o_kaddr, o_geo, o_queue;
     int pitch, lab_rows, kloc, rec_cap, q_cap, ntab, GX, GY;
@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_resident(ResParams q)
         {
             const int fb = s & 1;
             int *Ho = q.Hout[fb] + (long long)f * q.H_fs;
-            int *Ao = q.Aout[fb] + (long long)f * q.K;
+            int *Ao = q.Aout[fb] + (long long)f * q.A_fs;
             for (int k = wid; k < q.K; k += NW) {
                 const uint32_t m = q.kmap[k];
                 if ((int)(m & 0xFF) != c.rank) continue;

@@ -145,3 +145,25 @@ def test_c5_full_frame_properties_and_modes(torch_cuda, orc):
         r = orc.run(f, **p)
         np.testing.assert_array_equal(L, r.labels)
         np.testing.assert_array_equal(h.cpu().numpy(), r.hist)
+
+
+def test_multi_tile_plans_are_deterministic(torch_cuda):
+    """Plans whose CTAs own several tiles (TMA prefetch of the next tile while
+    the current one is decided): repeated runs through the device and the host
+    entry points give identical labels and histograms (c4 batch of 8 frames,
+    and the c5 frame)."""
+    torch = torch_cuda
+    for cfg, n in (("c4", 8), ("c5", 1)):
+        f = configs.frames(cfg, n=n)
+        p = configs.params(cfg)
+        s = ctx(f.shape[1:], p, "auto")
+        d = torch.from_numpy(f).cuda()
+        ref = s.batch(d).clone()
+        ref_h = s.read_state(n - 1)[0].clone()
+        for _ in range(3):
+            assert torch.equal(s.batch(d), ref)
+            assert torch.equal(s.read_state(n - 1)[0], ref_h)
+        out = np.empty((n,) + f.shape[1:3], np.int32)
+        s.batch_host(np.ascontiguousarray(f), out)
+        np.testing.assert_array_equal(out, ref.cpu().numpy())
+        s.close()
