@@ -551,3 +551,31 @@ def test_mosaic_generator_deterministic():
     b = mosaic.mosaic(64, 48, 10, 8.0, seed=3, grad=30.0)
     assert a.dtype == np.uint8 and a.shape == (48, 64, 3)
     np.testing.assert_array_equal(a, b)
+
+
+# ----------------------------------------------------------------------------
+# P1b: the initial superpixel histograms are the level sums of the block
+# histograms ("summing the histograms of the composing blocks")
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_initial_histograms_are_level_sums(orc, cfg):
+    img = configs.frames(cfg)[0]
+    p = configs.params(cfg)
+    H, W, _ = img.shape
+    r = orc.run(img, **dict(p, iters_per_level=0))  # I = 0: the grid (A30)
+    nx, ny, L = orc.geometry(W, H, p["n_superpixels"], p["n_levels"])
+    GX, GY = nx << L, ny << L
+    B = p["bins_per_channel"] ** 3
+    bins = bins_of(img, p["bins_per_channel"])
+    # level-0 block column i spans [floor(iW/GX), floor((i+1)W/GX)) (reading O2), rows alike
+    cs = [i * W // GX for i in range(GX + 1)]
+    rs = [j * H // GY for j in range(GY + 1)]
+    blk = np.zeros((GY, GX, B), np.int64)
+    for j in range(GY):
+        for i in range(GX):
+            blk[j, i] = np.bincount(bins[rs[j]:rs[j + 1], cs[i]:cs[i + 1]].ravel(), minlength=B)
+    for _ in range(L):  # parent = sum of its 2 x 2 children, level by level
+        blk = blk.reshape(blk.shape[0] // 2, 2, blk.shape[1] // 2, 2, B).sum(axis=(1, 3))
+    assert blk.shape[:2] == (ny, nx)
+    np.testing.assert_array_equal(blk.reshape(ny * nx, B), r.hist)
+    np.testing.assert_array_equal(blk.reshape(ny * nx, B).sum(1), r.sizes)
