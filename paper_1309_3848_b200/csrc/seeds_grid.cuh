@@ -844,16 +844,10 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                                 hn[d] = c.ldH(ob, n, j);
                                 An[d] = c.ldA(ob, n);
                             }
-                            int pass = 0;  // candidates passing the colour test (Prop. 1, one look-up)
-#pragma unroll
-                            for (int d = 0; d < 4; d++)
-                                pass |= (int)((nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d]) << d;
-#ifdef SEEDS_DETAIL
-                            dt1 = clk64();
-#endif
-                            if (!GAMMA) {
-                                if (pass) acc = (pass & 1) ? nb.v[0] : (pass & 2) ? nb.v[1] : (pass & 4) ? nb.v[2] : nb.v[3];
-                            } else if (pass) {
+                            // Prop. 2 for every candidate while the gathers are in flight
+                            // (it reads only the staged labels)
+                            int smok = 0xF;
+                            if (GAMMA) {
                                 uint16_t w[25];
 #pragma unroll
                                 for (int dy = -2; dy <= 2; dy++)
@@ -866,18 +860,34 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                                 for (int iy = 0; iy < 3; iy++)
                                     if (vy >> iy & 1) centres |= vx << (3 * iy);
                                 const int base_s = __popc(centres) - box_sum(win_mask(w, k), centres);
+                                smok = 0;
 #pragma unroll
                                 for (int d = 0; d < 4; d++)
-                                    if (acc < 0 && (pass >> d & 1) && base_s + box_sum(win_mask(w, nb.v[d]), centres) >= 0)
-                                        acc = nb.v[d];
+                                    if (nb.valid >> d & 1)
+                                        smok |= (int)(base_s + box_sum(win_mask(w, nb.v[d]), centres) >= 0) << d;
                             }
+                            int pass = 0;  // candidates passing the colour test (Prop. 1, one look-up)
+#pragma unroll
+                            for (int d = 0; d < 4; d++)
+                                pass |= (int)((nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d]) << d;
+#ifdef SEEDS_DETAIL
+                            dt1 = clk64();
+#endif
+                            pass &= smok;  // first candidate passing both tests (reading Q7)
+                            if (pass) acc = (pass & 1) ? nb.v[0] : (pass & 2) ? nb.v[1] : (pass & 4) ? nb.v[2] : nb.v[3];
                         }
                     }
 #ifdef SEEDS_DETAIL
                     dt2 = clk64();
 #endif
-                    count_moves(acc >= 0);
-                    const int slot = append_warp(rcount(ob), acc >= 0 ? 1 : 0);
+                    // one record per moved pixel: slots by ballot, one atomic per warp
+                    const unsigned mv = __ballot_sync(FULL, acc >= 0);
+                    int slot = 0;
+                    if (lane == 0 && mv) {
+                        slot = atomicAdd(rcount(ob), __popc(mv));
+                        atomicAdd(&q.moves[(long long)(s + 1) * q.nf + c.f], __popc(mv));
+                    }
+                    slot = __shfl_sync(FULL, slot, 0) + __popc(mv & ((1u << lane) - 1));
                     if (acc >= 0) {
                         emit(rec_list(ob), slot, k, acc, j, 1, yb_);
                         c.set(x, y, acc);
