@@ -439,10 +439,14 @@ def main():
              for k, v in prof.items() if v[1]}
     dom = max(kinds, key=lambda k: kinds[k]["ms_total"])
     hbm, hbm_src = peaks()
-    traffic = None
-    try:
+    traffic, inst = None, None
+    try:  # ncu evidence of the same launch (profiles/ncu_traffic.json, scripts/ncu_summary.py)
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(f"{name}/{mode_name}", {}).get(dom)
+        ent = tr.get(f"{name}/{mode_name}", {}).get(dom)
+        if isinstance(ent, dict):
+            traffic, inst = ent.get("dram_bytes"), ent.get("warp_inst")
+        else:
+            traffic = ent
     except Exception:
         pass
     achieved = kinds[dom]["gbps"]
@@ -452,6 +456,17 @@ def main():
                 "algorithmic_bytes_per_launch": ab[dom],
                 "note": "latency-bound: one grid barrier per sub-sweep dominates a single frame"
                         if wl.frames_per_step * wl.N < 4_000_000 else "per-launch algorithmic bytes / launch time"}
+
+    # Issue-rate roofline: the kernel is latency / issue bound, not HBM bound
+    # (DESIGN.md section 6): warp instructions of one launch (ncu) over the
+    # live launch time, against 4 issue slots x #SM x the sampled SM clock.
+    issue = None
+    if inst and kinds[dom]["avg_launch_us"]:
+        sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+        peak_gis = 4 * torch.cuda.get_device_properties(local).multi_processor_count * sm_mhz / 1e3
+        ach = inst / (kinds[dom]["avg_launch_us"] * 1e3)
+        issue = {"bound": "issue", "achieved": ach, "peak": peak_gis, "unit": "Gwarp-inst/s",
+                 "frac": ach / peak_gis, "warp_inst_per_launch": inst, "inst_source": "ncu smsp__inst_executed.sum"}
 
     # ---- end to end through the host-memory C-ABI entry point --------------
     for _ in range(3):
@@ -487,6 +502,7 @@ def main():
             "frames_per_s": wl.frames_per_step * world * args.steps / (tot_ms_max / 1e3),
             "e2e_hbm_frac": (fb * args.steps / (tot_ms_max / 1e3) / 1e9) / hbm,
             "roofline": roofline,
+            "issue_roofline": issue,
             "kernels": kinds,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wl.h2d_bytes()),
                     "d2h_bytes_per_step": int(wl.d2h_bytes())},
