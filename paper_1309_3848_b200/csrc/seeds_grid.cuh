@@ -797,118 +797,120 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                     nq = c.misc[2];
                 }
                 stamp(s + 1, 4);
-#ifdef SEEDS_DETAIL
-                unsigned *dmax = reinterpret_cast<unsigned *>(c.misc + 4);
-                if (tid < 7) dmax[tid] = 0;
-                __syncthreads();
-                const long long dt0 = clk64();
-                long long dt1 = dt0, dt2 = dt0, dta = dt0, dtb = dt0, dtp = dt0, dtu = dt0;
-#endif
-                for (int base = wid * 32; base < nq; base += NT) {
-                    const int e = base + lane;
-                    int acc = -1, k = 0, j = 0, x = 0, y = 0;
-                    if (e < nq) {
-#ifdef SEEDS_DETAIL
-                        dtp = clk64();
-#endif
-                        if (direct) {
-                            unit_xy(e, x, y);
-                        } else {
-                            const uint32_t v = c.queue[e];
-                            x = t.X0 + (int)(v & 0xFFFF);
-                            y = t.Y0 + (int)(v >> 16);
-                        }
-                        const uint16_t *a = c.cell(x, y);
-                        const int sp = c.sp;
-#ifdef SEEDS_DETAIL
-                        dtu = clk64();
-                        k = (int)(dtu & 0);
-#endif
-                        k = a[0];
-                        const Neigh nb = ring_at(a, sp, 1, sp);
-#ifdef SEEDS_DETAIL
-                        dta = clk64();
-                        if (nb.valid) k = (k + (int)(dta & 0)) ;
-#endif
-                        if (nb.valid && c.removable_s(nb.mask)) {
-                            j = c.bin(x, y);
-#ifdef SEEDS_DETAIL
-                            dtb = clk64();
-#endif
-                            // all gathers in flight together (invalid slots re-read k's row)
-                            const long long hk = c.ldH(ob, k, j), Ak = c.ldA(ob, k);
-                            long long hn[4], An[4];
-#pragma unroll
-                            for (int d = 0; d < 4; d++) {
-                                const int n = (nb.valid >> d & 1) ? nb.v[d] : k;
-                                hn[d] = c.ldH(ob, n, j);
-                                An[d] = c.ldA(ob, n);
-                            }
-                            // Prop. 2 for every candidate while the gathers are in flight
-                            // (it reads only the staged labels)
-                            int smok = 0xF;
-                            if (GAMMA) {
-                                uint16_t w[25];
-#pragma unroll
-                                for (int dy = -2; dy <= 2; dy++)
-#pragma unroll
-                                    for (int dx = -2; dx <= 2; dx++) w[(dy + 2) * 5 + dx + 2] = a[dy * sp + dx];
-                                const uint32_t vx = (x > 0 ? 1u : 0u) | 2u | (x + 1 < W ? 4u : 0u);
-                                const uint32_t vy = (y > 0 ? 1u : 0u) | 2u | (y + 1 < q.H ? 4u : 0u);
-                                uint32_t centres = 0;
-#pragma unroll
-                                for (int iy = 0; iy < 3; iy++)
-                                    if (vy >> iy & 1) centres |= vx << (3 * iy);
-                                const int base_s = __popc(centres) - box_sum(win_mask(w, k), centres);
-                                smok = 0;
-#pragma unroll
-                                for (int d = 0; d < 4; d++)
-                                    if (nb.valid >> d & 1)
-                                        smok |= (int)(base_s + box_sum(win_mask(w, nb.v[d]), centres) >= 0) << d;
-                            }
-                            int pass = 0;  // candidates passing the colour test (Prop. 1, one look-up)
-#pragma unroll
-                            for (int d = 0; d < 4; d++)
-                                pass |= (int)((nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d]) << d;
-#ifdef SEEDS_DETAIL
-                            dt1 = clk64();
-#endif
-                            pass &= smok;  // first candidate passing both tests (reading Q7)
-                            if (pass) acc = (pass & 1) ? nb.v[0] : (pass & 2) ? nb.v[1] : (pass & 4) ? nb.v[2] : nb.v[3];
-                        }
+                // Decide: each thread carries U queue entries through the chain
+                // together (U = 2 when the entries do not fit one pass), so the
+                // gathers of both are in flight at once.
+                struct PixUnit {
+                    int xy, k, j, acc, valid, hk, Ak, smok;  // xy = x | y << 16; valid = 0: no decision
+                    int v[4], hn[4], An[4];
+                };
+                const int sp = c.sp;
+                auto pix_load = [&](int e, PixUnit &u) {
+                    u.valid = 0;
+                    u.acc = -1;
+                    u.k = 0;
+                    u.j = 0;
+                    u.xy = 0;
+                    if (e >= nq) return;
+                    int x, y;
+                    if (direct) {
+                        unit_xy(e, x, y);
+                    } else {
+                        const uint32_t v = c.queue[e];
+                        x = t.X0 + (int)(v & 0xFFFF);
+                        y = t.Y0 + (int)(v >> 16);
                     }
-#ifdef SEEDS_DETAIL
-                    dt2 = clk64();
-#endif
-                    // one record per moved pixel: slots by ballot, one atomic per warp
-                    const unsigned mv = __ballot_sync(FULL, acc >= 0);
+                    u.xy = x | y << 16;
+                    const uint16_t *a = c.cell(x, y);
+                    u.k = a[0];
+                    const Neigh nb = ring_at(a, sp, 1, sp);
+                    if (!nb.valid || !c.removable_s(nb.mask)) return;
+                    u.valid = nb.valid;
+                    u.j = c.bin(x, y);
+                    // all gathers in flight together (invalid slots re-read k's row)
+                    u.hk = c.ldH(ob, u.k, u.j);
+                    u.Ak = c.ldA(ob, u.k);
+#pragma unroll
+                    for (int d = 0; d < 4; d++) {
+                        u.v[d] = nb.v[d];
+                        const int n = (nb.valid >> d & 1) ? nb.v[d] : u.k;
+                        u.hn[d] = c.ldH(ob, n, u.j);
+                        u.An[d] = c.ldA(ob, n);
+                    }
+                };
+                auto pix_decide = [&](PixUnit &u) {
+                    if (!u.valid) return;
+                    // Prop. 2 for every candidate while the gathers are in flight (it
+                    // reads only the staged labels)
+                    u.smok = 0xF;
+                    if (GAMMA) {
+                        // one pass over the 5x5 window builds the bit masks of k and of
+                        // the four candidates (bit (dy + 2) * 5 + dx + 2)
+                        uint32_t mk = 0, mn[4] = {0, 0, 0, 0};
+                        const uint16_t *a = c.cell(u.xy & 0xFFFF, u.xy >> 16);
+#pragma unroll
+                        for (int dy = -2; dy <= 2; dy++)
+#pragma unroll
+                            for (int dx = -2; dx <= 2; dx++) {
+                                const int lb = a[dy * sp + dx], bit = (dy + 2) * 5 + dx + 2;
+                                mk |= (uint32_t)(lb == u.k) << bit;
+#pragma unroll
+                                for (int d = 0; d < 4; d++) mn[d] |= (uint32_t)(lb == u.v[d]) << bit;
+                            }
+                        const uint32_t vx = ((u.xy & 0xFFFF) > 0 ? 1u : 0u) | 2u | ((u.xy & 0xFFFF) + 1 < W ? 4u : 0u);
+                        const uint32_t vy = ((u.xy >> 16) > 0 ? 1u : 0u) | 2u | ((u.xy >> 16) + 1 < q.H ? 4u : 0u);
+                        uint32_t centres = 0;
+#pragma unroll
+                        for (int iy = 0; iy < 3; iy++)
+                            if (vy >> iy & 1) centres |= vx << (3 * iy);
+                        const int base_s = __popc(centres) - box_sum(mk, centres);
+                        u.smok = 0;
+#pragma unroll
+                        for (int d = 0; d < 4; d++)
+                            if (u.valid >> d & 1) u.smok |= (int)(base_s + box_sum(mn[d], centres) >= 0) << d;
+                    }
+                    // colour test (Prop. 1, one look-up); the first candidate passing both (reading Q7)
+                    int pass = 0;
+#pragma unroll
+                    for (int d = 0; d < 4; d++)
+                        pass |= (int)((u.valid >> d & 1) &&
+                                      (long long)u.hn[d] * (u.Ak - 1) > (long long)(u.hk - 1) * u.An[d])
+                                << d;
+                    pass &= u.smok;
+                    if (pass) u.acc = (pass & 1) ? u.v[0] : (pass & 2) ? u.v[1] : (pass & 4) ? u.v[2] : u.v[3];
+                };
+                // one record per moved pixel: slots by ballot, one atomic per warp
+                auto pix_emit = [&](const PixUnit &u) {
+                    const unsigned mv = __ballot_sync(FULL, u.acc >= 0);
                     int slot = 0;
                     if (lane == 0 && mv) {
                         slot = atomicAdd(rcount(ob), __popc(mv));
                         atomicAdd(&q.moves[(long long)(s + 1) * q.nf + c.f], __popc(mv));
                     }
                     slot = __shfl_sync(FULL, slot, 0) + __popc(mv & ((1u << lane) - 1));
-                    if (acc >= 0) {
-                        emit(rec_list(ob), slot, k, acc, j, 1, yb_);
-                        c.set(x, y, acc);
+                    if (u.acc >= 0) {
+                        emit(rec_list(ob), slot, u.k, u.acc, u.j, 1, yb_);
+                        c.set(u.xy & 0xFFFF, u.xy >> 16, u.acc);
+                    }
+                };
+                if (GAMMA || nq <= NT) {  // (two entries per thread would spill with the Prop.-2 masks)
+                    for (int base = wid * 32; base < nq; base += NT) {
+                        PixUnit u;
+                        pix_load(base + lane, u);
+                        pix_decide(u);
+                        pix_emit(u);
+                    }
+                } else {
+                    for (int base = wid * 32; base < nq; base += 2 * NT) {
+                        PixUnit u0, u1;
+                        pix_load(base + lane, u0);
+                        pix_load(base + NT + lane, u1);
+                        pix_decide(u0);
+                        pix_decide(u1);
+                        pix_emit(u0);
+                        pix_emit(u1);
                     }
                 }
-#ifdef SEEDS_DETAIL
-                {
-                    const long long dt3 = clk64();
-                    atomicMax(&dmax[0], (unsigned)(dt1 - dt0));
-                    atomicMax(&dmax[1], (unsigned)(dt2 - dt0));
-                    atomicMax(&dmax[2], (unsigned)(dt3 - dt0));
-                    atomicMax(&dmax[3], (unsigned)(dta - dt0));
-                    atomicMax(&dmax[4], (unsigned)(dtb - dt0));
-                    atomicMax(&dmax[5], (unsigned)(dtp - dt0));
-                    atomicMax(&dmax[6], (unsigned)(dtu - dt0));
-                    __syncthreads();
-                    if (q.trace && tid == 0)
-                        for (int i = 0; i < 7; i++)
-                            q.trace[((long long)blockIdx.x * (q.S + 4) + s + 1) * 16 + 8 + i] = dmax[i];
-                }
-#endif
                 end_tile();
             }
             end_subsweep();
