@@ -131,7 +131,6 @@ struct seeds_ctx {
     size_t grid_smem = 0;
     GridParams gp{};
     int n_sm = 148;
-    bool pixel_tiled = true;  // SEEDS_PIXEL_TILED=0 selects the untiled pixel kernel
 };
 
 static seeds_status cuda_fail(seeds_ctx *c, cudaError_t e, const char *what)
@@ -385,17 +384,11 @@ static cudaError_t launch_block(seeds_ctx *ctx, const SweepParams &p, int nf, cu
 template <typename BinT>
 static cudaError_t launch_pixel(seeds_ctx *ctx, const SweepParams &p, int nf, cudaStream_t st)
 {
-    if (ctx->pixel_tiled) {
-        const int tx = (ctx->W + TILE_W - 1) / TILE_W, ty = (ctx->H + TILE_H - 1) / TILE_H;
-        const int ntiles = tx * ty;
-        const dim3 g(ctas_per_frame(ctx, ntiles, 1, nf), nf);
-        if (ctx->gamma) return launch_pdl(k_pixel_tile<BinT, 1, 3>, g, dim3(256), 0, st, p, tx, ntiles);
-        return launch_pdl(k_pixel_tile<BinT, 0, 2>, g, dim3(256), 0, st, p, tx, ntiles);
-    }
-    const long long units = (long long)p.uw * p.uh;
-    const dim3 g(ctas_per_frame(ctx, units, 256, nf), nf);
-    if (ctx->gamma) return launch_pdl(k_pixel<BinT, 1, 3>, g, dim3(256), 0, st, p);
-    return launch_pdl(k_pixel<BinT, 0, 2>, g, dim3(256), 0, st, p);
+    const int tx = (ctx->W + TILE_W - 1) / TILE_W, ty = (ctx->H + TILE_H - 1) / TILE_H;
+    const int ntiles = tx * ty;
+    const dim3 g(ctas_per_frame(ctx, ntiles, 1, nf), nf);
+    if (ctx->gamma) return launch_pdl(k_pixel_tile<BinT, 1, 3>, g, dim3(256), 0, st, p, tx, ntiles);
+    return launch_pdl(k_pixel_tile<BinT, 0, 2>, g, dim3(256), 0, st, p, tx, ntiles);
 }
 
 // Enqueue one whole run (cold or warm) of nf frames on stream st.
@@ -1219,7 +1212,6 @@ seeds_status seeds_create(int width, int height, int channels, int n_superpixels
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, ctx->dev);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) setup_resident(ctx);
-    if (const char *v = getenv("SEEDS_PIXEL_TILED")) ctx->pixel_tiled = atoi(v) != 0;
     if (e != cudaSuccess) {
         seeds_status st = e == cudaErrorMemoryAllocation ? SEEDS_ENOMEM : SEEDS_ECUDA;
         seeds_destroy(ctx);

@@ -484,82 +484,6 @@ __global__ void __launch_bounds__(256) k_block_large(SweepParams p)
 // and with gamma = 1 the Proposition-2 boundary test:
 //   S = sum_{i in W3(p)} (b_i(n) + 1 - b_i(k)) >= 0, patches clamped (Q15).
 // ---------------------------------------------------------------------------
-__device__ __noinline__ int smooth_sum(const uint16_t *L, int W, int H, int x, int y, int k, int n)
-{
-    // weight of each 5x5 cell = number of in-image 3x3 patch centres i in W3(p)
-    // with the cell in W3(i); S = |W3(p) in image| + sum_q w_q ([q = n] - [q = k]).
-    int S = 0;
-    for (int iy = y - 1; iy <= y + 1; iy++) {
-        if (iy < 0 || iy >= H) continue;
-        for (int ix = x - 1; ix <= x + 1; ix++) {
-            if (ix < 0 || ix >= W) continue;
-            int d = 1;  // the "+1" of the proposition
-            for (int qy = iy - 1; qy <= iy + 1; qy++) {
-                if (qy < 0 || qy >= H) continue;
-                const uint16_t *row = L + (long long)qy * W;
-                for (int qx = ix - 1; qx <= ix + 1; qx++) {
-                    if (qx < 0 || qx >= W) continue;
-                    const int v = row[qx];
-                    d += (v == n) - (v == k);
-                }
-            }
-            S += d;
-        }
-    }
-    return S;
-}
-
-// Threads t0 + threadIdx.x, t0 + T + threadIdx.x, ... of the frame (t0 and T
-// warp-uniform, T a multiple of 32).
-template <typename BinT, int GAMMA, int P>
-__device__ __forceinline__ void pixel_units(const SweepParams &p, int f, long long t0, long long T)
-{
-    uint16_t *L = p.map + f * p.map_fs;
-    const BinT *bins = static_cast<const BinT *>(p.bins) + f * p.N;
-    const int *Hx = p.Hx + f * p.H_fs;
-    const int *Ax = p.Ax + (long long)f * p.A_fs;
-    const long long nunits = (long long)p.uw * p.uh;
-
-    for (long long base = t0; base < nunits; base += T) {
-        const long long t = base + threadIdx.x;
-        int acc = -1, k = 0, j = 0, x = 0, y = 0;
-        if (t < nunits) {
-            const int tj = (int)(t / p.uw), ti = (int)(t - (long long)tj * p.uw);
-            x = p.cx + P * ti;
-            y = p.cy + P * tj;
-            k = L[(long long)y * p.W + x];
-            j = bins[(long long)y * p.W + x];
-            const Neigh nb = neighbourhood(L, p.W, p.H, x, y, k);
-            if (nb.valid && removable(nb.mask)) {
-                const long long hk = Hx[(long long)k * p.B + j], Ak = Ax[k];
-                long long hn[4], An[4];
-#pragma unroll
-                for (int d = 0; d < 4; d++) {
-                    const bool v = nb.valid >> d & 1;
-                    hn[d] = v ? Hx[(long long)nb.v[d] * p.B + j] : 0;
-                    An[d] = v ? Ax[nb.v[d]] : 1;
-                }
-#pragma unroll
-                for (int d = 0; d < 4; d++)
-                    if (acc < 0 && (nb.valid >> d & 1) && hn[d] * (Ak - 1) > (hk - 1) * An[d] &&
-                        (!GAMMA || smooth_sum(L, p.W, p.H, x, y, k, nb.v[d]) >= 0))
-                        acc = nb.v[d];
-            }
-        }
-        const int slot = reserve_warp(&p.cnt_out[f], &p.moves_out[f], acc >= 0 ? 1 : 0, acc >= 0);
-        if (acc >= 0) {
-            L[(long long)y * p.W + x] = (uint16_t)acc;
-            p.rec_out[f * p.rec_fs + slot] = Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)j | (1u << 16)};
-            int *Hy = p.Hy + f * p.H_fs;
-            int *Ay = p.Ay + (long long)f * p.A_fs;
-            atomicSub(&Hy[(long long)k * p.B + j], 1);
-            atomicAdd(&Hy[(long long)acc * p.B + j], 1);
-            atomicSub(&Ay[k], 1);
-            atomicAdd(&Ay[acc], 1);
-        }
-    }
-}
-
 // Tiled pixel sub-sweep: a CTA stages a TW x TH label tile plus a halo of R
 // (1 for gamma = 0, 2 for gamma = 1) in shared memory with coalesced loads,
 // each thread loads the bin of its units in the same phase, and the decisions
@@ -693,14 +617,6 @@ __global__ void __launch_bounds__(256) k_pixel_tile(SweepParams p, int tiles_x, 
     }
 }
 
-template <typename BinT, int GAMMA, int P>
-__global__ void __launch_bounds__(256) k_pixel(SweepParams p)
-{
-    pdl_enter();
-    const int f = blockIdx.y;
-    apply_prev(p, f, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
-    pixel_units<BinT, GAMMA, P>(p, f, (long long)blockIdx.x * blockDim.x, (long long)gridDim.x * blockDim.x);
-}
 
 // ---------------------------------------------------------------------------
 // Helpers shared by the persistent kernels (grid mode, seeds_grid.cuh, and
