@@ -1004,7 +1004,10 @@ static void setup_resident(seeds_ctx *c)
         bool need_tab = false;
         for (int l = 0; l < c->L; l++) {
             const int am = max_block_area(c, l);
-            q.bkind[l] = am <= 4 ? BK_T4 : am <= 16 ? BK_T16 : BK_WARP;
+            q.bkind[l] = am <= 4 ? BK_T4 : am <= 32 ? BK_T16 : BK_WARP;
+            int gs = 0;
+            while ((1 << gs) < am && gs < 5) gs++;
+            q.gshift[l] = gs;
             need_tab = need_tab || q.bkind[l] == BK_WARP;
         }
         const size_t tabw = (2 * (size_t)c->B + 2) * 4;

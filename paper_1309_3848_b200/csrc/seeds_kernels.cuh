@@ -787,4 +787,64 @@ __device__ __forceinline__ int block_thread(const Ctx &c, int ob, int k, const N
     return acc;
 }
 
+// Block colour test (Prop. 1, R1) of a block of alpha <= 4 pixels by one
+// thread, every gather issued before the first use (see block_thread).
+template <typename Ctx>
+__device__ __forceinline__ int block_t4(const Ctx &c, int ob, int k, const Neigh &nb, int xa, int ya, int rw,
+                                        int alpha, int (&bv)[4], int (&cnt)[4])
+{
+    {
+        int x = 0, y = 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            bv[i] = i < alpha ? c.bin(xa + x, ya + y) : -1 - i;
+            if (++x == rw) { x = 0; y++; }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        bool first = i < alpha;
+#pragma unroll
+        for (int j = 0; j < i; j++) first = first && bv[j] != bv[i];
+        int n = 1;
+#pragma unroll
+        for (int j = i + 1; j < 4; j++) n += bv[j] == bv[i];
+        cnt[i] = first ? n : 0;
+    }
+    int nn[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) nn[d] = (nb.valid >> d & 1) ? nb.v[d] : k;
+    const long long Ak = c.ldA(ob, k);
+    long long An[4], hk[4], hn[4][4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) An[d] = c.ldA(ob, nn[d]);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int b = bv[i] < 0 ? 0 : bv[i];
+        hk[i] = c.ldH(ob, k, b);
+#pragma unroll
+        for (int d = 0; d < 4; d++) hn[i][d] = c.ldH(ob, nn[d], b);
+    }
+    unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+    const long long al = alpha;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        if (!cnt[i]) continue;
+        const long long lb = cnt[i];
+        const long long u = (hk[i] - lb) * al, v = lb * (Ak - al);
+        Nk += (unsigned long long)(u < v ? u : v);
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const long long un = hn[i][d] * al, vn = lb * An[d];
+            Nn[d] += (unsigned long long)(un < vn ? un : vn);
+        }
+    }
+    int acc = -1;
+#pragma unroll
+    for (int d = 0; d < 4; d++)
+        if (acc < 0 && (nb.valid >> d & 1) && gt_prod(Nn[d], (unsigned long long)(Ak - al), Nk, (unsigned long long)An[d]))
+            acc = nb.v[d];
+    return acc;
+}
+
 }  // namespace seeds

@@ -47,7 +47,8 @@ struct ResParams {
     const int *band_y;     // CS + 1 row boundaries of the bands
     const int *band_top;   // CS + 1 top-level block row boundaries of the bands (L > 0)
     const uint32_t *kmap;  // K entries: owner CTA | local row << 8
-    int bkind[16];         // per level: BK_T4 (blocks <= 4 px), BK_T16 (<= 16 px), BK_WARP
+    int bkind[16];         // per level: BK_T4 (blocks <= 4 px), BK_T16 (<= 32 px, G-lane segments), BK_WARP
+    int gshift[16];        // per level: log2 G of the segment path
     int *moves;            // (S + 1) x nf accepted units per sub-sweep
     long long *trace;      // debug: per CTA, per phase (clock64 at work end, after barrier), or nullptr
     int *Hout[2], *Aout[2];  // final histograms go to buffer (sub-sweeps run) & 1
@@ -320,39 +321,27 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_resident(ResParams q)
                         }
                         __syncthreads();
                         const int nq = c.misc[2];
-                        if (kind != BK_WARP) {
-                            // one thread per block
+                        if (kind == BK_T4) {
+                            // one thread per block (<= 4 px), all gathers in flight together
                             for (int base = wid * 32; base < nq; base += NT) {
                                 const int e = base + lane;
                                 int acc = -1, k = 0, bi = 0, bj = 0, xa = 0, xb = 0, ya = 0, yb = 0, nd = 0;
-                                int bv[16], cnt[16];
+                                int bv[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
                                 if (e < nq) {
                                     rect((int)c.queue[e], bi, bj, xa, xb, ya, yb);
                                     const uint16_t *a = c.cell(xa, ya);
                                     k = a[0];
                                     const Neigh nb = ring_at(a, pitch, xb - xa, (yb - ya) * pitch);
-                                    const int alpha = (xb - xa) * (yb - ya);
-                                    if (kind == BK_T4) {
-                                        int bv4[4], cnt4[4];
-                                        acc = block_thread<4>(c, ob, k, nb, xa, ya, xb - xa, alpha, bv4, cnt4);
-#pragma unroll
-                                        for (int i = 0; i < 4; i++) { bv[i] = bv4[i]; cnt[i] = cnt4[i]; }
-#pragma unroll
-                                        for (int i = 4; i < 16; i++) cnt[i] = 0;
-                                    } else {
-                                        acc = block_thread<16>(c, ob, k, nb, xa, ya, xb - xa, alpha, bv, cnt);
-                                    }
-                                    if (acc >= 0) {
-#pragma unroll
-                                        for (int i = 0; i < 16; i++) nd += cnt[i] != 0;
-                                    }
+                                    const int rw = xb - xa, alpha = rw * (yb - ya);
+                                    acc = block_t4(c, ob, k, nb, xa, ya, rw, alpha, bv, cnt);
+                                    if (acc >= 0) nd = (cnt[0] != 0) + (cnt[1] != 0) + (cnt[2] != 0) + (cnt[3] != 0);
                                 }
                                 count_moves(acc >= 0);
                                 int slot = append_warp(&c.misc[ob], nd);
                                 if (acc >= 0) {
                                     Rec *r = c.rec + (size_t)ob * q.rec_cap;
 #pragma unroll
-                                    for (int i = 0; i < 16; i++)
+                                    for (int i = 0; i < 4; i++)
                                         if (cnt[i]) {
                                             r[slot++] = Rec{(uint32_t)k | ((uint32_t)acc << 16),
                                                             (uint32_t)bv[i] | ((uint32_t)cnt[i] << 16)};
@@ -360,6 +349,85 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_resident(ResParams q)
                                         }
                                     for (int y = ya; y < yb; y++)
                                         for (int x = xa; x < xb; x++) c.set(x, y, acc);
+                                }
+                            }
+                        } else if (kind != BK_WARP) {
+                            // G lanes per block (<= 32 px): lane i holds pixel i, equal
+                            // bins merged by __match_any_sync, segmented reduction (K5)
+                            const int gs = q.gshift[l], G = 1 << gs;
+                            const int segs = 32 >> gs, seg = lane >> gs, si = lane & (G - 1);
+                            for (int base = wid * segs; base < nq; base += NW * segs) {
+                                const int e = base + seg;
+                                int acc = -1, k = 0, xa = 0, xb = 0, ya = 0, yb = 0, rw = 1, alpha = 0;
+                                Neigh nb;
+                                nb.valid = 0;
+                                nb.mask = 0;
+                                if (e < nq) {
+                                    int bi, bj;
+                                    rect((int)c.queue[e], bi, bj, xa, xb, ya, yb);
+                                    const uint16_t *a = c.cell(xa, ya);
+                                    k = a[0];
+                                    nb = ring_at(a, pitch, xb - xa, (yb - ya) * pitch);
+                                    rw = xb - xa;
+                                    alpha = rw * (yb - ya);
+                                }
+                                const bool ok = nb.valid && removable(nb.mask);
+                                int b = -1;
+                                if (ok && si < alpha) {
+                                    const int dy = div_small(si, rw, 1.0f / (float)rw);
+                                    b = c.bin(xa + si - dy * rw, ya + dy);
+                                }
+                                const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : (seg << 16) | b);
+                                const bool leader = b >= 0 && lane == __ffs(m) - 1;
+                                const long long lb = __popc(m);
+                                unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+                                long long Ak = 1, An[4] = {1, 1, 1, 1};
+                                if (ok) {
+                                    const int bb = b < 0 ? 0 : b;
+                                    Ak = c.ldA(ob, k);
+                                    const long long hk = c.ldH(ob, k, bb);
+                                    long long hn[4];
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) {
+                                        const int n = (nb.valid >> d & 1) ? nb.v[d] : k;
+                                        An[d] = c.ldA(ob, n);
+                                        hn[d] = c.ldH(ob, n, bb);
+                                    }
+                                    if (leader) {
+                                        const long long al = alpha;
+                                        const long long uu = (hk - lb) * al, vv = lb * (Ak - al);
+                                        Nk = (unsigned long long)(uu < vv ? uu : vv);
+#pragma unroll
+                                        for (int d = 0; d < 4; d++) {
+                                            const long long un = hn[d] * al, vn = lb * An[d];
+                                            Nn[d] = (nb.valid >> d & 1) ? (unsigned long long)(un < vn ? un : vn) : 0ull;
+                                        }
+                                    }
+                                }
+                                for (int o = G >> 1; o >= 1; o >>= 1) {
+                                    Nk += __shfl_xor_sync(FULL, Nk, o);
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) Nn[d] += __shfl_xor_sync(FULL, Nn[d], o);
+                                }
+                                if (ok) {
+#pragma unroll
+                                    for (int d = 0; d < 4; d++)
+                                        if (acc < 0 && (nb.valid >> d & 1) &&
+                                            gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
+                                            acc = nb.v[d];
+                                }
+                                count_moves(acc >= 0 && si == 0);
+                                const int slot = append_warp(&c.misc[ob], acc >= 0 && leader ? 1 : 0);
+                                if (acc >= 0) {
+                                    if (leader) {
+                                        c.rec[(size_t)ob * q.rec_cap + slot] =
+                                            Rec{(uint32_t)k | ((uint32_t)acc << 16), (uint32_t)b | ((uint32_t)lb << 16)};
+                                        c.delta(yb_, k, acc, b, (int)lb);
+                                    }
+                                    if (si < alpha) {
+                                        const int dy = div_small(si, rw, 1.0f / (float)rw);
+                                        c.set(xa + si - dy * rw, ya + dy, acc);
+                                    }
                                 }
                             }
                         } else if (wid < q.ntab) {
