@@ -640,12 +640,18 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     int nsm = c->n_sm * cps;  // SEEDS_GRID_CTAS caps the CTAs (experiments)
     if (const char *v = getenv("SEEDS_GRID_CTAS")) nsm = std::max(1, std::min(nsm, atoi(v)));
     q = GridParams{};
+    int gw_iters = 2;
+    if (const char *v = getenv("SEEDS_GW_ITERS")) gw_iters = std::max(1, atoi(v));
     for (int l = 0; l < c->L; l++) {
         const int am = max_block_area(c, l);
         q.bkind[l] = am <= 4 ? BK_T4 : am <= 32 ? BK_T16 : BK_WARP;
         int gs = 0;
         while ((1 << gs) < am && gs < 5) gs++;
         q.gshift[l] = gs;
+        // a block's warps each take at least gw_iters 32-pixel slices of it
+        const int slices = (am + 31) / 32;
+        q.gwcap[l] = 1;
+        while (2 * q.gwcap[l] * gw_iters <= slices) q.gwcap[l] *= 2;
         need_tab = need_tab || q.bkind[l] == BK_WARP;
     }
     const size_t fixed = 128 + 16 + (need_tab ? tabw : 0);
@@ -750,6 +756,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.o_misc = (unsigned)off;  off = align16(off + 128);
         q.o_mbar = (unsigned)off;  off = align16(off + 16);
         q.o_tiles = (unsigned)off; off = align16(off + (size_t)q.tiles_per_cta * sizeof(GridTile));
+        q.o_scr = (unsigned)off;   off = align16(off + (need_tab ? (size_t)(nt / 32) * 6 * 8 : 0));
         // A cache (two copies of K_pad ints) when it leaves room for the tables
         q.acache = 0;
         if (!getenv_off("SEEDS_GRID_ACACHE") &&

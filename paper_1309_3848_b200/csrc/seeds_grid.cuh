@@ -74,11 +74,12 @@ struct GridParams {
     GRec *rec;             // per CTA: 2 lists of rec_cap records
     long long rec_cap;
     int bkind[16];         // per level: BK_T4 (thread per block), BK_T16 (G-lane segments), BK_WARP
+    int gwcap[16];         // per level: most warps per block of the BK_WARP path
     int gshift[16];        // per level: log2 G of the segment path
     void *binsp;           // padded bin planes (pitch bpitch) when the bins are staged
     long long binsp_fs;
     int bpitch;
-    unsigned o_stage, o_bins, o_queue, o_tab, o_misc, o_geo, o_rec, o_tiles, o_mbar, o_params;
+    unsigned o_stage, o_bins, o_queue, o_tab, o_misc, o_geo, o_rec, o_tiles, o_mbar, o_params, o_scr;
     int stage_bytes, bins_bytes;  // one stage buffer of labels / of bins (two of each), 128-byte multiples
     int tx_bytes;                 // bytes one tile's TMA loads deliver (label box + bin box)
     int bw, bbw, bh;              // TMA boxes: label box bw x bh, bin box bbw x (bh - 4)
@@ -194,6 +195,7 @@ struct GridCta {
     uint16_t *stage;   // the current tile's staged labels
     uint32_t *queue;   // surviving units of the current tile and sub-sweep
     uint32_t *tabs;    // ntab warp tables of 2B + 2 words
+    unsigned long long *scr;  // per warp: 6 partial sums of the multi-warp block path
     int *misc;         // [0], [1]: record counts of the two lists, [2]: queue length, [3]: cached rows,
                        // [4..7]: detail timing; the ring LUT follows at +64 bytes
     // current tile
@@ -216,6 +218,7 @@ struct GridCta {
         sAc = reinterpret_cast<int *>(smem + q.o_acache);
         queue = reinterpret_cast<uint32_t *>(smem + q.o_queue);
         tabs = reinterpret_cast<uint32_t *>(smem + q.o_tab);
+        scr = reinterpret_cast<unsigned long long *>(smem + q.o_scr);
         misc = reinterpret_cast<int *>(smem + q.o_misc);
     }
     __device__ __forceinline__ void select(const GridTile &t, int slot)
@@ -493,6 +496,13 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                             nq = c.misc[2];
                         }
                         stamp(s + 1, 4);
+                        // warps per block of the BK_WARP path
+                        int gw = 1;
+                        if (kind == BK_WARP) {
+                            while (gw < NW && gw < q.gwcap[l] && NW / (2 * gw) >= (nq > 0 ? nq : 1)) gw *= 2;
+                            if (gw > 1)
+                                while (NW / gw > q.ntab) gw *= 2;  // one table per group
+                        }
                         if (kind == BK_T4) {
                             // one thread per block (<= 4 px), all gathers in flight together
                             for (int base = wid * 32; base < nq; base += NT) {
@@ -595,6 +605,117 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                                         c.set(xa + si - dy * rw, ya + dy, acc);
                                     }
                                 }
+                            }
+                        } else if (NT <= 128 && gw > 1) {
+                            // gw > 1 warps per block (a power of two) when the tile has fewer blocks
+                            // than warps; per-group bin table + list of non-empty bins, partial
+                            // sums combined through shared memory, named barrier per group (K5)
+                            const int ngr = NW / gw, gi = wid / gw, wi = wid - gi * gw, gt = wi * 32 + lane;
+                            const int GT = gw * 32;
+                            auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "r"(GT) : "memory"); };
+                            uint32_t *cnt = c.tabs + (size_t)gi * TW, *list = cnt + B, *nlist = cnt + 2 * B;
+                            unsigned long long *scr = c.scr + (size_t)gi * gw * 6;
+                            for (int e = gi; e < nq; e += ngr) {
+                                int bi, bj, xa, xb, ya, yb;
+                                rect(direct ? e : (int)c.queue[e], bi, bj, xa, xb, ya, yb);
+                                const uint16_t *a = c.cell(xa, ya);
+                                const int k = a[0];
+                                const Neigh nb = ring_at(a, c.sp, xb - xa, (yb - ya) * c.sp);
+                                if (!nb.valid || !c.removable_s(nb.mask)) continue;
+                                const int rw = xb - xa, alpha = rw * (yb - ya);
+                                const float inv = 1.0f / (float)rw;
+                                // candidate sizes first: their loads overlap the histogram build
+                                const long long Ak = c.ldA(ob, k);
+                                long long An[4];
+#pragma unroll
+                                for (int d = 0; d < 4; d++) An[d] = c.ldA(ob, (nb.valid >> d & 1) ? nb.v[d] : k);
+                                for (int i0 = wi * 32; i0 < alpha; i0 += GT) {
+                                    const int i = i0 + lane;
+                                    int b = -1;
+                                    if (i < alpha) {
+                                        const int dy = div_small(i, rw, inv);
+                                        b = c.bin(xa + i - dy * rw, ya + dy);
+                                    }
+                                    const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : b);
+                                    if (b >= 0 && lane == __ffs(m) - 1 &&
+                                        atomicAdd(&cnt[b], (unsigned)__popc(m)) == 0u)
+                                        list[atomicAdd(nlist, 1u)] = (uint32_t)b;
+                                }
+                                gsync();
+                                const int ns = (int)*nlist;
+                                unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+                                for (int i = gt; i < ns; i += GT) {
+                                    const int b = list[i];
+                                    const long long lc = cnt[b];
+                                    const long long hk = c.ldH(ob, k, b);
+                                    long long hn[4];
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) hn[d] = c.ldH(ob, (nb.valid >> d & 1) ? nb.v[d] : k, b);
+                                    const long long u = (hk - lc) * alpha, v = lc * (Ak - alpha);
+                                    Nk += (unsigned long long)(u < v ? u : v);
+#pragma unroll
+                                    for (int d = 0; d < 4; d++)
+                                        if (nb.valid >> d & 1) {
+                                            const long long un = hn[d] * alpha, vn = lc * An[d];
+                                            Nn[d] += (unsigned long long)(un < vn ? un : vn);
+                                        }
+                                }
+                                // five independent butterfly reductions, interleaved
+#pragma unroll
+                                for (int o = 16; o >= 1; o >>= 1) {
+                                    Nk += __shfl_xor_sync(FULL, Nk, o);
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) Nn[d] += __shfl_xor_sync(FULL, Nn[d], o);
+                                }
+                                {  // every warp of the group sums the partials in the same order
+                                    if (lane == 0) {
+                                        scr[wi * 6] = Nk;
+#pragma unroll
+                                        for (int d = 0; d < 4; d++) scr[wi * 6 + 1 + d] = Nn[d];
+                                    }
+                                    gsync();
+                                    Nk = 0;
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) Nn[d] = 0;
+                                    for (int w = 0; w < gw; w++) {
+                                        Nk += scr[w * 6];
+#pragma unroll
+                                        for (int d = 0; d < 4; d++) Nn[d] += scr[w * 6 + 1 + d];
+                                    }
+                                }
+                                int acc = -1;
+#pragma unroll
+                                for (int d = 0; d < 4; d++)
+                                    if (acc < 0 && (nb.valid >> d & 1) &&
+                                        gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
+                                        acc = nb.v[d];
+                                if (acc >= 0) {
+                                    // this warp's share of the list: entries i0 + lane, i0 = wi * 32 + j * GT
+                                    int mine = 0;
+                                    for (int i0 = wi * 32; i0 < ns; i0 += GT) mine += min(32, ns - i0);
+                                    int base = 0;
+                                    if (lane == 0) {
+                                        if (mine) base = atomicAdd(rcount(ob), mine);
+                                        if (wi == 0) atomicAdd(&q.moves[(long long)(s + 1) * q.nf + c.f], 1);
+                                    }
+                                    base = __shfl_sync(FULL, base, 0);
+                                    GRec *r = rec_list(ob);
+                                    for (int i0 = wi * 32, j = 0; i0 < ns; i0 += GT, j += 32) {
+                                        const int i = i0 + lane;
+                                        if (i < ns) {
+                                            const int b = list[i];
+                                            emit(r, base + j + lane, k, acc, b, (int)cnt[b], yb_);
+                                        }
+                                    }
+                                    for (int i = gt; i < alpha; i += GT) {
+                                        const int dy = div_small(i, rw, inv);
+                                        c.set(xa + i - dy * rw, ya + dy, acc);
+                                    }
+                                }
+                                gsync();
+                                for (int i = gt; i < ns; i += GT) cnt[list[i]] = 0;
+                                if (gt == 0) *nlist = 0;
+                                gsync();
                             }
                         } else if (wid < q.ntab) {
                             // one warp per block; per-warp bin table + list of non-empty bins (K5)
