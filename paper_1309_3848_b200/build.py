@@ -35,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(r.stderr)
     with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+        # resource usage per kernel; the timing lines would make every rebuild a diff
+        f.write("".join(ln for ln in r.stderr.splitlines(True) if "Compile time" not in ln))
     os.replace(tmp, LIB)
     return LIB
 
