@@ -1,6 +1,7 @@
 """Build libseeds.so in-tree with nvcc for sm_100a (no JIT, no torch extension)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 
@@ -9,8 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libseeds.so")
 SOURCES = [os.path.join(CSRC, "seeds_engine.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "seeds_kernels.cuh"), os.path.join(CSRC, "seeds_resident.cuh"),
-        os.path.join(ROOT, "include", "seeds.h")]
+DEPS = SOURCES + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "seeds.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]
