@@ -65,7 +65,11 @@ def lib():
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
             P(Trace), ctypes.c_int, P(ctypes.c_int), ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
+            ctypes.c_int, ctypes.c_void_p,
         ]
+        _lib.oracle_means_test.restype = ctypes.c_int
+        _lib.oracle_means_test.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                           ctypes.c_void_p, ctypes.c_int64]
         _lib.oracle_geometry.restype = ctypes.c_int
         _lib.oracle_geometry.argtypes = [ctypes.c_int] * 4 + [P(ctypes.c_int)] * 3
         _lib.oracle_removable.restype = ctypes.c_int
@@ -142,12 +146,16 @@ class Result:
     sizes: np.ndarray       # (K_act,) int32
     trace: list             # per sub-sweep dicts
     k_act: int
+    sums: np.ndarray | None = None  # (K_act, 4) int64 channel sums (reading M1), if asked for
 
 
 def run(img: np.ndarray, n_superpixels: int, n_levels: int, bins_per_channel: int,
         smoothness_prior: int, iters_per_level: int, schedule: int = COL, rule: int = R1,
         init_labels: np.ndarray | None = None, want_energy: bool = False,
-        shuffle_seed: int = 0, max_subsweeps: int = -1, trace_cap: int = 4096) -> Result:
+        shuffle_seed: int = 0, max_subsweeps: int = -1, trace_cap: int = 4096,
+        means_iters: int = 0, want_sums: bool = False) -> Result:
+    """Refine `img` (H, W, C uint8).  means_iters > 0: the last means_iters
+    pixel iterations use the SPM nearest-mean test (reading M1)."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     if img.ndim == 2:
         img = img[:, :, None]
@@ -164,14 +172,26 @@ def run(img: np.ndarray, n_superpixels: int, n_levels: int, bins_per_channel: in
     if init_labels is not None:
         init_labels = np.ascontiguousarray(init_labels, dtype=np.int32)
         init_ptr = init_labels.ctypes.data
+    sums = np.empty((K, 4), np.int64) if want_sums else None
     k = lib().oracle_run(img.ctypes.data, W, H, C, n_superpixels, n_levels, bins_per_channel,
                          int(smoothness_prior), iters_per_level, schedule, rule, init_ptr,
                          labels.ctypes.data, hist.ctypes.data, sizes.ctypes.data, tr, trace_cap,
-                         ctypes.byref(tlen), int(want_energy), shuffle_seed, max_subsweeps)
+                         ctypes.byref(tlen), int(want_energy), shuffle_seed, max_subsweeps,
+                         int(means_iters), None if sums is None else sums.ctypes.data)
     if k < 0:
         raise ValueError("oracle_run rejected its arguments")
     trace = []
     for i in range(min(tlen.value, trace_cap)):
         t = tr[i]
         trace.append({f: getattr(t, f) for f, _ in Trace._fields_})
-    return Result(labels, hist, sizes, trace, k)
+    return Result(labels, hist, sizes, trace, k, sums)
+
+
+def means_test(v, Sk, Ak: int, Sn, An: int) -> bool:
+    """The means test (reading M1) on one proposal: pixel colour v (C values),
+    channel sums and sizes of k (the pixel counted in k) and of n."""
+    v = np.ascontiguousarray(v, dtype=np.uint8)
+    C = v.shape[0]
+    Sk = np.zeros(4, np.int64) + np.pad(np.asarray(Sk, np.int64), (0, 4 - C))
+    Sn = np.zeros(4, np.int64) + np.pad(np.asarray(Sn, np.int64), (0, 4 - C))
+    return bool(lib().oracle_means_test(v.ctypes.data, C, Sk.ctypes.data, int(Ak), Sn.ctypes.data, int(An)))

@@ -25,6 +25,11 @@
  *   R2 (rule 1): the raw-count form the proof ends on, eq:proof3
  *                 -- a test-only switch.
  *
+ * Means post-processing: the
+ * last `means_iters` pixel iterations replace the colour test by the nearest-
+ * mean test of SPM (reading M1 in DESIGN.md); n_levels = 0 with
+ * means_iters = iters is the SPM baseline, n_levels = 0 alone is SPH.
+ *
  * Arithmetic: counts in int64, products in __int128, so no width question can
  * arise here; the GPU path's int32/int64 widths are checked against this.
  */
@@ -105,6 +110,10 @@ typedef struct {
     int64_t *lblock;   /* B: block histogram scratch */
     const int *curM;   /* block phase: current block map (for traced energies) */
     int curl;          /* its level */
+    const uint8_t *img;  /* H*W*C input (means test) */
+    int means_iters;     /* the last means_iters pixel iterations use the means test */
+    int means_on;        /* current pixel iteration uses it */
+    int64_t *msum;       /* K*4: per-superpixel channel sums S[k][c] (reading M1) */
 } st_t;
 
 /* O1 quantiser: bin(p) = sum_c floor(v_c * bpc / 256) * bpc^(C-1-c), channel 0
@@ -204,6 +213,41 @@ static int colour_test_pixel(const st_t *s, int j, int k, int n)
     int64_t An = s->size[n], Ak = s->size[k];
     if (s->rule == ORACLE_R2) return hn > hk - 1;
     return (i128)hn * (Ak - 1) > (i128)(hk - 1) * An;
+}
+
+/* SPM colour test ("the mean-based distance measure from
+ * SLIC"; used for the last pixel-level updates, 901-903), reading M1: move
+ * pixel p of colour v from k to n iff v is strictly nearer (squared Euclidean
+ * distance over the C channels) to the mean colour of n than to that of k,
+ * the means mu_x = S_x / A_x taken from the sub-sweep's snapshot (p counted
+ * in k).  Cross-multiplied by A_n^2 A_k^2:
+ *   A_k^2 sum_c (A_n v_c - S_n,c)^2  <  A_n^2 sum_c (A_k v_c - S_k,c)^2.
+ * Both sides are below 4 * 2^16 * N^4 < 2^126 for N < 2^27 (checked at run). */
+typedef unsigned __int128 u128;
+static int means_test(const uint8_t *v, int C, const int64_t *Sk, int64_t Ak, const int64_t *Sn, int64_t An)
+{
+    u128 dn = 0, dk = 0;
+    for (int c = 0; c < C; c++) {
+        i128 en = (i128)An * v[c] - Sn[c], ek = (i128)Ak * v[c] - Sk[c];
+        dn += (u128)(en * en);
+        dk += (u128)(ek * ek);
+    }
+    return dn * (u128)(Ak * Ak) < dk * (u128)(An * An);
+}
+
+static int means_test_pixel(const st_t *s, int64_t p, int k, int n)
+{
+    return means_test(s->img + p * s->C, s->C, s->msum + (int64_t)k * 4, s->size[k],
+                      s->msum + (int64_t)n * 4, s->size[n]);
+}
+
+/* S[k][c] recounted from the labels and the image (start of the means phase). */
+static void means_recount(st_t *s)
+{
+    int64_t N = (int64_t)s->W * s->H;
+    memset(s->msum, 0, sizeof(int64_t) * 4 * (size_t)s->K);
+    for (int64_t p = 0; p < N; p++)
+        for (int c = 0; c < s->C; c++) s->msum[(int64_t)s->lab[p] * 4 + c] += s->img[p * s->C + c];
 }
 
 /* Block case: A_k^l is the block with histogram l (alpha pixels).
@@ -395,12 +439,17 @@ static void apply_block_move(st_t *s, int l, int bi, int bj, int k, int n)
     s->size[n] += alpha;
 }
 
-static void apply_pixel_move(st_t *s, int j, int k, int n)
+static void apply_pixel_move(st_t *s, int64_t p, int j, int k, int n)
 {
     s->hist[(int64_t)k * s->B + j]--;
     s->hist[(int64_t)n * s->B + j]++;
     s->size[k]--;
     s->size[n]++;
+    if (s->means_on)
+        for (int c = 0; c < s->C; c++) {
+            s->msum[(int64_t)k * 4 + c] -= s->img[p * s->C + c];
+            s->msum[(int64_t)n * 4 + c] += s->img[p * s->C + c];
+        }
 }
 
 /* decide for block (bi, bj) on map M (w x h) at level l; returns the accepted
@@ -436,7 +485,8 @@ static int decide_pixel(st_t *s, int x, int y, int *is_boundary, int *is_removab
     int j = s->bin[(int64_t)y * s->W + x];
     for (int c = 0; c < nc; c++) {
         int n = cand[c];
-        if (!colour_test_pixel(s, j, k, n)) continue;
+        if (s->means_on ? !means_test_pixel(s, (int64_t)y * s->W + x, k, n) : !colour_test_pixel(s, j, k, n))
+            continue;
         if (s->gamma && smooth_sum(s->lab, s->W, s->H, x, y, k, n) < 0) continue;
         return n;
     }
@@ -522,6 +572,11 @@ static void pixel_level(st_t *s)
     int64_t *order = (int64_t *)malloc(sizeof(int64_t) * N);
     move_t *moves = (move_t *)malloc(sizeof(move_t) * N);
     for (int it = 0; it < s->iters; it++) {
+        /* means post-processing: the last means_iters iterations (reading M1) */
+        if (!s->means_on && it >= s->iters - s->means_iters) {
+            s->means_on = 1;
+            means_recount(s);
+        }
         if (s->schedule == ORACLE_SEQ) {
             if (limit_reached(s)) break;
             int nm = 0;
@@ -533,7 +588,7 @@ static void pixel_level(st_t *s)
                     nb += isb; nr += isr;
                     if (n < 0) continue;
                     s->lab[y * s->W + x] = n;
-                    apply_pixel_move(s, s->bin[(int64_t)y * s->W + x], k, n);
+                    apply_pixel_move(s, (int64_t)y * s->W + x, s->bin[(int64_t)y * s->W + x], k, n);
                     nm++;
                 }
             s->subsweeps_done++;
@@ -560,7 +615,7 @@ static void pixel_level(st_t *s)
                 moves[nm].j = s->bin[order[i]];
                 nm++;
             }
-            for (int i = 0; i < nm; i++) apply_pixel_move(s, moves[i].j, moves[i].k, moves[i].n);
+            for (int i = 0; i < nm; i++) apply_pixel_move(s, moves[i].unit, moves[i].j, moves[i].k, moves[i].n);
             s->subsweeps_done++;
             push_trace(s, -1, it, c, nm, nu, nb, nr);
         }
@@ -578,14 +633,20 @@ static void pixel_level(st_t *s)
 /*   sizes_out:  K_act int32 (or NULL);  trace: per sub-sweep records         */
 /*   shuffle_seed: 0 = raster order inside a sub-sweep; else shuffled (P10)   */
 /*   max_subsweeps: -1 = all; else stop after that many (bisection hook)      */
+/*   means_iters: the last means_iters of the iters pixel iterations use the  */
+/*               means test (reading M1; 0 = off, needs N < 2^27)            */
+/*   sums_out:   K_act*4 int64 channel sums S[k][c] at the end, or NULL       */
 /* Returns K_act, or < 0 on invalid arguments.                                */
 /* ------------------------------------------------------------------------ */
 int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, int gamma, int iters,
                int schedule, int rule, const int32_t *init, int32_t *labels_out, int32_t *hist_out,
                int32_t *sizes_out, oracle_trace *trace, int trace_cap, int *trace_len,
-               int want_energy, uint64_t shuffle_seed, int max_subsweeps)
+               int want_energy, uint64_t shuffle_seed, int max_subsweeps, int means_iters,
+               int64_t *sums_out)
 {
     if (W < 1 || H < 1 || C < 1 || C > 4 || K < 1 || L < 0 || bpc < 1 || bpc > 256 || iters < 0)
+        return -1;
+    if (means_iters < 0 || means_iters > iters || (means_iters > 0 && (int64_t)W * H >= ((int64_t)1 << 27)))
         return -1;
     st_t s;
     memset(&s, 0, sizeof s);
@@ -601,12 +662,15 @@ int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, i
     s.trace = trace; s.trace_cap = trace ? trace_cap : 0; s.want_energy = want_energy;
     s.rng = shuffle_seed;
     s.max_subsweeps = max_subsweeps;
+    s.img = img;
+    s.means_iters = means_iters;
     int64_t N = (int64_t)W * H;
     s.bin = (int *)malloc(sizeof(int) * N);
     s.lab = (int *)malloc(sizeof(int) * N);
     s.hist = (int64_t *)calloc((size_t)s.K * s.B, sizeof(int64_t));
     s.size = (int64_t *)calloc(s.K, sizeof(int64_t));
     s.lblock = (int64_t *)malloc(sizeof(int64_t) * s.B);
+    s.msum = (int64_t *)calloc((size_t)s.K * 4, sizeof(int64_t));
     s.x0 = (int *)malloc(sizeof(int) * (s.GX + 1));
     s.y0 = (int *)malloc(sizeof(int) * (s.GY + 1));
     /* level-0 block column i spans [floor(i W / GX), floor((i+1) W / GX)) */
@@ -677,7 +741,12 @@ int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, i
     if (sizes_out)
         for (int k = 0; k < s.K; k++) sizes_out[k] = (int32_t)s.size[k];
     if (trace_len) *trace_len = s.trace_len;
+    if (sums_out) {
+        if (!s.means_on) means_recount(&s);
+        for (int64_t i = 0; i < (int64_t)s.K * 4; i++) sums_out[i] = s.msum[i];
+    }
     free(s.bin); free(s.lab); free(s.hist); free(s.size); free(s.lblock); free(s.x0); free(s.y0);
+    free(s.msum);
     return s.K;
 }
 
@@ -737,4 +806,11 @@ int oracle_smooth_sum(const int32_t *lab, int W, int H, int x, int y, int k, int
     int S = smooth_sum(l, W, H, x, y, k, n);
     free(l);
     return S;
+}
+
+/* The means test (reading M1) on one proposal: pixel colour v (C channels),
+ * channel sums Sk, Sn and sizes Ak, An of k (p counted in k) and n. */
+int oracle_means_test(const uint8_t *v, int C, const int64_t *Sk, int64_t Ak, const int64_t *Sn, int64_t An)
+{
+    return means_test(v, C, Sk, Ak, Sn, An);
 }
