@@ -143,6 +143,30 @@ seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *out);
 seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int32_t *sizes_out,
                               void *stream);
 
+/* seeds_set_means_iters -- means post-processing (SPM: "the
+ * mean-based distance measure from SLIC"; "running the last
+ * few pixel-level updates based on means").  The last means_iters of the
+ * iters_per_level pixel iterations of every later run accept a move k -> n
+ * of pixel p iff p's colour is strictly nearer (squared Euclidean distance
+ * over the channels, exact integers) to n's mean colour than to k's, the
+ * means taken from the sub-sweep's snapshot, together with Prop. 2 when
+ * smoothness_prior = 1 (reading M1).  0 (the default)
+ * turns it off; n_levels = 0 with means_iters = iters_per_level is the
+ * paper's SPM baseline.
+ *   SEEDS_EINVAL  means_iters outside [0, iters_per_level], or a row-band ctx
+ *   SEEDS_ERANGE  width*height >= 2^27 (the exact comparison needs < 2^128)
+ *   SEEDS_ESTATE  the ctx is forced to graph or resident mode (grid mode only;
+ *                 a later run also fails with SEEDS_ESTATE if no grid plan fits) */
+seeds_status seeds_set_means_iters(seeds_ctx *ctx, int means_iters);
+
+/* seeds_read_sums -- after a run with means post-processing: copy frame
+ * `frame`'s per-superpixel channel sums S[k][c] = sum of channel c over the
+ * pixels of k (for parity tests).
+ *   sums_out  device, K_act*4 int64 (channels >= C are 0)
+ * Synchronises `stream`.  SEEDS_ESTATE if the last run had no means
+ * iterations, before any run, or if frame is outside the last batch. */
+seeds_status seeds_read_sums(seeds_ctx *ctx, int frame, int64_t *sums_out, void *stream);
+
 /* seeds_debug_limit -- stop every later run after max_subsweeps sub-sweeps
  * (the block maps are still pushed down and expanded, so the labels are the
  * valid partition reached at that point); -1 turns the limit off.  Used to

@@ -31,10 +31,11 @@ struct GraphKey {
     int limit = -2;
     bool prof = false;
     int mode = -1;
+    int miters = 0;
     bool operator==(const GraphKey &o) const
     {
         return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof &&
-               mode == o.mode;
+               mode == o.mode && miters == o.miters;
     }
 };
 
@@ -58,6 +59,7 @@ struct seeds_ctx {
     uint16_t *d_M[2] = {nullptr, nullptr};
     int *d_H[2] = {nullptr, nullptr};
     int *d_A[2] = {nullptr, nullptr};
+    long long *d_S[2] = {nullptr, nullptr};  // means post-processing: channel sums, 4 per superpixel (grid mode)
     Rec *d_rec[2] = {nullptr, nullptr};
     int *d_cnt = nullptr;    // (S + 1) rows x cap_frames: delta entries per sub-sweep
     int *d_moves = nullptr;  // (S + 1) rows x cap_frames: accepted units per sub-sweep
@@ -79,6 +81,8 @@ struct seeds_ctx {
     unsigned long long tick = 0;
     // state of the last run
     int limit = -1;
+    int miters = 0;       // seeds_set_means_iters (reading M1)
+    int last_miters = 0;  // of the last run
     int last_nf = 0;
     int last_final = 0;  // H buffer holding the final state
     int last_done = 0;   // sub-sweeps run
@@ -290,6 +294,7 @@ static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
         release((void *&)ctx->d_M[i]);
         release((void *&)ctx->d_H[i]);
         release((void *&)ctx->d_A[i]);
+        release((void *&)ctx->d_S[i]);
         release((void *&)ctx->d_rec[i]);
     }
     release((void *&)ctx->d_cnt);
@@ -305,6 +310,7 @@ static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
         CK(cudaMalloc(&ctx->d_M[i], F * ctx->map_fs * 2));
         CK(cudaMalloc(&ctx->d_H[i], F * ctx->H_fs * 4));
         CK(cudaMalloc(&ctx->d_A[i], F * ctx->Afs * 4));
+        CK(cudaMalloc(&ctx->d_S[i], F * ctx->Afs * 4 * sizeof(long long)));
         CK(cudaMalloc(&ctx->d_rec[i], F * ctx->rec_fs * sizeof(Rec)));
     }
     release((void *&)ctx->d_labp);
@@ -508,10 +514,10 @@ static int resolved_mode(seeds_ctx *c, int nf)
 // they fit (else of one tile, restaged every sub-sweep), the unit queue, the
 // warp tables of the large-block path and the block geometry.
 // ---------------------------------------------------------------------------
-template <typename BinT, int GAMMA, int P, int NT>
-static int grid_occupancy(size_t smem)
+template <typename BinT, int GAMMA, int P, int NT, int MEANS>
+static int grid_occupancy_m(size_t smem)
 {
-    auto k = k_grid<BinT, GAMMA, P, NT>;
+    auto k = k_grid<BinT, GAMMA, P, NT, MEANS>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -522,6 +528,12 @@ static int grid_occupancy(size_t smem)
         return 0;
     }
     return n;
+}
+// both variants (with and without the means post-processing) get the opt-in
+template <typename BinT, int GAMMA, int P, int NT>
+static int grid_occupancy(size_t smem)
+{
+    return std::min(grid_occupancy_m<BinT, GAMMA, P, NT, 0>(smem), grid_occupancy_m<BinT, GAMMA, P, NT, 1>(smem));
 }
 
 template <int NT>
@@ -838,7 +850,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     return false;
 }
 
-template <typename BinT, int GAMMA, int P, int NT>
+template <typename BinT, int GAMMA, int P, int NT, int MEANS>
 static cudaError_t launch_grid_t(seeds_ctx *ctx, const GridParams &q, cudaStream_t st)
 {
     cudaLaunchConfig_t cfg = {};
@@ -851,7 +863,17 @@ static cudaError_t launch_grid_t(seeds_ctx *ctx, const GridParams &q, cudaStream
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_grid<BinT, GAMMA, P, NT>, q);
+    return cudaLaunchKernelEx(&cfg, k_grid<BinT, GAMMA, P, NT, MEANS>, q);
+}
+
+template <int NT, int MEANS>
+static cudaError_t launch_grid_nt(seeds_ctx *ctx, const GridParams &q, cudaStream_t st)
+{
+    if (ctx->bb == 1)
+        return ctx->gamma ? launch_grid_t<uint8_t, 1, 3, NT, MEANS>(ctx, q, st)
+                          : launch_grid_t<uint8_t, 0, 2, NT, MEANS>(ctx, q, st);
+    return ctx->gamma ? launch_grid_t<uint16_t, 1, 3, NT, MEANS>(ctx, q, st)
+                      : launch_grid_t<uint16_t, 0, 2, NT, MEANS>(ctx, q, st);
 }
 
 // Enqueue one grid-mode run: zero the histograms, move counters and the barrier
@@ -863,6 +885,8 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
         CK(cudaMemsetAsync(ctx->d_H[i], 0, (size_t)nf * ctx->H_fs * 4, st));
         CK(cudaMemsetAsync(ctx->d_A[i], 0, (size_t)nf * ctx->Afs * 4, st));
     }
+    if (ctx->miters > 0)
+        for (int i = 0; i < 2; i++) CK(cudaMemsetAsync(ctx->d_S[i], 0, (size_t)nf * ctx->Afs * 4 * sizeof(long long), st));
     CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)(ctx->S + 1) * nf * 4, st));
     CK(cudaMemsetAsync(ctx->d_sync, 0, 16, st));
     GridParams q = ctx->gp;
@@ -878,6 +902,10 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     }
     q.H_fs = ctx->H_fs;
     q.A_fs = ctx->Afs;
+    q.Sb[0] = ctx->d_S[0];
+    q.Sb[1] = ctx->d_S[1];
+    q.S_fs = ctx->Afs * 4;
+    q.miters = ctx->miters;
     q.moves = ctx->d_moves;
     q.sync = ctx->d_sync;
     q.trace = ctx->d_trace;
@@ -885,15 +913,10 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
     cudaError_t e;
     if (ctx->grid_nt == GRID_THREADS)
-        e = ctx->bb == 1 ? (ctx->gamma ? launch_grid_t<uint8_t, 1, 3, GRID_THREADS>(ctx, q, st)
-                                       : launch_grid_t<uint8_t, 0, 2, GRID_THREADS>(ctx, q, st))
-                         : (ctx->gamma ? launch_grid_t<uint16_t, 1, 3, GRID_THREADS>(ctx, q, st)
-                                       : launch_grid_t<uint16_t, 0, 2, GRID_THREADS>(ctx, q, st));
+        e = ctx->miters > 0 ? launch_grid_nt<GRID_THREADS, 1>(ctx, q, st) : launch_grid_nt<GRID_THREADS, 0>(ctx, q, st);
     else
-        e = ctx->bb == 1 ? (ctx->gamma ? launch_grid_t<uint8_t, 1, 3, GRID_THREADS_SMALL>(ctx, q, st)
-                                       : launch_grid_t<uint8_t, 0, 2, GRID_THREADS_SMALL>(ctx, q, st))
-                         : (ctx->gamma ? launch_grid_t<uint16_t, 1, 3, GRID_THREADS_SMALL>(ctx, q, st)
-                                       : launch_grid_t<uint16_t, 0, 2, GRID_THREADS_SMALL>(ctx, q, st));
+        e = ctx->miters > 0 ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
+                            : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid launch");
     CK(prof_end(ctx, st));
     const bool blocks = init == nullptr && ctx->L > 0;
@@ -1122,6 +1145,11 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     seeds_status r = ensure_frames(ctx, nf);
     if (r != SEEDS_OK) return r;
     const int mode = resolved_mode(ctx, nf);
+    if (ctx->miters > 0 && mode != SEEDS_MODE_GRID) {
+        snprintf(ctx->err, sizeof ctx->err, "the means post-processing runs in grid mode only, and no grid plan fits");
+        return SEEDS_ESTATE;
+    }
+    ctx->last_miters = ctx->miters;
     if (mode == SEEDS_MODE_RESIDENT) {
         ctx->ev_used = 0;
         r = run_resident(ctx, img, init, out, nf, st);
@@ -1133,6 +1161,7 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     GraphKey key;
     key.img = img; key.init = init; key.out = out; key.nf = nf; key.limit = ctx->limit; key.prof = ctx->prof;
     key.mode = mode;
+    key.miters = ctx->miters;
     seeds_ctx::GraphEntry *hit = nullptr;
     for (auto &g : ctx->graphs)
         if (g.key == key) hit = &g;
@@ -1360,6 +1389,10 @@ seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out,
 seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 {
     if (!ctx || mode < SEEDS_MODE_AUTO || mode > SEEDS_MODE_GRID) return SEEDS_EINVAL;
+    if (ctx->miters > 0 && (mode == SEEDS_MODE_GRAPH || mode == SEEDS_MODE_RESIDENT)) {
+        snprintf(ctx->err, sizeof ctx->err, "the means post-processing runs in grid mode only");
+        return SEEDS_ESTATE;
+    }
     if (mode == SEEDS_MODE_RESIDENT && ctx->cluster == 0) {
         snprintf(ctx->err, sizeof ctx->err, "the frame does not fit a co-schedulable cluster (resident mode)");
         return SEEDS_ESTATE;
@@ -1398,6 +1431,35 @@ seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps)
     return SEEDS_OK;
 }
 
+seeds_status seeds_set_means_iters(seeds_ctx *ctx, int means_iters)
+{
+    if (!ctx || means_iters < 0 || means_iters > ctx->iters) return SEEDS_EINVAL;
+    if (means_iters > 0) {
+        if (ctx->banded) {
+            snprintf(ctx->err, sizeof ctx->err, "the means post-processing is not available in row-band mode");
+            return SEEDS_EINVAL;
+        }
+        if (ctx->N >= (1LL << 27)) return SEEDS_ERANGE;
+        if (ctx->mode == SEEDS_MODE_GRAPH || ctx->mode == SEEDS_MODE_RESIDENT) {
+            snprintf(ctx->err, sizeof ctx->err, "the means post-processing runs in grid mode only");
+            return SEEDS_ESTATE;
+        }
+    }
+    ctx->miters = means_iters;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_read_sums(seeds_ctx *ctx, int frame, int64_t *sums_out, void *stream)
+{
+    if (!ctx || !sums_out) return SEEDS_EINVAL;
+    if (!ctx->ran || frame < 0 || frame >= ctx->last_nf || ctx->last_miters == 0) return SEEDS_ESTATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(sums_out, ctx->d_S[ctx->last_final] + (size_t)frame * ctx->Afs * 4,
+                       (size_t)ctx->K * 4 * sizeof(long long), cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return SEEDS_OK;
+}
+
 seeds_status seeds_sync(seeds_ctx *ctx, void *stream)
 {
     if (!ctx) return SEEDS_EINVAL;
@@ -1412,7 +1474,7 @@ void seeds_destroy(seeds_ctx *ctx)
     cudaDeviceSynchronize();
     drop_graphs(ctx);
     void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
-                    ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1],
+                    ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1], ctx->d_S[0], ctx->d_S[1],
                     ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band, ctx->d_kmap,
                     ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp, ctx->d_bcount,
                     ctx->d_init_stage, ctx->d_out_stage};
@@ -1545,15 +1607,10 @@ seeds_status seeds_band_subsweep(seeds_ctx *ctx, int s, const void *records_in, 
     q.rec_count = n_out;
     cudaError_t e;
     if (ctx->grid_nt == GRID_THREADS)
-        e = ctx->bb == 1 ? (ctx->gamma ? launch_grid_t<uint8_t, 1, 3, GRID_THREADS>(ctx, q, st)
-                                       : launch_grid_t<uint8_t, 0, 2, GRID_THREADS>(ctx, q, st))
-                         : (ctx->gamma ? launch_grid_t<uint16_t, 1, 3, GRID_THREADS>(ctx, q, st)
-                                       : launch_grid_t<uint16_t, 0, 2, GRID_THREADS>(ctx, q, st));
+        e = ctx->miters > 0 ? launch_grid_nt<GRID_THREADS, 1>(ctx, q, st) : launch_grid_nt<GRID_THREADS, 0>(ctx, q, st);
     else
-        e = ctx->bb == 1 ? (ctx->gamma ? launch_grid_t<uint8_t, 1, 3, GRID_THREADS_SMALL>(ctx, q, st)
-                                       : launch_grid_t<uint8_t, 0, 2, GRID_THREADS_SMALL>(ctx, q, st))
-                         : (ctx->gamma ? launch_grid_t<uint16_t, 1, 3, GRID_THREADS_SMALL>(ctx, q, st)
-                                       : launch_grid_t<uint16_t, 0, 2, GRID_THREADS_SMALL>(ctx, q, st));
+        e = ctx->miters > 0 ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
+                            : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid (band) launch");
     ctx->last_done = s + 1;
     return SEEDS_OK;

@@ -46,7 +46,9 @@ struct GridTile {
     int pad;
 };
 
-// A histogram delta of frame f (grid mode): k | n << 16, bin | count << 16.
+// A histogram delta of frame f (grid mode): k | n << 16, bin | count << 16;
+// `pad` carries the moved pixel's colour (one byte per channel) in the means
+// sub-sweeps.
 struct GRec {
     uint32_t kn, bc, f, pad;
 };
@@ -68,6 +70,9 @@ struct GridParams {
     long long N;
     int *Hb[2], *Ab[2];
     long long H_fs, A_fs;  // frame strides (A_fs = K rounded up to 4: 16-byte aligned frames)
+    long long *Sb[2];      // means post-processing: channel sums S[k][c] (4 per superpixel), double buffered
+    long long S_fs;        // their frame stride (4 A_fs)
+    int miters;            // the last miters pixel iterations use the means test (reading M1)
     int *moves;            // (S + 1) x nf accepted units per sub-sweep
     unsigned *sync;        // grid barrier counter (zero at launch)
     long long *trace;      // debug: per CTA, per phase (clock64 at work end, after barrier), or nullptr
@@ -294,7 +299,44 @@ __device__ __forceinline__ void gdelta(const GridParams &q, int buf, int f, int 
     atomicAdd(A + n, count);
 }
 
-template <typename BinT, int GAMMA, int P, int NT>
+// Channel-sum deltas of a pixel of colour `rgba` (one byte per channel) moved
+// k -> n (means sub-sweeps, reading M1).
+__device__ __forceinline__ void gdelta_s(const GridParams &q, int buf, int f, int k, int n, uint32_t rgba)
+{
+    unsigned long long *S = reinterpret_cast<unsigned long long *>((buf ? q.Sb[1] : q.Sb[0]) + (long long)f * q.S_fs);
+    for (int c = 0; c < q.C; c++) {
+        const unsigned long long v = (rgba >> (8 * c)) & 0xFF;
+        atomicAdd(S + (long long)k * 4 + c, (unsigned long long)(-(long long)v));
+        atomicAdd(S + (long long)n * 4 + c, v);
+    }
+}
+
+// Squared distance of colour v to the mean S / A, scaled by A^2 (exact, 128
+// bits): sum_c (A v_c - S_c)^2.  |A v_c - S_c| <= 255 A < 2^35 for A < 2^27.
+struct U128 {
+    unsigned long long lo, hi;
+};
+__device__ __forceinline__ U128 scaled_sqdist(uint32_t rgba, int C, const long long *S, long long A)
+{
+    U128 r{0, 0};
+#pragma unroll 1
+    for (int c = 0; c < C; c++) {
+        const long long e = A * (long long)((rgba >> (8 * c)) & 0xFF) - __ldcg(S + c);
+        const unsigned long long a = (unsigned long long)(e < 0 ? -e : e);
+        const unsigned long long lo = a * a, hi = __umul64hi(a, a);
+        r.lo += lo;
+        r.hi += hi + (r.lo < lo);
+    }
+    return r;
+}
+// x * m for x < 2^72 and a product below 2^128
+__device__ __forceinline__ U128 mul_u128(U128 x, unsigned long long m)
+{
+    return U128{x.lo * m, __umul64hi(x.lo, m) + x.hi * m};
+}
+__device__ __forceinline__ bool lt_u128(U128 a, U128 b) { return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo); }
+
+template <typename BinT, int GAMMA, int P, int NT, int MEANS>
 __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_constant__ GridParams qp)
 {
     extern __shared__ __align__(128) uint32_t smem[];
@@ -322,6 +364,11 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     unsigned phase0 = 0, phase1 = 0;  // parity of the next completion of each stage buffer
+    // sub-sweep s belongs to the means post-processing (reading M1); computed
+    // from the parameters each time so that nothing stays live across the run
+    auto means_sub = [&](int s_) {
+        return MEANS && s_ >= (q.init == nullptr && q.L > 0 ? 4 * q.L * q.iters : 0) + (q.iters - q.miters) * P * P;
+    };
     __syncthreads();
 
     // ---- seed: bins (reading Q1), labels (grid, or warm
@@ -401,6 +448,7 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
         for (int e = tid; e < nrec; e += NT) {
             const GRec x = r[e];
             gdelta(q, yb, (int)x.f, x.kn & 0xFFFF, x.kn >> 16, x.bc & 0xFFFF, x.bc >> 16);
+            if (means_sub(s - 1)) gdelta_s(q, yb, (int)x.f, x.kn & 0xFFFF, x.kn >> 16, x.pad);
         }
         if (tid == 0 && !q.band) c.misc[yb ^ 1] = 0;  // list yb^1 was last read before the barrier
         __syncthreads();  // the reset precedes every append of this sub-sweep
@@ -819,6 +867,43 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                 continue;
             }
             if (q.s1 >= 0 && s >= q.s1) break;
+            if (MEANS && it == q.iters - q.miters && col == 0) {
+                // channel sums S[k][c] of the current labels into both buffers
+                // (reading M1), warp-aggregated per label
+                for (int ti = 0; ti < ntl; ti++) {
+                    const GridTile t = c.tiles[ti];
+                    const uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
+                    const long long fN = (long long)t.f * q.N;
+                    unsigned long long *S0 = reinterpret_cast<unsigned long long *>(q.Sb[0] + (long long)t.f * q.S_fs);
+                    unsigned long long *S1 = reinterpret_cast<unsigned long long *>(q.Sb[1] + (long long)t.f * q.S_fs);
+                    for (int y = t.Y0 + wid; y < t.Y1; y += NW)
+                        for (int x0 = t.X0; x0 < t.X1; x0 += 32) {
+                            const int x = x0 + lane;
+                            int k = -1;
+                            uint32_t rgba = 0;
+                            if (x < t.X1) {
+                                k = __ldcg(gl + (long long)(y + 2) * q.lpitch + x + 2);
+                                const uint8_t *px = q.img + (fN + (long long)y * W + x) * q.C;
+                                for (int ch = 0; ch < q.C; ch++) rgba |= (uint32_t)px[ch] << (8 * ch);
+                            }
+                            unsigned todo = __ballot_sync(FULL, k >= 0);
+                            while (todo) {
+                                const int kl = __shfl_sync(FULL, k, __ffs(todo) - 1);
+                                const bool mine = k == kl;
+                                todo &= ~__ballot_sync(FULL, mine);
+#pragma unroll 1
+                                for (int ch = 0; ch < q.C; ch++) {
+                                    const unsigned sum = __reduce_add_sync(FULL, mine ? (rgba >> (8 * ch)) & 0xFF : 0u);
+                                    if (lane == 0) {
+                                        atomicAdd(S0 + (long long)kl * 4 + ch, (unsigned long long)sum);
+                                        atomicAdd(S1 + (long long)kl * 4 + ch, (unsigned long long)sum);
+                                    }
+                                }
+                            }
+                        }
+                }
+                grid_barrier(q.sync, target);
+            }
             const int cx = col % P, cy = col / P;
             const int ob = q.band ? 0 : s & 1, yb_ = ob ^ 1;
             begin_subsweep(yb_);
@@ -899,6 +984,38 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                         u.An[d] = c.ldA(ob, n);
                     }
                 };
+                // Prop. 2 for every candidate (bit d: candidate d passes; reads only
+                // the staged labels)
+                auto prop2 = [&](const PixUnit &u) -> int {
+                    int smok = 0xF;
+                    if (GAMMA) {
+                        // one pass over the 5x5 window builds the bit masks of k and of
+                        // the four candidates (bit (dy + 2) * 5 + dx + 2)
+                        uint32_t mk = 0, mn[4] = {0, 0, 0, 0};
+                        const uint16_t *a = c.cell(u.xy & 0xFFFF, u.xy >> 16);
+#pragma unroll
+                        for (int dy = -2; dy <= 2; dy++)
+#pragma unroll
+                            for (int dx = -2; dx <= 2; dx++) {
+                                const int lb = a[dy * sp + dx], bit = (dy + 2) * 5 + dx + 2;
+                                mk |= (uint32_t)(lb == u.k) << bit;
+#pragma unroll
+                                for (int d = 0; d < 4; d++) mn[d] |= (uint32_t)(lb == u.v[d]) << bit;
+                            }
+                        const uint32_t vx = ((u.xy & 0xFFFF) > 0 ? 1u : 0u) | 2u | ((u.xy & 0xFFFF) + 1 < W ? 4u : 0u);
+                        const uint32_t vy = ((u.xy >> 16) > 0 ? 1u : 0u) | 2u | ((u.xy >> 16) + 1 < q.H ? 4u : 0u);
+                        uint32_t centres = 0;
+#pragma unroll
+                        for (int iy = 0; iy < 3; iy++)
+                            if (vy >> iy & 1) centres |= vx << (3 * iy);
+                        const int base_s = __popc(centres) - box_sum(mk, centres);
+                        smok = 0;
+#pragma unroll
+                        for (int d = 0; d < 4; d++)
+                            if (u.valid >> d & 1) smok |= (int)(base_s + box_sum(mn[d], centres) >= 0) << d;
+                    }
+                    return smok;
+                };
                 auto pix_decide = [&](PixUnit &u) {
                     if (!u.valid) return;
                     // Prop. 2 for every candidate while the gathers are in flight (it
@@ -954,7 +1071,74 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                         c.set(u.xy & 0xFFFF, u.xy >> 16, u.acc);
                     }
                 };
-                if (GAMMA || nq <= NT) {  // (two entries per thread would spill with the Prop.-2 masks)
+                if (MEANS && it >= q.iters - q.miters) {
+                    // means sub-sweep (reading M1): one thread per unit; the first
+                    // candidate (W, E, N, S) whose mean colour is strictly nearer
+                    // than k's and that passes Prop. 2
+                    for (int base = wid * 32; base < nq; base += NT) {
+                        PixUnit u;
+                        u.valid = 0;
+                        u.acc = -1;
+                        u.k = 0;
+                        u.j = 0;
+                        u.xy = 0;
+                        uint32_t rgba = 0;
+                        const int e = base + lane;
+                        if (e < nq) {
+                            int x, y;
+                            if (direct) {
+                                unit_xy(e, x, y);
+                            } else {
+                                const uint32_t v = c.queue[e];
+                                x = t.X0 + (int)(v & 0xFFFF);
+                                y = t.Y0 + (int)(v >> 16);
+                            }
+                            u.xy = x | y << 16;
+                            const uint16_t *a = c.cell(x, y);
+                            u.k = a[0];
+                            const Neigh nb = ring_at(a, sp, 1, sp);
+                            if (nb.valid && c.removable_s(nb.mask)) {
+                                u.valid = nb.valid;
+                                u.j = c.bin(x, y);
+#pragma unroll
+                                for (int d = 0; d < 4; d++) u.v[d] = nb.v[d];
+                                const uint8_t *px = q.img + ((long long)c.f * q.N + (long long)y * W + x) * q.C;
+                                for (int ch = 0; ch < q.C; ch++) rgba |= (uint32_t)px[ch] << (8 * ch);
+                            }
+                        }
+                        if (u.valid) {
+                            const int smok = prop2(u);
+                            const long long *S = q.Sb[ob] + (long long)c.f * q.S_fs;
+                            const long long Ak = c.ldA(ob, u.k);
+                            const U128 dk = scaled_sqdist(rgba, q.C, S + (long long)u.k * 4, Ak);
+#pragma unroll 1
+                            for (int d = 0; d < 4; d++) {
+                                const int n = d == 0 ? u.v[0] : d == 1 ? u.v[1] : d == 2 ? u.v[2] : u.v[3];
+                                if (u.acc < 0 && (u.valid >> d & 1) && (smok >> d & 1)) {
+                                    const long long An = c.ldA(ob, n);
+                                    const U128 dn = scaled_sqdist(rgba, q.C, S + (long long)n * 4, An);
+                                    if (lt_u128(mul_u128(dn, (unsigned long long)(Ak * Ak)),
+                                                mul_u128(dk, (unsigned long long)(An * An))))
+                                        u.acc = n;
+                                }
+                            }
+                        }
+                        const unsigned mv = __ballot_sync(FULL, u.acc >= 0);
+                        int slot = 0;
+                        if (lane == 0 && mv) {
+                            slot = atomicAdd(rcount(ob), __popc(mv));
+                            atomicAdd(&q.moves[(long long)(s + 1) * q.nf + c.f], __popc(mv));
+                        }
+                        slot = __shfl_sync(FULL, slot, 0) + __popc(mv & ((1u << lane) - 1));
+                        if (u.acc >= 0) {
+                            rec_list(ob)[slot] = GRec{(uint32_t)u.k | ((uint32_t)u.acc << 16), (uint32_t)u.j | (1u << 16),
+                                                      (uint32_t)c.f, rgba};
+                            gdelta(q, yb_, c.f, u.k, u.acc, u.j, 1);
+                            gdelta_s(q, yb_, c.f, u.k, u.acc, rgba);
+                            c.set(u.xy & 0xFFFF, u.xy >> 16, u.acc);
+                        }
+                    }
+                } else if (GAMMA || nq <= NT) {  // (two entries per thread would spill with the Prop.-2 masks)
                     for (int base = wid * 32; base < nq; base += NT) {
                         PixUnit u;
                         pix_load(base + lane, u);

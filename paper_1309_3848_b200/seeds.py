@@ -23,7 +23,8 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_read_state", "seeds_debug_limit", "seeds_stats", "seeds_sync", "seeds_destroy",
            "seeds_profile", "seeds_profile_collect", "seeds_set_mode", "seeds_debug_trace",
            "seeds_status_string", "seeds_last_error", "seeds_create_banded", "seeds_band_info",
-           "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish"]
+           "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish",
+           "seeds_set_means_iters", "seeds_read_sums"]
 
 
 class SeedsError(RuntimeError):
@@ -60,6 +61,8 @@ def load(path: str = LIB_PATH):
         "seeds_query": ([vp, ctypes.POINTER(Info)], i),
         "seeds_read_state": ([vp, i, vp, vp, vp], i),
         "seeds_debug_limit": ([vp, i], i),
+        "seeds_set_means_iters": ([vp, i], i),
+        "seeds_read_sums": ([vp, i, vp, vp], i),
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
         "seeds_profile": ([vp, i], i),
@@ -245,6 +248,19 @@ class Seeds:
         out = np.zeros(n, np.int64)
         self._check(self._lib.seeds_debug_trace(self._ctx, int(enable), out.ctypes.data if enable else None, n))
         return out.reshape(cs, self.info.subsweeps + 4, 16)
+
+    def set_means_iters(self, means_iters: int):
+        """The last means_iters pixel iterations use the means test (SPM
+        post-processing, include/seeds.h seeds_set_means_iters)."""
+        self._check(self._lib.seeds_set_means_iters(self._ctx, int(means_iters)))
+
+    def read_sums(self, frame: int = 0, stream=None):
+        """(K_act, 4) int64 CUDA tensor: channel sums S[k][c] after the last run
+        (means post-processing only)."""
+        import torch
+        out = torch.empty((self.info.k_actual, 4), dtype=torch.int64, device="cuda")
+        self._check(self._lib.seeds_read_sums(self._ctx, frame, out.data_ptr(), _stream_ptr(stream)))
+        return out
 
     def debug_limit(self, max_subsweeps: int):
         self._check(self._lib.seeds_debug_limit(self._ctx, max_subsweeps))
