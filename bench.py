@@ -321,12 +321,15 @@ def oracle_frames(imgs, p, workers):
         list(ex.map(lambda img: oracle.run(img, **p), list(imgs)))
 
 
-def cpu_baseline(name, budget_s=10.0):
+def cpu_baseline(name, budget_s=10.0, means_iters=0):
     """The oracle as it stands (COL schedule) on a bounded sample: one thread
     on single-frame configs (the paper's setting); frame-parallel on all host
     cores for the batch configs c3 and c4, with the one-thread figure beside it."""
     import oracle
     imgs, p, note = reference_sample(name)
+    if means_iters:
+        p = dict(p, means_iters=means_iters)
+        note += f", last {means_iters} pixel iterations on means"
     oracle.build()
     n, px, t0 = 0, 0, time.perf_counter()
     while True:
@@ -343,6 +346,8 @@ def cpu_baseline(name, budget_s=10.0):
         return single
     workers = host_cores()
     imgs, p, note = parallel_sample(name, workers)
+    if means_iters:
+        p = dict(p, means_iters=means_iters)
     t0 = time.perf_counter()
     oracle_frames(imgs, p, workers)
     el = time.perf_counter() - t0
@@ -367,6 +372,9 @@ def run_reference(args):
     else:
         imgs, p, note = reference_sample(name)
         batches = [imgs[i:i + 1] for i in range(len(imgs))]
+    if args.means_iters:
+        p = dict(p, means_iters=args.means_iters)
+        note += f", last {args.means_iters} pixel iterations on means"
     for i in range(args.warmup):
         oracle_frames(batches[i % len(batches)][:1], p, 1)
     t, px = [], 0
@@ -402,6 +410,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--bands", action="store_true", help="c5: row-band mode even on one rank")
+    ap.add_argument("--means-iters", type=int, default=0,
+                    help="SPM means post-processing: the last M pixel iterations use the means test (reading M1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -431,6 +441,8 @@ def main():
     s = wl.make_context()
     if not banded:
         s.set_mode(args.mode)
+        if args.means_iters:
+            s.set_means_iters(args.means_iters)
     info = s.info
     stream = torch.cuda.current_stream()
     wl.setup(torch, s)
@@ -549,6 +561,7 @@ def main():
             "config": {"workload": wl.describe(info),
                        "frames_per_step_per_rank": wl.frames_per_step,
                        "exec_mode": mode_name,
+                       "means_iters": args.means_iters,
                        "grid_ctas": info.grid_ctas, "grid_tiles_per_frame": info.grid_tiles,
                        "parallelism": wl.parallelism,
                        "exchange": "NCCL all-gather of delta records + halo send/recv per sub-sweep" if banded else None,
@@ -564,7 +577,7 @@ def main():
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget)
+            line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget, args.means_iters)
         out = json.dumps(line)
         print(out)
         if args.json_out:
