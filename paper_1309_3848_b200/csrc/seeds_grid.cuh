@@ -313,15 +313,26 @@ __device__ __forceinline__ void gdelta_s(const GridParams &q, int buf, int f, in
 
 // Squared distance of colour v to the mean S / A, scaled by A^2 (exact, 128
 // bits): sum_c (A v_c - S_c)^2.  |A v_c - S_c| <= 255 A < 2^35 for A < 2^27.
+// All four channel slots: the unused ones hold v_c = 0 and S_c = 0.
 struct U128 {
     unsigned long long lo, hi;
 };
-__device__ __forceinline__ U128 scaled_sqdist(uint32_t rgba, int C, const long long *S, long long A)
+struct S4 {
+    long long c[4];
+};
+// one superpixel's channel sums: two 16-byte L2-coherent loads
+__device__ __forceinline__ S4 ld_sums(const long long *S, int k)
+{
+    const longlong2 *p = reinterpret_cast<const longlong2 *>(S + (long long)k * 4);
+    const longlong2 a = __ldcg(p), b = __ldcg(p + 1);
+    return S4{{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ U128 scaled_sqdist(uint32_t rgba, const S4 &S, long long A)
 {
     U128 r{0, 0};
-#pragma unroll 1
-    for (int c = 0; c < C; c++) {
-        const long long e = A * (long long)((rgba >> (8 * c)) & 0xFF) - __ldcg(S + c);
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const long long e = A * (long long)((rgba >> (8 * c)) & 0xFF) - S.c[c];
         const unsigned long long a = (unsigned long long)(e < 0 ? -e : e);
         const unsigned long long lo = a * a, hi = __umul64hi(a, a);
         r.lo += lo;
@@ -869,13 +880,26 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
             if (q.s1 >= 0 && s >= q.s1) break;
             if (MEANS && it == q.iters - q.miters && col == 0) {
                 // channel sums S[k][c] of the current labels into both buffers
-                // (reading M1), warp-aggregated per label
+                // (reading M1): warp-aggregated per label, then combined per CTA in a
+                // small direct-mapped table (key = frame << 16 | label) kept in the
+                // idle TMA stage buffers, so that one pair of global atomics per
+                // (label, channel) and CTA remains; a slot held by another key falls
+                // back to global atomics
+                constexpr unsigned EMPTY = 0xFFFFFFFFu;
+                int hn = 1;
+                while (hn < 1024 && (size_t)(2 * hn) * 40 <= (size_t)2 * q.stage_bytes) hn *= 2;
+                unsigned *hkey = reinterpret_cast<unsigned *>(c.stage0);
+                unsigned long long *hsum = reinterpret_cast<unsigned long long *>(hkey + hn);  // hn x 4
+                for (int i = tid; i < hn; i += NT) {
+                    hkey[i] = EMPTY;
+#pragma unroll
+                    for (int ch = 0; ch < 4; ch++) hsum[i * 4 + ch] = 0;
+                }
+                __syncthreads();
                 for (int ti = 0; ti < ntl; ti++) {
                     const GridTile t = c.tiles[ti];
                     const uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
                     const long long fN = (long long)t.f * q.N;
-                    unsigned long long *S0 = reinterpret_cast<unsigned long long *>(q.Sb[0] + (long long)t.f * q.S_fs);
-                    unsigned long long *S1 = reinterpret_cast<unsigned long long *>(q.Sb[1] + (long long)t.f * q.S_fs);
                     for (int y = t.Y0 + wid; y < t.Y1; y += NW)
                         for (int x0 = t.X0; x0 < t.X1; x0 += 32) {
                             const int x = x0 + lane;
@@ -891,16 +915,43 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                                 const int kl = __shfl_sync(FULL, k, __ffs(todo) - 1);
                                 const bool mine = k == kl;
                                 todo &= ~__ballot_sync(FULL, mine);
-#pragma unroll 1
-                                for (int ch = 0; ch < q.C; ch++) {
-                                    const unsigned sum = __reduce_add_sync(FULL, mine ? (rgba >> (8 * ch)) & 0xFF : 0u);
-                                    if (lane == 0) {
-                                        atomicAdd(S0 + (long long)kl * 4 + ch, (unsigned long long)sum);
-                                        atomicAdd(S1 + (long long)kl * 4 + ch, (unsigned long long)sum);
+                                unsigned sum[4];
+#pragma unroll
+                                for (int ch = 0; ch < 4; ch++)
+                                    sum[ch] = __reduce_add_sync(FULL, mine ? (rgba >> (8 * ch)) & 0xFF : 0u);
+                                if (lane == 0) {
+                                    const unsigned key = (unsigned)t.f << 16 | (unsigned)kl;
+                                    const int slot = (int)((key * 2654435761u) >> 8) & (hn - 1);
+                                    const unsigned old = atomicCAS(&hkey[slot], EMPTY, key);
+                                    if (old == EMPTY || old == key) {
+#pragma unroll
+                                        for (int ch = 0; ch < 4; ch++)
+                                            if (sum[ch]) atomicAdd(&hsum[slot * 4 + ch], (unsigned long long)sum[ch]);
+                                    } else {
+                                        unsigned long long *S0 = reinterpret_cast<unsigned long long *>(q.Sb[0] + (long long)t.f * q.S_fs);
+                                        unsigned long long *S1 = reinterpret_cast<unsigned long long *>(q.Sb[1] + (long long)t.f * q.S_fs);
+#pragma unroll
+                                        for (int ch = 0; ch < 4; ch++)
+                                            if (ch < q.C) {
+                                                atomicAdd(S0 + (long long)kl * 4 + ch, (unsigned long long)sum[ch]);
+                                                atomicAdd(S1 + (long long)kl * 4 + ch, (unsigned long long)sum[ch]);
+                                            }
                                     }
                                 }
                             }
                         }
+                }
+                __syncthreads();
+                for (int i = tid; i < hn; i += NT) {
+                    const unsigned key = hkey[i];
+                    if (key == EMPTY) continue;
+                    const int f = (int)(key >> 16), kl = (int)(key & 0xFFFF);
+                    unsigned long long *S0 = reinterpret_cast<unsigned long long *>(q.Sb[0] + (long long)f * q.S_fs);
+                    unsigned long long *S1 = reinterpret_cast<unsigned long long *>(q.Sb[1] + (long long)f * q.S_fs);
+                    for (int ch = 0; ch < q.C; ch++) {
+                        atomicAdd(S0 + (long long)kl * 4 + ch, hsum[i * 4 + ch]);
+                        atomicAdd(S1 + (long long)kl * 4 + ch, hsum[i * 4 + ch]);
+                    }
                 }
                 grid_barrier(q.sync, target);
             }
@@ -1106,21 +1157,29 @@ __global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_con
                                 for (int ch = 0; ch < q.C; ch++) rgba |= (uint32_t)px[ch] << (8 * ch);
                             }
                         }
-                        if (u.valid) {
-                            const int smok = prop2(u);
+                        // candidates passing Prop. 2, tested in order (W, E, N, S); the
+                        // first one's sums are gathered together with k's, later ones
+                        // (rare: most boundary pixels have one candidate) one at a time
+                        int cand = u.valid ? (u.valid & prop2(u)) : 0;
+                        if (cand) {
+                            auto pick = [&](int d) { return d == 0 ? u.v[0] : d == 1 ? u.v[1] : d == 2 ? u.v[2] : u.v[3]; };
                             const long long *S = q.Sb[ob] + (long long)c.f * q.S_fs;
-                            const long long Ak = c.ldA(ob, u.k);
-                            const U128 dk = scaled_sqdist(rgba, q.C, S + (long long)u.k * 4, Ak);
+                            const int n0 = pick(__ffs(cand) - 1);
+                            const S4 sk = ld_sums(S, u.k), s0 = ld_sums(S, n0);
+                            const long long Ak = c.ldA(ob, u.k), A0 = c.ldA(ob, n0);
+                            const U128 dk = scaled_sqdist(rgba, sk, Ak);
+                            const unsigned long long Ak2 = (unsigned long long)(Ak * Ak);
+                            if (lt_u128(mul_u128(scaled_sqdist(rgba, s0, A0), Ak2), mul_u128(dk, (unsigned long long)(A0 * A0))))
+                                u.acc = n0;
+                            cand &= cand - 1;
 #pragma unroll 1
-                            for (int d = 0; d < 4; d++) {
-                                const int n = d == 0 ? u.v[0] : d == 1 ? u.v[1] : d == 2 ? u.v[2] : u.v[3];
-                                if (u.acc < 0 && (u.valid >> d & 1) && (smok >> d & 1)) {
-                                    const long long An = c.ldA(ob, n);
-                                    const U128 dn = scaled_sqdist(rgba, q.C, S + (long long)n * 4, An);
-                                    if (lt_u128(mul_u128(dn, (unsigned long long)(Ak * Ak)),
-                                                mul_u128(dk, (unsigned long long)(An * An))))
-                                        u.acc = n;
-                                }
+                            while (u.acc < 0 && cand) {
+                                const int n = pick(__ffs(cand) - 1);
+                                const long long An = c.ldA(ob, n);
+                                if (lt_u128(mul_u128(scaled_sqdist(rgba, ld_sums(S, n), An), Ak2),
+                                            mul_u128(dk, (unsigned long long)(An * An))))
+                                    u.acc = n;
+                                cand &= cand - 1;
                             }
                         }
                         const unsigned mv = __ballot_sync(FULL, u.acc >= 0);

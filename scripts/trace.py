@@ -20,6 +20,8 @@ p = configs.params(cfg)
 s = Seeds(img.shape[1], img.shape[0], img.shape[2], *[p[k] for k in (
     "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
 s.set_mode(mode)
+if os.environ.get("MEANS_ITERS"):
+    s.set_means_iters(int(os.environ["MEANS_ITERS"]))
 s.debug_trace(True)
 d = torch.from_numpy(img).cuda()
 for _ in range(3):
@@ -57,3 +59,7 @@ for name, n in groups:
         line += " | " + " ".join(f"{k} {v[:, sl].mean():5.0f}/{v[:, sl].max(0).mean():5.0f}" for k, v in parts.items())
     print(line)
     i += n
+if os.environ.get("TRACE_S"):  # phases of chosen sub-sweeps (mean / max over CTAs)
+    for si in (int(v) for v in os.environ["TRACE_S"].split(",")):
+        print(f"sub-sweep {si}: work {work[:, si].mean():.0f}/{work[:, si].max():.0f} barrier {bar[:, si].mean():.0f} | "
+              + " ".join(f"{k} {v[:, si].mean():.0f}/{v[:, si].max():.0f}" for k, v in parts.items()))
