@@ -67,6 +67,8 @@ def lib():
             P(Trace), ctypes.c_int, P(ctypes.c_int), ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
             ctypes.c_int, ctypes.c_void_p,
         ]
+        _lib.oracle_metrics.restype = ctypes.c_int
+        _lib.oracle_metrics.argtypes = [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int] * 5 + [ctypes.c_void_p]
         _lib.oracle_means_test.restype = ctypes.c_int
         _lib.oracle_means_test.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                            ctypes.c_void_p, ctypes.c_int64]
@@ -195,3 +197,17 @@ def means_test(v, Sk, Ak: int, Sn, An: int) -> bool:
     Sk = np.zeros(4, np.int64) + np.pad(np.asarray(Sk, np.int64), (0, 4 - C))
     Sn = np.zeros(4, np.int64) + np.pad(np.asarray(Sn, np.int64), (0, 4 - C))
     return bool(lib().oracle_means_test(v.ctypes.data, C, Sk.ctypes.data, int(Ak), Sn.ctypes.data, int(An)))
+
+
+def metrics(labels, gt, K: int, R: int, eps: int = 2) -> dict:
+    """Quality metrics of a partition against ground-truth segments (SURVEY
+    8(f) rank 2): integer numerators and the ratios."""
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    gt = np.ascontiguousarray(gt, dtype=np.int32)
+    H, W = labels.shape
+    out = np.zeros(7, np.int64)
+    if lib().oracle_metrics(labels.ctypes.data, gt.ctypes.data, W, H, int(K), int(R), int(eps), out.ctypes.data):
+        raise ValueError("oracle_metrics rejected its arguments")
+    n, ue, cue, asa, nb, hits, most = (int(v) for v in out)
+    return dict(n=n, ue_num=ue, cue_num=cue, asa_num=asa, gt_boundary=nb, br_hits=hits, max_segments=most,
+                ue=ue / n, cue=cue / n, asa=asa / n, br=hits / nb if nb else 1.0)

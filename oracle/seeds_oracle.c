@@ -814,3 +814,86 @@ int oracle_means_test(const uint8_t *v, int C, const int64_t *Sk, int64_t Ak, co
 {
     return means_test(v, C, Sk, Ak, Sn, An);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Quality metrics of a partition against ground-truth segments (SURVEY.md   */
+/* 8(f) rank 2, S6.1), each written as its definition:     */
+/*   UE  = sum_i sum_{k: s_k cap g_i != 0} |s_k - g_i| / sum_i |g_i|   (Eq. ue) */
+/*   CUE = sum_k |s_k - g_max(s_k)| / sum_i |g_i|,                            */
+/*         g_max(s_k) = argmax_i |s_k cap g_i| */
+/*   ASA = sum_k max_i |s_k cap g_i| / sum_i |g_i| */
+/*   BR  = #{p in B(g): min_{q in B(s)} ||p - q|| < eps} / |B(g)| */
+/* with B(x) = the pixels having an in-image 4-neighbour of another segment  */
+/* (reading M2) and the Euclidean distance strict against eps (the paper's   */
+/* eps = 2).  Writes the integer numerators: out[0] = N, [1] = UE numerator, */
+/* [2] = CUE numerator, [3] = ASA numerator, [4] = |B(g)|, [5] = BR hits,    */
+/* [6] = most ground-truth segments meeting one superpixel.                   */
+/* Returns 0, or -1 on a label outside [0, K) / a segment outside [0, R).    */
+/* ------------------------------------------------------------------------ */
+static int cmp_i64(const void *a, const void *b)
+{
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return (x > y) - (x < y);
+}
+
+static int seg_boundary(const int32_t *lab, int W, int H, int x, int y)
+{
+    int v = lab[(int64_t)y * W + x];
+    if (x > 0 && lab[(int64_t)y * W + x - 1] != v) return 1;
+    if (x + 1 < W && lab[(int64_t)y * W + x + 1] != v) return 1;
+    if (y > 0 && lab[(int64_t)(y - 1) * W + x] != v) return 1;
+    if (y + 1 < H && lab[(int64_t)(y + 1) * W + x] != v) return 1;
+    return 0;
+}
+
+int oracle_metrics(const int32_t *labels, const int32_t *gt, int W, int H, int K, int R, int eps, int64_t *out)
+{
+    int64_t N = (int64_t)W * H;
+    if (W < 1 || H < 1 || K < 1 || R < 1 || eps < 1) return -1;
+    for (int64_t p = 0; p < N; p++)
+        if (labels[p] < 0 || labels[p] >= K || gt[p] < 0 || gt[p] >= R) return -1;
+    int64_t *keys = (int64_t *)malloc(sizeof(int64_t) * N);
+    int64_t *size = (int64_t *)calloc(K, sizeof(int64_t));
+    int64_t *best = (int64_t *)calloc(K, sizeof(int64_t));
+    int64_t *nseg = (int64_t *)calloc(K, sizeof(int64_t));
+    for (int64_t p = 0; p < N; p++) {
+        keys[p] = (int64_t)labels[p] * R + gt[p];
+        size[labels[p]]++;
+    }
+    qsort(keys, (size_t)N, sizeof(int64_t), cmp_i64);
+    int64_t ue = 0;
+    for (int64_t a = 0; a < N;) {
+        int64_t b = a;
+        while (b < N && keys[b] == keys[a]) b++;
+        int k = (int)(keys[a] / R);
+        int64_t inter = b - a;           /* |s_k cap g_i| > 0 */
+        ue += size[k] - inter;           /* |s_k - g_i| */
+        if (inter > best[k]) best[k] = inter;
+        nseg[k]++;
+        a = b;
+    }
+    int64_t cue = 0, asa = 0, most = 0;
+    for (int k = 0; k < K; k++) {
+        cue += size[k] - best[k];
+        asa += best[k];
+        if (nseg[k] > most) most = nseg[k];
+    }
+    int64_t nb = 0, hits = 0;
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            if (!seg_boundary(gt, W, H, x, y)) continue;
+            nb++;
+            int hit = 0;
+            for (int dy = -eps; dy <= eps && !hit; dy++)
+                for (int dx = -eps; dx <= eps && !hit; dx++) {
+                    if (dx * dx + dy * dy >= eps * eps) continue;
+                    int qx = x + dx, qy = y + dy;
+                    if (qx < 0 || qx >= W || qy < 0 || qy >= H) continue;
+                    hit = seg_boundary(labels, W, H, qx, qy);
+                }
+            hits += hit;
+        }
+    out[0] = N; out[1] = ue; out[2] = cue; out[3] = asa; out[4] = nb; out[5] = hits; out[6] = most;
+    free(keys); free(size); free(best); free(nseg);
+    return 0;
+}

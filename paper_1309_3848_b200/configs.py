@@ -87,3 +87,43 @@ def _frames(cfg: str, n: int):
         out[i] = mosaic.mosaic(c["W"], c["H"], c["R"], c["sigma"], seed=seed + i, C=c["C"],
                                grad=c["grad"])
     return out
+
+
+def regions(cfg: str, n: int | None = None) -> np.ndarray:
+    """(n, H, W) int32 ground-truth region maps of ``frames(cfg, n)``: the
+    Voronoi region of every pixel (the mosaic's objects), for the quality
+    metrics of SURVEY 8(f) rank 2.  Large maps are cached like the frames."""
+    c = CONFIGS[cfg]
+    n_ = c["frames"] if n is None else n
+    path = os.path.join(CACHE_DIR, f"{cfg}_{c['index']}_{n_}_regions.npy")
+    big = c["W"] * c["H"] * n_ >= 4_000_000
+    if big:
+        try:
+            out = np.load(path)
+            if out.shape == (n_, c["H"], c["W"]) and out.dtype == np.int32:
+                return out
+        except Exception:
+            pass
+    seed = 1000 * c["index"]
+    if cfg == "c3":
+        _, out = mosaic.mosaic_batch(n_, c["W"], c["H"], c["R"][0], c["R"][1], c["sigma"][0], c["sigma"][1],
+                                     seed=seed, grad=c["grad"], C=c["C"], return_regions=True)
+    elif cfg == "c4":
+        _, out = mosaic.moving_mosaic(n_, c["W"], c["H"], c["R"], c["sigma"], seed=seed, grad=c["grad"], C=c["C"])
+    else:
+        out = np.stack([mosaic.mosaic(c["W"], c["H"], c["R"], c["sigma"], seed=seed + i, C=c["C"], grad=c["grad"],
+                                      return_regions=True)[1] for i in range(n_)])
+    if big:
+        try:
+            os.makedirs(CACHE_DIR, exist_ok=True)
+            tmp = f"{path}.{os.getpid()}.npy"
+            np.save(tmp, out)
+            os.replace(tmp, path)
+        except Exception:
+            pass
+    return out
+
+
+def n_regions(cfg: str, frame: int = 0) -> int:
+    """Number of ground-truth regions of frame ``frame`` (ids are 0..R-1)."""
+    return int(regions(cfg, frame + 1)[frame].max()) + 1

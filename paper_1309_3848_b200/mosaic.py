@@ -69,15 +69,20 @@ def mosaic(W: int, H: int, R: int, sigma: float, seed: int, C: int = 3, grad: fl
 
 
 def mosaic_batch(n: int, W: int, H: int, r_lo: int, r_hi: int, s_lo: float, s_hi: float,
-                 seed: int, grad: float = 30.0, C: int = 3) -> np.ndarray:
+                 seed: int, grad: float = 30.0, C: int = 3, return_regions: bool = False):
     """n independent frames (c3): R ~ U{r_lo..r_hi}, sigma ~ U[s_lo, s_hi] per frame."""
     out = np.empty((n, H, W, C), np.uint8)
+    regions = np.empty((n, H, W), np.int32) if return_regions else None
     for f in range(n):
         rng = np.random.Generator(np.random.PCG64(seed * 100003 + f))
         R = int(rng.integers(r_lo, r_hi + 1))
         sigma = float(rng.uniform(s_lo, s_hi))
-        out[f] = mosaic(W, H, R, sigma, seed=seed * 100003 + f + 7, C=C, grad=grad)
-    return out
+        r = mosaic(W, H, R, sigma, seed=seed * 100003 + f + 7, C=C, grad=grad, return_regions=return_regions)
+        if return_regions:
+            out[f], regions[f] = r
+        else:
+            out[f] = r
+    return (out, regions) if return_regions else out
 
 
 def moving_mosaic(n_frames: int, W: int, H: int, R: int, sigma: float, seed: int,
