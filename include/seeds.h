@@ -167,6 +167,34 @@ seeds_status seeds_set_means_iters(seeds_ctx *ctx, int means_iters);
  * iterations, before any run, or if frame is outside the last batch. */
 seeds_status seeds_read_sums(seeds_ctx *ctx, int frame, int64_t *sums_out, void *stream);
 
+/* Quality metrics of a partition against ground-truth segments (SURVEY.md 8(f)
+ * rank 2, S6.1).  Integer numerators (exact) and ratios:
+ *   UE  = sum_i sum_{k: s_k meets g_i} |s_k - g_i| / N   (Eq. ue)
+ *   CUE = sum_k |s_k - g_max(s_k)| / N
+ *   ASA = sum_k max_i |s_k cap g_i| / N
+ *   BR  = #{p in B(g): some q in B(s) with ||p - q|| < eps} / |B(g)|
+ * B(x): the pixels with an in-image 4-neighbour in another segment (reading
+ * M2); BR = 1 when the ground truth has no boundary. */
+typedef struct {
+    long long n;            /* pixels = sum_i |g_i| */
+    long long ue_num, cue_num, asa_num;
+    long long gt_boundary;  /* |B(g)| */
+    long long br_hits;
+    int max_segments;       /* most ground-truth segments meeting one superpixel */
+    double ue, cue, asa, br;
+} seeds_metrics_t;
+
+/* seeds_metrics -- metrics of one frame's labels against its ground truth.
+ *   labels      device, height*width int32 in [0, K_act) (e.g. labels_out)
+ *   gt          device, height*width int32 segment ids in [0, n_segments)
+ *   eps         boundary-recall tolerance in pixels (the paper's 2), 1..64
+ *   out         host struct, filled on SEEDS_OK
+ * Runs two kernels on `stream` (contingency slots + reduction) and
+ * synchronises it.  SEEDS_EINVAL for ids out of range, SEEDS_ERANGE if a
+ * superpixel meets more than 32 segments (its slot table overflows). */
+seeds_status seeds_metrics(seeds_ctx *ctx, const int32_t *labels, const int32_t *gt, int n_segments, int eps,
+                           seeds_metrics_t *out, void *stream);
+
 /* seeds_debug_limit -- stop every later run after max_subsweeps sub-sweeps
  * (the block maps are still pushed down and expanded, so the labels are the
  * valid partition reached at that point); -1 turns the limit off.  Used to

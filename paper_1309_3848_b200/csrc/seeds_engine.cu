@@ -18,6 +18,7 @@
 #include "seeds_kernels.cuh"
 #include "seeds_resident.cuh"
 #include "seeds_grid.cuh"
+#include "seeds_metrics.cuh"
 
 using namespace seeds;
 
@@ -134,6 +135,10 @@ struct seeds_ctx {
     const int32_t *band_init = nullptr;
     size_t grid_smem = 0;
     GridParams gp{};
+    // quality metrics (seeds_metrics): per-superpixel contingency slots + accumulators
+    int *d_met_key = nullptr;
+    unsigned *d_met_cnt = nullptr;
+    unsigned long long *d_met_acc = nullptr;
     int n_sm = 148;
 };
 
@@ -1460,6 +1465,52 @@ seeds_status seeds_read_sums(seeds_ctx *ctx, int frame, int64_t *sums_out, void 
     return SEEDS_OK;
 }
 
+seeds_status seeds_metrics(seeds_ctx *ctx, const int32_t *labels, const int32_t *gt, int n_segments, int eps,
+                           seeds_metrics_t *out, void *stream)
+{
+    if (!ctx || !labels || !gt || !out || n_segments < 1 || eps < 1 || eps > 64) return SEEDS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t slots = (size_t)ctx->K * MET_SLOTS;
+    if (!ctx->d_met_key) {
+        CK(cudaMalloc(&ctx->d_met_key, slots * sizeof(int)));
+        CK(cudaMalloc(&ctx->d_met_cnt, slots * sizeof(unsigned)));
+        CK(cudaMalloc(&ctx->d_met_acc, 8 * sizeof(unsigned long long)));
+    }
+    CK(cudaMemsetAsync(ctx->d_met_key, 0xFF, slots * sizeof(int), st));
+    CK(cudaMemsetAsync(ctx->d_met_cnt, 0, slots * sizeof(unsigned), st));
+    CK(cudaMemsetAsync(ctx->d_met_acc, 0, 8 * sizeof(unsigned long long), st));
+    const long long blocks = std::min<long long>((ctx->N + 255) / 256, (long long)ctx->n_sm * 8);
+    k_met_count<<<(unsigned)blocks, 256, 0, st>>>(labels, gt, ctx->W, ctx->H, ctx->K, n_segments, eps, ctx->d_met_key,
+                                                  ctx->d_met_cnt, ctx->d_met_acc);
+    CK(cudaGetLastError());
+    k_met_reduce<<<(ctx->K + 255) / 256, 256, 0, st>>>(ctx->K, ctx->d_met_key, ctx->d_met_cnt, ctx->d_met_acc);
+    CK(cudaGetLastError());
+    unsigned long long acc[8];
+    CK(cudaMemcpyAsync(acc, ctx->d_met_acc, sizeof acc, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (acc[3]) {
+        snprintf(ctx->err, sizeof ctx->err, "%llu labels or segment ids out of range", acc[3]);
+        return SEEDS_EINVAL;
+    }
+    if (acc[2]) {
+        snprintf(ctx->err, sizeof ctx->err, "a superpixel meets more than %d ground-truth segments", MET_SLOTS);
+        return SEEDS_ERANGE;
+    }
+    const double N = (double)ctx->N;
+    out->n = ctx->N;
+    out->ue_num = (long long)acc[4];
+    out->asa_num = (long long)acc[5];
+    out->cue_num = ctx->N - (long long)acc[5];
+    out->gt_boundary = (long long)acc[0];
+    out->br_hits = (long long)acc[1];
+    out->max_segments = (int)acc[6];
+    out->ue = acc[4] / N;
+    out->asa = acc[5] / N;
+    out->cue = out->cue_num / N;
+    out->br = acc[0] ? (double)acc[1] / (double)acc[0] : 1.0;
+    return SEEDS_OK;
+}
+
 seeds_status seeds_sync(seeds_ctx *ctx, void *stream)
 {
     if (!ctx) return SEEDS_EINVAL;
@@ -1477,7 +1528,7 @@ void seeds_destroy(seeds_ctx *ctx)
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1], ctx->d_S[0], ctx->d_S[1],
                     ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band, ctx->d_kmap,
                     ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp, ctx->d_bcount,
-                    ctx->d_init_stage, ctx->d_out_stage};
+                    ctx->d_init_stage, ctx->d_out_stage, ctx->d_met_key, ctx->d_met_cnt, ctx->d_met_acc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);

@@ -24,7 +24,14 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_profile", "seeds_profile_collect", "seeds_set_mode", "seeds_debug_trace",
            "seeds_status_string", "seeds_last_error", "seeds_create_banded", "seeds_band_info",
            "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish",
-           "seeds_set_means_iters", "seeds_read_sums"]
+           "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics"]
+
+
+class _Metrics(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_longlong), ("ue_num", ctypes.c_longlong), ("cue_num", ctypes.c_longlong),
+                ("asa_num", ctypes.c_longlong), ("gt_boundary", ctypes.c_longlong), ("br_hits", ctypes.c_longlong),
+                ("max_segments", ctypes.c_int), ("ue", ctypes.c_double), ("cue", ctypes.c_double),
+                ("asa", ctypes.c_double), ("br", ctypes.c_double)]
 
 
 class SeedsError(RuntimeError):
@@ -63,6 +70,7 @@ def load(path: str = LIB_PATH):
         "seeds_debug_limit": ([vp, i], i),
         "seeds_set_means_iters": ([vp, i], i),
         "seeds_read_sums": ([vp, i, vp, vp], i),
+        "seeds_metrics": ([vp, vp, vp, i, i, vp, vp], i),
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
         "seeds_profile": ([vp, i], i),
@@ -261,6 +269,14 @@ class Seeds:
         out = torch.empty((self.info.k_actual, 4), dtype=torch.int64, device="cuda")
         self._check(self._lib.seeds_read_sums(self._ctx, frame, out.data_ptr(), _stream_ptr(stream)))
         return out
+
+    def metrics(self, labels, gt, n_segments: int, eps: int = 2, stream=None) -> dict:
+        """UE / CUE / ASA / BR of (H, W) int32 CUDA labels against (H, W) int32
+        CUDA ground-truth segment ids (include/seeds.h seeds_metrics)."""
+        out = _Metrics()
+        self._check(self._lib.seeds_metrics(self._ctx, labels.data_ptr(), gt.data_ptr(), int(n_segments), int(eps),
+                                            ctypes.byref(out), _stream_ptr(stream)))
+        return {f: getattr(out, f) for f, _ in _Metrics._fields_}
 
     def debug_limit(self, max_subsweeps: int):
         self._check(self._lib.seeds_debug_limit(self._ctx, max_subsweeps))
