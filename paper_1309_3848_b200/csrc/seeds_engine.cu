@@ -1479,8 +1479,8 @@ seeds_status seeds_metrics(seeds_ctx *ctx, const int32_t *labels, const int32_t 
     CK(cudaMemsetAsync(ctx->d_met_key, 0xFF, slots * sizeof(int), st));
     CK(cudaMemsetAsync(ctx->d_met_cnt, 0, slots * sizeof(unsigned), st));
     CK(cudaMemsetAsync(ctx->d_met_acc, 0, 8 * sizeof(unsigned long long), st));
-    const long long blocks = std::min<long long>((ctx->N + 255) / 256, (long long)ctx->n_sm * 8);
-    k_met_count<<<(unsigned)blocks, 256, 0, st>>>(labels, gt, ctx->W, ctx->H, ctx->K, n_segments, eps, ctx->d_met_key,
+    const int blocks = std::min(ctx->H, ctx->n_sm * 6);  // row bands (6 CTAs of 256 threads fit an SM)
+    k_met_count<<<blocks, 256, 0, st>>>(labels, gt, ctx->W, ctx->H, ctx->K, n_segments, eps, ctx->d_met_key,
                                                   ctx->d_met_cnt, ctx->d_met_acc);
     CK(cudaGetLastError());
     k_met_reduce<<<(ctx->K + 255) / 256, 256, 0, st>>>(ctx->K, ctx->d_met_key, ctx->d_met_cnt, ctx->d_met_acc);
