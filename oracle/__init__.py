@@ -46,7 +46,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle with gcc -O2 (plain C, no vectorisation flags)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -67,6 +67,8 @@ def lib():
             P(Trace), ctypes.c_int, P(ctypes.c_int), ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
             ctypes.c_int, ctypes.c_void_p,
         ]
+        _lib.oracle_rgb_to_lab.restype = None
+        _lib.oracle_rgb_to_lab.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         _lib.oracle_metrics.restype = ctypes.c_int
         _lib.oracle_metrics.argtypes = [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int] * 5 + [ctypes.c_void_p]
         _lib.oracle_means_test.restype = ctypes.c_int
@@ -155,10 +157,16 @@ def run(img: np.ndarray, n_superpixels: int, n_levels: int, bins_per_channel: in
         smoothness_prior: int, iters_per_level: int, schedule: int = COL, rule: int = R1,
         init_labels: np.ndarray | None = None, want_energy: bool = False,
         shuffle_seed: int = 0, max_subsweeps: int = -1, trace_cap: int = 4096,
-        means_iters: int = 0, want_sums: bool = False) -> Result:
+        means_iters: int = 0, want_sums: bool = False, colour: str = "rgb") -> Result:
     """Refine `img` (H, W, C uint8).  means_iters > 0: the last means_iters
-    pixel iterations use the SPM nearest-mean test (reading M1)."""
+    pixel iterations use the SPM nearest-mean test (reading M1).  colour =
+    "lab": the 8-bit CIELAB pre-pass (reading M3) first; every later step
+    (bins, means) sees the converted image."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
+    if colour == "lab":
+        img = rgb_to_lab(img)
+    elif colour != "rgb":
+        raise ValueError(f"unknown colour space {colour!r}")
     if img.ndim == 2:
         img = img[:, :, None]
     H, W, C = img.shape
@@ -211,3 +219,14 @@ def metrics(labels, gt, K: int, R: int, eps: int = 2) -> dict:
     n, ue, cue, asa, nb, hits, most = (int(v) for v in out)
     return dict(n=n, ue_num=ue, cue_num=cue, asa_num=asa, gt_boundary=nb, br_hits=hits, max_segments=most,
                 ue=ue / n, cue=cue / n, asa=asa / n, br=hits / nb if nb else 1.0)
+
+
+def rgb_to_lab(img: np.ndarray) -> np.ndarray:
+    """8-bit sRGB (..., 3) -> 8-bit CIELAB (L 255/100, a + 128, b + 128), the
+    integer fixed-point conversion of reading M3."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    if img.shape[-1] != 3:
+        raise ValueError("the LAB pre-pass needs 3 channels")
+    out = np.empty_like(img)
+    lib().oracle_rgb_to_lab(img.ctypes.data, img.size // 3, out.ctypes.data)
+    return out

@@ -33,6 +33,7 @@
  * Arithmetic: counts in int64, products in __int128, so no width question can
  * arise here; the GPU path's int32/int64 widths are checked against this.
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -896,4 +897,72 @@ int oracle_metrics(const int32_t *labels, const int32_t *gt, int W, int H, int K
     out[0] = N; out[1] = ue; out[2] = cue; out[3] = asa; out[4] = nb; out[5] = hits; out[6] = most;
     free(keys); free(size); free(best); free(nseg);
     return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O0 (optional): 8-bit CIELAB pre-pass (the paper    */
+/* bins LAB), reading M3 in DESIGN.md: an integer          */
+/* fixed-point conversion of 8-bit sRGB (D65) so that both implementations   */
+/* agree bit for bit.  Written here from the CIE definitions:                */
+/*   lin(c)  = c/12.92 (c <= 0.04045) else ((c + 0.055)/1.055)^2.4, c = v/255  */
+/*             -> LIN[v] = round(65535 lin)                                  */
+/*   X/Xn, Y/Yn, Z/Zn = rows of the sRGB->XYZ matrix divided by the white    */
+/*             point (each row sums to 1), in 1/4096 units with every row    */
+/*             summing to exactly 4096 (so greys give X = Y = Z):             */
+/*             T_i = (sum_j m_ij LIN_j + 2048) >> 12 in [0, 65535]           */
+/*   f(t)    = t^(1/3) (t > (6/29)^3) else t/(3 (6/29)^2) + 4/29, t = T/65535  */
+/*             -> F[T] = round(65536 f)                                      */
+/*   L = 116 f(Y) - 16, a = 500 (f(X) - f(Y)), b = 200 (f(Y) - f(Z))          */
+/*   8-bit: L8 = round(L 255/100), a8 = 128 + round(a), b8 = 128 + round(b), */
+/*          rounding half up, clamped to [0, 255].                           */
+/* ------------------------------------------------------------------------ */
+static const double LAB_M[3][3] = {{0.412453, 0.357580, 0.180423},
+                                   {0.212671, 0.715160, 0.072169},
+                                   {0.019334, 0.119193, 0.950227}};
+
+static void lab_tables(int32_t lin[256], int32_t m[3][3], int32_t *F /* 65536 */)
+{
+    for (int v = 0; v < 256; v++) {
+        double c = v / 255.0;
+        double l = c <= 0.04045 ? c / 12.92 : pow((c + 0.055) / 1.055, 2.4);
+        lin[v] = (int32_t)floor(l * 65535.0 + 0.5);
+    }
+    for (int i = 0; i < 3; i++) {
+        double s = LAB_M[i][0] + LAB_M[i][1] + LAB_M[i][2];
+        int sum = 0, big = 0;
+        for (int j = 0; j < 3; j++) {
+            m[i][j] = (int32_t)floor(LAB_M[i][j] / s * 4096.0 + 0.5);
+            sum += m[i][j];
+            if (m[i][j] > m[i][big]) big = j;
+        }
+        m[i][big] += 4096 - sum;
+    }
+    const double d = 6.0 / 29.0;
+    for (int t = 0; t < 65536; t++) {
+        double x = t / 65535.0;
+        double f = x > d * d * d ? cbrt(x) : x / (3.0 * d * d) + 4.0 / 29.0;
+        F[t] = (int32_t)floor(f * 65536.0 + 0.5);
+    }
+}
+
+static int clamp255(int64_t v) { return v < 0 ? 0 : v > 255 ? 255 : (int)v; }
+
+void oracle_rgb_to_lab(const uint8_t *rgb, int64_t n, uint8_t *lab)
+{
+    int32_t lin[256], m[3][3];
+    int32_t *F = (int32_t *)malloc(sizeof(int32_t) * 65536);
+    lab_tables(lin, m, F);
+    for (int64_t p = 0; p < n; p++) {
+        int64_t l[3] = {lin[rgb[3 * p]], lin[rgb[3 * p + 1]], lin[rgb[3 * p + 2]]};
+        int64_t T[3];
+        for (int i = 0; i < 3; i++) T[i] = (m[i][0] * l[0] + m[i][1] * l[1] + m[i][2] * l[2] + 2048) >> 12;
+        int64_t fx = F[T[0]], fy = F[T[1]], fz = F[T[2]];
+        int64_t Lfp = 116 * fy - 16 * 65536;           /* L in 1/65536 */
+        int64_t L8 = (Lfp * 255 + 50 * 65536) / (100 * 65536);
+        int64_t afp = 500 * (fx - fy), bfp = 200 * (fy - fz);
+        lab[3 * p] = (uint8_t)clamp255(Lfp < 0 ? 0 : L8);
+        lab[3 * p + 1] = (uint8_t)clamp255(128 + ((afp + 32768) >> 16));
+        lab[3 * p + 2] = (uint8_t)clamp255(128 + ((bfp + 32768) >> 16));
+    }
+    free(F);
 }
