@@ -159,6 +159,23 @@ seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int3
  *                 a later run also fails with SEEDS_ESTATE if no grid plan fits) */
 seeds_status seeds_set_means_iters(seeds_ctx *ctx, int means_iters);
 
+/* seeds_set_colour_space -- the colour space the method bins (and the means
+ * post-processing averages).  SEEDS_COLOUR_RGB (default): the caller's 8-bit
+ * channels as given (reading Q1).  SEEDS_COLOUR_LAB: every later run first
+ * converts the 8-bit sRGB (D65) frames to 8-bit CIELAB (L 255/100, a + 128,
+ * b + 128; the paper's colour space) in integer fixed point
+ * (reading M3) into a context buffer, inside the run.
+ * SEEDS_EINVAL: an unknown space, or LAB with channels != 3. */
+enum { SEEDS_COLOUR_RGB = 0, SEEDS_COLOUR_LAB = 1 };
+seeds_status seeds_set_colour_space(seeds_ctx *ctx, int space);
+
+/* seeds_rgb_to_lab -- the LAB pre-pass alone (reading M3), enqueued on
+ * `stream`: device rgb[3 n_pixels] 8-bit sRGB -> device lab_out[3 n_pixels]
+ * (L 255/100, a + 128, b + 128).  Any context works (it only holds the
+ * tables).  SEEDS_EINVAL for NULL pointers or n_pixels < 0. */
+seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pixels, uint8_t *lab_out,
+                              void *stream);
+
 /* seeds_read_sums -- after a run with means post-processing: copy frame
  * `frame`'s per-superpixel channel sums S[k][c] = sum of channel c over the
  * pixels of k (for parity tests).

@@ -19,6 +19,7 @@
 #include "seeds_resident.cuh"
 #include "seeds_grid.cuh"
 #include "seeds_metrics.cuh"
+#include "seeds_lab.cuh"
 
 using namespace seeds;
 
@@ -33,10 +34,11 @@ struct GraphKey {
     bool prof = false;
     int mode = -1;
     int miters = 0;
+    int colour = 0;
     bool operator==(const GraphKey &o) const
     {
         return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof &&
-               mode == o.mode && miters == o.miters;
+               mode == o.mode && miters == o.miters && colour == o.colour;
     }
 };
 
@@ -139,6 +141,11 @@ struct seeds_ctx {
     int *d_met_key = nullptr;
     unsigned *d_met_cnt = nullptr;
     unsigned long long *d_met_acc = nullptr;
+    // LAB pre-pass (seeds_set_colour_space): tables and the converted frames
+    int colour = SEEDS_COLOUR_RGB;
+    int32_t *d_lab_tab = nullptr;
+    uint8_t *d_labimg = nullptr;
+    size_t labimg_frames = 0;
     int n_sm = 148;
 };
 
@@ -1144,10 +1151,67 @@ static seeds_status run_resident(seeds_ctx *ctx, const uint8_t *img, const int32
     return SEEDS_OK;
 }
 
+// Reading M3: the fixed-point tables of the 8-bit CIELAB pre-pass, from the CIE
+// formulas (sRGB decoding, the D65 sRGB->XYZ matrix normalised by the white
+// point with rows summing to 4096, the cube-root companding f).
+static void lab_tables(std::vector<int32_t> &t)
+{
+    static const double M[3][3] = {{0.412453, 0.357580, 0.180423},
+                                   {0.212671, 0.715160, 0.072169},
+                                   {0.019334, 0.119193, 0.950227}};
+    t.assign(LAB_TAB_WORDS, 0);
+    for (int v = 0; v < 256; v++) {
+        const double c = v / 255.0;
+        const double l = c <= 0.04045 ? c / 12.92 : std::pow((c + 0.055) / 1.055, 2.4);
+        t[v] = (int32_t)std::floor(l * 65535.0 + 0.5);
+    }
+    for (int i = 0; i < 3; i++) {
+        const double s = M[i][0] + M[i][1] + M[i][2];
+        int sum = 0, big = 0;
+        for (int j = 0; j < 3; j++) {
+            t[256 + 3 * i + j] = (int32_t)std::floor(M[i][j] / s * 4096.0 + 0.5);
+            sum += t[256 + 3 * i + j];
+            if (t[256 + 3 * i + j] > t[256 + 3 * i + big]) big = j;
+        }
+        t[256 + 3 * i + big] += 4096 - sum;
+    }
+    const double d = 6.0 / 29.0;
+    for (int u = 0; u < 65536; u++) {
+        const double x = u / 65535.0;
+        const double f = x > d * d * d ? std::cbrt(x) : x / (3.0 * d * d) + 4.0 / 29.0;
+        t[256 + 9 + u] = (int32_t)std::floor(f * 65536.0 + 0.5);
+    }
+}
+
+// LAB mode: convert nf frames into the context's buffer (allocated outside
+// any capture by ensure_labimg) and return it as the image of the run.
+static seeds_status ensure_labimg(seeds_ctx *ctx, int nf)
+{
+    if (ctx->colour != SEEDS_COLOUR_LAB || (size_t)nf <= ctx->labimg_frames) return SEEDS_OK;
+    CK(cudaDeviceSynchronize());
+    drop_graphs(ctx);
+    if (ctx->d_labimg) cudaFree(ctx->d_labimg);
+    ctx->d_labimg = nullptr;
+    ctx->labimg_frames = 0;
+    CK(cudaMalloc(&ctx->d_labimg, (size_t)nf * ctx->N * 3));
+    ctx->labimg_frames = nf;
+    return SEEDS_OK;
+}
+static const uint8_t *enqueue_lab(seeds_ctx *ctx, const uint8_t *img, int nf, cudaStream_t st)
+{
+    if (ctx->colour != SEEDS_COLOUR_LAB) return img;
+    const long long n = (long long)nf * ctx->N;
+    const long long blocks = std::min<long long>((n + 255) / 256, (long long)ctx->n_sm * 8);
+    k_rgb2lab<<<(unsigned)blocks, 256, 0, st>>>(img, n, ctx->d_labimg, ctx->d_lab_tab);
+    return ctx->d_labimg;
+}
+
 static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
                         cudaStream_t st)
 {
     seeds_status r = ensure_frames(ctx, nf);
+    if (r != SEEDS_OK) return r;
+    r = ensure_labimg(ctx, nf);
     if (r != SEEDS_OK) return r;
     const int mode = resolved_mode(ctx, nf);
     if (ctx->miters > 0 && mode != SEEDS_MODE_GRID) {
@@ -1157,6 +1221,8 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     ctx->last_miters = ctx->miters;
     if (mode == SEEDS_MODE_RESIDENT) {
         ctx->ev_used = 0;
+        img = enqueue_lab(ctx, img, nf, st);
+        CK(cudaGetLastError());
         r = run_resident(ctx, img, init, out, nf, st);
         if (r != SEEDS_OK) return r;
         ctx->last_nf = nf;
@@ -1167,6 +1233,7 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     key.img = img; key.init = init; key.out = out; key.nf = nf; key.limit = ctx->limit; key.prof = ctx->prof;
     key.mode = mode;
     key.miters = ctx->miters;
+    key.colour = ctx->colour;
     seeds_ctx::GraphEntry *hit = nullptr;
     for (auto &g : ctx->graphs)
         if (g.key == key) hit = &g;
@@ -1184,9 +1251,10 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
             ctx->graphs.erase(ctx->graphs.begin() + lru);
         }
         CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-        seeds_status er = mode == SEEDS_MODE_GRID ? enqueue_grid(ctx, img, init, out, nf, ctx->cap_stream)
-                          : ctx->bb == 1          ? enqueue<uint8_t>(ctx, img, init, out, nf, ctx->cap_stream)
-                                                  : enqueue<uint16_t>(ctx, img, init, out, nf, ctx->cap_stream);
+        const uint8_t *im = enqueue_lab(ctx, img, nf, ctx->cap_stream);
+        seeds_status er = mode == SEEDS_MODE_GRID ? enqueue_grid(ctx, im, init, out, nf, ctx->cap_stream)
+                          : ctx->bb == 1          ? enqueue<uint8_t>(ctx, im, init, out, nf, ctx->cap_stream)
+                                                  : enqueue<uint16_t>(ctx, im, init, out, nf, ctx->cap_stream);
         cudaGraph_t graph = nullptr;
         cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
         if (er != SEEDS_OK) {
@@ -1454,6 +1522,40 @@ seeds_status seeds_set_means_iters(seeds_ctx *ctx, int means_iters)
     return SEEDS_OK;
 }
 
+seeds_status seeds_set_colour_space(seeds_ctx *ctx, int space)
+{
+    if (!ctx || (space != SEEDS_COLOUR_RGB && space != SEEDS_COLOUR_LAB)) return SEEDS_EINVAL;
+    if (space == SEEDS_COLOUR_LAB && ctx->C != 3) {
+        snprintf(ctx->err, sizeof ctx->err, "the LAB pre-pass needs 3 channels");
+        return SEEDS_EINVAL;
+    }
+    if (space == SEEDS_COLOUR_LAB && !ctx->d_lab_tab) {
+        std::vector<int32_t> t;
+        lab_tables(t);
+        CK(cudaMalloc(&ctx->d_lab_tab, t.size() * sizeof(int32_t)));
+        CK(cudaMemcpy(ctx->d_lab_tab, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    ctx->colour = space;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pixels, uint8_t *lab_out, void *stream)
+{
+    if (!ctx || !rgb || !lab_out || n_pixels < 0) return SEEDS_EINVAL;
+    if (!ctx->d_lab_tab) {
+        std::vector<int32_t> t;
+        lab_tables(t);
+        CK(cudaMalloc(&ctx->d_lab_tab, t.size() * sizeof(int32_t)));
+        CK(cudaMemcpy(ctx->d_lab_tab, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    if (n_pixels == 0) return SEEDS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long blocks = std::min<long long>((n_pixels + 255) / 256, (long long)ctx->n_sm * 8);
+    k_rgb2lab<<<(unsigned)blocks, 256, 0, st>>>(rgb, n_pixels, lab_out, ctx->d_lab_tab);
+    CK(cudaGetLastError());
+    return SEEDS_OK;
+}
+
 seeds_status seeds_read_sums(seeds_ctx *ctx, int frame, int64_t *sums_out, void *stream)
 {
     if (!ctx || !sums_out) return SEEDS_EINVAL;
@@ -1528,7 +1630,8 @@ void seeds_destroy(seeds_ctx *ctx)
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1], ctx->d_S[0], ctx->d_S[1],
                     ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band, ctx->d_kmap,
                     ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp, ctx->d_bcount,
-                    ctx->d_init_stage, ctx->d_out_stage, ctx->d_met_key, ctx->d_met_cnt, ctx->d_met_acc};
+                    ctx->d_init_stage, ctx->d_out_stage, ctx->d_met_key, ctx->d_met_cnt, ctx->d_met_acc,
+                    ctx->d_lab_tab, ctx->d_labimg};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -1597,6 +1700,9 @@ seeds_status seeds_band_seed(seeds_ctx *ctx, const uint8_t *image_u8, const int3
     if (!ctx || !ctx->banded || !image_u8) return SEEDS_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     if (!plan_grid(ctx, 1)) return SEEDS_ESTATE;
+    seeds_status r = ensure_labimg(ctx, 1);
+    if (r != SEEDS_OK) return r;
+    image_u8 = enqueue_lab(ctx, image_u8, 1, st);
     CK(cudaMemsetAsync(ctx->d_H[0], 0, (size_t)ctx->H_fs * 4, st));
     CK(cudaMemsetAsync(ctx->d_A[0], 0, (size_t)ctx->K * 4, st));
     CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)(ctx->S + 1) * 4, st));

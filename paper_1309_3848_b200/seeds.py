@@ -24,7 +24,8 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_profile", "seeds_profile_collect", "seeds_set_mode", "seeds_debug_trace",
            "seeds_status_string", "seeds_last_error", "seeds_create_banded", "seeds_band_info",
            "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish",
-           "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics"]
+           "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics", "seeds_set_colour_space",
+           "seeds_rgb_to_lab"]
 
 
 class _Metrics(ctypes.Structure):
@@ -71,6 +72,8 @@ def load(path: str = LIB_PATH):
         "seeds_set_means_iters": ([vp, i], i),
         "seeds_read_sums": ([vp, i, vp, vp], i),
         "seeds_metrics": ([vp, vp, vp, i, i, vp, vp], i),
+        "seeds_set_colour_space": ([vp, i], i),
+        "seeds_rgb_to_lab": ([vp, vp, ctypes.c_longlong, vp, vp], i),
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
         "seeds_profile": ([vp, i], i),
@@ -261,6 +264,21 @@ class Seeds:
         """The last means_iters pixel iterations use the means test (SPM
         post-processing, include/seeds.h seeds_set_means_iters)."""
         self._check(self._lib.seeds_set_means_iters(self._ctx, int(means_iters)))
+
+    COLOURS = {"rgb": 0, "lab": 1}
+
+    def set_colour_space(self, space: str):
+        """"rgb" (default) or "lab": the 8-bit CIELAB pre-pass of reading M3
+        (include/seeds.h seeds_set_colour_space)."""
+        self._check(self._lib.seeds_set_colour_space(self._ctx, self.COLOURS[space]))
+
+    def rgb_to_lab(self, rgb, stream=None):
+        """(..., 3) uint8 CUDA tensor of sRGB -> the same shape of 8-bit CIELAB."""
+        import torch
+        out = torch.empty_like(rgb)
+        self._check(self._lib.seeds_rgb_to_lab(self._ctx, rgb.data_ptr(), rgb.numel() // 3, out.data_ptr(),
+                                               _stream_ptr(stream)))
+        return out
 
     def read_sums(self, frame: int = 0, stream=None):
         """(K_act, 4) int64 CUDA tensor: channel sums S[k][c] after the last run
