@@ -321,7 +321,7 @@ def oracle_frames(imgs, p, workers):
         list(ex.map(lambda img: oracle.run(img, **p), list(imgs)))
 
 
-def cpu_baseline(name, budget_s=10.0, means_iters=0):
+def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb"):
     """The oracle as it stands (COL schedule) on a bounded sample: one thread
     on single-frame configs (the paper's setting); frame-parallel on all host
     cores for the batch configs c3 and c4, with the one-thread figure beside it."""
@@ -330,6 +330,9 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0):
     if means_iters:
         p = dict(p, means_iters=means_iters)
         note += f", last {means_iters} pixel iterations on means"
+    if colour != "rgb":
+        p = dict(p, colour=colour)
+        note += f", {colour} pre-pass"
     oracle.build()
     n, px, t0 = 0, 0, time.perf_counter()
     while True:
@@ -348,6 +351,8 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0):
     imgs, p, note = parallel_sample(name, workers)
     if means_iters:
         p = dict(p, means_iters=means_iters)
+    if colour != "rgb":
+        p = dict(p, colour=colour)
     t0 = time.perf_counter()
     oracle_frames(imgs, p, workers)
     el = time.perf_counter() - t0
@@ -375,6 +380,9 @@ def run_reference(args):
     if args.means_iters:
         p = dict(p, means_iters=args.means_iters)
         note += f", last {args.means_iters} pixel iterations on means"
+    if args.colour != "rgb":
+        p = dict(p, colour=args.colour)
+        note += f", {args.colour} pre-pass"
     for i in range(args.warmup):
         oracle_frames(batches[i % len(batches)][:1], p, 1)
     t, px = [], 0
@@ -410,6 +418,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--bands", action="store_true", help="c5: row-band mode even on one rank")
+    ap.add_argument("--colour", default="rgb", choices=["rgb", "lab"],
+                    help="lab: the 8-bit CIELAB pre-pass inside the timed run (reading M3)")
     ap.add_argument("--means-iters", type=int, default=0,
                     help="SPM means post-processing: the last M pixel iterations use the means test (reading M1)")
     args = ap.parse_args()
@@ -443,6 +453,8 @@ def main():
         s.set_mode(args.mode)
         if args.means_iters:
             s.set_means_iters(args.means_iters)
+    if args.colour != "rgb":
+        s.set_colour_space(args.colour)
     info = s.info
     stream = torch.cuda.current_stream()
     wl.setup(torch, s)
@@ -562,6 +574,7 @@ def main():
                        "frames_per_step_per_rank": wl.frames_per_step,
                        "exec_mode": mode_name,
                        "means_iters": args.means_iters,
+                       "colour": args.colour,
                        "grid_ctas": info.grid_ctas, "grid_tiles_per_frame": info.grid_tiles,
                        "parallelism": wl.parallelism,
                        "exchange": "NCCL all-gather of delta records + halo send/recv per sub-sweep" if banded else None,
@@ -577,7 +590,7 @@ def main():
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget, args.means_iters)
+            line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget, args.means_iters, args.colour)
         out = json.dumps(line)
         print(out)
         if args.json_out:
