@@ -105,28 +105,36 @@ struct GridParams {
 };
 
 // Split grid barrier: arrive (CTA barrier, then thread 0 publishes the CTA's
-// writes with a GPU-scope fence and counts in) ... wait (thread 0 polls for
-// every CTA's arrival, acquire, then a CTA barrier).  Local work that touches
+// writes with a GPU-scope release add on the counter) ... wait (thread 0 polls
+// the counter with relaxed loads, then a CTA barrier).  Local work that touches
 // no state another CTA writes may run between the two.
+//
+// No acquire-side L1 invalidation (CCTL.IVALL): every read of state that other
+// CTAs write bypasses L1 -- ld.global.cg for H / A, TMA (after
+// fence.proxy.async) for the label and bin planes, L2 atomics for the records
+// -- so the release on the writer side and the L2 coherence point order them.
+__device__ __forceinline__ void grid_signal(unsigned *ctr)
+{
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+}
+__device__ __forceinline__ void grid_poll(unsigned *ctr, unsigned target)
+{
+    unsigned v;
+    long long spins = 0;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        if (++spins > (1LL << 26)) __trap();  // a CTA that never arrives: fail loudly instead of hanging
+    } while ((int)(v - target) < 0);
+}
 __device__ __forceinline__ void grid_arrive(unsigned *ctr, unsigned &target)
 {
     __syncthreads();
     target += gridDim.x;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
-    }
+    if (threadIdx.x == 0) grid_signal(ctr);
 }
 __device__ __forceinline__ void grid_wait(unsigned *ctr, unsigned target)
 {
-    if (threadIdx.x == 0) {
-        unsigned v;
-        long long spins = 0;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-            if (++spins > (1LL << 26)) __trap();  // a CTA that never arrives: fail loudly instead of hanging
-        } while ((int)(v - target) < 0);
-    }
+    if (threadIdx.x == 0) grid_poll(ctr, target);
     __syncthreads();
 }
 
@@ -135,14 +143,8 @@ __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned &target)
     __syncthreads();
     target += gridDim.x;
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
-        unsigned v;
-        long long spins = 0;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-            if (++spins > (1LL << 26)) __trap();  // a CTA that never arrives: fail loudly instead of hanging
-        } while ((int)(v - target) < 0);
+        grid_signal(ctr);
+        grid_poll(ctr, target);
     }
     __syncthreads();
 }
