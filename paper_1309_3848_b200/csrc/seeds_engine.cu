@@ -653,10 +653,11 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     for (int i = 0; i < TX; i++) muw = std::max(muw, ux(i + 1) - ux(i));
     for (int j = 0; j < TY; j++) muh = std::max(muh, uy(j + 1) - uy(j));
     // CTAs per SM: 1 x 512 or 4 x 128 threads, 128 registers each.  (8 x 128
-    // at 64 registers made c4 20% faster but spills; a spilled register that
-    // is live across the grid barrier's fence (CCTL.IVALL) is not safe, and c3
-    // came out wrong.)
-    const int cps = GRID_THREADS / nt;
+    // at 64 registers -- -DSEEDS_CPS8 -- spills ~600 bytes per thread.  With the
+    // old fence-based grid barrier (an L1 invalidation, CCTL.IVALL) that build
+    // gave wrong c3 results; with the release / relaxed barrier it is correct
+    // but only +-2% against this plan, so the spill-free plan stays.)
+    const int cps = nt == GRID_THREADS_SMALL ? GRID_SMALL_CPS : GRID_THREADS / nt;
     const size_t limit = cps == 1 ? 227 * 1024 : (228 * 1024) / cps - 1024;
     const size_t tabw = (2 * (size_t)c->B + 2) * 4;
     bool need_tab = false;

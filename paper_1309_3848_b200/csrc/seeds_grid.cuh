@@ -37,6 +37,13 @@ namespace seeds {
 // latencies).
 constexpr int GRID_THREADS = 512;
 constexpr int GRID_THREADS_SMALL = 128;
+#ifdef SEEDS_CPS8
+constexpr int GRID_SMALL_CPS = 8;  // experiment: 8 x 128 threads per SM, 64 registers
+#else
+constexpr int GRID_SMALL_CPS = 4;
+#endif
+template <int NT>
+constexpr int grid_cps() { return NT == GRID_THREADS_SMALL ? GRID_SMALL_CPS : GRID_THREADS / NT; }
 
 struct GridTile {
     int f;               // frame
@@ -350,7 +357,7 @@ __device__ __forceinline__ U128 mul_u128(U128 x, unsigned long long m)
 __device__ __forceinline__ bool lt_u128(U128 a, U128 b) { return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo); }
 
 template <typename BinT, int GAMMA, int P, int NT, int MEANS>
-__global__ void __launch_bounds__(NT, GRID_THREADS / NT) k_grid(const __grid_constant__ GridParams qp)
+__global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_constant__ GridParams qp)
 {
     extern __shared__ __align__(128) uint32_t smem[];
     const GridParams &q = qp;
