@@ -652,10 +652,26 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                         }
                                     }
                                 }
-                                for (int o = G >> 1; o >= 1; o >>= 1) {
-                                    Nk += __shfl_xor_sync(FULL, Nk, o);
+                                if (q.N < (1LL << 27)) {
+                                    // alpha <= 32: each sum is at most alpha A < 32 N < 2^32, so the
+                                    // segment reductions run on 32-bit halves (half the shuffles)
+                                    unsigned nk = (unsigned)Nk, nn[4];
 #pragma unroll
-                                    for (int d = 0; d < 4; d++) Nn[d] += __shfl_xor_sync(FULL, Nn[d], o);
+                                    for (int d = 0; d < 4; d++) nn[d] = (unsigned)Nn[d];
+                                    for (int o = G >> 1; o >= 1; o >>= 1) {
+                                        nk += __shfl_xor_sync(FULL, nk, o);
+#pragma unroll
+                                        for (int d = 0; d < 4; d++) nn[d] += __shfl_xor_sync(FULL, nn[d], o);
+                                    }
+                                    Nk = nk;
+#pragma unroll
+                                    for (int d = 0; d < 4; d++) Nn[d] = nn[d];
+                                } else {
+                                    for (int o = G >> 1; o >= 1; o >>= 1) {
+                                        Nk += __shfl_xor_sync(FULL, Nk, o);
+#pragma unroll
+                                        for (int d = 0; d < 4; d++) Nn[d] += __shfl_xor_sync(FULL, Nn[d], o);
+                                    }
                                 }
                                 if (ok) {
 #pragma unroll
