@@ -78,51 +78,96 @@ def algorithmic_bytes(info, C, nf, N, iters):
 
 
 class Clocks:
-    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line): an in-process NVML thread polling every
+    2 ms between start() and stop(); nvidia-smi (-lms 20, only the samples taken
+    between start and stop kept) when NVML is not importable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, index):
         self.index = index
+        self.samples = []
+        self.max_mhz = 0.0
+        self.thread = None
         self.proc = None
-        self.path = None
+        self.run = False
 
     def start(self):
+        import threading
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            try:  # the CUDA device's own PCI address (CUDA and NVML orders can differ)
+                import torch
+                pr = torch.cuda.get_device_properties(self.index)
+                h = nv.nvmlDeviceGetHandleByPciBusId(
+                    f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0")
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            bits = {n: getattr(nv, a, 0) for n, a in self.REASONS.items()}
+        except Exception:
+            return self._start_smi()
+        self.run = True
+
+        def poll():
+            while self.run:
+                try:
+                    mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((mhz, sorted(n for n, b in bits.items() if b and r & b)))
+                except Exception:
+                    pass
+                time.sleep(0.002)
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
+        t0 = time.perf_counter()
+        while not self.samples and time.perf_counter() - t0 < 1.0:  # the sampler is live before timing starts
+            time.sleep(0.001)
+        self.samples.clear()
+
+    def _start_smi(self):
         if not shutil.which("nvidia-smi"):
             return
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
-        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits", "-lms", "100"],
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits", "-lms", "20"],
                                      stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        time.sleep(0.5)  # let it start before timing
 
     def stop(self):
-        if self.proc is None:
+        if self.thread is not None:
+            self.run = False
+            self.thread.join()
+            data = list(self.samples)
+        elif self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            data = []
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                try:
+                    self.max_mhz = max(self.max_mhz, float(f[1]))
+                    data.append((float(f[0]), sorted(n for n, v in zip(self.REASONS, f[2:6]) if v.lower() == "active")))
+                except (ValueError, IndexError):
+                    continue
+            os.unlink(self.path)
+        else:
             return None
-        self.proc.terminate()
-        self.proc.wait()
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        os.unlink(self.path)
-        if not sm:
+        if not data:
             return None
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sm = sorted(d[0] for d in data)
+        reasons = sorted({r for d in data for r in d[1]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(sm),
+                "sampler": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
 class BandWorkload:
