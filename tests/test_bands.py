@@ -19,12 +19,14 @@ def torch_cuda():
     return torch
 
 
-def band_run(torch, img, p, n_bands, init=None):
+def band_run(torch, img, p, n_bands, init=None, colour="rgb"):
     from paper_1309_3848_b200 import bands
     from paper_1309_3848_b200.seeds import SeedsBand
     H, W, C = img.shape
     bs = [SeedsBand(W, H, C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
                     p["smoothness_prior"], p["iters_per_level"], b, n_bands) for b in range(n_bands)]
+    for b in bs:
+        b.set_colour_space(colour)
     d = torch.from_numpy(np.ascontiguousarray(img)).cuda()
     di = None if init is None else torch.from_numpy(np.ascontiguousarray(init, np.int32)).cuda()
     lab = bands.local_run(bs, d, di)
@@ -79,3 +81,23 @@ def test_c5_crop_bands_equal_single(torch_cuda, orc):
     r = orc.run(f, **p)
     np.testing.assert_array_equal(lab, r.labels)
     np.testing.assert_array_equal(hs[1][0].cpu().numpy(), r.hist)
+
+
+@pytest.mark.parametrize("n_bands", [1, 3])
+def test_c2_bands_lab(torch_cuda, orc, n_bands):
+    """The LAB pre-pass (reading M3) in row-band mode: every band converts the
+    replicated frame and the result equals the oracle's LAB run."""
+    img = configs.frames("c2")[0]
+    p = configs.params("c2")
+    lab, hs, _ = band_run(torch_cuda, img, p, n_bands, colour="lab")
+    r = orc.run(img, **p, colour="lab")
+    np.testing.assert_array_equal(lab, r.labels)
+    np.testing.assert_array_equal(hs[0][0].cpu().numpy(), r.hist)
+
+
+def test_bands_reject_means(torch_cuda):
+    from paper_1309_3848_b200.seeds import SeedsBand, SeedsError
+    b = SeedsBand(64, 48, 3, 12, 2, 4, 1, 3, 0, 2)
+    with pytest.raises(SeedsError):
+        b.set_means_iters(1)
+    b.close()
