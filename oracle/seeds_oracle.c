@@ -107,6 +107,7 @@ typedef struct {
     int trace_cap, trace_len;
     int want_energy;
     int max_subsweeps; /* -1 = unlimited (bisection hook) */
+    int block_lo, block_hi; /* block levels that run (reading M4); the others only push down */
     int subsweeps_done;
     int64_t *lblock;   /* B: block histogram scratch */
     const int *curM;   /* block phase: current block map (for traced energies) */
@@ -503,6 +504,10 @@ static int limit_reached(const st_t *s)
  * size, and then hierarchically move on to smaller block sizes"). */
 static void block_level(st_t *s, int *M, int l)
 {
+    /* reading M4: a level outside [block_lo, block_hi] runs no iteration (its map
+     * is still pushed down by the caller); [l, l] is the single-block-size
+     * variant of the authors' earlier SEEDS */
+    if (l < s->block_lo || l > s->block_hi) return;
     int w = s->GX >> l, h = s->GY >> l;
     int64_t nunits = (int64_t)w * h;
     s->curM = M;
@@ -637,13 +642,14 @@ static void pixel_level(st_t *s)
 /*   means_iters: the last means_iters of the iters pixel iterations use the  */
 /*               means test (reading M1; 0 = off, needs N < 2^27)            */
 /*   sums_out:   K_act*4 int64 channel sums S[k][c] at the end, or NULL       */
+/*   block_lo, block_hi: only block levels in [lo, hi] run (-1: 0 / L_eff-1)  */
 /* Returns K_act, or < 0 on invalid arguments.                                */
 /* ------------------------------------------------------------------------ */
 int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, int gamma, int iters,
                int schedule, int rule, const int32_t *init, int32_t *labels_out, int32_t *hist_out,
                int32_t *sizes_out, oracle_trace *trace, int trace_cap, int *trace_len,
                int want_energy, uint64_t shuffle_seed, int max_subsweeps, int means_iters,
-               int64_t *sums_out)
+               int64_t *sums_out, int block_lo, int block_hi)
 {
     if (W < 1 || H < 1 || C < 1 || C > 4 || K < 1 || L < 0 || bpc < 1 || bpc > 256 || iters < 0)
         return -1;
@@ -663,6 +669,8 @@ int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, i
     s.trace = trace; s.trace_cap = trace ? trace_cap : 0; s.want_energy = want_energy;
     s.rng = shuffle_seed;
     s.max_subsweeps = max_subsweeps;
+    s.block_lo = block_lo < 0 ? 0 : block_lo;
+    s.block_hi = block_hi < 0 ? 1 << 30 : block_hi;
     s.img = img;
     s.means_iters = means_iters;
     int64_t N = (int64_t)W * H;
