@@ -176,6 +176,17 @@ seeds_status seeds_set_colour_space(seeds_ctx *ctx, int space);
 seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pixels, uint8_t *lab_out,
                               void *stream);
 
+/* seeds_set_block_levels -- block levels lo..hi (0 = finest) run in every later
+ * cold run; the other levels run no iteration (their labels pass down
+ * unchanged).  lo = hi gives one block size, the variant of the authors'
+ * earlier SEEDS that the hierarchy replaced; lo > hi runs
+ * no block level (= n_levels 0, SPH); hi = -1 means L_eff - 1 (reading M4).
+ * The sub-sweep count (seeds_stats, the anytime limit) counts only the
+ * levels that run.  Default 0, -1 (all).
+ *   SEEDS_EINVAL  lo < 0, hi < -1, or a row-band ctx
+ *   SEEDS_ESTATE  a non-default range on a ctx forced to graph or resident mode */
+seeds_status seeds_set_block_levels(seeds_ctx *ctx, int lo, int hi);
+
 /* seeds_read_sums -- after a run with means post-processing: copy frame
  * `frame`'s per-superpixel channel sums S[k][c] = sum of channel c over the
  * pixels of k (for parity tests).

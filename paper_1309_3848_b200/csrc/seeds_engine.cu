@@ -35,10 +35,11 @@ struct GraphKey {
     int mode = -1;
     int miters = 0;
     int colour = 0;
+    int blk_lo = 0, blk_hi = 0;
     bool operator==(const GraphKey &o) const
     {
         return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof &&
-               mode == o.mode && miters == o.miters && colour == o.colour;
+               mode == o.mode && miters == o.miters && colour == o.colour && blk_lo == o.blk_lo && blk_hi == o.blk_hi;
     }
 };
 
@@ -85,6 +86,7 @@ struct seeds_ctx {
     // state of the last run
     int limit = -1;
     int miters = 0;       // seeds_set_means_iters (reading M1)
+    int blk_lo = 0, blk_hi = 1 << 20;  // seeds_set_block_levels (reading M4): all levels by default
     int last_miters = 0;  // of the last run
     int last_nf = 0;
     int last_final = 0;  // H buffer holding the final state
@@ -511,6 +513,13 @@ static size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 
 // Execution mode of a run of nf frames: AUTO takes the grid mode whenever its
 // tile plan fits, else the graph mode.
+// block levels a cold run refines (reading M4)
+static int block_levels_run(const seeds_ctx *c)
+{
+    return std::max(0, std::min(c->blk_hi, c->L - 1) - c->blk_lo + 1);
+}
+static bool default_levels(const seeds_ctx *c) { return c->blk_lo == 0 && c->blk_hi >= c->L - 1; }
+
 static int resolved_mode(seeds_ctx *c, int nf)
 {
     if (c->mode == SEEDS_MODE_GRAPH || c->mode == SEEDS_MODE_RESIDENT) return c->mode;
@@ -801,6 +810,8 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.band = 0;  // whole-run launch: every sub-sweep (seeds_band_subsweep overrides these)
         q.s0 = 0;
         q.s1 = -1;
+        q.blk_lo = 0;  // every block level (enqueue_grid applies seeds_set_block_levels)
+        q.blk_hi = 1 << 20;
         q.tx_bytes = q.bw * q.bh * 2 + (res ? 0 : q.bbw * (q.bh - 4) * c->bb) + (q.acache ? (int)c->Afs * 4 : 0);
         q.q_cap = (int)qcap + 32;
         q.GX = c->GX;
@@ -919,6 +930,8 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     q.Sb[1] = ctx->d_S[1];
     q.S_fs = ctx->Afs * 4;
     q.miters = ctx->miters;
+    q.blk_lo = ctx->blk_lo;
+    q.blk_hi = ctx->blk_hi;
     q.moves = ctx->d_moves;
     q.sync = ctx->d_sync;
     q.trace = ctx->d_trace;
@@ -933,7 +946,7 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid launch");
     CK(prof_end(ctx, st));
     const bool blocks = init == nullptr && ctx->L > 0;
-    const int total = (blocks ? 4 * ctx->L * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
+    const int total = (blocks ? 4 * block_levels_run(ctx) * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
     ctx->last_done = ctx->limit >= 0 ? std::min(ctx->limit, total) : total;
     ctx->last_final = ctx->last_done & 1;
     return SEEDS_OK;
@@ -1145,7 +1158,7 @@ static seeds_status run_resident(seeds_ctx *ctx, const uint8_t *img, const int32
     // sub-sweeps run: the schedule is data independent
     const bool blocks = init == nullptr && ctx->L > 0;
     int s = 0;
-    const int total = (blocks ? 4 * ctx->L * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
+    const int total = (blocks ? 4 * block_levels_run(ctx) * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
     s = ctx->limit >= 0 ? std::min(ctx->limit, total) : total;
     ctx->last_done = s;
     ctx->last_final = s & 1;
@@ -1215,8 +1228,9 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     r = ensure_labimg(ctx, nf);
     if (r != SEEDS_OK) return r;
     const int mode = resolved_mode(ctx, nf);
-    if (ctx->miters > 0 && mode != SEEDS_MODE_GRID) {
-        snprintf(ctx->err, sizeof ctx->err, "the means post-processing runs in grid mode only, and no grid plan fits");
+    if ((ctx->miters > 0 || !default_levels(ctx)) && mode != SEEDS_MODE_GRID) {
+        snprintf(ctx->err, sizeof ctx->err,
+                 "the means post-processing / a block-level range run in grid mode only, and no grid plan fits");
         return SEEDS_ESTATE;
     }
     ctx->last_miters = ctx->miters;
@@ -1234,6 +1248,8 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     key.img = img; key.init = init; key.out = out; key.nf = nf; key.limit = ctx->limit; key.prof = ctx->prof;
     key.mode = mode;
     key.miters = ctx->miters;
+    key.blk_lo = ctx->blk_lo;
+    key.blk_hi = ctx->blk_hi;
     key.colour = ctx->colour;
     seeds_ctx::GraphEntry *hit = nullptr;
     for (auto &g : ctx->graphs)
@@ -1463,8 +1479,8 @@ seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out,
 seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 {
     if (!ctx || mode < SEEDS_MODE_AUTO || mode > SEEDS_MODE_GRID) return SEEDS_EINVAL;
-    if (ctx->miters > 0 && (mode == SEEDS_MODE_GRAPH || mode == SEEDS_MODE_RESIDENT)) {
-        snprintf(ctx->err, sizeof ctx->err, "the means post-processing runs in grid mode only");
+    if ((ctx->miters > 0 || !default_levels(ctx)) && (mode == SEEDS_MODE_GRAPH || mode == SEEDS_MODE_RESIDENT)) {
+        snprintf(ctx->err, sizeof ctx->err, "the means post-processing / a block-level range run in grid mode only");
         return SEEDS_ESTATE;
     }
     if (mode == SEEDS_MODE_RESIDENT && ctx->cluster == 0) {
@@ -1554,6 +1570,24 @@ seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pi
     const long long blocks = std::min<long long>((n_pixels + 255) / 256, (long long)ctx->n_sm * 8);
     k_rgb2lab<<<(unsigned)blocks, 256, 0, st>>>(rgb, n_pixels, lab_out, ctx->d_lab_tab);
     CK(cudaGetLastError());
+    return SEEDS_OK;
+}
+
+seeds_status seeds_set_block_levels(seeds_ctx *ctx, int lo, int hi)
+{
+    if (!ctx || lo < 0 || hi < -1) return SEEDS_EINVAL;
+    if (ctx->banded) {
+        snprintf(ctx->err, sizeof ctx->err, "a block-level range is not available in row-band mode");
+        return SEEDS_EINVAL;
+    }
+    const int nlo = lo, nhi = hi < 0 ? 1 << 20 : hi;
+    const bool dflt = nlo == 0 && nhi >= ctx->L - 1;
+    if (!dflt && (ctx->mode == SEEDS_MODE_GRAPH || ctx->mode == SEEDS_MODE_RESIDENT)) {
+        snprintf(ctx->err, sizeof ctx->err, "a block-level range runs in grid mode only");
+        return SEEDS_ESTATE;
+    }
+    ctx->blk_lo = nlo;
+    ctx->blk_hi = nhi;
     return SEEDS_OK;
 }
 

@@ -80,6 +80,7 @@ struct GridParams {
     long long *Sb[2];      // means post-processing: channel sums S[k][c] (4 per superpixel), double buffered
     long long S_fs;        // their frame stride (4 A_fs)
     int miters;            // the last miters pixel iterations use the means test (reading M1)
+    int blk_lo, blk_hi;    // block levels that run (reading M4; default 0 .. L - 1)
     int *moves;            // (S + 1) x nf accepted units per sub-sweep
     unsigned *sync;        // grid barrier counter (zero at launch)
     long long *trace;      // debug: per CTA, per phase (clock64 at work end, after barrier), or nullptr
@@ -387,7 +388,8 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     // sub-sweep s belongs to the means post-processing (reading M1); computed
     // from the parameters each time so that nothing stays live across the run
     auto means_sub = [&](int s_) {
-        return MEANS && s_ >= (q.init == nullptr && q.L > 0 ? 4 * q.L * q.iters : 0) + (q.iters - q.miters) * P * P;
+        const int nlev = q.init == nullptr ? max(0, min(q.blk_hi, q.L - 1) - q.blk_lo + 1) : 0;
+        return MEANS && s_ >= 4 * nlev * q.iters + (q.iters - q.miters) * P * P;
     };
     __syncthreads();
 
@@ -514,7 +516,8 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
         for (int l = q.L - 1; l >= 0; l--) {
             const int kind = q.bkind[l];
             const int gs = q.gshift[l], G = 1 << gs;
-            for (int it = 0; it < q.iters; it++)
+            // reading M4: a level outside [blk_lo, blk_hi] runs no iteration
+            for (int it = l > q.blk_hi || l < q.blk_lo ? q.iters : 0; it < q.iters; it++)
                 for (int col = 0; col < 4; col++) {
                     if (q.limit >= 0 && s >= q.limit) break;
                     if (s < q.s0) {  // band mode: sub-sweeps of earlier launches
