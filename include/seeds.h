@@ -125,10 +125,21 @@ seeds_status seeds_batch(seeds_ctx *ctx, const uint8_t *images, int n_frames,
 /* seeds_batch_host -- seeds_batch from and to HOST memory: copies the frames
  * in, runs, copies the labels out and synchronises `stream`.  Pinned host
  * buffers give the fastest copies; pageable ones work.  init_labels_host may
- * be NULL (cold). */
+ * be NULL (cold).  A batch of several frames is cut into 2-4 equal chunks
+ * (seeds_set_host_chunks) whose copies in and out run on two copy streams
+ * while the neighbouring chunks are refined; the frames being independent, the
+ * labels are those of one seeds_batch.  After a chunked call the context holds
+ * only the last chunk's state: seeds_read_state / seeds_stats return
+ * SEEDS_ESTATE until the next seeds_batch / seeds_iterate. */
 seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
                               const int32_t *init_labels_host, int32_t *labels_out_host,
                               void *stream);
+
+/* seeds_set_host_chunks -- chunks of the seeds_batch_host pipeline: 0 (default)
+ * picks the largest of 4, 3, 2 dividing n_frames; 1 turns the pipeline off
+ * (one copy in, one run, one copy out); 2..4 the largest count <= chunks
+ * dividing n_frames.  SEEDS_EINVAL outside 0..4. */
+seeds_status seeds_set_host_chunks(seeds_ctx *ctx, int chunks);
 
 /* seeds_query -- derived geometry and sizes (see seeds_info). */
 seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *out);

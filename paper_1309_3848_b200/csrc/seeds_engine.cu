@@ -74,6 +74,10 @@ struct seeds_ctx {
     int32_t *d_init_stage = nullptr, *d_out_stage = nullptr;
     // graph
     cudaStream_t cap_stream = nullptr;
+    // seeds_batch_host pipeline: copy-in / copy-out streams and chunk events
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t pev[16] = {};
+    int host_chunks = 0;  // seeds_set_host_chunks (0 = automatic)
     // instantiated runs, keyed by their pointers / sizes (least recently used dropped)
     struct GraphEntry {
         GraphKey key;
@@ -1379,6 +1383,55 @@ seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_
         CK(cudaMalloc(&ctx->d_init_stage, (size_t)n_frames * ctx->N * 4));
         ctx->stage_frames = n_frames;
     }
+    // Independent frames: the batch is cut into nc chunks whose copies in and out
+    // (two copy streams) overlap the refinement of the neighbouring chunks.
+    int nc = 1;
+    if (ctx->host_chunks > 0) {
+        nc = std::min(ctx->host_chunks, n_frames);
+        while (n_frames % nc) nc--;
+    } else {
+        for (int c : {4, 3, 2})
+            if (n_frames % c == 0) {
+                nc = c;
+                break;
+            }
+    }
+    if (nc > 1) {
+        if (!ctx->h2d_stream) {
+            CK(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+            for (auto &ev : ctx->pev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        }
+        const int m = n_frames / nc;
+        const size_t fi = (size_t)ctx->N * ctx->C, fo = (size_t)ctx->N * 4;
+        CK(cudaEventRecord(ctx->pev[15], st));  // the staging buffers are free once earlier work on st is done
+        CK(cudaStreamWaitEvent(ctx->h2d_stream, ctx->pev[15], 0));
+        for (int i = 0; i < nc; i++) {
+            const size_t f0 = (size_t)i * m;
+            CK(cudaMemcpyAsync(ctx->d_img_stage + f0 * fi, images_host + f0 * fi, m * fi, cudaMemcpyHostToDevice,
+                               ctx->h2d_stream));
+            if (init_labels_host)
+                CK(cudaMemcpyAsync(ctx->d_init_stage + f0 * ctx->N, init_labels_host + f0 * ctx->N, m * fo,
+                                   cudaMemcpyHostToDevice, ctx->h2d_stream));
+            CK(cudaEventRecord(ctx->pev[i], ctx->h2d_stream));
+        }
+        for (int i = 0; i < nc; i++) {
+            const size_t f0 = (size_t)i * m;
+            CK(cudaStreamWaitEvent(st, ctx->pev[i], 0));
+            seeds_status r = run(ctx, ctx->d_img_stage + f0 * fi, init_labels_host ? ctx->d_init_stage + f0 * ctx->N : nullptr,
+                                 ctx->d_out_stage + f0 * ctx->N, m, st);
+            if (r != SEEDS_OK) return r;
+            CK(cudaEventRecord(ctx->pev[4 + i], st));
+            CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->pev[4 + i], 0));
+            CK(cudaMemcpyAsync(labels_out_host + f0 * ctx->N, ctx->d_out_stage + f0 * ctx->N, m * fo,
+                               cudaMemcpyDeviceToHost, ctx->d2h_stream));
+        }
+        CK(cudaEventRecord(ctx->pev[14], ctx->d2h_stream));
+        CK(cudaStreamWaitEvent(st, ctx->pev[14], 0));
+        CK(cudaStreamSynchronize(st));
+        ctx->ran = false;  // the context's state is that of the last chunk only (seeds_read_state: ESTATE)
+        return SEEDS_OK;
+    }
     CK(cudaMemcpyAsync(ctx->d_img_stage, images_host, (size_t)n_frames * ctx->N * ctx->C,
                        cudaMemcpyHostToDevice, st));
     const int32_t *init = nullptr;
@@ -1392,6 +1445,13 @@ seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_
     CK(cudaMemcpyAsync(labels_out_host, ctx->d_out_stage, (size_t)n_frames * ctx->N * 4, cudaMemcpyDeviceToHost,
                        st));
     CK(cudaStreamSynchronize(st));
+    return SEEDS_OK;
+}
+
+seeds_status seeds_set_host_chunks(seeds_ctx *ctx, int chunks)
+{
+    if (!ctx || chunks < 0 || chunks > 4) return SEEDS_EINVAL;
+    ctx->host_chunks = chunks;
     return SEEDS_OK;
 }
 
@@ -1670,6 +1730,10 @@ void seeds_destroy(seeds_ctx *ctx)
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
+    if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+    for (auto &ev : ctx->pev)
+        if (ev) cudaEventDestroy(ev);
     delete ctx;
 }
 

@@ -25,7 +25,7 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_status_string", "seeds_last_error", "seeds_create_banded", "seeds_band_info",
            "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish",
            "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics", "seeds_set_colour_space",
-           "seeds_rgb_to_lab", "seeds_set_block_levels"]
+           "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks"]
 
 
 class _Metrics(ctypes.Structure):
@@ -74,6 +74,7 @@ def load(path: str = LIB_PATH):
         "seeds_metrics": ([vp, vp, vp, i, i, vp, vp], i),
         "seeds_set_colour_space": ([vp, i], i),
         "seeds_set_block_levels": ([vp, i, i], i),
+        "seeds_set_host_chunks": ([vp, i], i),
         "seeds_rgb_to_lab": ([vp, vp, ctypes.c_longlong, vp, vp], i),
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
@@ -269,6 +270,10 @@ class Seeds:
     def set_block_levels(self, lo: int, hi: int = -1):
         """Only block levels lo..hi run (include/seeds.h seeds_set_block_levels)."""
         self._check(self._lib.seeds_set_block_levels(self._ctx, int(lo), int(hi)))
+
+    def set_host_chunks(self, chunks: int):
+        """Chunks of the batch_host copy / compute pipeline (0 = automatic, 1 = off)."""
+        self._check(self._lib.seeds_set_host_chunks(self._ctx, int(chunks)))
 
     COLOURS = {"rgb": 0, "lab": 1}
 
