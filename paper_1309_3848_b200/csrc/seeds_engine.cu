@@ -1470,7 +1470,8 @@ seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *o)
         o->grid_ctas = ok ? m->grid_G : 0;
         o->grid_tiles = ok ? m->gp.ntiles : 0;
     }
-    o->kernels_per_run = o->exec_mode == SEEDS_MODE_GRAPH ? ctx->kernels_per_run : 1;
+    o->kernels_per_run = (o->exec_mode == SEEDS_MODE_GRAPH ? ctx->kernels_per_run : 1) +
+                         (ctx->colour == SEEDS_COLOUR_LAB ? 1 : 0);  // + the LAB pre-pass
     o->workspace_bytes_per_frame = (size_t)ctx->N * (ctx->bb + 2) +
                                    (size_t)(((long long)ctx->GX * ctx->GY + 7) / 8 * 8) * 4 +
                                    (size_t)ctx->K * (ctx->B + 1) * 8 + (size_t)ctx->N * sizeof(Rec) * 2;
