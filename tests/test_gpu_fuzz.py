@@ -67,3 +67,60 @@ def test_random_case(torch_cuda, orc, case, mode):
         np.testing.assert_array_equal(h.cpu().numpy(), r.hist, err_msg=f"hist frame {f}")
         np.testing.assert_array_equal(a.cpu().numpy(), r.sizes, err_msg=f"sizes frame {f}")
     s.close()
+
+
+FEATURE_CASES = []
+for i in range(40):
+    W = int(RNG.integers(8, 260))
+    H = int(RNG.integers(8, 180))
+    C = int(RNG.choice([1, 3, 3, 4]))
+    bpc = int(RNG.choice([2, 3, 4, 5]))
+    K = int(RNG.integers(1, max(2, W * H // 30)))
+    L = int(RNG.integers(0, 5))
+    gamma = int(RNG.integers(0, 2))
+    iters = int(RNG.integers(1, 5))
+    nf = int(RNG.choice([1, 2, 4]))
+    lab = bool(C == 3 and RNG.integers(0, 2))
+    means = int(RNG.integers(0, iters + 1)) if RNG.integers(0, 2) else 0
+    lo = int(RNG.integers(0, 3))
+    hi = int(RNG.integers(-1, 4))
+    warm = bool(RNG.integers(0, 4) == 0)
+    host = bool(RNG.integers(0, 2))
+    FEATURE_CASES.append((i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host))
+
+
+@pytest.mark.parametrize("case", FEATURE_CASES, ids=[f"feat{c[0]}" for c in FEATURE_CASES])
+def test_random_feature_combination(torch_cuda, orc, case):
+    """Grid mode with the SURVEY 8(f) options combined at random (LAB pre-pass,
+    means post-processing, block-level range, warm starts, the chunked host
+    entry point): labels equal the oracle's with the same options."""
+    from paper_1309_3848_b200.seeds import Seeds, SeedsError
+    torch = torch_cuda
+    i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host = case
+    p = dict(n_superpixels=K, n_levels=L, bins_per_channel=bpc, smoothness_prior=gamma, iters_per_level=iters)
+    imgs = np.stack([mosaic.mosaic(W, H, int(RNG.integers(1, 30)), 10.0, seed=7000 + 10 * i + f, C=C, grad=20.0)
+                     for f in range(nf)])
+    try:
+        s = Seeds(W, H, C, K, L, bpc, gamma, iters)
+    except SeedsError:
+        pytest.skip("geometry rejected")
+    if lab:
+        s.set_colour_space("lab")
+    s.set_means_iters(means)
+    s.set_block_levels(lo, hi)
+    opts = dict(colour="lab" if lab else "rgb", means_iters=means, block_levels=(lo, hi if hi >= 0 else 99))
+    init = np.stack([orc.run(im, **p, **opts).labels for im in imgs]) if warm else None
+    if host:
+        out = np.empty((nf, H, W), np.int32)
+        s.batch_host(np.ascontiguousarray(imgs), out, init_labels=None if init is None else np.ascontiguousarray(init))
+    else:
+        d = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
+        di = None if init is None else torch.from_numpy(np.ascontiguousarray(init, np.int32)).cuda()
+        out = s.batch(d, init_labels=di).cpu().numpy()
+    for f in range(nf):
+        r = orc.run(imgs[f], **p, **opts, init_labels=None if init is None else init[f])
+        np.testing.assert_array_equal(out[f], r.labels, err_msg=f"labels frame {f}")
+        if not host:
+            h, a = s.read_state(f)
+            np.testing.assert_array_equal(h.cpu().numpy(), r.hist, err_msg=f"hist frame {f}")
+    s.close()
