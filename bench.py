@@ -339,31 +339,49 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def parallel_sample(name, workers):
-    """Batch configs (c3, c4): independent frames, one oracle call per host
-    core at a time (frame- / clip-parallel on all host cores).
-    c4 uses the cold first frames of its clips (a warm frame needs its
-    predecessor's labels)."""
-    import numpy as np
+def parallel_sample(name, workers, clip_len=None):
+    """Batch configs (c3, c4): frame- / clip-parallel on the host
+    cores.  c3: min(cores, 256) independent frames.  c4: the whole video -- its
+    8 clips in parallel, each a warm-started chain (frame 0 cold, frames 1..7
+    from the previous labels, reading Q14/O9): shape (8, 8, H, W, C)."""
     p = configs.params(name)
     if name == "c3":
         f = configs.frames(name, n=min(workers, 256))
         return f, p, f"{len(f)} frames of c3"
-    f = np.ascontiguousarray(configs.clips(name)[:, 0])
-    return f, p, f"the {len(f)} cold clip-start frames of c4"
+    f = configs.clips(name)
+    if clip_len:
+        f = f[:, :clip_len]
+    return f, p, f"the {f.shape[0]} clips x {f.shape[1]} warm-chained frames of c4"
 
 
 def oracle_frames(imgs, p, workers):
-    """Run the oracle once on every frame of `imgs` with `workers` threads
-    (ctypes releases the GIL; the oracle keeps no global state)."""
+    """Run the oracle on every frame of `imgs` with `workers` threads (ctypes
+    releases the GIL; the oracle keeps no global state).  A 5-D `imgs` is a
+    set of clips: each thread runs one clip's warm-started chain."""
     import oracle
     from concurrent.futures import ThreadPoolExecutor
+
+    def one(img):
+        if img.ndim == 4:  # a clip: frame t warm-started from frame t - 1's labels
+            prev = None
+            for fr in img:
+                prev = oracle.run(fr, **p, init_labels=prev).labels
+        else:
+            oracle.run(img, **p)
     if workers <= 1:
         for img in imgs:
-            oracle.run(img, **p)
+            one(img)
         return
     with ThreadPoolExecutor(max_workers=workers) as ex:
-        list(ex.map(lambda img: oracle.run(img, **p), list(imgs)))
+        list(ex.map(one, list(imgs)))
+
+
+def sample_pixels(imgs):
+    """Pixels of a sample of frames (4-D) or clips (5-D)."""
+    n = 1
+    for d in imgs.shape[:-3]:
+        n *= d
+    return n * imgs.shape[-3] * imgs.shape[-2]
 
 
 def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb"):
@@ -392,8 +410,8 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb"):
               "sample": f"{n} runs of {note}, single thread, COL schedule, {el:.1f} s"}
     if name not in ("c3", "c4"):
         return single
-    workers = host_cores()
-    imgs, p, note = parallel_sample(name, workers)
+    imgs, p, note = parallel_sample(name, host_cores())
+    workers = min(host_cores(), len(imgs))  # threads actually used
     if means_iters:
         p = dict(p, means_iters=means_iters)
     if colour != "rgb":
@@ -401,9 +419,9 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb"):
     t0 = time.perf_counter()
     oracle_frames(imgs, p, workers)
     el = time.perf_counter() - t0
-    px = len(imgs) * imgs.shape[1] * imgs.shape[2]
+    px = sample_pixels(imgs)
     return {"value": px / el / 1e6, "unit": UNIT, "cores": workers, "kind": "oracle",
-            "sample": f"{note}, frame-parallel on {workers} host threads, COL schedule, {el:.1f} s",
+            "sample": f"{note}, in parallel on {workers} host threads, COL schedule, {el:.1f} s",
             "single_thread": single}
 
 
@@ -415,10 +433,11 @@ def run_reference(args):
     name = args.config
     oracle.build()
     workers = host_cores() if name in ("c3", "c4") else 1
-    if workers > 1:  # batch configs: each step is one frame-parallel batch on all host cores
-        imgs, p, note = parallel_sample(name, workers)
+    if workers > 1:  # batch configs: each step is one parallel batch on the host cores
+        imgs, p, note = parallel_sample(name, workers, clip_len=2)  # c4: each step 8 clips x 2 frames
+        workers = min(workers, len(imgs))
         batches = [imgs[i:i + workers] for i in range(0, len(imgs), workers)]
-        note = f"{len(batches[0])} frames ({note}) frame-parallel on {workers} host threads"
+        note = f"{note}, in parallel on {workers} host threads"
     else:
         imgs, p, note = reference_sample(name)
         batches = [imgs[i:i + 1] for i in range(len(imgs))]
@@ -429,14 +448,15 @@ def run_reference(args):
         p = dict(p, colour=args.colour)
         note += f", {args.colour} pre-pass"
     for i in range(args.warmup):
-        oracle_frames(batches[i % len(batches)][:1], p, 1)
+        b0 = batches[i % len(batches)][:1]
+        oracle_frames(b0[:, :1] if b0.ndim == 5 else b0, p, 1)
     t, px = [], 0
     for i in range(args.steps):
         bt = batches[i % len(batches)]
         t0 = time.perf_counter()
         oracle_frames(bt, p, workers)
         t.append(time.perf_counter() - t0)
-        px += len(bt) * bt.shape[1] * bt.shape[2]
+        px += sample_pixels(bt)
     tot = sum(t)
     v = px / tot / 1e6
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
