@@ -603,6 +603,10 @@ def main():
     # Issue-rate roofline: the kernel is latency / issue bound, not HBM bound
     # (DESIGN.md section 6): warp instructions of one launch (ncu) over the
     # live launch time, against 4 issue slots x #SM x the sampled SM clock.
+    # SURVEY 8(d) fraction (1): the DRAM bandwidth ncu measured for the launch
+    if traffic and ncu_us:
+        roofline["ncu_dram_gbs"] = traffic / (ncu_us * 1e3)
+        roofline["ncu_dram_frac"] = roofline["ncu_dram_gbs"] / hbm
     # The instruction count and its time come from the same ncu capture (for
     # c4 that capture is a cold 8-frame launch while the bench averages cold
     # and warm launches, so the live average would not pair with it).
