@@ -591,11 +591,6 @@ static bool getenv_off(const char *name)
     const char *v = getenv(name);
     return v && atoi(v) == 0;
 }
-static bool getenv_on(const char *name)
-{
-    const char *v = getenv(name);
-    return v && atoi(v) != 0;
-}
 
 // TMA descriptors of the grid plan: the padded label planes (u16, x y frame,
 // box bw x bh) and, when the bins are staged, the padded bin planes.
