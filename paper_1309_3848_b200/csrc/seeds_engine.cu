@@ -1189,11 +1189,32 @@ static void lab_tables(std::vector<int32_t> &t)
         t[256 + 3 * i + big] += 4096 - sum;
     }
     const double d = 6.0 / 29.0;
+    std::vector<int32_t> F(65536);
     for (int u = 0; u < 65536; u++) {
         const double x = u / 65535.0;
         const double f = x > d * d * d ? std::cbrt(x) : x / (3.0 * d * d) + 4.0 / 29.0;
-        t[256 + 9 + u] = (int32_t)std::floor(f * 65536.0 + 0.5);
+        F[u] = (int32_t)std::floor(f * 65536.0 + 0.5);
     }
+    // F16 = F - F[0] (the kernel uses differences of F only; F is increasing, F[65535] - F[0] < 2^16)
+    uint16_t *F16 = reinterpret_cast<uint16_t *>(t.data() + LAB_F16_OFF);
+    for (int u = 0; u < 65536; u++) F16[u] = (uint16_t)(F[u] - F[0]);
+    // L8 for every T_Y: round((116 F - 16 * 65536) * 255 / (100 * 65536)), clamped to [0, 255]
+    uint8_t *L8 = reinterpret_cast<uint8_t *>(t.data() + LAB_L8_OFF);
+    for (int u = 0; u < 65536; u++) {
+        const long long Lfp = 116LL * F[u] - 16LL * 65536;
+        const long long L = Lfp < 0 ? 0 : (Lfp * 255 + 50LL * 65536) / (100LL * 65536);
+        L8[u] = (uint8_t)(L > 255 ? 255 : L);
+    }
+}
+static seeds_status ensure_lab_tables(seeds_ctx *ctx)
+{
+    if (ctx->d_lab_tab) return SEEDS_OK;
+    std::vector<int32_t> t;
+    lab_tables(t);
+    CK(cudaFuncSetAttribute(k_rgb2lab, cudaFuncAttributeMaxDynamicSharedMemorySize, LAB_SMEM));
+    CK(cudaMalloc(&ctx->d_lab_tab, t.size() * sizeof(int32_t)));
+    CK(cudaMemcpy(ctx->d_lab_tab, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    return SEEDS_OK;
 }
 
 // LAB mode: convert nf frames into the context's buffer (allocated outside
@@ -1214,8 +1235,8 @@ static const uint8_t *enqueue_lab(seeds_ctx *ctx, const uint8_t *img, int nf, cu
 {
     if (ctx->colour != SEEDS_COLOUR_LAB) return img;
     const long long n = (long long)nf * ctx->N;
-    const long long blocks = std::min<long long>((n + 255) / 256, (long long)ctx->n_sm * 8);
-    k_rgb2lab<<<(unsigned)blocks, 256, 0, st>>>(img, n, ctx->d_labimg, ctx->d_lab_tab);
+    const long long blocks = std::min<long long>((n + 4 * LAB_THREADS - 1) / (4 * LAB_THREADS), ctx->n_sm);
+    k_rgb2lab<<<(unsigned)blocks, LAB_THREADS, LAB_SMEM, st>>>(img, n, ctx->d_labimg, ctx->d_lab_tab);
     return ctx->d_labimg;
 }
 
@@ -1602,11 +1623,9 @@ seeds_status seeds_set_colour_space(seeds_ctx *ctx, int space)
         snprintf(ctx->err, sizeof ctx->err, "the LAB pre-pass needs 3 channels");
         return SEEDS_EINVAL;
     }
-    if (space == SEEDS_COLOUR_LAB && !ctx->d_lab_tab) {
-        std::vector<int32_t> t;
-        lab_tables(t);
-        CK(cudaMalloc(&ctx->d_lab_tab, t.size() * sizeof(int32_t)));
-        CK(cudaMemcpy(ctx->d_lab_tab, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (space == SEEDS_COLOUR_LAB) {
+        seeds_status r = ensure_lab_tables(ctx);
+        if (r != SEEDS_OK) return r;
     }
     ctx->colour = space;
     return SEEDS_OK;
@@ -1615,16 +1634,12 @@ seeds_status seeds_set_colour_space(seeds_ctx *ctx, int space)
 seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pixels, uint8_t *lab_out, void *stream)
 {
     if (!ctx || !rgb || !lab_out || n_pixels < 0) return SEEDS_EINVAL;
-    if (!ctx->d_lab_tab) {
-        std::vector<int32_t> t;
-        lab_tables(t);
-        CK(cudaMalloc(&ctx->d_lab_tab, t.size() * sizeof(int32_t)));
-        CK(cudaMemcpy(ctx->d_lab_tab, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    }
+    seeds_status r = ensure_lab_tables(ctx);
+    if (r != SEEDS_OK) return r;
     if (n_pixels == 0) return SEEDS_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const long long blocks = std::min<long long>((n_pixels + 255) / 256, (long long)ctx->n_sm * 8);
-    k_rgb2lab<<<(unsigned)blocks, 256, 0, st>>>(rgb, n_pixels, lab_out, ctx->d_lab_tab);
+    const long long blocks = std::min<long long>((n_pixels + 4 * LAB_THREADS - 1) / (4 * LAB_THREADS), ctx->n_sm);
+    k_rgb2lab<<<(unsigned)blocks, LAB_THREADS, LAB_SMEM, st>>>(rgb, n_pixels, lab_out, ctx->d_lab_tab);
     CK(cudaGetLastError());
     return SEEDS_OK;
 }
