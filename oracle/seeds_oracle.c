@@ -108,6 +108,8 @@ typedef struct {
     int want_energy;
     int max_subsweeps; /* -1 = unlimited (bisection hook) */
     int block_lo, block_hi; /* block levels that run (reading M4); the others only push down */
+    int compact;            /* compactness prior at the pixel level (reading M5) */
+    int64_t *cen;           /* K*2: integer centroids (x, y) at the start of the pixel iteration */
     int subsweeps_done;
     int64_t *lblock;   /* B: block histogram scratch */
     const int *curM;   /* block phase: current block map (for traced energies) */
@@ -474,6 +476,37 @@ static int decide_block(st_t *s, int *M, int w, int h, int l, int bi, int bj, in
 }
 
 /* decide for pixel (x, y) on the label plane. */
+/* Compactness prior ("minimize the distance between the
+ * pixels on the superpixel boundary and the center of gravity of the
+ * superpixel"), reading M5: a pixel-level move k -> n also needs p strictly
+ * nearer (squared Euclidean, integers) to n's centre of gravity than to k's,
+ * the centres recomputed at the start of every pixel iteration and rounded to
+ * the nearest pixel (half up): c = floor((2 S + A) / (2 A)). */
+static void compact_recount(st_t *s)
+{
+    int64_t *sx = (int64_t *)calloc((size_t)s->K * 3, sizeof(int64_t));
+    for (int y = 0; y < s->H; y++)
+        for (int x = 0; x < s->W; x++) {
+            int k = s->lab[y * s->W + x];
+            sx[3 * k] += x;
+            sx[3 * k + 1] += y;
+            sx[3 * k + 2] += 1;
+        }
+    for (int k = 0; k < s->K; k++) {
+        int64_t a = sx[3 * k + 2] > 0 ? sx[3 * k + 2] : 1;
+        s->cen[2 * k] = (2 * sx[3 * k] + a) / (2 * a);
+        s->cen[2 * k + 1] = (2 * sx[3 * k + 1] + a) / (2 * a);
+    }
+    free(sx);
+}
+
+static int compact_test(const st_t *s, int x, int y, int k, int n)
+{
+    int64_t dxn = x - s->cen[2 * n], dyn = y - s->cen[2 * n + 1];
+    int64_t dxk = x - s->cen[2 * k], dyk = y - s->cen[2 * k + 1];
+    return dxn * dxn + dyn * dyn < dxk * dxk + dyk * dyk;
+}
+
 static int decide_pixel(st_t *s, int x, int y, int *is_boundary, int *is_removable)
 {
     int k = s->lab[y * s->W + x];
@@ -490,6 +523,7 @@ static int decide_pixel(st_t *s, int x, int y, int *is_boundary, int *is_removab
         if (s->means_on ? !means_test_pixel(s, (int64_t)y * s->W + x, k, n) : !colour_test_pixel(s, j, k, n))
             continue;
         if (s->gamma && smooth_sum(s->lab, s->W, s->H, x, y, k, n) < 0) continue;
+        if (s->compact && !compact_test(s, x, y, k, n)) continue;
         return n;
     }
     return -1;
@@ -583,6 +617,7 @@ static void pixel_level(st_t *s)
             s->means_on = 1;
             means_recount(s);
         }
+        if (s->compact) compact_recount(s);  /* reading M5: centres of this iteration */
         if (s->schedule == ORACLE_SEQ) {
             if (limit_reached(s)) break;
             int nm = 0;
@@ -643,13 +678,14 @@ static void pixel_level(st_t *s)
 /*               means test (reading M1; 0 = off, needs N < 2^27)            */
 /*   sums_out:   K_act*4 int64 channel sums S[k][c] at the end, or NULL       */
 /*   block_lo, block_hi: only block levels in [lo, hi] run (-1: 0 / L_eff-1)  */
+/*   compact:    compactness prior at the pixel level (reading M5)            */
 /* Returns K_act, or < 0 on invalid arguments.                                */
 /* ------------------------------------------------------------------------ */
 int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, int gamma, int iters,
                int schedule, int rule, const int32_t *init, int32_t *labels_out, int32_t *hist_out,
                int32_t *sizes_out, oracle_trace *trace, int trace_cap, int *trace_len,
                int want_energy, uint64_t shuffle_seed, int max_subsweeps, int means_iters,
-               int64_t *sums_out, int block_lo, int block_hi)
+               int64_t *sums_out, int block_lo, int block_hi, int compact)
 {
     if (W < 1 || H < 1 || C < 1 || C > 4 || K < 1 || L < 0 || bpc < 1 || bpc > 256 || iters < 0)
         return -1;
@@ -671,6 +707,7 @@ int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, i
     s.max_subsweeps = max_subsweeps;
     s.block_lo = block_lo < 0 ? 0 : block_lo;
     s.block_hi = block_hi < 0 ? 1 << 30 : block_hi;
+    s.compact = compact ? 1 : 0;
     s.img = img;
     s.means_iters = means_iters;
     int64_t N = (int64_t)W * H;
@@ -680,6 +717,7 @@ int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, i
     s.size = (int64_t *)calloc(s.K, sizeof(int64_t));
     s.lblock = (int64_t *)malloc(sizeof(int64_t) * s.B);
     s.msum = (int64_t *)calloc((size_t)s.K * 4, sizeof(int64_t));
+    s.cen = (int64_t *)calloc((size_t)s.K * 2, sizeof(int64_t));
     s.x0 = (int *)malloc(sizeof(int) * (s.GX + 1));
     s.y0 = (int *)malloc(sizeof(int) * (s.GY + 1));
     /* level-0 block column i spans [floor(i W / GX), floor((i+1) W / GX)) */
@@ -756,6 +794,7 @@ int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, i
     }
     free(s.bin); free(s.lab); free(s.hist); free(s.size); free(s.lblock); free(s.x0); free(s.y0);
     free(s.msum);
+    free(s.cen);
     return s.K;
 }
 
