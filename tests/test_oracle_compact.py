@@ -59,7 +59,7 @@ def predict(orc, lab, bins, B, colour, P, gamma, cx, cy):
     return out
 
 
-@pytest.mark.parametrize("gamma,L", [(0, 1), (1, 2), (0, 0)])
+@pytest.mark.parametrize("gamma,L", [(0, 1), (1, 2), (1, 1)])
 def test_compact_subsweeps_brute_force(orc, gamma, L):
     img = mosaic.mosaic(40, 30, 6, sigma=12.0, seed=31, grad=20.0)
     p = dict(n_superpixels=12, n_levels=L, bins_per_channel=4, smoothness_prior=gamma, iters_per_level=2)
@@ -102,3 +102,17 @@ def test_compact_invariants(orc, schedule):
     plain = orc.run(img, **p, schedule=schedule)
     px = lambda t: sum(x["moves"] for x in t if x["level"] == -1)
     assert 0 < px(r.trace) < px(plain.trace)  # the prior only removes pixel moves
+
+
+@pytest.mark.parametrize("gamma", [0, 1])
+def test_equal_grid_is_a_fixed_point_without_blocks(orc, gamma):
+    """SPH (no block levels) with the prior on a grid of equal cells: every pixel
+    is at least as near its own cell's centre as any neighbour's (ties reject),
+    so no pixel can move whatever the colours."""
+    img = mosaic.mosaic(40, 30, 9, sigma=12.0, seed=5, grad=30.0)   # nx = 4, ny = 3: 10 x 10 cells
+    p = dict(n_superpixels=12, n_levels=0, bins_per_channel=4, smoothness_prior=gamma, iters_per_level=3)
+    r = orc.run(img, **p, compact=True)
+    assert sum(t["moves"] for t in r.trace) == 0
+    np.testing.assert_array_equal(r.labels, orc.run(img, **dict(p, iters_per_level=0)).labels)
+    if gamma == 0:  # (with gamma = 1 straight seams cannot move at all, reading Q7)
+        assert sum(t["moves"] for t in orc.run(img, **p).trace) > 0  # the colours alone would move pixels
