@@ -187,6 +187,17 @@ seeds_status seeds_set_colour_space(seeds_ctx *ctx, int space);
 seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pixels, uint8_t *lab_out,
                               void *stream);
 
+/* seeds_set_compactness -- the compactness prior ("minimize
+ * the distance between the pixels on the superpixel boundary and the center of
+ * gravity of the superpixel"), reading M5: every later run's pixel-level moves
+ * k -> n also need the pixel strictly nearer (squared Euclidean, integers) to
+ * n's centre of gravity than to k's, the centres -- rounded to the nearest pixel,
+ * half up -- recomputed at the start of every pixel iteration.  Block moves are
+ * unaffected (like G).  on: 0 (default) or 1.
+ *   SEEDS_EINVAL  on not 0/1, or a row-band ctx
+ *   SEEDS_ESTATE  the ctx is forced to graph or resident mode (grid mode only) */
+seeds_status seeds_set_compactness(seeds_ctx *ctx, int on);
+
 /* seeds_set_block_levels -- block levels lo..hi (0 = finest) run in every later
  * cold run; the other levels run no iteration (their labels pass down
  * unchanged).  lo = hi gives one block size, the variant of the authors'

@@ -36,10 +36,12 @@ struct GraphKey {
     int miters = 0;
     int colour = 0;
     int blk_lo = 0, blk_hi = 0;
+    int compact = 0;
     bool operator==(const GraphKey &o) const
     {
         return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof &&
-               mode == o.mode && miters == o.miters && colour == o.colour && blk_lo == o.blk_lo && blk_hi == o.blk_hi;
+               mode == o.mode && miters == o.miters && colour == o.colour && blk_lo == o.blk_lo && blk_hi == o.blk_hi &&
+               compact == o.compact;
     }
 };
 
@@ -64,6 +66,8 @@ struct seeds_ctx {
     int *d_H[2] = {nullptr, nullptr};
     int *d_A[2] = {nullptr, nullptr};
     long long *d_S[2] = {nullptr, nullptr};  // means post-processing: channel sums, 4 per superpixel (grid mode)
+    long long *d_csum = nullptr;  // compactness prior: coordinate sums and counts, 4 per superpixel
+    int2 *d_cen = nullptr;        // compactness prior: centres of the current pixel iteration
     Rec *d_rec[2] = {nullptr, nullptr};
     int *d_cnt = nullptr;    // (S + 1) rows x cap_frames: delta entries per sub-sweep
     int *d_moves = nullptr;  // (S + 1) rows x cap_frames: accepted units per sub-sweep
@@ -91,6 +95,7 @@ struct seeds_ctx {
     int limit = -1;
     int miters = 0;       // seeds_set_means_iters (reading M1)
     int blk_lo = 0, blk_hi = 1 << 20;  // seeds_set_block_levels (reading M4): all levels by default
+    int compact = 0;                   // seeds_set_compactness (reading M5)
     int last_miters = 0;  // of the last run
     int last_nf = 0;
     int last_final = 0;  // H buffer holding the final state
@@ -316,6 +321,8 @@ static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
         release((void *&)ctx->d_rec[i]);
     }
     release((void *&)ctx->d_cnt);
+    release((void *&)ctx->d_csum);
+    release((void *&)ctx->d_cen);
     release((void *&)ctx->d_moves);
     ctx->cap_frames = 0;
     const size_t F = nf;
@@ -339,6 +346,8 @@ static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
     if (!ctx->d_sync) CK(cudaMalloc(&ctx->d_sync, 16));
     ctx->grid_nf = -1;
     CK(cudaMalloc(&ctx->d_cnt, (size_t)(ctx->S + 1) * F * 4));
+    CK(cudaMalloc(&ctx->d_csum, F * ctx->Afs * 4 * sizeof(long long)));
+    CK(cudaMalloc(&ctx->d_cen, F * ctx->Afs * sizeof(int2)));
     CK(cudaMalloc(&ctx->d_moves, (size_t)(ctx->S + 1) * F * 4));
     ctx->cap_frames = nf;
     return SEEDS_OK;
@@ -523,6 +532,10 @@ static int block_levels_run(const seeds_ctx *c)
     return std::max(0, std::min(c->blk_hi, c->L - 1) - c->blk_lo + 1);
 }
 static bool default_levels(const seeds_ctx *c) { return c->blk_lo == 0 && c->blk_hi >= c->L - 1; }
+// the extended pixel path (k_grid<..., 1>): means post-processing or the compactness prior
+static bool ext_pixel(const seeds_ctx *c) { return c->miters > 0 || c->compact; }
+// options that only grid mode implements
+static bool grid_only(const seeds_ctx *c) { return ext_pixel(c) || !default_levels(c); }
 
 static int resolved_mode(seeds_ctx *c, int nf)
 {
@@ -910,6 +923,7 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     }
     if (ctx->miters > 0)
         for (int i = 0; i < 2; i++) CK(cudaMemsetAsync(ctx->d_S[i], 0, (size_t)nf * ctx->Afs * 4 * sizeof(long long), st));
+    if (ctx->compact) CK(cudaMemsetAsync(ctx->d_csum, 0, (size_t)nf * ctx->Afs * 4 * sizeof(long long), st));
     CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)(ctx->S + 1) * nf * 4, st));
     CK(cudaMemsetAsync(ctx->d_sync, 0, 16, st));
     GridParams q = ctx->gp;
@@ -931,6 +945,9 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     q.miters = ctx->miters;
     q.blk_lo = ctx->blk_lo;
     q.blk_hi = ctx->blk_hi;
+    q.compact = ctx->compact;
+    q.csum = ctx->d_csum;
+    q.cen = ctx->d_cen;
     q.moves = ctx->d_moves;
     q.sync = ctx->d_sync;
     q.trace = ctx->d_trace;
@@ -938,10 +955,10 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
     cudaError_t e;
     if (ctx->grid_nt == GRID_THREADS)
-        e = ctx->miters > 0 ? launch_grid_nt<GRID_THREADS, 1>(ctx, q, st) : launch_grid_nt<GRID_THREADS, 0>(ctx, q, st);
+        e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS, 1>(ctx, q, st) : launch_grid_nt<GRID_THREADS, 0>(ctx, q, st);
     else
-        e = ctx->miters > 0 ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
-                            : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
+        e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
+                           : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid launch");
     CK(prof_end(ctx, st));
     const bool blocks = init == nullptr && ctx->L > 0;
@@ -1248,9 +1265,10 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     r = ensure_labimg(ctx, nf);
     if (r != SEEDS_OK) return r;
     const int mode = resolved_mode(ctx, nf);
-    if ((ctx->miters > 0 || !default_levels(ctx)) && mode != SEEDS_MODE_GRID) {
+    if (grid_only(ctx) && mode != SEEDS_MODE_GRID) {
         snprintf(ctx->err, sizeof ctx->err,
-                 "the means post-processing / a block-level range run in grid mode only, and no grid plan fits");
+                 "the means post-processing, the compactness prior and block-level ranges run in grid mode only, "
+                 "and no grid plan fits");
         return SEEDS_ESTATE;
     }
     ctx->last_miters = ctx->miters;
@@ -1270,6 +1288,7 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     key.miters = ctx->miters;
     key.blk_lo = ctx->blk_lo;
     key.blk_hi = ctx->blk_hi;
+    key.compact = ctx->compact;
     key.colour = ctx->colour;
     seeds_ctx::GraphEntry *hit = nullptr;
     for (auto &g : ctx->graphs)
@@ -1556,8 +1575,9 @@ seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out,
 seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 {
     if (!ctx || mode < SEEDS_MODE_AUTO || mode > SEEDS_MODE_GRID) return SEEDS_EINVAL;
-    if ((ctx->miters > 0 || !default_levels(ctx)) && (mode == SEEDS_MODE_GRAPH || mode == SEEDS_MODE_RESIDENT)) {
-        snprintf(ctx->err, sizeof ctx->err, "the means post-processing / a block-level range run in grid mode only");
+    if (grid_only(ctx) && (mode == SEEDS_MODE_GRAPH || mode == SEEDS_MODE_RESIDENT)) {
+        snprintf(ctx->err, sizeof ctx->err,
+                 "the means post-processing, the compactness prior and block-level ranges run in grid mode only");
         return SEEDS_ESTATE;
     }
     if (mode == SEEDS_MODE_RESIDENT && ctx->cluster == 0) {
@@ -1641,6 +1661,21 @@ seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pi
     const long long blocks = std::min<long long>((n_pixels + 4 * LAB_THREADS - 1) / (4 * LAB_THREADS), ctx->n_sm);
     k_rgb2lab<<<(unsigned)blocks, LAB_THREADS, LAB_SMEM, st>>>(rgb, n_pixels, lab_out, ctx->d_lab_tab);
     CK(cudaGetLastError());
+    return SEEDS_OK;
+}
+
+seeds_status seeds_set_compactness(seeds_ctx *ctx, int on)
+{
+    if (!ctx || (on != 0 && on != 1)) return SEEDS_EINVAL;
+    if (on && ctx->banded) {
+        snprintf(ctx->err, sizeof ctx->err, "the compactness prior is not available in row-band mode");
+        return SEEDS_EINVAL;
+    }
+    if (on && (ctx->mode == SEEDS_MODE_GRAPH || ctx->mode == SEEDS_MODE_RESIDENT)) {
+        snprintf(ctx->err, sizeof ctx->err, "the compactness prior runs in grid mode only");
+        return SEEDS_ESTATE;
+    }
+    ctx->compact = on;
     return SEEDS_OK;
 }
 
@@ -1874,10 +1909,10 @@ seeds_status seeds_band_subsweep(seeds_ctx *ctx, int s, const void *records_in, 
     q.rec_count = n_out;
     cudaError_t e;
     if (ctx->grid_nt == GRID_THREADS)
-        e = ctx->miters > 0 ? launch_grid_nt<GRID_THREADS, 1>(ctx, q, st) : launch_grid_nt<GRID_THREADS, 0>(ctx, q, st);
+        e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS, 1>(ctx, q, st) : launch_grid_nt<GRID_THREADS, 0>(ctx, q, st);
     else
-        e = ctx->miters > 0 ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
-                            : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
+        e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
+                           : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid (band) launch");
     ctx->last_done = s + 1;
     return SEEDS_OK;

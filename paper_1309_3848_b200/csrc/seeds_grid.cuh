@@ -80,6 +80,9 @@ struct GridParams {
     long long *Sb[2];      // means post-processing: channel sums S[k][c] (4 per superpixel), double buffered
     long long S_fs;        // their frame stride (4 A_fs)
     int miters;            // the last miters pixel iterations use the means test (reading M1)
+    int compact;           // compactness prior at the pixel level (reading M5)
+    long long *csum;       // per frame and superpixel: sum x, sum y, count (4 int64) for the centres
+    int2 *cen;             // per frame and superpixel: the centre of gravity of this pixel iteration
     int blk_lo, blk_hi;    // block levels that run (reading M4; default 0 .. L - 1)
     int *moves;            // (S + 1) x nf accepted units per sub-sweep
     unsigned *sync;        // grid barrier counter (zero at launch)
@@ -983,6 +986,71 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                 }
                 grid_barrier(q.sync, target);
             }
+            if (MEANS && q.compact && col == 0) {
+                // reading M5: centres of gravity of the current labels for this pixel
+                // iteration -- coordinate sums per label (warp-aggregated, then one set
+                // of atomics per label and CTA through a shared-memory table), a grid
+                // barrier, the rounded centres (each CTA a slice of the superpixels,
+                // whose sums it zeroes for the next iteration), a grid barrier
+                constexpr unsigned EMPTY = 0xFFFFFFFFu;
+                int hn = 1;
+                while (hn < 1024 && (size_t)(2 * hn) * 32 <= (size_t)2 * q.stage_bytes) hn *= 2;
+                unsigned *hkey = reinterpret_cast<unsigned *>(c.stage0);
+                unsigned long long *hsum = reinterpret_cast<unsigned long long *>(hkey + hn + (hn & 1));  // hn x 3
+                for (int i = tid; i < hn; i += NT) {
+                    hkey[i] = EMPTY;
+                    hsum[3 * i] = hsum[3 * i + 1] = hsum[3 * i + 2] = 0;
+                }
+                __syncthreads();
+                for (int ti = 0; ti < ntl; ti++) {
+                    const GridTile t = c.tiles[ti];
+                    const uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
+                    for (int y = t.Y0 + wid; y < t.Y1; y += NW)
+                        for (int x0 = t.X0; x0 < t.X1; x0 += 32) {
+                            const int x = x0 + lane;
+                            const int k = x < t.X1 ? (int)__ldcg(gl + (long long)(y + 2) * q.lpitch + x + 2) : -1;
+                            unsigned todo = __ballot_sync(FULL, k >= 0);
+                            while (todo) {
+                                const int kl = __shfl_sync(FULL, k, __ffs(todo) - 1);
+                                const bool mine = k == kl;
+                                const unsigned m = __ballot_sync(FULL, mine);
+                                todo &= ~m;
+                                const unsigned sxs = __reduce_add_sync(FULL, mine ? (unsigned)x : 0u);
+                                if (lane == 0) {
+                                    const unsigned long long v[3] = {sxs, (unsigned long long)y * __popc(m),
+                                                                     (unsigned long long)__popc(m)};
+                                    const unsigned key = (unsigned)t.f << 16 | (unsigned)kl;
+                                    const int slot = (int)((key * 2654435761u) >> 8) & (hn - 1);
+                                    const unsigned old = atomicCAS(&hkey[slot], EMPTY, key);
+                                    unsigned long long *dst = old == EMPTY || old == key
+                                                                  ? hsum + 3 * slot
+                                                                  : reinterpret_cast<unsigned long long *>(
+                                                                        q.csum + ((long long)t.f * q.A_fs + kl) * 4);
+#pragma unroll
+                                    for (int i = 0; i < 3; i++) atomicAdd(dst + i, v[i]);
+                                }
+                            }
+                        }
+                }
+                __syncthreads();
+                for (int i = tid; i < hn; i += NT) {
+                    const unsigned key = hkey[i];
+                    if (key == EMPTY) continue;
+                    unsigned long long *dst = reinterpret_cast<unsigned long long *>(
+                        q.csum + ((long long)(key >> 16) * q.A_fs + (key & 0xFFFF)) * 4);
+#pragma unroll
+                    for (int j = 0; j < 3; j++) atomicAdd(dst + j, hsum[3 * i + j]);
+                }
+                grid_barrier(q.sync, target);
+                for (long long gk = (long long)blockIdx.x * NT + tid; gk < (long long)q.nf * q.A_fs;
+                     gk += (long long)gridDim.x * NT) {
+                    long long *cs = q.csum + gk * 4;
+                    const long long a = __ldcg(cs + 2) > 0 ? __ldcg(cs + 2) : 1;
+                    q.cen[gk] = make_int2((int)((2 * __ldcg(cs) + a) / (2 * a)), (int)((2 * __ldcg(cs + 1) + a) / (2 * a)));
+                    cs[0] = cs[1] = cs[2] = 0;
+                }
+                grid_barrier(q.sync, target);
+            }
             const int cx = col % P, cy = col / P;
             const int ob = q.band ? 0 : s & 1, yb_ = ob ^ 1;
             begin_subsweep(yb_);
@@ -1150,10 +1218,12 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                         c.set(u.xy & 0xFFFF, u.xy >> 16, u.acc);
                     }
                 };
-                if (MEANS && it >= q.iters - q.miters) {
-                    // means sub-sweep (reading M1): one thread per unit; the first
-                    // candidate (W, E, N, S) whose mean colour is strictly nearer
-                    // than k's and that passes Prop. 2
+                if (MEANS && (q.compact || it >= q.iters - q.miters)) {
+                    // extended pixel sub-sweep: one thread per unit; the first candidate
+                    // (W, E, N, S) passing the colour test -- the means test in the means
+                    // iterations (reading M1), Prop. 1 otherwise -- Prop. 2 and, with the
+                    // compactness prior, the centre-of-gravity test (reading M5)
+                    const bool mit = it >= q.iters - q.miters;
                     for (int base = wid * 32; base < nq; base += NT) {
                         PixUnit u;
                         u.valid = 0;
@@ -1181,16 +1251,41 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                 u.j = c.bin(x, y);
 #pragma unroll
                                 for (int d = 0; d < 4; d++) u.v[d] = nb.v[d];
-                                const uint8_t *px = q.img + ((long long)c.f * q.N + (long long)y * W + x) * q.C;
-                                for (int ch = 0; ch < q.C; ch++) rgba |= (uint32_t)px[ch] << (8 * ch);
+                                if (mit) {
+                                    const uint8_t *px = q.img + ((long long)c.f * q.N + (long long)y * W + x) * q.C;
+                                    for (int ch = 0; ch < q.C; ch++) rgba |= (uint32_t)px[ch] << (8 * ch);
+                                }
                             }
                         }
                         // candidates passing Prop. 2, tested in order (W, E, N, S); the
                         // first one's sums are gathered together with k's, later ones
                         // (rare: most boundary pixels have one candidate) one at a time
                         int cand = u.valid ? (u.valid & prop2(u)) : 0;
-                        if (cand) {
-                            auto pick = [&](int d) { return d == 0 ? u.v[0] : d == 1 ? u.v[1] : d == 2 ? u.v[2] : u.v[3]; };
+                        auto pick = [&](int d) { return d == 0 ? u.v[0] : d == 1 ? u.v[1] : d == 2 ? u.v[2] : u.v[3]; };
+                        if (cand && q.compact) {  // reading M5: strictly nearer to n's centre than to k's
+                            const int2 *cf = q.cen + (long long)c.f * q.A_fs;
+                            const int px = u.xy & 0xFFFF, py = u.xy >> 16;
+                            const int2 ck = __ldcg(cf + u.k);
+                            const long long dk = (long long)(px - ck.x) * (px - ck.x) + (long long)(py - ck.y) * (py - ck.y);
+                            int ok = 0;
+#pragma unroll
+                            for (int d = 0; d < 4; d++)
+                                if (cand >> d & 1) {
+                                    const int2 cn = __ldcg(cf + pick(d));
+                                    ok |= (int)((long long)(px - cn.x) * (px - cn.x) + (long long)(py - cn.y) * (py - cn.y) < dk) << d;
+                                }
+                            cand &= ok;
+                        }
+                        if (cand && !mit) {  // Prop. 1, one look-up (reading R1)
+                            const long long hk = c.ldH(ob, u.k, u.j), Ak = c.ldA(ob, u.k);
+#pragma unroll 1
+                            while (u.acc < 0 && cand) {
+                                const int n = pick(__ffs(cand) - 1);
+                                if ((long long)c.ldH(ob, n, u.j) * (Ak - 1) > (hk - 1) * (long long)c.ldA(ob, n)) u.acc = n;
+                                cand &= cand - 1;
+                            }
+                        }
+                        if (cand && mit) {
                             const long long *S = q.Sb[ob] + (long long)c.f * q.S_fs;
                             const int n0 = pick(__ffs(cand) - 1);
                             const S4 sk = ld_sums(S, u.k), s0 = ld_sums(S, n0);
@@ -1221,7 +1316,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                             rec_list(ob)[slot] = GRec{(uint32_t)u.k | ((uint32_t)u.acc << 16), (uint32_t)u.j | (1u << 16),
                                                       (uint32_t)c.f, rgba};
                             gdelta(q, yb_, c.f, u.k, u.acc, u.j, 1);
-                            gdelta_s(q, yb_, c.f, u.k, u.acc, rgba);
+                            if (mit) gdelta_s(q, yb_, c.f, u.k, u.acc, rgba);
                             c.set(u.xy & 0xFFFF, u.xy >> 16, u.acc);
                         }
                     }

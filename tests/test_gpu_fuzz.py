@@ -86,17 +86,19 @@ for i in range(40):
     hi = int(RNG.integers(-1, 4))
     warm = bool(RNG.integers(0, 4) == 0)
     host = bool(RNG.integers(0, 2))
-    FEATURE_CASES.append((i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host))
+    compact = bool(RNG.integers(0, 2))
+    FEATURE_CASES.append((i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host, compact))
 
 
 @pytest.mark.parametrize("case", FEATURE_CASES, ids=[f"feat{c[0]}" for c in FEATURE_CASES])
 def test_random_feature_combination(torch_cuda, orc, case):
     """Grid mode with the SURVEY 8(f) options combined at random (LAB pre-pass,
-    means post-processing, block-level range, warm starts, the chunked host
-    entry point): labels equal the oracle's with the same options."""
+    means post-processing, compactness prior, block-level range, warm starts,
+    the chunked host entry point): labels equal the oracle's with the same
+    options."""
     from paper_1309_3848_b200.seeds import Seeds, SeedsError
     torch = torch_cuda
-    i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host = case
+    i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host, compact = case
     p = dict(n_superpixels=K, n_levels=L, bins_per_channel=bpc, smoothness_prior=gamma, iters_per_level=iters)
     imgs = np.stack([mosaic.mosaic(W, H, int(RNG.integers(1, 30)), 10.0, seed=7000 + 10 * i + f, C=C, grad=20.0)
                      for f in range(nf)])
@@ -108,7 +110,9 @@ def test_random_feature_combination(torch_cuda, orc, case):
         s.set_colour_space("lab")
     s.set_means_iters(means)
     s.set_block_levels(lo, hi)
-    opts = dict(colour="lab" if lab else "rgb", means_iters=means, block_levels=(lo, hi if hi >= 0 else 99))
+    s.set_compactness(compact)
+    opts = dict(colour="lab" if lab else "rgb", means_iters=means, block_levels=(lo, hi if hi >= 0 else 99),
+                compact=compact)
     init = np.stack([orc.run(im, **p, **opts).labels for im in imgs]) if warm else None
     if host:
         out = np.empty((nf, H, W), np.int32)
