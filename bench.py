@@ -384,7 +384,7 @@ def sample_pixels(imgs):
     return n * imgs.shape[-3] * imgs.shape[-2]
 
 
-def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb"):
+def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb", compact=False):
     """The oracle as it stands (COL schedule) on a bounded sample: one thread
     on single-frame configs (the paper's setting); frame-parallel on all host
     cores for the batch configs c3 and c4, with the one-thread figure beside it."""
@@ -396,6 +396,9 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb"):
     if colour != "rgb":
         p = dict(p, colour=colour)
         note += f", {colour} pre-pass"
+    if compact:
+        p = dict(p, compact=True)
+        note += ", compactness prior"
     oracle.build()
     n, px, t0 = 0, 0, time.perf_counter()
     while True:
@@ -416,6 +419,8 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb"):
         p = dict(p, means_iters=means_iters)
     if colour != "rgb":
         p = dict(p, colour=colour)
+    if compact:
+        p = dict(p, compact=True)
     t0 = time.perf_counter()
     oracle_frames(imgs, p, workers)
     el = time.perf_counter() - t0
@@ -447,6 +452,9 @@ def run_reference(args):
     if args.colour != "rgb":
         p = dict(p, colour=args.colour)
         note += f", {args.colour} pre-pass"
+    if args.compact:
+        p = dict(p, compact=True)
+        note += ", compactness prior"
     for i in range(args.warmup):
         b0 = batches[i % len(batches)][:1]
         oracle_frames(b0[:, :1] if b0.ndim == 5 else b0, p, 1)
@@ -485,6 +493,7 @@ def main():
     ap.add_argument("--bands", action="store_true", help="c5: row-band mode even on one rank")
     ap.add_argument("--colour", default="rgb", choices=["rgb", "lab"],
                     help="lab: the 8-bit CIELAB pre-pass inside the timed run (reading M3)")
+    ap.add_argument("--compact", action="store_true", help="the compactness prior at the pixel level (reading M5)")
     ap.add_argument("--means-iters", type=int, default=0,
                     help="SPM means post-processing: the last M pixel iterations use the means test (reading M1)")
     args = ap.parse_args()
@@ -518,6 +527,8 @@ def main():
         s.set_mode(args.mode)
         if args.means_iters:
             s.set_means_iters(args.means_iters)
+        if args.compact:
+            s.set_compactness(True)
     if args.colour != "rgb":
         s.set_colour_space(args.colour)
     info = s.info
@@ -652,6 +663,7 @@ def main():
                        "exec_mode": mode_name,
                        "means_iters": args.means_iters,
                        "colour": args.colour,
+                       "compact": args.compact,
                        "grid_ctas": info.grid_ctas, "grid_tiles_per_frame": info.grid_tiles,
                        "parallelism": wl.parallelism,
                        "exchange": "NCCL all-gather of delta records + halo send/recv per sub-sweep" if banded else None,
@@ -667,7 +679,7 @@ def main():
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget, args.means_iters, args.colour)
+            line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget, args.means_iters, args.colour, args.compact)
         out = json.dumps(line)
         print(out)
         if args.json_out:
