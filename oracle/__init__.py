@@ -65,7 +65,7 @@ def lib():
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
             P(Trace), ctypes.c_int, P(ctypes.c_int), ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
-            ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
         ]
         _lib.oracle_rgb_to_lab.restype = None
         _lib.oracle_rgb_to_lab.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
@@ -158,13 +158,14 @@ def run(img: np.ndarray, n_superpixels: int, n_levels: int, bins_per_channel: in
         init_labels: np.ndarray | None = None, want_energy: bool = False,
         shuffle_seed: int = 0, max_subsweeps: int = -1, trace_cap: int = 4096,
         means_iters: int = 0, want_sums: bool = False, colour: str = "rgb",
-        block_levels: tuple | None = None, compact: bool = False) -> Result:
+        block_levels: tuple | None = None, compact: bool = False, edge_tau: int = 0) -> Result:
     """Refine `img` (H, W, C uint8).  means_iters > 0: the last means_iters
     pixel iterations use the SPM nearest-mean test (reading M1).  colour =
     "lab": the 8-bit CIELAB pre-pass (reading M3) first; every later step
     (bins, means) sees the converted image.  block_levels = (lo, hi): only
     block levels lo..hi run (reading M4; (l, l) = one block size).  compact:
-    the compactness prior at the pixel level (reading M5)."""
+    the compactness prior at the pixel level (reading M5).  edge_tau > 0: the
+    edge prior with that colour-difference threshold (reading M6)."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     if colour == "lab":
         img = rgb_to_lab(img)
@@ -192,7 +193,8 @@ def run(img: np.ndarray, n_superpixels: int, n_levels: int, bins_per_channel: in
                          ctypes.byref(tlen), int(want_energy), shuffle_seed, max_subsweeps,
                          int(means_iters), None if sums is None else sums.ctypes.data,
                          -1 if block_levels is None else int(block_levels[0]),
-                         -1 if block_levels is None else int(block_levels[1]), int(bool(compact)))
+                         -1 if block_levels is None else int(block_levels[1]), int(bool(compact)),
+                         int(edge_tau))
     if k < 0:
         raise ValueError("oracle_run rejected its arguments")
     trace = []

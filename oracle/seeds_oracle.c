@@ -109,6 +109,7 @@ typedef struct {
     int max_subsweeps; /* -1 = unlimited (bisection hook) */
     int block_lo, block_hi; /* block levels that run (reading M4); the others only push down */
     int compact;            /* compactness prior at the pixel level (reading M5) */
+    int edge_tau;           /* edge prior (reading M6): 0 = off, else the colour-difference threshold */
     int64_t *cen;           /* K*2: integer centroids (x, y) at the start of the pixel iteration */
     int subsweeps_done;
     int64_t *lblock;   /* B: block histogram scratch */
@@ -507,6 +508,26 @@ static int compact_test(const st_t *s, int x, int y, int k, int n)
     return dxn * dxn + dyn * dyn < dxk * dxk + dyk * dyk;
 }
 
+/* Edge prior ("If a boundary is near an edge, it snaps to
+ * this edge and is no longer updated from there on forward"), reading M6: an
+ * edge separates 4-adjacent pixels whose colours differ by more than edge_tau
+ * (sum of the absolute channel differences, 8-bit units); at the pixel level a
+ * pixel with a differently labelled 4-neighbour across an edge does not move. */
+static int edge_frozen(const st_t *s, int x, int y, int k)
+{
+    static const int DX[4] = {-1, 1, 0, 0}, DY[4] = {0, 0, -1, 1};
+    const uint8_t *v = s->img + ((int64_t)y * s->W + x) * s->C;
+    for (int d = 0; d < 4; d++) {
+        int qx = x + DX[d], qy = y + DY[d];
+        if (qx < 0 || qx >= s->W || qy < 0 || qy >= s->H || s->lab[qy * s->W + qx] == k) continue;
+        const uint8_t *w = s->img + ((int64_t)qy * s->W + qx) * s->C;
+        int diff = 0;
+        for (int c = 0; c < s->C; c++) diff += v[c] > w[c] ? v[c] - w[c] : w[c] - v[c];
+        if (diff > s->edge_tau) return 1;
+    }
+    return 0;
+}
+
 static int decide_pixel(st_t *s, int x, int y, int *is_boundary, int *is_removable)
 {
     int k = s->lab[y * s->W + x];
@@ -517,6 +538,7 @@ static int decide_pixel(st_t *s, int x, int y, int *is_boundary, int *is_removab
     if (nc == 0) return -1;
     if (!oracle_removable(ring_mask(s->lab, s->W, s->H, x, y, k))) return -1;
     *is_removable = 1;
+    if (s->edge_tau > 0 && edge_frozen(s, x, y, k)) return -1;
     int j = s->bin[(int64_t)y * s->W + x];
     for (int c = 0; c < nc; c++) {
         int n = cand[c];
@@ -679,13 +701,14 @@ static void pixel_level(st_t *s)
 /*   sums_out:   K_act*4 int64 channel sums S[k][c] at the end, or NULL       */
 /*   block_lo, block_hi: only block levels in [lo, hi] run (-1: 0 / L_eff-1)  */
 /*   compact:    compactness prior at the pixel level (reading M5)            */
+/*   edge_tau:   edge prior threshold (reading M6), 0 = off                   */
 /* Returns K_act, or < 0 on invalid arguments.                                */
 /* ------------------------------------------------------------------------ */
 int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, int gamma, int iters,
                int schedule, int rule, const int32_t *init, int32_t *labels_out, int32_t *hist_out,
                int32_t *sizes_out, oracle_trace *trace, int trace_cap, int *trace_len,
                int want_energy, uint64_t shuffle_seed, int max_subsweeps, int means_iters,
-               int64_t *sums_out, int block_lo, int block_hi, int compact)
+               int64_t *sums_out, int block_lo, int block_hi, int compact, int edge_tau)
 {
     if (W < 1 || H < 1 || C < 1 || C > 4 || K < 1 || L < 0 || bpc < 1 || bpc > 256 || iters < 0)
         return -1;
@@ -708,6 +731,7 @@ int oracle_run(const uint8_t *img, int W, int H, int C, int K, int L, int bpc, i
     s.block_lo = block_lo < 0 ? 0 : block_lo;
     s.block_hi = block_hi < 0 ? 1 << 30 : block_hi;
     s.compact = compact ? 1 : 0;
+    s.edge_tau = edge_tau > 0 ? edge_tau : 0;
     s.img = img;
     s.means_iters = means_iters;
     int64_t N = (int64_t)W * H;
