@@ -455,6 +455,9 @@ def run_reference(args):
     if args.compact:
         p = dict(p, compact=True)
         note += ", compactness prior"
+    if args.edge:
+        p = dict(p, edge_tau=args.edge)
+        note += f", edge prior tau {args.edge}"
     for i in range(args.warmup):
         b0 = batches[i % len(batches)][:1]
         oracle_frames(b0[:, :1] if b0.ndim == 5 else b0, p, 1)
@@ -494,6 +497,7 @@ def main():
     ap.add_argument("--colour", default="rgb", choices=["rgb", "lab"],
                     help="lab: the 8-bit CIELAB pre-pass inside the timed run (reading M3)")
     ap.add_argument("--compact", action="store_true", help="the compactness prior at the pixel level (reading M5)")
+    ap.add_argument("--edge", type=int, default=0, help="the edge prior with this colour threshold (reading M6)")
     ap.add_argument("--means-iters", type=int, default=0,
                     help="SPM means post-processing: the last M pixel iterations use the means test (reading M1)")
     args = ap.parse_args()
@@ -529,6 +533,8 @@ def main():
             s.set_means_iters(args.means_iters)
         if args.compact:
             s.set_compactness(True)
+        if args.edge:
+            s.set_edge_prior(args.edge)
     if args.colour != "rgb":
         s.set_colour_space(args.colour)
     info = s.info
@@ -664,6 +670,7 @@ def main():
                        "means_iters": args.means_iters,
                        "colour": args.colour,
                        "compact": args.compact,
+                       "edge_tau": args.edge,
                        "grid_ctas": info.grid_ctas, "grid_tiles_per_frame": info.grid_tiles,
                        "parallelism": wl.parallelism,
                        "exchange": "NCCL all-gather of delta records + halo send/recv per sub-sweep" if banded else None,

@@ -198,6 +198,17 @@ seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pi
  *   SEEDS_ESTATE  the ctx is forced to graph or resident mode (grid mode only) */
 seeds_status seeds_set_compactness(seeds_ctx *ctx, int on);
 
+/* seeds_set_edge_prior -- the edge prior ("If a boundary is near
+ * an edge, it snaps to this edge and is no longer updated"), reading M6: an edge
+ * separates 4-adjacent pixels whose colours (in the colour space in effect)
+ * differ by more than tau (sum of absolute channel differences); at the pixel
+ * level a pixel with a differently labelled 4-neighbour across an edge does not
+ * move.  With smoothness_prior = 1 and the compactness prior this is the
+ * paper's combined prior.  tau = 0 (default) turns it off.
+ *   SEEDS_EINVAL  tau outside 0..1020, or a row-band ctx
+ *   SEEDS_ESTATE  the ctx is forced to graph or resident mode (grid mode only) */
+seeds_status seeds_set_edge_prior(seeds_ctx *ctx, int tau);
+
 /* seeds_set_block_levels -- block levels lo..hi (0 = finest) run in every later
  * cold run; the other levels run no iteration (their labels pass down
  * unchanged).  lo = hi gives one block size, the variant of the authors'

@@ -36,12 +36,12 @@ struct GraphKey {
     int miters = 0;
     int colour = 0;
     int blk_lo = 0, blk_hi = 0;
-    int compact = 0;
+    int compact = 0, edge_tau = 0;
     bool operator==(const GraphKey &o) const
     {
         return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof &&
                mode == o.mode && miters == o.miters && colour == o.colour && blk_lo == o.blk_lo && blk_hi == o.blk_hi &&
-               compact == o.compact;
+               compact == o.compact && edge_tau == o.edge_tau;
     }
 };
 
@@ -96,6 +96,7 @@ struct seeds_ctx {
     int miters = 0;       // seeds_set_means_iters (reading M1)
     int blk_lo = 0, blk_hi = 1 << 20;  // seeds_set_block_levels (reading M4): all levels by default
     int compact = 0;                   // seeds_set_compactness (reading M5)
+    int edge_tau = 0;                  // seeds_set_edge_prior (reading M6)
     int last_miters = 0;  // of the last run
     int last_nf = 0;
     int last_final = 0;  // H buffer holding the final state
@@ -533,7 +534,7 @@ static int block_levels_run(const seeds_ctx *c)
 }
 static bool default_levels(const seeds_ctx *c) { return c->blk_lo == 0 && c->blk_hi >= c->L - 1; }
 // the extended pixel path (k_grid<..., 1>): means post-processing or the compactness prior
-static bool ext_pixel(const seeds_ctx *c) { return c->miters > 0 || c->compact; }
+static bool ext_pixel(const seeds_ctx *c) { return c->miters > 0 || c->compact || c->edge_tau > 0; }
 // options that only grid mode implements
 static bool grid_only(const seeds_ctx *c) { return ext_pixel(c) || !default_levels(c); }
 
@@ -946,6 +947,7 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     q.blk_lo = ctx->blk_lo;
     q.blk_hi = ctx->blk_hi;
     q.compact = ctx->compact;
+    q.edge_tau = ctx->edge_tau;
     q.csum = ctx->d_csum;
     q.cen = ctx->d_cen;
     q.moves = ctx->d_moves;
@@ -1289,6 +1291,7 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     key.blk_lo = ctx->blk_lo;
     key.blk_hi = ctx->blk_hi;
     key.compact = ctx->compact;
+    key.edge_tau = ctx->edge_tau;
     key.colour = ctx->colour;
     seeds_ctx::GraphEntry *hit = nullptr;
     for (auto &g : ctx->graphs)
@@ -1676,6 +1679,21 @@ seeds_status seeds_set_compactness(seeds_ctx *ctx, int on)
         return SEEDS_ESTATE;
     }
     ctx->compact = on;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_set_edge_prior(seeds_ctx *ctx, int tau)
+{
+    if (!ctx || tau < 0 || tau > 255 * 4) return SEEDS_EINVAL;
+    if (tau && ctx->banded) {
+        snprintf(ctx->err, sizeof ctx->err, "the edge prior is not available in row-band mode");
+        return SEEDS_EINVAL;
+    }
+    if (tau && (ctx->mode == SEEDS_MODE_GRAPH || ctx->mode == SEEDS_MODE_RESIDENT)) {
+        snprintf(ctx->err, sizeof ctx->err, "the edge prior runs in grid mode only");
+        return SEEDS_ESTATE;
+    }
+    ctx->edge_tau = tau;
     return SEEDS_OK;
 }
 

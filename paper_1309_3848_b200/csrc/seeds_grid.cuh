@@ -81,6 +81,7 @@ struct GridParams {
     long long S_fs;        // their frame stride (4 A_fs)
     int miters;            // the last miters pixel iterations use the means test (reading M1)
     int compact;           // compactness prior at the pixel level (reading M5)
+    int edge_tau;          // edge prior threshold (reading M6), 0 = off
     long long *csum;       // per frame and superpixel: sum x, sum y, count (4 int64) for the centres
     int2 *cen;             // per frame and superpixel: the centre of gravity of this pixel iteration
     int blk_lo, blk_hi;    // block levels that run (reading M4; default 0 .. L - 1)
@@ -1218,11 +1219,12 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                         c.set(u.xy & 0xFFFF, u.xy >> 16, u.acc);
                     }
                 };
-                if (MEANS && (q.compact || it >= q.iters - q.miters)) {
-                    // extended pixel sub-sweep: one thread per unit; the first candidate
-                    // (W, E, N, S) passing the colour test -- the means test in the means
-                    // iterations (reading M1), Prop. 1 otherwise -- Prop. 2 and, with the
-                    // compactness prior, the centre-of-gravity test (reading M5)
+                if (MEANS && (q.compact || q.edge_tau || it >= q.iters - q.miters)) {
+                    // extended pixel sub-sweep: one thread per unit, no move across a colour
+                    // edge with the edge prior (reading M6); the first candidate (W, E, N, S)
+                    // passing the colour test -- the means test in the means iterations
+                    // (reading M1), Prop. 1 otherwise -- Prop. 2 and, with the compactness
+                    // prior, the centre-of-gravity test (reading M5)
                     const bool mit = it >= q.iters - q.miters;
                     for (int base = wid * 32; base < nq; base += NT) {
                         PixUnit u;
@@ -1246,7 +1248,21 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                             const uint16_t *a = c.cell(x, y);
                             u.k = a[0];
                             const Neigh nb = ring_at(a, sp, 1, sp);
-                            if (nb.valid && c.removable_s(nb.mask)) {
+                            bool frozen = false;
+                            if (q.edge_tau && nb.valid && c.removable_s(nb.mask)) {
+                                // reading M6: a differently labelled 4-neighbour across a colour edge
+                                const uint8_t *pv = q.img + ((long long)c.f * q.N + (long long)y * W + x) * q.C;
+#pragma unroll
+                                for (int d = 0; d < 4; d++) {
+                                    const int qx = x + (d == 0 ? -1 : d == 1 ? 1 : 0), qy = y + (d == 2 ? -1 : d == 3 ? 1 : 0);
+                                    if (qx < 0 || qx >= W || qy < 0 || qy >= q.H || c.cell(qx, qy)[0] == u.k) continue;
+                                    const uint8_t *qv = pv + ((long long)(qy - y) * W + (qx - x)) * q.C;
+                                    int diff = 0;
+                                    for (int ch = 0; ch < q.C; ch++) diff += abs((int)pv[ch] - (int)qv[ch]);
+                                    frozen = frozen || diff > q.edge_tau;
+                                }
+                            }
+                            if (nb.valid && c.removable_s(nb.mask) && !frozen) {
                                 u.valid = nb.valid;
                                 u.j = c.bin(x, y);
 #pragma unroll

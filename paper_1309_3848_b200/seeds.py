@@ -25,7 +25,8 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_status_string", "seeds_last_error", "seeds_create_banded", "seeds_band_info",
            "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish",
            "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics", "seeds_set_colour_space",
-           "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks", "seeds_set_compactness"]
+           "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks", "seeds_set_compactness",
+           "seeds_set_edge_prior"]
 
 
 class _Metrics(ctypes.Structure):
@@ -76,6 +77,7 @@ def load(path: str = LIB_PATH):
         "seeds_set_block_levels": ([vp, i, i], i),
         "seeds_set_host_chunks": ([vp, i], i),
         "seeds_set_compactness": ([vp, i], i),
+        "seeds_set_edge_prior": ([vp, i], i),
         "seeds_rgb_to_lab": ([vp, vp, ctypes.c_longlong, vp, vp], i),
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
@@ -271,6 +273,11 @@ class Seeds:
     def set_compactness(self, on: bool = True):
         """The compactness prior at the pixel level (include/seeds.h seeds_set_compactness)."""
         self._check(self._lib.seeds_set_compactness(self._ctx, int(bool(on))))
+
+    def set_edge_prior(self, tau: int):
+        """The edge prior with colour-difference threshold tau (0 = off;
+        include/seeds.h seeds_set_edge_prior)."""
+        self._check(self._lib.seeds_set_edge_prior(self._ctx, int(tau)))
 
     def set_block_levels(self, lo: int, hi: int = -1):
         """Only block levels lo..hi run (include/seeds.h seeds_set_block_levels)."""

@@ -87,7 +87,8 @@ for i in range(40):
     warm = bool(RNG.integers(0, 4) == 0)
     host = bool(RNG.integers(0, 2))
     compact = bool(RNG.integers(0, 2))
-    FEATURE_CASES.append((i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host, compact))
+    edge = int(RNG.choice([0, 0, 20, 60]))
+    FEATURE_CASES.append((i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host, compact, edge))
 
 
 @pytest.mark.parametrize("case", FEATURE_CASES, ids=[f"feat{c[0]}" for c in FEATURE_CASES])
@@ -98,7 +99,7 @@ def test_random_feature_combination(torch_cuda, orc, case):
     options."""
     from paper_1309_3848_b200.seeds import Seeds, SeedsError
     torch = torch_cuda
-    i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host, compact = case
+    i, W, H, C, bpc, K, L, gamma, iters, nf, lab, means, lo, hi, warm, host, compact, edge = case
     p = dict(n_superpixels=K, n_levels=L, bins_per_channel=bpc, smoothness_prior=gamma, iters_per_level=iters)
     imgs = np.stack([mosaic.mosaic(W, H, int(RNG.integers(1, 30)), 10.0, seed=7000 + 10 * i + f, C=C, grad=20.0)
                      for f in range(nf)])
@@ -111,8 +112,9 @@ def test_random_feature_combination(torch_cuda, orc, case):
     s.set_means_iters(means)
     s.set_block_levels(lo, hi)
     s.set_compactness(compact)
+    s.set_edge_prior(edge)
     opts = dict(colour="lab" if lab else "rgb", means_iters=means, block_levels=(lo, hi if hi >= 0 else 99),
-                compact=compact)
+                compact=compact, edge_tau=edge)
     init = np.stack([orc.run(im, **p, **opts).labels for im in imgs]) if warm else None
     if host:
         out = np.empty((nf, H, W), np.int32)
