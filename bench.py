@@ -384,7 +384,7 @@ def sample_pixels(imgs):
     return n * imgs.shape[-3] * imgs.shape[-2]
 
 
-def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb", compact=False):
+def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb", compact=False, edge=0):
     """The oracle as it stands (COL schedule) on a bounded sample: one thread
     on single-frame configs (the paper's setting); frame-parallel on all host
     cores for the batch configs c3 and c4, with the one-thread figure beside it."""
@@ -399,6 +399,9 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb", compact=False
     if compact:
         p = dict(p, compact=True)
         note += ", compactness prior"
+    if edge:
+        p = dict(p, edge_tau=edge)
+        note += f", edge prior tau {edge}"
     oracle.build()
     n, px, t0 = 0, 0, time.perf_counter()
     while True:
@@ -421,6 +424,8 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb", compact=False
         p = dict(p, colour=colour)
     if compact:
         p = dict(p, compact=True)
+    if edge:
+        p = dict(p, edge_tau=edge)
     t0 = time.perf_counter()
     oracle_frames(imgs, p, workers)
     el = time.perf_counter() - t0
@@ -686,7 +691,8 @@ def main():
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget, args.means_iters, args.colour, args.compact)
+            line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget, args.means_iters, args.colour, args.compact,
+                                                args.edge)
         out = json.dumps(line)
         print(out)
         if args.json_out:
