@@ -79,12 +79,30 @@ __global__ void __launch_bounds__(256) k_met_count(const int32_t *lab, const int
             bad = k < 0 || k >= K || g < 0 || g >= R;
             if (bad) k = g = -1;
             gb = met_boundary(gt, W, H, x, y);
-            for (int dy = -eps + 1; dy < eps && gb && !hit; dy++)
-                for (int dx = -eps + 1; dx < eps && !hit; dx++) {
-                    if (dx * dx + dy * dy >= eps * eps) continue;
-                    const int qx = x + dx, qy = y + dy;
-                    if (qx >= 0 && qx < W && qy >= 0 && qy < H) hit = met_boundary(lab, W, H, qx, qy);
-                }
+            if (gb && eps == 2 && x >= 2 && x + 2 < W && y >= 2 && y + 2 < H) {
+                // the paper's eps = 2 away from the border: the 3x3 centres' boundary
+                // bits from one 5x5 window of labels (25 loads instead of 45)
+                int w5[5][5];
+#pragma unroll
+                for (int dy = 0; dy < 5; dy++)
+#pragma unroll
+                    for (int dx = 0; dx < 5; dx++)
+                        if ((dy != 0 && dy != 4) || (dx != 0 && dx != 4)) w5[dy][dx] = lab[(y + dy - 2) * W + x + dx - 2];
+#pragma unroll
+                for (int cy = 1; cy <= 3; cy++)
+#pragma unroll
+                    for (int cx = 1; cx <= 3; cx++) {
+                        const int v = w5[cy][cx];
+                        hit = hit || w5[cy][cx - 1] != v || w5[cy][cx + 1] != v || w5[cy - 1][cx] != v || w5[cy + 1][cx] != v;
+                    }
+            } else {
+                for (int dy = -eps + 1; dy < eps && gb && !hit; dy++)
+                    for (int dx = -eps + 1; dx < eps && !hit; dx++) {
+                        if (dx * dx + dy * dy >= eps * eps) continue;
+                        const int qx = x + dx, qy = y + dy;
+                        if (qx >= 0 && qx < W && qy >= 0 && qy < H) hit = met_boundary(lab, W, H, qx, qy);
+                    }
+            }
         }
         const unsigned long long key = k < 0 ? MET_EMPTY - 1 - lane : ((unsigned long long)k << 32) | (unsigned)g;
         // 32-bit match when k R + g fits (a single match instruction)
