@@ -605,7 +605,10 @@ def main():
     dom = max(kinds, key=lambda k: kinds[k]["ms_total"])
     hbm, hbm_src = peaks()
     traffic, inst, ncu_us = None, None, None
+    default_path = not (args.means_iters or args.compact or args.edge or args.colour != "rgb")
     try:  # ncu evidence of the same launch (profiles/ncu_traffic.json, scripts/gpu_final_profiles.sh)
+        if not default_path:
+            raise KeyError("the ncu captures are of the default path")
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         ent = tr.get(f"{name}/{mode_name}", {}).get(dom)
         if isinstance(ent, dict):
