@@ -192,3 +192,33 @@ def test_modes_resolved(torch_cuda):
     assert s.info.exec_mode == 1 and s.info.kernels_per_run == 107
     s.set_mode("grid")
     assert s.info.exec_mode == 3 and s.info.kernels_per_run == 1
+
+
+def test_two_contexts_on_two_streams(torch_cuda, orc):
+    """Two contexts of different frame sizes enqueue on two streams at once
+    (their persistent launches each span every SM; the runtime serialises
+    them): both results equal the oracle's and neither run deadlocks."""
+    from paper_1309_3848_b200.seeds import Seeds
+    torch = torch_cuda
+    f1, f2 = configs.frames("c1")[0], configs.frames("c2")[0]
+    p1, p2 = configs.params("c1"), configs.params("c2")
+    mk = lambda f, p: Seeds(f.shape[1], f.shape[0], 3, *[p[k] for k in (
+        "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    s1, s2 = mk(f1, p1), mk(f2, p2)
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    d1, d2 = torch.from_numpy(f1).cuda(), torch.from_numpy(f2).cuda()
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(a):
+            l1 = s1.iterate(d1, stream=a)
+        with torch.cuda.stream(b):
+            l2 = s2.iterate(d2, stream=b)
+        outs.append((l1, l2))
+    torch.cuda.synchronize()
+    r1, r2 = orc.run(f1, **p1).labels, orc.run(f2, **p2).labels
+    for l1, l2 in outs:
+        np.testing.assert_array_equal(l1.cpu().numpy(), r1)
+        np.testing.assert_array_equal(l2.cpu().numpy(), r2)
+    s1.close()
+    s2.close()
