@@ -414,6 +414,10 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb", compact=False
             break
     single = {"value": px / el / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
               "sample": f"{n} runs of {note}, single thread, COL schedule, {el:.1f} s"}
+    # the paper's sequential sweep (SEQ) on the same sample, beside it
+    t0 = time.perf_counter()
+    oracle.run(imgs[0], **p, schedule=oracle.SEQ)
+    single["seq_value"] = imgs[0].shape[0] * imgs[0].shape[1] / (time.perf_counter() - t0) / 1e6
     if name not in ("c3", "c4"):
         return single
     imgs, p, note = parallel_sample(name, host_cores())
