@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -149,6 +150,22 @@ struct seeds_ctx {
     const int32_t *band_init = nullptr;
     size_t grid_smem = 0;
     GridParams gp{};
+    // tile plans of the last few batch sizes (plan_grid): the active one is
+    // copied into gp / grid_* / d_tiles / d_grec; each owns its tiles and records
+    struct PlanSlot {
+        int nf = -1;
+        bool ok = false;
+        GridParams gp{};
+        int G = 0, nt = 0;
+        size_t smem = 0;
+        GridTile *tiles = nullptr;
+        size_t tiles_cap = 0;
+        GRec *grec = nullptr;
+        size_t grec_bytes = 0;
+        unsigned long long used = 0;
+    };
+    PlanSlot plans[4];
+    unsigned long long plan_tick = 0;
     // quality metrics (seeds_metrics): per-superpixel contingency slots + accumulators
     int *d_met_key = nullptr;
     unsigned *d_met_cnt = nullptr;
@@ -303,6 +320,23 @@ static void drop_graphs(seeds_ctx *c)
     c->graphs.clear();
 }
 
+// Forget every tile plan (the caller has synchronised the device: running
+// launches may read their tiles / records).
+static void drop_plans(seeds_ctx *c)
+{
+    for (auto &p : c->plans) {
+        if (p.tiles) cudaFree(p.tiles);
+        if (p.grec) cudaFree(p.grec);
+        p = seeds_ctx::PlanSlot{};
+    }
+    c->d_tiles = nullptr;
+    c->tiles_cap = 0;
+    c->d_grec = nullptr;
+    c->grec_bytes = 0;
+    c->grid_nf = -1;
+    c->grid_ok = false;
+}
+
 static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
 {
     if (nf <= ctx->cap_frames) return SEEDS_OK;
@@ -345,7 +379,7 @@ static seeds_status ensure_frames(seeds_ctx *ctx, int nf)
     CK(cudaMalloc(&ctx->d_labp, F * ctx->labp_fs * 2));
     CK(cudaMemset(ctx->d_labp, 0xFF, F * ctx->labp_fs * 2));  // sentinel border (never written)
     if (!ctx->d_sync) CK(cudaMalloc(&ctx->d_sync, 16));
-    ctx->grid_nf = -1;
+    drop_plans(ctx);  // their TMA maps describe the freed planes
     CK(cudaMalloc(&ctx->d_cnt, (size_t)(ctx->S + 1) * F * 4));
     CK(cudaMalloc(&ctx->d_csum, F * ctx->Afs * 4 * sizeof(long long)));
     CK(cudaMalloc(&ctx->d_cen, F * ctx->Afs * sizeof(int2)));
@@ -557,9 +591,17 @@ template <typename BinT, int GAMMA, int P, int NT, int MEANS>
 static int grid_occupancy_m(size_t smem)
 {
     auto k = k_grid<BinT, GAMMA, P, NT, MEANS>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
+    // The opt-in is a property of the function, shared by every context and
+    // plan: only ever raise it, so a plan made later with less shared memory
+    // does not break the launches of an earlier (larger) one.
+    static std::atomic<int> optin{0};
+    int cur = optin.load();
+    while ((int)smem > cur) {
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        if (optin.compare_exchange_weak(cur, (int)smem)) break;
     }
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT, smem) != cudaSuccess) {
@@ -647,21 +689,74 @@ static bool plan_try(seeds_ctx *c, int nf, int nt);
 // Plan for nf frames: one 512-thread CTA per SM, unless that leaves CTAs with
 // several tiles -- then four 128-thread CTAs per SM (each with its own tiles
 // and TMA pipeline) when such a plan fits.
+//
+// The plans of the last four batch sizes stay cached (PlanSlot), so a caller
+// alternating batch sizes -- or seeds_query's nf = 1 probe between batches --
+// switches plans without a device synchronisation, and the graphs captured
+// with each plan stay valid.  A new plan evicts the least recently used one
+// (after a synchronisation, dropping the graphs that may point at it).
 static bool plan_grid(seeds_ctx *c, int nf)
 {
     if (c->cap_frames < nf && ensure_frames(c, nf) != SEEDS_OK) return false;  // the TMA maps need the planes
     if (c->grid_nf == nf) return c->grid_ok;
-    cudaDeviceSynchronize();  // a running launch may still read the old plan's tiles / records
-    drop_graphs(c);           // graphs captured with the old plan read its tiles / records
+    seeds_ctx::PlanSlot *hit = nullptr, *slot = &c->plans[0];
+    for (auto &p : c->plans) {
+        if (p.nf == nf) hit = &p;
+        if (p.used < slot->used) slot = &p;
+    }
+    if (hit) slot = hit;
+    else {
+        cudaDeviceSynchronize();  // a running launch may still read the evicted plan's tiles / records
+        if (slot->nf >= 0) drop_graphs(c);
+        if (slot->tiles) cudaFree(slot->tiles);
+        if (slot->grec) cudaFree(slot->grec);
+        *slot = seeds_ctx::PlanSlot{};
+        c->d_tiles = nullptr;  // plan_try allocates the new plan's own
+        c->tiles_cap = 0;
+        c->d_grec = nullptr;
+        c->grec_bytes = 0;
+        void *const binsp0 = c->d_binsp;
+        bool ok = false;
+        if (c->W <= 32000 && c->H <= 32000) {
+            const char *v = getenv("SEEDS_GRID_NT");
+            const int force = v ? atoi(v) : 0;
+            if (force == GRID_THREADS || force == GRID_THREADS_SMALL) ok = plan_try(c, nf, force);
+            else if (plan_try(c, nf, GRID_THREADS)) {
+                if (c->gp.tiles_per_cta >= 2 && !plan_try(c, nf, GRID_THREADS_SMALL)) plan_try(c, nf, GRID_THREADS);
+                ok = true;
+            }
+        }
+        if (binsp0 && c->d_binsp != binsp0) {  // the other plans' TMA maps describe the freed bin planes
+            drop_graphs(c);
+            for (auto &p : c->plans) {
+                if (&p == slot) continue;
+                if (p.tiles) cudaFree(p.tiles);
+                if (p.grec) cudaFree(p.grec);
+                p = seeds_ctx::PlanSlot{};
+            }
+        }
+        slot->nf = nf;
+        slot->ok = ok;
+        slot->gp = c->gp;
+        slot->G = c->grid_G;
+        slot->nt = c->grid_nt;
+        slot->smem = c->grid_smem;
+        slot->tiles = c->d_tiles;
+        slot->tiles_cap = c->tiles_cap;
+        slot->grec = c->d_grec;
+        slot->grec_bytes = c->grec_bytes;
+    }
+    slot->used = ++c->plan_tick;
+    c->gp = slot->gp;
+    c->grid_G = slot->G;
+    c->grid_nt = slot->nt;
+    c->grid_smem = slot->smem;
+    c->d_tiles = slot->tiles;
+    c->tiles_cap = slot->tiles_cap;
+    c->d_grec = slot->grec;
+    c->grec_bytes = slot->grec_bytes;
     c->grid_nf = nf;
-    c->grid_ok = false;
-    if (c->W > 32000 || c->H > 32000) return false;
-    const char *v = getenv("SEEDS_GRID_NT");
-    const int force = v ? atoi(v) : 0;
-    if (force == GRID_THREADS || force == GRID_THREADS_SMALL) return c->grid_ok = plan_try(c, nf, force);
-    if (!plan_try(c, nf, GRID_THREADS)) return false;
-    if (c->gp.tiles_per_cta >= 2 && !plan_try(c, nf, GRID_THREADS_SMALL)) plan_try(c, nf, GRID_THREADS);
-    return c->grid_ok = true;
+    return c->grid_ok = slot->ok;
 }
 
 static bool plan_try(seeds_ctx *c, int nf, int nt)
@@ -1785,6 +1880,7 @@ void seeds_destroy(seeds_ctx *ctx)
     if (!ctx) return;
     cudaDeviceSynchronize();
     drop_graphs(ctx);
+    drop_plans(ctx);
     void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1], ctx->d_S[0], ctx->d_S[1],
                     ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band, ctx->d_kmap,

@@ -222,3 +222,49 @@ def test_two_contexts_on_two_streams(torch_cuda, orc):
         np.testing.assert_array_equal(l2.cpu().numpy(), r2)
     s1.close()
     s2.close()
+
+
+def test_alternating_batch_sizes(torch_cuda, orc):
+    """One context alternating batch sizes (24, 1, 8, 24, 1, query, 8): the
+    cached tile plans (plan_grid's PlanSlot) are switched without re-planning
+    and every result still equals the oracle's, including batches run after a
+    fifth batch size evicted the oldest plan."""
+    from paper_1309_3848_b200.seeds import Seeds
+    torch = torch_cuda
+    f = configs.frames("c3", n=24)
+    p = configs.params("c3")
+    s = Seeds(f.shape[2], f.shape[1], 3, *[p[k] for k in (
+        "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    d = torch.from_numpy(f).cuda()
+    ref = {i: orc.run(f[i], **p).labels for i in (0, 3, 5, 23)}
+    for n in (24, 1, 8, 24, 1, 5, 3, 2, 24, 8):
+        lab = s.batch(d[:n]).cpu().numpy()
+        s._refresh()  # seeds_query plans nf = 1
+        for i in ref:
+            if i < n:
+                np.testing.assert_array_equal(lab[i], ref[i])
+    s.close()
+
+
+@pytest.mark.parametrize("big_first", [True, False])
+def test_interleaved_contexts_same_kernel(torch_cuda, orc, big_first):
+    """Two contexts with the same parameters (so the same k_grid
+    instantiation) but different frame sizes, hence different dynamic shared
+    memory per CTA: creating the second must not lower the first one's
+    opt-in, whichever is larger."""
+    from paper_1309_3848_b200.seeds import Seeds
+    torch = torch_cuda
+    p = configs.params("c3")
+    big = configs.frames("c3", n=1)[0]
+    small = np.ascontiguousarray(big[:96, :128])
+    ps = dict(p, n_superpixels=max(4, p["n_superpixels"] * 96 * 128 // (big.shape[0] * big.shape[1])))
+    mk = lambda f, q: Seeds(f.shape[1], f.shape[0], 3, *[q[k] for k in (
+        "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    order = [(big, p), (small, ps)] if big_first else [(small, ps), (big, p)]
+    ctx = [mk(f, q) for f, q in order]
+    for _ in range(2):
+        for s, (f, q) in zip(ctx, order):
+            lab = s.iterate(torch.from_numpy(f).cuda()).cpu().numpy()
+            np.testing.assert_array_equal(lab, orc.run(f, **q).labels)
+    for s in ctx:
+        s.close()
