@@ -8,7 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -587,22 +587,28 @@ static int resolved_mode(seeds_ctx *c, int nf)
 // they fit (else of one tile, restaged every sub-sweep), the unit queue, the
 // warp tables of the large-block path and the block geometry.
 // ---------------------------------------------------------------------------
+// The dynamic-shared-memory opt-in is a property of the function, shared by
+// every context and plan: only ever raise it (under a lock), so a plan made
+// later with less shared memory cannot break the launches of a larger one.
+static bool raise_optin(const void *k, int &optin, size_t smem)
+{
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    if ((int)smem <= optin) return true;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    optin = (int)smem;
+    return true;
+}
+
 template <typename BinT, int GAMMA, int P, int NT, int MEANS>
 static int grid_occupancy_m(size_t smem)
 {
     auto k = k_grid<BinT, GAMMA, P, NT, MEANS>;
-    // The opt-in is a property of the function, shared by every context and
-    // plan: only ever raise it, so a plan made later with less shared memory
-    // does not break the launches of an earlier (larger) one.
-    static std::atomic<int> optin{0};
-    int cur = optin.load();
-    while ((int)smem > cur) {
-        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-            cudaGetLastError();
-            return 0;
-        }
-        if (optin.compare_exchange_weak(cur, (int)smem)) break;
-    }
+    static int optin = 0;
+    if (!raise_optin((const void *)k, optin, smem)) return 0;
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT, smem) != cudaSuccess) {
         cudaGetLastError();
@@ -1069,8 +1075,9 @@ template <typename BinT, int GAMMA, int P>
 static int resident_clusters(int cs, size_t smem)
 {
     auto k = k_resident<BinT, GAMMA, P>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    static int optin = 0;
+    if (!raise_optin((const void *)k, optin, smem)) return 0;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }

@@ -246,22 +246,30 @@ def test_alternating_batch_sizes(torch_cuda, orc):
     s.close()
 
 
+@pytest.mark.parametrize("mode", ["auto", "resident"])
 @pytest.mark.parametrize("big_first", [True, False])
-def test_interleaved_contexts_same_kernel(torch_cuda, orc, big_first):
+def test_interleaved_contexts_same_kernel(torch_cuda, orc, big_first, mode):
     """Two contexts with the same parameters (so the same k_grid
     instantiation) but different frame sizes, hence different dynamic shared
     memory per CTA: creating the second must not lower the first one's
     opt-in, whichever is larger."""
-    from paper_1309_3848_b200.seeds import Seeds
+    from paper_1309_3848_b200.seeds import Seeds, SeedsError
     torch = torch_cuda
     p = configs.params("c3")
     big = configs.frames("c3", n=1)[0]
+    if mode == "resident":
+        big = np.ascontiguousarray(big[:160, :240])
     small = np.ascontiguousarray(big[:96, :128])
     ps = dict(p, n_superpixels=max(4, p["n_superpixels"] * 96 * 128 // (big.shape[0] * big.shape[1])))
     mk = lambda f, q: Seeds(f.shape[1], f.shape[0], 3, *[q[k] for k in (
         "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
     order = [(big, p), (small, ps)] if big_first else [(small, ps), (big, p)]
     ctx = [mk(f, q) for f, q in order]
+    try:
+        for s in ctx:
+            s.set_mode(mode)
+    except SeedsError:
+        pytest.skip(f"{mode} mode does not fit")
     for _ in range(2):
         for s, (f, q) in zip(ctx, order):
             lab = s.iterate(torch.from_numpy(f).cuda()).cpu().numpy()
