@@ -301,11 +301,15 @@ class Workload:
     def host_step(self, s, stream):
         """Through the host-memory C-ABI entry point: copies in, runs, copies out."""
         for i, h in enumerate(self.h_in):
-            init = self.h_out[i - 1].numpy() if self.warm[i] else None
-            s.batch_host(h.numpy(), self.h_out[i].numpy(), init_labels=init, stream=stream)
+            # a warm group continues each clip from the previous group's labels,
+            # which the previous host call left on the device (seeds_batch_host_warm)
+            if self.warm[i]:
+                s.batch_host_warm(h.numpy(), self.h_out[i].numpy(), stream=stream)
+            else:
+                s.batch_host(h.numpy(), self.h_out[i].numpy(), stream=stream)
 
     def h2d_bytes(self):
-        return sum(g.nbytes for g in self.groups) + sum(self.nf * self.N * 4 for w in self.warm if w)
+        return sum(g.nbytes for g in self.groups)
 
     def d2h_bytes(self):
         return len(self.groups) * self.nf * self.N * 4

@@ -135,6 +135,17 @@ seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_
                               const int32_t *init_labels_host, int32_t *labels_out_host,
                               void *stream);
 
+/* seeds_batch_host_warm -- the next frames of n_frames video streams, from and
+ * to host memory: as seeds_batch_host with init_labels = this context's output
+ * of the previous seeds_batch_host / seeds_batch_host_warm call (warm start,
+ * reading O9), taken from the device copy that call left behind instead of
+ * being copied in again -- frame i continues stream i.  SEEDS_ESTATE, with
+ * nothing run, when that call had a different n_frames or there was none (a
+ * host call that failed ends the chain); images and labels are otherwise as
+ * for seeds_batch_host. */
+seeds_status seeds_batch_host_warm(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
+                                   int32_t *labels_out_host, void *stream);
+
 /* seeds_set_host_chunks -- chunks of the seeds_batch_host pipeline: 0 (default)
  * picks the largest of 4, 3, 2 dividing n_frames; 1 turns the pipeline off
  * (one copy in, one run, one copy out); 2..4 the largest count <= chunks

@@ -83,6 +83,7 @@ struct seeds_ctx {
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t pev[16] = {};
     int host_chunks = 0;  // seeds_set_host_chunks (0 = automatic)
+    int host_prev_nf = 0; // frames of the last successful host call (its labels stay in d_out_stage)
     // instantiated runs, keyed by their pointers / sizes (least recently used dropped)
     struct GraphEntry {
         GraphKey key;
@@ -1506,11 +1507,17 @@ seeds_status seeds_iterate(seeds_ctx *ctx, const uint8_t *image_u8, int32_t *lab
     return seeds_batch(ctx, image_u8, 1, nullptr, labels_out, stream);
 }
 
-seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
-                              const int32_t *init_labels_host, int32_t *labels_out_host, void *stream)
+// seeds_batch_host(_warm): warm = initialise from the previous call's output,
+// still in d_out_stage (copied to d_init_stage: a run may not read and write
+// the same labels).
+static seeds_status batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
+                               const int32_t *init_labels_host, bool warm, int32_t *labels_out_host,
+                               cudaStream_t st)
 {
-    if (!ctx || !images_host || !labels_out_host || n_frames < 1 || n_frames > 65535) return SEEDS_EINVAL;
-    cudaStream_t st = (cudaStream_t)stream;
+    const bool has_init = init_labels_host || warm;
+    if (warm)
+        CK(cudaMemcpyAsync(ctx->d_init_stage, ctx->d_out_stage, (size_t)n_frames * ctx->N * 4,
+                           cudaMemcpyDeviceToDevice, st));
     if (n_frames > ctx->stage_frames) {
         CK(cudaStreamSynchronize(st));
         if (ctx->d_img_stage) cudaFree(ctx->d_img_stage);
@@ -1550,7 +1557,7 @@ seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_
             const size_t f0 = (size_t)i * m;
             CK(cudaMemcpyAsync(ctx->d_img_stage + f0 * fi, images_host + f0 * fi, m * fi, cudaMemcpyHostToDevice,
                                ctx->h2d_stream));
-            if (init_labels_host)
+            if (init_labels_host && !warm)
                 CK(cudaMemcpyAsync(ctx->d_init_stage + f0 * ctx->N, init_labels_host + f0 * ctx->N, m * fo,
                                    cudaMemcpyHostToDevice, ctx->h2d_stream));
             CK(cudaEventRecord(ctx->pev[i], ctx->h2d_stream));
@@ -1558,7 +1565,7 @@ seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_
         for (int i = 0; i < nc; i++) {
             const size_t f0 = (size_t)i * m;
             CK(cudaStreamWaitEvent(st, ctx->pev[i], 0));
-            seeds_status r = run(ctx, ctx->d_img_stage + f0 * fi, init_labels_host ? ctx->d_init_stage + f0 * ctx->N : nullptr,
+            seeds_status r = run(ctx, ctx->d_img_stage + f0 * fi, has_init ? ctx->d_init_stage + f0 * ctx->N : nullptr,
                                  ctx->d_out_stage + f0 * ctx->N, m, st);
             if (r != SEEDS_OK) return r;
             CK(cudaEventRecord(ctx->pev[4 + i], st));
@@ -1574,18 +1581,42 @@ seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_
     }
     CK(cudaMemcpyAsync(ctx->d_img_stage, images_host, (size_t)n_frames * ctx->N * ctx->C,
                        cudaMemcpyHostToDevice, st));
-    const int32_t *init = nullptr;
-    if (init_labels_host) {
+    const int32_t *init = has_init ? ctx->d_init_stage : nullptr;
+    if (init_labels_host && !warm)
         CK(cudaMemcpyAsync(ctx->d_init_stage, init_labels_host, (size_t)n_frames * ctx->N * 4,
                            cudaMemcpyHostToDevice, st));
-        init = ctx->d_init_stage;
-    }
     seeds_status r = run(ctx, ctx->d_img_stage, init, ctx->d_out_stage, n_frames, st);
     if (r != SEEDS_OK) return r;
     CK(cudaMemcpyAsync(labels_out_host, ctx->d_out_stage, (size_t)n_frames * ctx->N * 4, cudaMemcpyDeviceToHost,
                        st));
     CK(cudaStreamSynchronize(st));
     return SEEDS_OK;
+}
+
+seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
+                              const int32_t *init_labels_host, int32_t *labels_out_host, void *stream)
+{
+    if (!ctx || !images_host || !labels_out_host || n_frames < 1 || n_frames > 65535) return SEEDS_EINVAL;
+    ctx->host_prev_nf = 0;
+    seeds_status r = batch_host(ctx, images_host, n_frames, init_labels_host, false, labels_out_host,
+                                (cudaStream_t)stream);
+    if (r == SEEDS_OK) ctx->host_prev_nf = n_frames;
+    return r;
+}
+
+seeds_status seeds_batch_host_warm(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
+                                   int32_t *labels_out_host, void *stream)
+{
+    if (!ctx || !images_host || !labels_out_host || n_frames < 1 || n_frames > 65535) return SEEDS_EINVAL;
+    if (ctx->host_prev_nf != n_frames) {
+        snprintf(ctx->err, sizeof ctx->err, "seeds_batch_host_warm: the previous host call had %d frames, not %d",
+                 ctx->host_prev_nf, n_frames);
+        return SEEDS_ESTATE;
+    }
+    ctx->host_prev_nf = 0;
+    seeds_status r = batch_host(ctx, images_host, n_frames, nullptr, true, labels_out_host, (cudaStream_t)stream);
+    if (r == SEEDS_OK) ctx->host_prev_nf = n_frames;
+    return r;
 }
 
 seeds_status seeds_set_host_chunks(seeds_ctx *ctx, int chunks)

@@ -26,7 +26,7 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish",
            "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics", "seeds_set_colour_space",
            "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks", "seeds_set_compactness",
-           "seeds_set_edge_prior"]
+           "seeds_set_edge_prior", "seeds_batch_host_warm"]
 
 
 class _Metrics(ctypes.Structure):
@@ -67,6 +67,7 @@ def load(path: str = LIB_PATH):
         "seeds_iterate": ([vp, vp, vp, vp], i),
         "seeds_batch": ([vp, vp, i, vp, vp, vp], i),
         "seeds_batch_host": ([vp, vp, i, vp, vp, vp], i),
+        "seeds_batch_host_warm": ([vp, vp, i, vp, vp], i),
         "seeds_query": ([vp, ctypes.POINTER(Info)], i),
         "seeds_read_state": ([vp, i, vp, vp, vp], i),
         "seeds_debug_limit": ([vp, i], i),
@@ -213,6 +214,17 @@ class Seeds:
             init_ptr = init_labels.ctypes.data
         self._check(self._lib.seeds_batch_host(self._ctx, images.ctypes.data, n, init_ptr,
                                                labels_out.ctypes.data, _stream_ptr(stream)))
+        return labels_out
+
+    def batch_host_warm(self, images: np.ndarray, labels_out: np.ndarray, stream=None):
+        """Next frames of n video streams from host memory, each warm-started
+        from the previous host call's labels still on the device
+        (seeds_batch_host_warm)."""
+        n = images.size // (self.width * self.height * self.channels)
+        assert images.flags.c_contiguous and images.dtype == np.uint8
+        assert labels_out.flags.c_contiguous and labels_out.dtype == np.int32
+        self._check(self._lib.seeds_batch_host_warm(self._ctx, images.ctypes.data, n, labels_out.ctypes.data,
+                                                    _stream_ptr(stream)))
         return labels_out
 
     def read_state(self, frame: int = 0, stream=None):

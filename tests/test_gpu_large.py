@@ -167,3 +167,25 @@ def test_multi_tile_plans_are_deterministic(torch_cuda):
         s.batch_host(np.ascontiguousarray(f), out)
         np.testing.assert_array_equal(out, ref.cpu().numpy())
         s.close()
+
+
+def test_c4_host_warm_chain_matches_device(torch_cuda):
+    """The c4 video (8 clips) through seeds_batch_host_warm, frame 0 cold, then
+    frames 1-3 warm from the labels the previous host call left on the device
+    (device-entry runs in between do not disturb them): identical to the device entry point given the previous labels explicitly."""
+    torch = torch_cuda
+    cl = configs.clips("c4")[:, :4]
+    p = configs.params("c4")
+    s = ctx(cl.shape[2:], p, "auto")
+    out = np.empty((cl.shape[0],) + cl.shape[2:4], np.int32)
+    prev = None
+    for t in range(cl.shape[1]):
+        x = np.ascontiguousarray(cl[:, t])
+        if t == 0:
+            s.batch_host(x, out)
+        else:
+            s.batch_host_warm(x, out)
+        ref = s.batch(torch.from_numpy(x).cuda(), init_labels=prev)
+        np.testing.assert_array_equal(out, ref.cpu().numpy())
+        prev = ref.clone()
+    s.close()

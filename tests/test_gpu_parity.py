@@ -276,3 +276,39 @@ def test_interleaved_contexts_same_kernel(torch_cuda, orc, big_first, mode):
             np.testing.assert_array_equal(lab, orc.run(f, **q).labels)
     for s in ctx:
         s.close()
+
+
+@pytest.mark.parametrize("chunks", [0, 1])
+def test_batch_host_warm_chain(torch_cuda, orc, chunks):
+    """seeds_batch_host_warm: four streams of three frames each from host
+    memory, every frame warm-started from the previous call's labels left on
+    the device; equals the oracle's warm chain (reading O9) frame by frame, with
+    and without the chunked copy pipeline.  A different frame count than the
+    previous host call, or no previous call, is SEEDS_ESTATE (and leaves the
+    chain as it was)."""
+    from paper_1309_3848_b200.seeds import Seeds, SeedsError
+    f = configs.frames("c2", n=12)
+    p = configs.params("c2")
+    streams = f.reshape(3, 4, *f.shape[1:])  # time x stream
+    s = Seeds(f.shape[2], f.shape[1], 3, *[p[k] for k in (
+        "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    s.set_host_chunks(chunks)
+    out = np.empty((4,) + f.shape[1:3], np.int32)
+    with pytest.raises(SeedsError):
+        s.batch_host_warm(np.ascontiguousarray(streams[0]), out)
+    prev = [None] * 4
+    for t in range(3):
+        if t == 0:
+            s.batch_host(np.ascontiguousarray(streams[0]), out)
+        else:
+            s.batch_host_warm(np.ascontiguousarray(streams[t]), out)
+        for i in range(4):
+            r = orc.run(streams[t, i], **p, init_labels=prev[i]).labels
+            np.testing.assert_array_equal(out[i], r)
+            prev[i] = r
+    with pytest.raises(SeedsError):
+        s.batch_host_warm(np.ascontiguousarray(streams[0, :2]), np.empty((2,) + f.shape[1:3], np.int32))
+    s.batch_host_warm(np.ascontiguousarray(streams[0]), out)  # the rejected call left the chain intact
+    for i in range(4):
+        np.testing.assert_array_equal(out[i], orc.run(streams[0, i], **p, init_labels=prev[i]).labels)
+    s.close()
