@@ -1,5 +1,6 @@
 """Per-CTA clock64 trace of one resident / grid run: work and barrier cycles
-per sub-sweep (max / min over CTAs), summarised per phase group."""
+per sub-sweep (max / min over CTAs), summarised per phase group.
+Usage: [NF=frames] trace.py [cfg] [mode] [HxW crop]"""
 import os
 import sys
 
@@ -12,12 +13,14 @@ from paper_1309_3848_b200.seeds import Seeds  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 mode = sys.argv[2] if len(sys.argv) > 2 else "resident"
-img = configs.frames(cfg, n=1)[0]
+NF = int(os.environ.get("NF", "1"))  # frames per run (multi-tile plans)
+img = configs.frames(cfg, n=NF)
+img = img[0] if NF == 1 else img
 if len(sys.argv) > 3:  # crop HxW
     hh, ww = (int(v) for v in sys.argv[3].split("x"))
-    img = np.ascontiguousarray(img[:hh, :ww])
+    img = np.ascontiguousarray(img[..., :hh, :ww, :])
 p = configs.params(cfg)
-s = Seeds(img.shape[1], img.shape[0], img.shape[2], *[p[k] for k in (
+s = Seeds(img.shape[-2], img.shape[-3], img.shape[-1], *[p[k] for k in (
     "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
 s.set_mode(mode)
 if os.environ.get("MEANS_ITERS"):
@@ -25,7 +28,7 @@ if os.environ.get("MEANS_ITERS"):
 s.debug_trace(True)
 d = torch.from_numpy(img).cuda()
 for _ in range(3):
-    out = s.iterate(d)
+    out = s.iterate(d) if NF == 1 else s.batch(d)
 torch.cuda.synchronize()
 tr = s.debug_trace(True)
 S = s.info.subsweeps
