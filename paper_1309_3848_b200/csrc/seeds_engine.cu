@@ -796,6 +796,20 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.bkind[l] = am <= 4 ? BK_T4 : am <= 32 ? BK_T16 : BK_WARP;
         int gs = 0;
         while ((1 << gs) < am && gs < 5) gs++;
+        // G lanes per block of the segment path: one pixel per lane (G >= am), or
+        // two (G >= am / 2: a warp decides twice the blocks per pass) when a CTA's
+        // blocks of one colour do not fit one pass of its warps (c3: +17%; on c2
+        // they do, and the second slot's bookkeeping would only add latency).
+        // SEEDS_SEG2=0 / 1 forces one / two pixels per lane.  Two only in the
+        // 128-thread kernels (the 512-thread ones have no registers to spare).
+        if (q.bkind[l] == BK_T16 && nt == GRID_THREADS_SMALL) {
+            const long long per_cta =
+                ((long long)(c->GX >> l) * (c->GY >> l) * nf / 4 + nsm - 1) / nsm;
+            const char *sv = getenv("SEEDS_SEG2");
+            const bool two = sv ? atoi(sv) != 0 : per_cta > (long long)(nt / 32) * (32 >> gs);
+            if (two)
+                while (gs > 0 && 2 * (1 << (gs - 1)) >= am) gs--;
+        }
         q.gshift[l] = gs;
         // a block's warps each take at least gw_iters 32-pixel slices of it
         const int slices = (am + 31) / 32;

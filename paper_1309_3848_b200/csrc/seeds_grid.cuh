@@ -608,9 +608,11 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                 }
                             }
                         } else if (kind != BK_WARP) {
-                            // G lanes per block (<= 32 px): lane i holds pixel i, equal
-                            // bins merged by __match_any_sync, segmented reduction (K5)
+                            // G lanes per block (<= 32 px, <= 2G): lane i holds pixels i and
+                            // i + G; equal bins merged by __match_any_sync per slot plus a
+                            // cross count between the slots, segmented reduction (K5)
                             const int segs = 32 >> gs, seg = lane >> gs, si = lane & (G - 1);
+                            const int sbase = lane & ~(G - 1);
                             for (int base = wid * segs; base < nq; base += NW * segs) {
                                 const int e = base + seg;
                                 int acc = -1, k = 0, xa = 0, xb = 0, ya = 0, yb = 0, rw = 1, alpha = 0;
@@ -627,37 +629,80 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                     alpha = rw * (yb - ya);
                                 }
                                 const bool ok = nb.valid && c.removable_s(nb.mask);
-                                int b = -1;
+                                int b = -1, b2 = -1;
                                 if (ok && si < alpha) {
                                     const int dy = div_small(si, rw, 1.0f / (float)rw);
                                     b = c.bin(xa + si - dy * rw, ya + dy);
                                 }
+                                if (NT <= 128 && ok && si + G < alpha) {  // two pixels per lane: 128-thread plans only
+                                    const int dy = div_small(si + G, rw, 1.0f / (float)rw);
+                                    b2 = c.bin(xa + si + G - dy * rw, ya + dy);
+                                }
                                 const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : (seg << 16) | b);
+                                // second slot (warp-uniform): its bins, how many of them equal my
+                                // first bin, and whether my second bin is some lane's first one
+                                const bool two = NT <= 128 && __any_sync(FULL, b2 >= 0);
+                                unsigned m2 = 0;
+                                int x01 = 0;
+                                bool in0 = false;
+                                if (two) {
+                                    m2 = __match_any_sync(FULL, b2 < 0 ? -1 - lane : (seg << 16) | b2);
+                                    // only lanes j < alpha - G of a segment hold a second pixel:
+                                    // broadcast each one's bin to its segment
+                                    const unsigned segmask = G == 32 ? FULL : ((1u << G) - 1) << sbase;
+                                    const int jmax = (int)__reduce_max_sync(FULL, (unsigned)max(alpha - G, 0));
+#pragma unroll 1
+                                    for (int j = 0; j < jmax; j++) {
+                                        const int v1 = __shfl_sync(FULL, b2, sbase + j);
+                                        const bool hit = b >= 0 && v1 == b;
+                                        x01 += hit;
+                                        const unsigned hm = __ballot_sync(FULL, hit) & segmask;
+                                        if (si == j) in0 = hm != 0;
+                                    }
+                                }
                                 const bool leader = b >= 0 && lane == __ffs(m) - 1;
-                                const long long lb = __popc(m);
+                                const bool leader2 = b2 >= 0 && !in0 && lane == __ffs(m2) - 1;
+                                const int l2 = leader2 ? __popc(m2) : 0;
+                                // one gather round: a lane leads the bin of its first pixel, else
+                                // (if any) a bin only second pixels hold; a lane leading both
+                                // takes the second one in a (rare) extra round
+                                const bool use2 = leader2 && !leader;
+                                const int gb = use2 ? b2 : b < 0 ? 0 : b;
+                                const int lb = use2 ? l2 : __popc(m) + x01;
                                 unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
-                                long long Ak = 1, An[4] = {1, 1, 1, 1};
+                                int Ak = 1, An[4] = {1, 1, 1, 1};
                                 if (ok) {
-                                    const int bb = b < 0 ? 0 : b;
                                     Ak = c.ldA(ob, k);
-                                    const long long hk = c.ldH(ob, k, bb);
-                                    long long hn[4];
+                                    const int hk = c.ldH(ob, k, gb);
+                                    int hn[4];
 #pragma unroll
                                     for (int d = 0; d < 4; d++) {
                                         const int n = (nb.valid >> d & 1) ? nb.v[d] : k;
                                         An[d] = c.ldA(ob, n);
-                                        hn[d] = c.ldH(ob, n, bb);
+                                        hn[d] = c.ldH(ob, n, gb);
                                     }
-                                    if (leader) {
-                                        const long long al = alpha;
-                                        const long long uu = (hk - lb) * al, vv = lb * (Ak - al);
+                                    if (leader || use2) {
+                                        const long long al = alpha, lc = lb;
+                                        const long long uu = (hk - lc) * al, vv = lc * (Ak - al);
                                         Nk = (unsigned long long)(uu < vv ? uu : vv);
 #pragma unroll
                                         for (int d = 0; d < 4; d++) {
-                                            const long long un = hn[d] * al, vn = lb * An[d];
+                                            const long long un = (long long)hn[d] * al, vn = lc * An[d];
                                             Nn[d] = (nb.valid >> d & 1) ? (unsigned long long)(un < vn ? un : vn) : 0ull;
                                         }
                                     }
+                                }
+                                if (leader && leader2) {
+                                    const long long al = alpha, lc = l2;
+                                    const long long hk = c.ldH(ob, k, b2);
+                                    const long long uu = (hk - lc) * al, vv = lc * (Ak - al);
+                                    Nk += (unsigned long long)(uu < vv ? uu : vv);
+#pragma unroll
+                                    for (int d = 0; d < 4; d++)
+                                        if (nb.valid >> d & 1) {
+                                            const long long un = (long long)c.ldH(ob, nb.v[d], b2) * al, vn = lc * An[d];
+                                            Nn[d] += (unsigned long long)(un < vn ? un : vn);
+                                        }
                                 }
                                 if (q.N < (1LL << 27)) {
                                     // alpha <= 32: each sum is at most alpha A < 32 N < 2^32, so the
@@ -688,12 +733,18 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                             acc = nb.v[d];
                                 }
                                 count_moves(acc >= 0 && si == 0);
-                                const int slot = append_warp(rcount(ob), acc >= 0 && leader ? 1 : 0);
+                                const int nrec = acc >= 0 ? (int)leader + (int)leader2 : 0;
+                                const int slot = append_warp(rcount(ob), nrec);
                                 if (acc >= 0) {
                                     if (leader) emit(rec_list(ob), slot, k, acc, b, (int)lb, yb_);
+                                    if (leader2) emit(rec_list(ob), slot + (int)leader, k, acc, b2, l2, yb_);
                                     if (si < alpha) {
                                         const int dy = div_small(si, rw, 1.0f / (float)rw);
                                         c.set(xa + si - dy * rw, ya + dy, acc);
+                                    }
+                                    if (NT <= 128 && si + G < alpha) {
+                                        const int dy = div_small(si + G, rw, 1.0f / (float)rw);
+                                        c.set(xa + si + G - dy * rw, ya + dy, acc);
                                     }
                                 }
                             }

@@ -312,3 +312,20 @@ def test_batch_host_warm_chain(torch_cuda, orc, chunks):
     for i in range(4):
         np.testing.assert_array_equal(out[i], orc.run(streams[0, i], **p, init_labels=prev[i]).labels)
     s.close()
+
+
+@pytest.mark.parametrize("nt", ["512", "128"])
+@pytest.mark.parametrize("seg2", ["0", "1"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c4"])
+def test_segment_path_layouts(torch_cuda, orc, monkeypatch, cfg, seg2, nt):
+    """The G-lane segment path of the small block levels with one pixel per
+    lane (SEEDS_SEG2=0) and with two (SEEDS_SEG2=1: G >= area / 2, a cross
+    count between the two slots of a lane; 128-thread plans only) -- AUTO
+    picks per level and plan -- in both plan shapes (SEEDS_GRID_NT) equal the
+    oracle bit for bit (labels, histograms, sizes)."""
+    monkeypatch.setenv("SEEDS_SEG2", seg2)
+    monkeypatch.setenv("SEEDS_GRID_NT", nt)
+    torch = torch_cuda
+    img = configs.frames(cfg, n=1)[0]
+    p = configs.params(cfg)
+    assert_parity(torch, orc, img, p, mode="grid")
