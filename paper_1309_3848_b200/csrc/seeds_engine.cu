@@ -939,6 +939,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.band = 0;  // whole-run launch: every sub-sweep (seeds_band_subsweep overrides these)
         q.s0 = 0;
         q.s1 = -1;
+        q.filt2 = !getenv_off("SEEDS_FILT2");
         q.blk_lo = 0;  // every block level (enqueue_grid applies seeds_set_block_levels)
         q.blk_hi = 1 << 20;
         q.tx_bytes = q.bw * q.bh * 2 + (res ? 0 : q.bbw * (q.bh - 4) * c->bb) + (q.acache ? (int)c->Afs * 4 : 0);

@@ -82,6 +82,7 @@ struct GridParams {
     int miters;            // the last miters pixel iterations use the means test (reading M1)
     int compact;           // compactness prior at the pixel level (reading M5)
     int edge_tau;          // edge prior threshold (reading M6), 0 = off
+    int filt2;             // 128-thread kernels: two filter units per lane (SEEDS_FILT2=0: one)
     long long *csum;       // per frame and superpixel: sum x, sum y, count (4 int64) for the centres
     int2 *cen;             // per frame and superpixel: the centre of gravity of this pixel iteration
     int blk_lo, blk_hi;    // block levels that run (reading M4; default 0 .. L - 1)
@@ -556,16 +557,24 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                         const bool direct = (long long)nunits * per_unit <= NT;
                         int nq = nunits;
                         if (!direct) {
-                            for (int base = wid * 32; base < nunits; base += NT) {
-                                const int u = base + lane;
-                                bool take = false;
-                                if (u < nunits) {
-                                    int bi, bj, xa, xb, ya, yb;
-                                    rect(u, bi, bj, xa, xb, ya, yb);
-                                    const Neigh nb = ring_at(c.cell(xa, ya), c.sp, xb - xa, (yb - ya) * c.sp);
-                                    take = nb.valid && c.removable_s(nb.mask);
+                            auto probe = [&](int u) -> bool {
+                                if (u >= nunits) return false;
+                                int bi, bj, xa, xb, ya, yb;
+                                rect(u, bi, bj, xa, xb, ya, yb);
+                                const Neigh nb = ring_at(c.cell(xa, ya), c.sp, xb - xa, (yb - ya) * c.sp);
+                                return nb.valid && c.removable_s(nb.mask);
+                            };
+                            if (NT <= 128 && q.filt2) {  // two units per lane in flight
+                                for (int base = wid * 32; base < nunits; base += 2 * NT) {
+                                    const int u0 = base + lane, u1 = u0 + NT;
+                                    const bool t0 = probe(u0), t1 = probe(u1);
+                                    push_warp2(c.queue, &c.misc[2], t0, (uint32_t)u0, t1, (uint32_t)u1);
                                 }
-                                push_warp(c.queue, &c.misc[2], take, (uint32_t)u);
+                            } else {
+                                for (int base = wid * 32; base < nunits; base += NT) {
+                                    const int u = base + lane;
+                                    push_warp(c.queue, &c.misc[2], probe(u), (uint32_t)u);
+                                }
                             }
                             __syncthreads();
                             nq = c.misc[2];
@@ -1125,18 +1134,27 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                 int nq = nunits;
                 if (!direct) {
                     // filter: boundary + ring test, survivors (x | y << 16, tile-relative) to the queue
-                    for (int base = wid * 32; base < nunits; base += NT) {
-                        const int u = base + lane;
-                        bool take = false;
-                        uint32_t v = 0;
-                        if (u < nunits) {
-                            int x, y;
-                            unit_xy(u, x, y);
-                            const Neigh nb = ring_at(c.cell(x, y), c.sp, 1, c.sp);
-                            take = nb.valid && c.removable_s(nb.mask);
-                            v = (uint32_t)(x - t.X0) | (uint32_t)(y - t.Y0) << 16;
+                    auto probe = [&](int u, uint32_t &v) -> bool {
+                        v = 0;
+                        if (u >= nunits) return false;
+                        int x, y;
+                        unit_xy(u, x, y);
+                        const Neigh nb = ring_at(c.cell(x, y), c.sp, 1, c.sp);
+                        v = (uint32_t)(x - t.X0) | (uint32_t)(y - t.Y0) << 16;
+                        return nb.valid && c.removable_s(nb.mask);
+                    };
+                    if (NT <= 128 && q.filt2) {  // two units per lane in flight
+                        for (int base = wid * 32; base < nunits; base += 2 * NT) {
+                            uint32_t v0, v1;
+                            const bool t0 = probe(base + lane, v0), t1 = probe(base + NT + lane, v1);
+                            push_warp2(c.queue, &c.misc[2], t0, v0, t1, v1);
                         }
-                        push_warp(c.queue, &c.misc[2], take, v);
+                    } else {
+                        for (int base = wid * 32; base < nunits; base += NT) {
+                            uint32_t v;
+                            const bool take = probe(base + lane, v);
+                            push_warp(c.queue, &c.misc[2], take, v);
+                        }
                     }
                     __syncthreads();
                     nq = c.misc[2];

@@ -702,6 +702,20 @@ __device__ __forceinline__ void push_warp(uint32_t *queue, int *count, bool take
     if (take) queue[base + __popc(b & ((1u << lane) - 1))] = v;
 }
 
+// push_warp for two entries per lane (one atomic for both)
+__device__ __forceinline__ void push_warp2(uint32_t *queue, int *count, bool t0, uint32_t v0, bool t1, uint32_t v1)
+{
+    const unsigned b0 = __ballot_sync(FULL, t0), b1 = __ballot_sync(FULL, t1);
+    if (!(b0 | b1)) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(count, __popc(b0) + __popc(b1));
+    base = __shfl_sync(FULL, base, 0);
+    const unsigned below = (1u << lane) - 1;
+    if (t0) queue[base + __popc(b0 & below)] = v0;
+    if (t1) queue[base + __popc(b0) + __popc(b1 & below)] = v1;
+}
+
 // Proposition 2 on the 5x5 label window of p, as bit masks:
 // bit (dy + 2) * 5 + (dx + 2).  S(n) = sum over the in-image patch centres i
 // of W3(p) of (1 + |W3(i) n n| - |W3(i) n k|), |.| counting cells of that
