@@ -37,10 +37,16 @@ def torch_cuda():
 
 
 @pytest.mark.parametrize("case", CASES, ids=[f"case{c[0]}" for c in CASES])
-@pytest.mark.parametrize("mode", ["grid", "graph", "resident"])
-def test_random_case(torch_cuda, orc, case, mode):
+@pytest.mark.parametrize("mode", ["grid", "grid128", "graph", "resident"])
+def test_random_case(torch_cuda, orc, monkeypatch, case, mode):
+    """grid128: grid mode on the 128-thread plans with two pixels per lane in
+    the segment path (SEEDS_GRID_NT=128, SEEDS_SEG2=1)."""
     from paper_1309_3848_b200.seeds import Seeds, SeedsError
     torch = torch_cuda
+    if mode == "grid128":
+        monkeypatch.setenv("SEEDS_GRID_NT", "128")
+        monkeypatch.setenv("SEEDS_SEG2", "1")
+        mode = "grid"
     i, W, H, C, bpc, K, L, gamma, iters, nf, warm = case
     p = dict(n_superpixels=K, n_levels=L, bins_per_channel=bpc, smoothness_prior=gamma, iters_per_level=iters)
     imgs = np.stack([mosaic.mosaic(W, H, int(RNG.integers(1, 30)), 10.0, seed=1000 * i + f, C=C, grad=20.0)
