@@ -18,7 +18,7 @@ with --bands) is refined as N row bands, one per rank, exchanging sparse
 histogram-delta records (all-gather) and two-row label halos (send/recv) over
 torch.distributed after every sub-sweep ("strong", include/seeds.h row-band mode).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--mode auto|grid|graph|resident]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--mode auto|grid|graph]
   python bench.py --impl reference ...   # the CPU oracle, timed as it stands
 
 L2: a 512 MiB buffer (> 126 MB L2) is rewritten between timed steps, outside
@@ -42,7 +42,7 @@ from paper_1309_3848_b200 import configs  # noqa: E402
 
 METRIC = "Mpixels/s SEEDS refinement (481x321 frames/s, 200 SP); % of B200 HBM peak"
 UNIT = "Mpixels/s"
-MODE_NAMES = {1: "graph", 2: "resident", 3: "grid"}
+MODE_NAMES = {1: "graph", 3: "grid"}
 
 
 def peaks():
@@ -502,7 +502,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="auto", choices=["auto", "graph", "resident", "grid"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "graph", "grid"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--json-out", default=None)

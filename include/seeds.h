@@ -71,8 +71,7 @@ typedef struct {
     int subsweeps;       /* 4 L_eff I + P^2 I sub-sweeps per cold frame */
     int max_block_area;  /* largest top-level block, pixels */
     int kernels_per_run; /* kernel launches of one cold run in the resolved mode */
-    int exec_mode;       /* resolved execution mode of a one-frame run (SEEDS_MODE_GRAPH, _RESIDENT, _GRID) */
-    int cluster_size;    /* CTAs per cluster of the resident kernel (0: frame does not fit) */
+    int exec_mode;       /* resolved execution mode of a one-frame run (SEEDS_MODE_GRAPH, _GRID) */
     int grid_ctas;       /* CTAs of the grid-mode launch for one frame (0: no tile plan fits) */
     int grid_tiles;      /* tiles of one frame in grid mode */
     size_t workspace_bytes_per_frame;
@@ -88,7 +87,10 @@ typedef struct {
  *                      the pixel level is not counted); clamped to L_eff so
  *                      that the finest blocks have >= 1 pixel
  *   bins_per_channel   1..256 uniform bins per 8-bit channel (reading Q1);
- *                      B = bins_per_channel^channels must be <= 4096
+ *                      B = bins_per_channel^channels must be <= 4096 (the
+ *                      large-block colour test keeps a dense per-warp bin
+ *                      table of 2B + 2 words in shared memory; SURVEY.md
+ *                      8(b)'s 65,536 is narrowed)
  *   smoothness_prior   gamma in {0, 1}: 1 adds the 3x3 boundary term G at the
  *                      pixel level
  *   iters_per_level    I >= 0 iterations (each = every colour class once) per
@@ -116,8 +118,13 @@ seeds_status seeds_iterate(seeds_ctx *ctx, const uint8_t *image_u8, int32_t *lab
  *                every superpixel non-empty and 4-connected: the frame's
  *                histograms are recounted from them, the block phase is
  *                skipped and only the pixel phase runs (warm start, reading
- *                O9).  Labels violating the precondition give undefined
- *                (but memory-safe) results.
+ *                O9).  A label outside [0, K_act) is counted as label 0
+ *                (so every index stays in bounds) and flags the run: the next
+ *                call that synchronises the context (seeds_sync,
+ *                seeds_read_state, seeds_stats, the *_host entry points)
+ *                returns SEEDS_ESTATE.  Missing or non-4-connected labels are
+ *                memory-safe but give results outside the method's contract;
+ *                seeds_set_validate(ctx, 1) checks all three before the run.
  *   labels_out   device, n_frames*height*width int32 */
 seeds_status seeds_batch(seeds_ctx *ctx, const uint8_t *images, int n_frames,
                          const int32_t *init_labels, int32_t *labels_out, void *stream);
@@ -177,7 +184,7 @@ seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int3
  * paper's SPM baseline.
  *   SEEDS_EINVAL  means_iters outside [0, iters_per_level], or a row-band ctx
  *   SEEDS_ERANGE  width*height >= 2^27 (the exact comparison needs < 2^128)
- *   SEEDS_ESTATE  the ctx is forced to graph or resident mode (grid mode only;
+ *   SEEDS_ESTATE  the ctx is forced to graph mode (grid mode only;
  *                 a later run also fails with SEEDS_ESTATE if no grid plan fits) */
 seeds_status seeds_set_means_iters(seeds_ctx *ctx, int means_iters);
 
@@ -206,7 +213,7 @@ seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pi
  * half up -- recomputed at the start of every pixel iteration.  Block moves are
  * unaffected (like G).  on: 0 (default) or 1.
  *   SEEDS_EINVAL  on not 0/1, or a row-band ctx
- *   SEEDS_ESTATE  the ctx is forced to graph or resident mode (grid mode only) */
+ *   SEEDS_ESTATE  the ctx is forced to graph mode (grid mode only) */
 seeds_status seeds_set_compactness(seeds_ctx *ctx, int on);
 
 /* seeds_set_edge_prior -- the edge prior ("If a boundary is near
@@ -217,7 +224,7 @@ seeds_status seeds_set_compactness(seeds_ctx *ctx, int on);
  * move.  With smoothness_prior = 1 and the compactness prior this is the
  * paper's combined prior.  tau = 0 (default) turns it off.
  *   SEEDS_EINVAL  tau outside 0..1020, or a row-band ctx
- *   SEEDS_ESTATE  the ctx is forced to graph or resident mode (grid mode only) */
+ *   SEEDS_ESTATE  the ctx is forced to graph mode (grid mode only) */
 seeds_status seeds_set_edge_prior(seeds_ctx *ctx, int tau);
 
 /* seeds_set_block_levels -- block levels lo..hi (0 = finest) run in every later
@@ -228,7 +235,7 @@ seeds_status seeds_set_edge_prior(seeds_ctx *ctx, int tau);
  * The sub-sweep count (seeds_stats, the anytime limit) counts only the
  * levels that run.  Default 0, -1 (all).
  *   SEEDS_EINVAL  lo < 0, hi < -1, or a row-band ctx
- *   SEEDS_ESTATE  a non-default range on a ctx forced to graph or resident mode */
+ *   SEEDS_ESTATE  a non-default range on a ctx forced to graph mode */
 seeds_status seeds_set_block_levels(seeds_ctx *ctx, int lo, int hi);
 
 /* seeds_read_sums -- after a run with means post-processing: copy frame
@@ -267,17 +274,36 @@ typedef struct {
 seeds_status seeds_metrics(seeds_ctx *ctx, const int32_t *labels, const int32_t *gt, int n_segments, int eps,
                            seeds_metrics_t *out, void *stream);
 
+/* seeds_set_time_budget -- anytime termination (S5.4: the
+ * hill climbing "can be stopped at any time", with "a time budget on the
+ * fly").  budget_us > 0: every later run stops at the first sub-sweep boundary
+ * at which more than budget_us microseconds have passed since its launch
+ * started (device clock %globaltimer, checked by CTA 0 and published through
+ * the grid barrier, so every CTA stops after the same sub-sweep); the labels
+ * are the valid partition reached there (every sub-sweep keeps the partition
+ * valid, reading O7), and seeds_last_subsweeps reports how many sub-sweeps
+ * ran -- a count that seeds_debug_limit (or the oracle's max_subsweeps)
+ * replays bit for bit.  0 (default) turns it off.
+ *   SEEDS_EINVAL  budget_us < 0 or > 2^40, or a row-band ctx
+ *   SEEDS_ESTATE  the ctx is forced to graph mode (grid mode only) */
+seeds_status seeds_set_time_budget(seeds_ctx *ctx, long long budget_us);
+
+/* seeds_last_subsweeps -- sub-sweeps the last run performed (with a time
+ * budget: where it stopped; otherwise the schedule's count, capped by
+ * seeds_debug_limit).  Synchronises `stream`.  SEEDS_ESTATE before any run. */
+seeds_status seeds_last_subsweeps(seeds_ctx *ctx, int *subsweeps_host, void *stream);
+
 /* seeds_debug_limit -- stop every later run after max_subsweeps sub-sweeps
  * (the block maps are still pushed down and expanded, so the labels are the
  * valid partition reached at that point); -1 turns the limit off.  Used to
  * bisect a divergence against the oracle's max_subsweeps. */
 seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps);
 
-/* seeds_debug_trace -- resident / grid mode only: enable (1) per-CTA clock64
+/* seeds_debug_trace -- grid mode only: enable (1) per-CTA clock64
  * stamps of every sub-sweep (slot 0 work finished, 1 barrier passed; grid mode
  * also 2 replayed, 3 staged, 4 filtered, 5 decided; 8.. detail builds), copy
  * them to host_out[min(cap, ctas*(subsweeps+4)*16)] (int64, layout [cta][phase][16],
- * ctas = max(4 #SM, cluster_size)), or disable (0) and free the buffer.
+ * ctas = 4 #SM), or disable (0) and free the buffer.
  * Synchronises the device when host_out is given.  Diagnostic; not part of
  * the hot path. */
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap);
@@ -294,7 +320,7 @@ enum {
     SEEDS_KIND_BLOCK = 1, /* one block-level sub-sweep */
     SEEDS_KIND_PIXEL = 2, /* one pixel-level sub-sweep */
     SEEDS_KIND_EMIT = 3,  /* labels -> int32 output */
-    SEEDS_KIND_FRAME = 4, /* one resident whole-refinement launch */
+    SEEDS_KIND_FRAME = 4, /* one grid-mode whole-refinement launch */
     SEEDS_KIND_COUNT = 5
 };
 
@@ -302,20 +328,18 @@ enum {
  *  GRAPH:    one kernel per sub-sweep, the run captured as a CUDA graph with
  *            programmatic dependent launch; every kernel spans all frames of
  *            the batch, state in HBM/L2 (any frame size).
- *  RESIDENT: one launch for the whole run; a thread-block cluster per frame
- *            keeps labels, bins and histograms in (distributed) shared memory
- *            and separates sub-sweeps by cluster barriers; clusters loop over
- *            the frames of the batch (frames that fit a cluster, e.g. 481x321).
  *  GRID:     one cooperative launch over every SM for the whole run: the batch
  *            is cut into tiles of top-level blocks owned by fixed CTAs, state
  *            in L2, one grid barrier per sub-sweep (frames up to 32000 px wide
  *            whose tile plan fits shared memory).
  *  AUTO:     GRID when its tile plan fits, else GRAPH. */
-enum { SEEDS_MODE_AUTO = 0, SEEDS_MODE_GRAPH = 1, SEEDS_MODE_RESIDENT = 2, SEEDS_MODE_GRID = 3 };
+/* (value 2 was the round-1 cluster-resident mode, removed: slower than GRID on
+ * every configuration) */
+enum { SEEDS_MODE_AUTO = 0, SEEDS_MODE_GRAPH = 1, SEEDS_MODE_GRID = 3 };
 
 /* seeds_set_mode -- pick the execution mode for later runs.  SEEDS_EINVAL for
- * an unknown mode; SEEDS_ESTATE if RESIDENT is requested but the frame does
- * not fit a co-schedulable cluster, or GRID but no tile plan fits. */
+ * an unknown mode (including the removed value 2); SEEDS_ESTATE if GRID is
+ * requested but no tile plan fits. */
 seeds_status seeds_set_mode(seeds_ctx *ctx, int mode);
 
 /* seeds_profile -- enable (1) or disable (0) per-kernel device timing: later
@@ -394,6 +418,26 @@ seeds_status seeds_band_halo(seeds_ctx *ctx, int put, uint16_t *top, uint16_t *b
  * then returns this band's replica of the histograms (equal on every band). */
 seeds_status seeds_band_finish(seeds_ctx *ctx, const void *records_in, const int32_t *n_in, int32_t *labels_out,
                                void *stream);
+
+/* seeds_validate_labels -- is every frame of `labels` a valid partition
+ * (the set S -- every superpixel one non-empty, spatially
+ * connected blob; 4-connectivity, reading Q8)?  Runs a union-find connected-
+ * components pass on the GPU (seeds_validate.cuh) and synchronises `stream`.
+ *   labels       device, n_frames*height*width int32
+ *   report_host  NULL or host long long[3]: labels outside [0, K_act); the
+ *                first missing superpixel as frame*K_act + k (-1: none); the
+ *                first superpixel of more than one component, likewise
+ * SEEDS_OK if valid, SEEDS_ESTATE (seeds_last_error names the first defect)
+ * if not, SEEDS_EINVAL for NULL labels or n_frames < 1. */
+seeds_status seeds_validate_labels(seeds_ctx *ctx, const int32_t *labels, int n_frames, long long *report_host,
+                                   void *stream);
+
+/* seeds_set_validate -- on = 1: every later seeds_batch / seeds_batch_host with
+ * init_labels first runs seeds_validate_labels on them (synchronising) and
+ * returns its SEEDS_ESTATE without running; 0 (default) turns it off.  The
+ * SEEDS_ESTATE check of the batch contract ("checked in debug
+ * mode").  SEEDS_EINVAL for on not 0/1. */
+seeds_status seeds_set_validate(seeds_ctx *ctx, int on);
 
 /* seeds_sync -- wait for `stream` and report any pending CUDA error. */
 seeds_status seeds_sync(seeds_ctx *ctx, void *stream);

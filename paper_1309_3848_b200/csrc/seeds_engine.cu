@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -17,10 +18,10 @@
 
 #include "../../include/seeds.h"
 #include "seeds_kernels.cuh"
-#include "seeds_resident.cuh"
 #include "seeds_grid.cuh"
 #include "seeds_metrics.cuh"
 #include "seeds_lab.cuh"
+#include "seeds_validate.cuh"
 
 using namespace seeds;
 
@@ -38,11 +39,12 @@ struct GraphKey {
     int colour = 0;
     int blk_lo = 0, blk_hi = 0;
     int compact = 0, edge_tau = 0;
+    long long budget = 0;
     bool operator==(const GraphKey &o) const
     {
         return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof &&
                mode == o.mode && miters == o.miters && colour == o.colour && blk_lo == o.blk_lo && blk_hi == o.blk_hi &&
-               compact == o.compact && edge_tau == o.edge_tau;
+               compact == o.compact && edge_tau == o.edge_tau && budget == o.budget;
     }
 };
 
@@ -113,16 +115,9 @@ struct seeds_ctx {
     double prof_ms[SEEDS_KIND_COUNT] = {0};
     long long prof_n[SEEDS_KIND_COUNT] = {0};
     int kernels_per_run = 0;
-    // execution mode: SEEDS_MODE_AUTO / _GRAPH / _RESIDENT
+    // execution mode: SEEDS_MODE_AUTO / _GRAPH / _GRID
     int mode = SEEDS_MODE_AUTO;
-    int cluster = 0;          // resident kernel cluster size (0 = unavailable)
-    int max_clusters = 0;     // co-resident clusters of that size
-    size_t res_smem = 0;
-    int ntab = 0;
-    ResParams rp{};           // resident layout (pointers filled per run)
-    int *d_band = nullptr;    // band_y (CS+1) then band_top (CS+1)
-    uint32_t *d_kmap = nullptr;  // resident: home CTA | local row << 8 per superpixel
-    long long *d_trace = nullptr;  // resident-kernel phase clocks (seeds_debug_trace)
+    long long *d_trace = nullptr;  // grid-kernel phase clocks (seeds_debug_trace)
     // grid mode (seeds_grid.cuh): padded label planes, records, barrier counter, tile plan
     uint16_t *d_labp = nullptr;
     long long labp_fs = 0;
@@ -177,7 +172,18 @@ struct seeds_ctx {
     uint8_t *d_labimg = nullptr;
     size_t labimg_frames = 0;
     int n_sm = 148;
+    // device status word: bit 0 = a warm-start label outside [0, K) (kernels
+    // set it with atomicOr; check_err reports and clears it after a sync)
+    int *d_err = nullptr;
+    // label validation (seeds_validate_labels, seeds_set_validate)
+    bool validate = false;
+    int *d_cc_par = nullptr, *d_cc_roots = nullptr;
+    ValidateOut *d_vout = nullptr;
+    // anytime termination (seeds_set_time_budget): d_err[1] = stop boundary, d_err[2] = sub-sweeps run
+    long long budget_ns = 0;
+    bool last_dynamic = false;
 };
+
 
 static seeds_status cuda_fail(seeds_ctx *c, cudaError_t e, const char *what)
 {
@@ -190,6 +196,35 @@ static seeds_status cuda_fail(seeds_ctx *c, cudaError_t e, const char *what)
         cudaError_t e_ = (call);                                    \
         if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);   \
     } while (0)
+
+// After a synchronisation: report (and clear) a status the kernels flagged
+// since the last check -- SEEDS_ESTATE for warm-start labels outside [0, K)
+// (include/seeds.h seeds_batch).
+static seeds_status check_err(seeds_ctx *ctx)
+{
+    int h = 0;
+    CK(cudaMemcpy(&h, ctx->d_err, sizeof h, cudaMemcpyDeviceToHost));
+    if (!h) return SEEDS_OK;
+    CK(cudaMemset(ctx->d_err, 0, sizeof h));
+    snprintf(ctx->err, sizeof ctx->err,
+             "init_labels held a label outside [0, K_act) (counted as label 0; the run's output is not meaningful)");
+    return SEEDS_ESTATE;
+}
+
+// After a run with a time budget: the sub-sweeps it performed (written by the
+// kernel) decide which histogram buffer holds the final state.  Synchronises
+// the device work of the context's last run.
+static seeds_status settle_done(seeds_ctx *ctx, cudaStream_t st)
+{
+    if (!ctx->last_dynamic) return SEEDS_OK;
+    int d = 0;
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(&d, ctx->d_err + 2, sizeof d, cudaMemcpyDeviceToHost));
+    ctx->last_done = d;
+    ctx->last_final = d & 1;
+    ctx->last_dynamic = false;
+    return SEEDS_OK;
+}
 
 // ---------------------------------------------------------------------------
 // Geometry (reading O2).  nx = sqrt(K W / H) rounded half up (exact integer
@@ -478,7 +513,7 @@ static seeds_status enqueue(seeds_ctx *ctx, const uint8_t *img, const int32_t *i
         const dim3 g = grid1(ctx->N, 256, nf);
         SeedArgs a{img, ctx->W, ctx->C, ctx->bpc, ctx->L, ctx->nx, ctx->B, ctx->K, ctx->N, ctx->H_fs, ctx->Afs,
                    ctx->d_bxof, ctx->d_byof, init, ctx->d_bins, blocks ? nullptr : ctx->d_lab,
-                   ctx->d_H[0], ctx->d_A[0]};
+                   ctx->d_H[0], ctx->d_A[0], ctx->d_err};
         CK(launch_pdl(k_seed<BinT>, g, dim3(256), 0, st, a));
     }
     CK(prof_end(ctx, st));
@@ -571,11 +606,11 @@ static bool default_levels(const seeds_ctx *c) { return c->blk_lo == 0 && c->blk
 // the extended pixel path (k_grid<..., 1>): means post-processing or the compactness prior
 static bool ext_pixel(const seeds_ctx *c) { return c->miters > 0 || c->compact || c->edge_tau > 0; }
 // options that only grid mode implements
-static bool grid_only(const seeds_ctx *c) { return ext_pixel(c) || !default_levels(c); }
+static bool grid_only(const seeds_ctx *c) { return ext_pixel(c) || !default_levels(c) || c->budget_ns > 0; }
 
 static int resolved_mode(seeds_ctx *c, int nf)
 {
-    if (c->mode == SEEDS_MODE_GRAPH || c->mode == SEEDS_MODE_RESIDENT) return c->mode;
+    if (c->mode == SEEDS_MODE_GRAPH) return c->mode;
     return plan_grid(c, nf) ? SEEDS_MODE_GRID : SEEDS_MODE_GRAPH;
 }
 
@@ -588,19 +623,27 @@ static int resolved_mode(seeds_ctx *c, int nf)
 // they fit (else of one tile, restaged every sub-sweep), the unit queue, the
 // warp tables of the large-block path and the block geometry.
 // ---------------------------------------------------------------------------
-// The dynamic-shared-memory opt-in is a property of the function, shared by
-// every context and plan: only ever raise it (under a lock), so a plan made
-// later with less shared memory cannot break the launches of a larger one.
-static bool raise_optin(const void *k, int &optin, size_t smem)
+// The dynamic-shared-memory opt-in is a property of the function on the
+// current device, shared by every context and plan there: only ever raise it
+// (under a lock), so a plan made later with less shared memory cannot break the
+// launches of a larger one.  Tracked per device ordinal (the attribute is per
+// device).
+constexpr int MAX_DEVICES = 64;
+static bool raise_optin(const void *k, int (&optin)[MAX_DEVICES], size_t smem)
 {
     static std::mutex mu;
     std::lock_guard<std::mutex> g(mu);
-    if ((int)smem <= optin) return true;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEVICES) {
+        cudaGetLastError();
+        return false;
+    }
+    if ((int)smem <= optin[dev]) return true;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    optin = (int)smem;
+    optin[dev] = (int)smem;
     return true;
 }
 
@@ -608,7 +651,7 @@ template <typename BinT, int GAMMA, int P, int NT, int MEANS>
 static int grid_occupancy_m(size_t smem)
 {
     auto k = k_grid<BinT, GAMMA, P, NT, MEANS>;
-    static int optin = 0;
+    static int optin[MAX_DEVICES] = {};
     if (!raise_optin((const void *)k, optin, smem)) return 0;
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT, smem) != cudaSuccess) {
@@ -1045,7 +1088,7 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)(ctx->S + 1) * nf * 4, st));
     CK(cudaMemsetAsync(ctx->d_sync, 0, 16, st));
     GridParams q = ctx->gp;
-    q.img = img; q.init = init; q.out = out;
+    q.img = img; q.init = init; q.out = out; q.err = ctx->d_err;
     q.W = ctx->W; q.H = ctx->H; q.C = ctx->C; q.bpc = ctx->bpc; q.B = ctx->B; q.K = ctx->K; q.nx = ctx->nx;
     q.L = ctx->L; q.iters = ctx->iters; q.limit = ctx->limit; q.S = ctx->S; q.nf = nf;
     q.colstart = ctx->d_colstart; q.rowstart = ctx->d_rowstart; q.bxof = ctx->d_bxof; q.byof = ctx->d_byof;
@@ -1070,6 +1113,10 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     q.moves = ctx->d_moves;
     q.sync = ctx->d_sync;
     q.trace = ctx->d_trace;
+    q.budget_ns = ctx->budget_ns;
+    q.stop = ctx->d_err + 1;
+    q.done = ctx->d_err + 2;
+    CK(cudaMemsetAsync(ctx->d_err + 1, 0x7F, 4, st));  // STOP_NONE
     ctx->ev_used = 0;
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
     cudaError_t e;
@@ -1084,220 +1131,6 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     const int total = (blocks ? 4 * block_levels_run(ctx) * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
     ctx->last_done = ctx->limit >= 0 ? std::min(ctx->limit, total) : total;
     ctx->last_final = ctx->last_done & 1;
-    return SEEDS_OK;
-}
-
-template <typename BinT, int GAMMA, int P>
-static int resident_clusters(int cs, size_t smem)
-{
-    auto k = k_resident<BinT, GAMMA, P>;
-    static int optin = 0;
-    if (!raise_optin((const void *)k, optin, smem)) return 0;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(RES_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return n;
-}
-
-static int resident_clusters_for(const seeds_ctx *c, int cs, size_t smem)
-{
-    if (c->bb == 1) return c->gamma ? resident_clusters<uint8_t, 1, 3>(cs, smem) : resident_clusters<uint8_t, 0, 2>(cs, smem);
-    return c->gamma ? resident_clusters<uint16_t, 1, 3>(cs, smem) : resident_clusters<uint16_t, 0, 2>(cs, smem);
-}
-
-// Resident mode (seeds_resident.cuh): partition the rows into CS bands aligned
-// with the top-level block rows (each >= 2 pixel rows), give every superpixel
-// a home CTA (the band holding the centre row of its grid cell), lay out the
-// shared memory and check that a cluster of CS CTAs can be co-scheduled.
-static void setup_resident(seeds_ctx *c)
-{
-    c->cluster = 0;
-    if (c->GX > 16383 || c->GY > 16383 || c->L > 8 || c->K > 8192) return;  // record / table limits
-    const int T = c->L > 0 ? (c->GY >> (c->L - 1)) : c->H;     // row units the bands are made of
-    auto unit_row = [&](int t) { return c->L > 0 ? c->rowstart[(size_t)t << (c->L - 1)] : t; };
-    for (int cs = std::min(16, T); cs >= 1; cs--) {
-        // prefer the smallest cluster with the least rows per band
-        const int per = (T + cs - 1) / cs;
-        const int cs_min = (T + per - 1) / per;
-        if (cs != cs_min) continue;
-        std::vector<int> top(cs + 1), ys(cs + 1);
-        for (int r = 0; r <= cs; r++) {
-            top[r] = (int)((long long)r * T / cs);
-            ys[r] = unit_row(top[r]);
-        }
-        int bmin = 1 << 30, bmax = 0;
-        for (int r = 0; r < cs; r++) {
-            bmin = std::min(bmin, ys[r + 1] - ys[r]);
-            bmax = std::max(bmax, ys[r + 1] - ys[r]);
-        }
-        if (cs > 1 && bmin < 2) continue;
-        // home CTA of each superpixel
-        std::vector<uint32_t> kmap(c->K);
-        std::vector<int> nloc(cs, 0);
-        for (int k = 0; k < c->K; k++) {
-            const int gy = k / c->nx;
-            const int yc = (c->rowstart[(size_t)gy << c->L] + c->rowstart[(size_t)(gy + 1) << c->L]) / 2;
-            int r = 0;
-            while (r + 1 < cs && ys[r + 1] <= yc) r++;
-            kmap[k] = (uint32_t)r | (uint32_t)(nloc[r]++) << 8;
-        }
-        ResParams &q = c->rp;
-        q = ResParams{};
-        q.kloc = *std::max_element(nloc.begin(), nloc.end());
-        // queue capacity: the most units of one colour class in a band (pixel
-        // level and every block level); record capacity: the most histogram
-        // deltas one sub-sweep of a band can emit (one per pixel unit, or per
-        // distinct bin of each block: at most min(alpha, B))
-        long long qcap = (long long)((c->W + c->P - 1) / c->P) * ((bmax + c->P - 1) / c->P);
-        long long rcap = qcap;
-        for (int l = 0; l < c->L; l++) {
-            const int GXl = c->GX >> l;
-            for (int r = 0; r < cs; r++) {
-                const int j0 = top[r] << (c->L - 1 - l), j1 = top[r + 1] << (c->L - 1 - l);
-                qcap = std::max(qcap, (long long)((GXl + 1) / 2) * ((j1 - j0 + 1) / 2));
-                for (int cy = 0; cy < 2; cy++)
-                    for (int cx = 0; cx < 2; cx++) {
-                        long long sum = 0;
-                        for (int bj = j0; bj < j1; bj++) {
-                            if ((bj & 1) != cy) continue;
-                            const int h = c->rowstart[(size_t)(bj + 1) << l] - c->rowstart[(size_t)bj << l];
-                            for (int bi = cx; bi < GXl; bi += 2) {
-                                const int w = c->colstart[(size_t)(bi + 1) << l] - c->colstart[(size_t)bi << l];
-                                sum += std::min(w * h, c->B);
-                            }
-                        }
-                        rcap = std::max(rcap, sum);
-                    }
-            }
-        }
-        q.q_cap = (int)qcap + 32;
-        q.rec_cap = (int)rcap + 32;
-        q.pitch = c->W + 2 * RES_PAD;
-        q.lab_rows = bmax + 4;
-        q.GX = c->GX;
-        q.GY = c->GY;
-        bool need_tab = false;
-        for (int l = 0; l < c->L; l++) {
-            const int am = max_block_area(c, l);
-            q.bkind[l] = am <= 4 ? BK_T4 : am <= 32 ? BK_T16 : BK_WARP;
-            int gs = 0;
-            while ((1 << gs) < am && gs < 5) gs++;
-            q.gshift[l] = gs;
-            need_tab = need_tab || q.bkind[l] == BK_WARP;
-        }
-        const size_t tabw = (2 * (size_t)c->B + 2) * 4;
-        size_t off = 0;
-        q.o_lab = (unsigned)off;   off = align16(off + (size_t)q.lab_rows * q.pitch * 2);
-        q.o_bins = (unsigned)off;  off = align16(off + (size_t)bmax * c->W * c->bb);
-        q.o_H = (unsigned)off;     off = align16(off + 2 * (size_t)q.kloc * c->B * 4);
-        q.o_A = (unsigned)off;     off = align16(off + 2 * (size_t)q.kloc * 4);
-        q.o_rec = (unsigned)off;   off = align16(off + 2 * (size_t)q.rec_cap * sizeof(Rec));
-        q.o_misc = (unsigned)off;  off = align16(off + 16);
-        q.o_kaddr = (unsigned)off; off = align16(off + 2 * (size_t)c->K * 4);
-        q.o_geo = (unsigned)off;   off = align16(off + (size_t)(c->GX + c->GY + 2) * 4);
-        q.o_queue = (unsigned)off; off = align16(off + (size_t)q.q_cap * 4);
-        q.o_tab = (unsigned)off;
-        const size_t limit = 227 * 1024;
-        if (off + (need_tab ? tabw : 0) > limit) continue;
-        q.ntab = need_tab ? (int)std::min<size_t>(RES_THREADS / 32, (limit - off) / tabw) : 0;
-        const size_t smem = off + q.ntab * tabw;
-        const int n = resident_clusters_for(c, cs, smem);
-        if (n <= 0) continue;
-        std::vector<int> h(2 * (cs + 1));
-        for (int r = 0; r <= cs; r++) {
-            h[r] = ys[r];
-            h[cs + 1 + r] = top[r];
-        }
-        if (c->d_band) cudaFree(c->d_band);
-        c->d_band = nullptr;
-        if (c->d_kmap) cudaFree(c->d_kmap);
-        c->d_kmap = nullptr;
-        if (cudaMalloc(&c->d_band, h.size() * sizeof(int)) != cudaSuccess ||
-            cudaMemcpy(c->d_band, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMalloc(&c->d_kmap, kmap.size() * sizeof(uint32_t)) != cudaSuccess ||
-            cudaMemcpy(c->d_kmap, kmap.data(), kmap.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) !=
-                cudaSuccess) {
-            cudaGetLastError();
-            return;
-        }
-        q.band_y = c->d_band;
-        q.band_top = c->d_band + cs + 1;
-        q.kmap = c->d_kmap;
-        c->cluster = cs;
-        c->max_clusters = n;
-        c->res_smem = smem;
-        return;
-    }
-}
-
-template <typename BinT, int GAMMA, int P>
-static cudaError_t launch_resident_t(seeds_ctx *ctx, const ResParams &q, int ncl, cudaStream_t st)
-{
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = ctx->cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(ncl * ctx->cluster);
-    cfg.blockDim = dim3(RES_THREADS);
-    cfg.dynamicSmemBytes = ctx->res_smem;
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_resident<BinT, GAMMA, P>, q);
-}
-
-static seeds_status run_resident(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
-                                 cudaStream_t st)
-{
-    ResParams q = ctx->rp;
-    q.img = img; q.init = init; q.out = out;
-    q.W = ctx->W; q.H = ctx->H; q.C = ctx->C; q.bpc = ctx->bpc; q.B = ctx->B; q.K = ctx->K; q.nx = ctx->nx;
-    q.L = ctx->L; q.iters = ctx->iters; q.limit = ctx->limit; q.S = ctx->S; q.nf = nf;
-    q.colstart = ctx->d_colstart; q.rowstart = ctx->d_rowstart; q.bxof = ctx->d_bxof; q.byof = ctx->d_byof;
-    q.moves = ctx->d_moves;
-    for (int i = 0; i < 2; i++) {
-        q.Hout[i] = ctx->d_H[i];
-        q.Aout[i] = ctx->d_A[i];
-    }
-    q.H_fs = ctx->H_fs;
-    q.A_fs = ctx->Afs;
-    q.trace = ctx->d_trace;
-    const int ncl = std::max(1, std::min(nf, ctx->max_clusters));
-    CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
-    cudaError_t e;
-    if (ctx->bb == 1)
-        e = ctx->gamma ? launch_resident_t<uint8_t, 1, 3>(ctx, q, ncl, st) : launch_resident_t<uint8_t, 0, 2>(ctx, q, ncl, st);
-    else
-        e = ctx->gamma ? launch_resident_t<uint16_t, 1, 3>(ctx, q, ncl, st)
-                       : launch_resident_t<uint16_t, 0, 2>(ctx, q, ncl, st);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_resident launch");
-    CK(prof_end(ctx, st));
-    // sub-sweeps run: the schedule is data independent
-    const bool blocks = init == nullptr && ctx->L > 0;
-    int s = 0;
-    const int total = (blocks ? 4 * block_levels_run(ctx) * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
-    s = ctx->limit >= 0 ? std::min(ctx->limit, total) : total;
-    ctx->last_done = s;
-    ctx->last_final = s & 1;
     return SEEDS_OK;
 }
 
@@ -1377,9 +1210,62 @@ static const uint8_t *enqueue_lab(seeds_ctx *ctx, const uint8_t *img, int nf, cu
     return ctx->d_labimg;
 }
 
+// Validity of nf label maps (device, frame-major): every label in [0, K_act),
+// present and one 4-connected component.  Synchronises st.
+// rep (host, may be NULL): out-of-range count, first missing f*K + k, first
+// split f*K + k (-1 when none).
+static seeds_status validate_labels(seeds_ctx *ctx, const int32_t *labels, int nf, long long *rep, cudaStream_t st)
+{
+    if (!ctx->d_cc_par) {
+        CK(cudaMalloc(&ctx->d_cc_par, (size_t)ctx->N * sizeof(int)));
+        CK(cudaMalloc(&ctx->d_cc_roots, (size_t)ctx->K * sizeof(int)));
+        CK(cudaMalloc(&ctx->d_vout, sizeof(ValidateOut)));
+    }
+    ValidateOut h{0ull, LLONG_MAX, LLONG_MAX};
+    CK(cudaMemcpyAsync(ctx->d_vout, &h, sizeof h, cudaMemcpyHostToDevice, st));
+    const unsigned g = (unsigned)std::min<long long>((ctx->N + 255) / 256, (long long)ctx->n_sm * 8);
+    const unsigned gk = (unsigned)std::min<long long>((ctx->K + 255) / 256, (long long)ctx->n_sm * 8);
+    for (int f = 0; f < nf; f++) {
+        const int32_t *l = labels + (size_t)f * ctx->N;
+        k_cc_init<<<g, 256, 0, st>>>(ctx->d_cc_par, ctx->N);
+        k_cc_union<<<g, 256, 0, st>>>(l, ctx->W, ctx->H, ctx->K, ctx->d_cc_par, ctx->d_vout);
+        CK(cudaMemsetAsync(ctx->d_cc_roots, 0, (size_t)ctx->K * sizeof(int), st));
+        k_cc_roots<<<g, 256, 0, st>>>(l, ctx->N, ctx->K, ctx->d_cc_par, ctx->d_cc_roots);
+        k_cc_check<<<gk, 256, 0, st>>>(ctx->d_cc_roots, ctx->K, (long long)f * ctx->K, ctx->d_vout);
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(&h, ctx->d_vout, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const long long miss = h.first_missing == LLONG_MAX ? -1 : h.first_missing;
+    const long long split = h.first_split == LLONG_MAX ? -1 : h.first_split;
+    if (rep) {
+        rep[0] = (long long)h.out_of_range;
+        rep[1] = miss;
+        rep[2] = split;
+    }
+    if (h.out_of_range) {
+        snprintf(ctx->err, sizeof ctx->err, "%llu labels outside [0, %d)", h.out_of_range, ctx->K);
+        return SEEDS_ESTATE;
+    }
+    if (miss >= 0) {
+        snprintf(ctx->err, sizeof ctx->err, "frame %lld: superpixel %lld has no pixel", miss / ctx->K, miss % ctx->K);
+        return SEEDS_ESTATE;
+    }
+    if (split >= 0) {
+        snprintf(ctx->err, sizeof ctx->err, "frame %lld: superpixel %lld is not 4-connected", split / ctx->K,
+                 split % ctx->K);
+        return SEEDS_ESTATE;
+    }
+    return SEEDS_OK;
+}
+
 static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
                         cudaStream_t st)
 {
+    if (ctx->validate && init) {  // debug mode: the warm-start precondition, checked before anything runs
+        seeds_status v = validate_labels(ctx, init, nf, nullptr, st);
+        if (v != SEEDS_OK) return v;
+    }
     seeds_status r = ensure_frames(ctx, nf);
     if (r != SEEDS_OK) return r;
     r = ensure_labimg(ctx, nf);
@@ -1392,16 +1278,6 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
         return SEEDS_ESTATE;
     }
     ctx->last_miters = ctx->miters;
-    if (mode == SEEDS_MODE_RESIDENT) {
-        ctx->ev_used = 0;
-        img = enqueue_lab(ctx, img, nf, st);
-        CK(cudaGetLastError());
-        r = run_resident(ctx, img, init, out, nf, st);
-        if (r != SEEDS_OK) return r;
-        ctx->last_nf = nf;
-        ctx->ran = true;
-        return SEEDS_OK;
-    }
     GraphKey key;
     key.img = img; key.init = init; key.out = out; key.nf = nf; key.limit = ctx->limit; key.prof = ctx->prof;
     key.mode = mode;
@@ -1410,6 +1286,7 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     key.blk_hi = ctx->blk_hi;
     key.compact = ctx->compact;
     key.edge_tau = ctx->edge_tau;
+    key.budget = ctx->budget_ns;
     key.colour = ctx->colour;
     seeds_ctx::GraphEntry *hit = nullptr;
     for (auto &g : ctx->graphs)
@@ -1449,6 +1326,7 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     hit->used = ++ctx->tick;
     ctx->last_done = hit->done;
     ctx->last_final = hit->done & 1;
+    ctx->last_dynamic = ctx->budget_ns > 0;  // the sub-sweeps run are known after the run (*d_done)
     CK(cudaGraphLaunch(hit->exec, st));
     ctx->last_nf = nf;
     ctx->ran = true;
@@ -1500,7 +1378,8 @@ seeds_status seeds_create(int width, int height, int channels, int n_superpixels
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block_large<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, ctx->dev);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) setup_resident(ctx);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_err, 16);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, 16);
     if (e != cudaSuccess) {
         seeds_status st = e == cudaErrorMemoryAllocation ? SEEDS_ENOMEM : SEEDS_ECUDA;
         seeds_destroy(ctx);
@@ -1592,7 +1471,7 @@ static seeds_status batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n
         CK(cudaStreamWaitEvent(st, ctx->pev[14], 0));
         CK(cudaStreamSynchronize(st));
         ctx->ran = false;  // the context's state is that of the last chunk only (seeds_read_state: ESTATE)
-        return SEEDS_OK;
+        return check_err(ctx);
     }
     CK(cudaMemcpyAsync(ctx->d_img_stage, images_host, (size_t)n_frames * ctx->N * ctx->C,
                        cudaMemcpyHostToDevice, st));
@@ -1605,7 +1484,7 @@ static seeds_status batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n
     CK(cudaMemcpyAsync(labels_out_host, ctx->d_out_stage, (size_t)n_frames * ctx->N * 4, cudaMemcpyDeviceToHost,
                        st));
     CK(cudaStreamSynchronize(st));
-    return SEEDS_OK;
+    return check_err(ctx);
 }
 
 seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
@@ -1649,7 +1528,6 @@ seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *o)
     o->grid_x = ctx->GX; o->grid_y = ctx->GY; o->colour_period = ctx->P; o->bins_total = ctx->B;
     o->bin_bytes = ctx->bb; o->subsweeps = ctx->S; o->max_block_area = ctx->amax;
     o->exec_mode = resolved_mode(const_cast<seeds_ctx *>(ctx), 1);
-    o->cluster_size = ctx->cluster;
     {
         seeds_ctx *m = const_cast<seeds_ctx *>(ctx);
         const bool ok = plan_grid(m, 1);
@@ -1669,6 +1547,8 @@ seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int3
     if (!ctx) return SEEDS_EINVAL;
     if (!ctx->ran || frame < 0 || frame >= ctx->last_nf) return SEEDS_ESTATE;
     cudaStream_t st = (cudaStream_t)stream;
+    seeds_status sd = settle_done(ctx, st);
+    if (sd != SEEDS_OK) return sd;
     const int b = ctx->last_final;
     if (hist_out)
         CK(cudaMemcpyAsync(hist_out, ctx->d_H[b] + (size_t)frame * ctx->H_fs, (size_t)ctx->H_fs * 4,
@@ -1677,7 +1557,7 @@ seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int3
         CK(cudaMemcpyAsync(sizes_out, ctx->d_A[b] + (size_t)frame * ctx->Afs, (size_t)ctx->K * 4,
                            cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
-    return SEEDS_OK;
+    return check_err(ctx);
 }
 
 seeds_status seeds_stats(seeds_ctx *ctx, int frame, int32_t *moves_out_host, int cap, void *stream)
@@ -1686,6 +1566,10 @@ seeds_status seeds_stats(seeds_ctx *ctx, int frame, int32_t *moves_out_host, int
     if (!ctx->ran || frame < 0 || frame >= ctx->last_nf) return SEEDS_ESTATE;
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaStreamSynchronize(st));
+    seeds_status es = check_err(ctx);
+    if (es != SEEDS_OK) return es;
+    es = settle_done(ctx, st);
+    if (es != SEEDS_OK) return es;
     const int n = std::min(cap, ctx->last_done);
     std::vector<int32_t> all((size_t)(ctx->S + 1) * ctx->last_nf);
     CK(cudaMemcpy(all.data(), ctx->d_moves, all.size() * 4, cudaMemcpyDeviceToHost));
@@ -1725,14 +1609,10 @@ seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out,
 
 seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 {
-    if (!ctx || mode < SEEDS_MODE_AUTO || mode > SEEDS_MODE_GRID) return SEEDS_EINVAL;
-    if (grid_only(ctx) && (mode == SEEDS_MODE_GRAPH || mode == SEEDS_MODE_RESIDENT)) {
+    if (!ctx || mode < SEEDS_MODE_AUTO || mode > SEEDS_MODE_GRID || mode == 2) return SEEDS_EINVAL;
+    if (grid_only(ctx) && mode == SEEDS_MODE_GRAPH) {
         snprintf(ctx->err, sizeof ctx->err,
                  "the means post-processing, the compactness prior and block-level ranges run in grid mode only");
-        return SEEDS_ESTATE;
-    }
-    if (mode == SEEDS_MODE_RESIDENT && ctx->cluster == 0) {
-        snprintf(ctx->err, sizeof ctx->err, "the frame does not fit a co-schedulable cluster (resident mode)");
         return SEEDS_ESTATE;
     }
     if (mode == SEEDS_MODE_GRID && !plan_grid(ctx, 1)) {
@@ -1746,7 +1626,7 @@ seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap)
 {
     if (!ctx) return SEEDS_EINVAL;
-    const size_t n = (size_t)std::max(4 * ctx->n_sm, ctx->cluster) * (ctx->S + 4) * 16;
+    const size_t n = (size_t)(4 * ctx->n_sm) * (ctx->S + 4) * 16;
     if (enable && !ctx->d_trace) {
         CK(cudaMalloc(&ctx->d_trace, n * sizeof(long long)));
         CK(cudaMemset(ctx->d_trace, 0, n * sizeof(long long)));
@@ -1778,7 +1658,7 @@ seeds_status seeds_set_means_iters(seeds_ctx *ctx, int means_iters)
             return SEEDS_EINVAL;
         }
         if (ctx->N >= (1LL << 27)) return SEEDS_ERANGE;
-        if (ctx->mode == SEEDS_MODE_GRAPH || ctx->mode == SEEDS_MODE_RESIDENT) {
+        if (ctx->mode == SEEDS_MODE_GRAPH) {
             snprintf(ctx->err, sizeof ctx->err, "the means post-processing runs in grid mode only");
             return SEEDS_ESTATE;
         }
@@ -1822,7 +1702,7 @@ seeds_status seeds_set_compactness(seeds_ctx *ctx, int on)
         snprintf(ctx->err, sizeof ctx->err, "the compactness prior is not available in row-band mode");
         return SEEDS_EINVAL;
     }
-    if (on && (ctx->mode == SEEDS_MODE_GRAPH || ctx->mode == SEEDS_MODE_RESIDENT)) {
+    if (on && (ctx->mode == SEEDS_MODE_GRAPH)) {
         snprintf(ctx->err, sizeof ctx->err, "the compactness prior runs in grid mode only");
         return SEEDS_ESTATE;
     }
@@ -1837,7 +1717,7 @@ seeds_status seeds_set_edge_prior(seeds_ctx *ctx, int tau)
         snprintf(ctx->err, sizeof ctx->err, "the edge prior is not available in row-band mode");
         return SEEDS_EINVAL;
     }
-    if (tau && (ctx->mode == SEEDS_MODE_GRAPH || ctx->mode == SEEDS_MODE_RESIDENT)) {
+    if (tau && (ctx->mode == SEEDS_MODE_GRAPH)) {
         snprintf(ctx->err, sizeof ctx->err, "the edge prior runs in grid mode only");
         return SEEDS_ESTATE;
     }
@@ -1854,7 +1734,7 @@ seeds_status seeds_set_block_levels(seeds_ctx *ctx, int lo, int hi)
     }
     const int nlo = lo, nhi = hi < 0 ? 1 << 20 : hi;
     const bool dflt = nlo == 0 && nhi >= ctx->L - 1;
-    if (!dflt && (ctx->mode == SEEDS_MODE_GRAPH || ctx->mode == SEEDS_MODE_RESIDENT)) {
+    if (!dflt && (ctx->mode == SEEDS_MODE_GRAPH)) {
         snprintf(ctx->err, sizeof ctx->err, "a block-level range runs in grid mode only");
         return SEEDS_ESTATE;
     }
@@ -1868,10 +1748,12 @@ seeds_status seeds_read_sums(seeds_ctx *ctx, int frame, int64_t *sums_out, void 
     if (!ctx || !sums_out) return SEEDS_EINVAL;
     if (!ctx->ran || frame < 0 || frame >= ctx->last_nf || ctx->last_miters == 0) return SEEDS_ESTATE;
     cudaStream_t st = (cudaStream_t)stream;
+    seeds_status sd = settle_done(ctx, st);
+    if (sd != SEEDS_OK) return sd;
     CK(cudaMemcpyAsync(sums_out, ctx->d_S[ctx->last_final] + (size_t)frame * ctx->Afs * 4,
                        (size_t)ctx->K * 4 * sizeof(long long), cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
-    return SEEDS_OK;
+    return check_err(ctx);
 }
 
 seeds_status seeds_metrics(seeds_ctx *ctx, const int32_t *labels, const int32_t *gt, int n_segments, int eps,
@@ -1920,12 +1802,51 @@ seeds_status seeds_metrics(seeds_ctx *ctx, const int32_t *labels, const int32_t 
     return SEEDS_OK;
 }
 
+seeds_status seeds_validate_labels(seeds_ctx *ctx, const int32_t *labels, int n_frames, long long *report_host,
+                                   void *stream)
+{
+    if (!ctx || !labels || n_frames < 1) return SEEDS_EINVAL;
+    return validate_labels(ctx, labels, n_frames, report_host, (cudaStream_t)stream);
+}
+
+seeds_status seeds_set_validate(seeds_ctx *ctx, int on)
+{
+    if (!ctx || (on != 0 && on != 1)) return SEEDS_EINVAL;
+    ctx->validate = on != 0;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_set_time_budget(seeds_ctx *ctx, long long budget_us)
+{
+    if (!ctx || budget_us < 0 || budget_us > (1LL << 40)) return SEEDS_EINVAL;
+    if (budget_us && ctx->banded) {
+        snprintf(ctx->err, sizeof ctx->err, "the time budget is not available in row-band mode");
+        return SEEDS_EINVAL;
+    }
+    if (budget_us && ctx->mode == SEEDS_MODE_GRAPH) {
+        snprintf(ctx->err, sizeof ctx->err, "the time budget runs in grid mode only");
+        return SEEDS_ESTATE;
+    }
+    ctx->budget_ns = budget_us * 1000;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_last_subsweeps(seeds_ctx *ctx, int *subsweeps_host, void *stream)
+{
+    if (!ctx || !subsweeps_host) return SEEDS_EINVAL;
+    if (!ctx->ran) return SEEDS_ESTATE;
+    seeds_status sd = settle_done(ctx, (cudaStream_t)stream);
+    if (sd != SEEDS_OK) return sd;
+    *subsweeps_host = ctx->last_done;
+    return SEEDS_OK;
+}
+
 seeds_status seeds_sync(seeds_ctx *ctx, void *stream)
 {
     if (!ctx) return SEEDS_EINVAL;
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     CK(cudaGetLastError());
-    return SEEDS_OK;
+    return check_err(ctx);
 }
 
 void seeds_destroy(seeds_ctx *ctx)
@@ -1936,10 +1857,10 @@ void seeds_destroy(seeds_ctx *ctx)
     drop_plans(ctx);
     void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1], ctx->d_S[0], ctx->d_S[1],
-                    ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage, ctx->d_band, ctx->d_kmap,
+                    ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage,
                     ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp, ctx->d_bcount,
                     ctx->d_init_stage, ctx->d_out_stage, ctx->d_met_key, ctx->d_met_cnt, ctx->d_met_acc,
-                    ctx->d_lab_tab, ctx->d_labimg};
+                    ctx->d_lab_tab, ctx->d_labimg, ctx->d_err, ctx->d_cc_par, ctx->d_cc_roots, ctx->d_vout};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -2023,11 +1944,11 @@ seeds_status seeds_band_seed(seeds_ctx *ctx, const uint8_t *image_u8, const int3
     if (ctx->bb == 1)
         k_band_seed<uint8_t><<<g, 256, 0, st>>>(image_u8, init_labels, ctx->W, ctx->H, ctx->C, ctx->bpc, ctx->L,
                                                 ctx->nx, ctx->B, ctx->K, ctx->d_bxof, ctx->d_byof, ctx->d_labp,
-                                                ctx->lpitch, (uint8_t *)q.binsp, q.bpitch, ctx->d_H[0], ctx->d_A[0]);
+                                                ctx->lpitch, (uint8_t *)q.binsp, q.bpitch, ctx->d_H[0], ctx->d_A[0], ctx->d_err);
     else
         k_band_seed<uint16_t><<<g, 256, 0, st>>>(image_u8, init_labels, ctx->W, ctx->H, ctx->C, ctx->bpc, ctx->L,
                                                  ctx->nx, ctx->B, ctx->K, ctx->d_bxof, ctx->d_byof, ctx->d_labp,
-                                                 ctx->lpitch, (uint16_t *)q.binsp, q.bpitch, ctx->d_H[0], ctx->d_A[0]);
+                                                 ctx->lpitch, (uint16_t *)q.binsp, q.bpitch, ctx->d_H[0], ctx->d_A[0], ctx->d_err);
     CK(cudaGetLastError());
     ctx->band_total = (init_labels ? 0 : 4 * ctx->L * ctx->iters) + ctx->P * ctx->P * ctx->iters;
     ctx->band_seeded = true;

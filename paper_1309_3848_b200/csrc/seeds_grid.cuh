@@ -36,6 +36,7 @@ namespace seeds {
 // several tiles, so that four independent tile pipelines hide each other's
 // latencies).
 constexpr int GRID_THREADS = 512;
+constexpr int STOP_NONE = 0x7F7F7F7F;  // "no stop" (a byte-wise memset value)
 constexpr int GRID_THREADS_SMALL = 128;
 #ifdef SEEDS_CPS8
 constexpr int GRID_SMALL_CPS = 8;  // experiment: 8 x 128 threads per SM, 64 registers
@@ -66,6 +67,7 @@ struct GridParams {
     const uint8_t *img;
     const int32_t *init;  // warm-start labels or nullptr
     int32_t *out;
+    int *err;             // bit 0: a warm-start label outside [0, K) (checked_label)
     int W, H, C, bpc, B, K, nx, L, iters, limit, S, nf;
     const int *colstart, *rowstart, *bxof, *byof;
     const GridTile *tiles;
@@ -115,7 +117,22 @@ struct GridParams {
     GRec *rec_out;
     int *rec_count;
     float invGX, invGY;
+    // anytime termination: with budget_ns > 0, CTA 0 compares
+    // the device clock with the launch start at every sub-sweep boundary and,
+    // once the budget is spent, publishes the boundary in *stop before it
+    // arrives at the grid barrier; every CTA reads it after the barrier, so all
+    // stop after the same sub-sweep with a valid partition.  *done receives the
+    // sub-sweeps run.
+    long long budget_ns;
+    int *stop, *done;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Split grid barrier: arrive (CTA barrier, then thread 0 publishes the CTA's
 // writes with a GPU-scope release add on the counter) ... wait (thread 0 polls
@@ -138,6 +155,12 @@ __device__ __forceinline__ void grid_poll(unsigned *ctr, unsigned target)
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
         if (++spins > (1LL << 26)) __trap();  // a CTA that never arrives: fail loudly instead of hanging
     } while ((int)(v - target) < 0);
+#ifndef SEEDS_RELAXED_BARRIER
+    // the relaxed poll that observed every arrival + this fence = an acquire
+    // pattern: every write the other CTAs released before arriving is visible
+    // to this CTA's later (generic-proxy) reads under the PTX memory model
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
 }
 __device__ __forceinline__ void grid_arrive(unsigned *ctr, unsigned &target)
 {
@@ -381,6 +404,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
 
     for (int i = tid; i < q.ntab * TW; i += NT) c.tabs[i] = 0;
     if (tid < 4) c.misc[tid] = 0;
+    if (tid == 8) c.misc[8] = STOP_NONE;  // sub-sweeps after which the anytime budget stops the run
     if (tid < 8) c.rem[tid] = c_removable[tid];
     const int ntl = blockIdx.x < q.ntiles ? (q.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // tiles of this CTA
     for (int i = tid; i < ntl; i += NT) c.tiles[i] = q.tiles[blockIdx.x + (long long)i * gridDim.x];
@@ -419,7 +443,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                     for (int ch = 0; ch < q.C; ch++) b = b * q.bpc + (((int)v[ch] * q.bpc) >> 8);
                     if (q.bins_res) tb[(y - t.Y0) * tw + x - t.X0] = (BinT)b;
                     else tb[(long long)y * q.bpitch + x] = (BinT)b;
-                    k = q.init ? q.init[fN + (long long)y * W + x] : gy + (q.bxof[x] >> q.L);
+                    k = q.init ? checked_label(q.init[fN + (long long)y * W + x], q.K, q.err) : gy + (q.bxof[x] >> q.L);
                     gl[(long long)(y + 2) * q.lpitch + x + 2] = (uint16_t)k;
                     key = k * B + b;
                 }
@@ -436,9 +460,29 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
             }
         }
     }
-    if (!q.band) grid_barrier(q.sync, target);
+    // Grid barrier at a sub-sweep boundary, after which `next` sub-sweeps are
+    // done; it carries the anytime stop decision (q.budget_ns).
+    const unsigned long long t_start = globaltimer();
+    auto boundary = [&](int next) {
+        __syncthreads();
+        target += gridDim.x;
+        if (tid == 0) {
+            if (q.budget_ns > 0 && blockIdx.x == 0 && (long long)(globaltimer() - t_start) >= q.budget_ns)
+                asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(q.stop), "r"(next) : "memory");
+            grid_signal(q.sync);
+            grid_poll(q.sync, target);
+            if (q.budget_ns > 0) {
+                int v;
+                asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(q.stop) : "memory");
+                c.misc[8] = v;
+            }
+        }
+        __syncthreads();
+    };
+    if (!q.band) boundary(0);
 
     int s = 0;
+    auto stopped = [&]() { return (q.limit >= 0 && s >= q.limit) || s >= c.misc[8]; };
     // debug trace [cta][phase][8]: 0 work done, 1 barrier passed, 2 replayed,
     // 3 last tile staged, 4 last tile filtered, 5 last tile decided
     // slots 6, 7, 15: per sub-sweep sums over the CTA's tiles of the staging
@@ -505,7 +549,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     };
     auto end_subsweep = [&]() {
         stamp(s + 1, 0);
-        grid_barrier(q.sync, target);
+        boundary(s + 1);
         stamp(s + 1, 1);
         s++;
     };
@@ -524,7 +568,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
             // reading M4: a level outside [blk_lo, blk_hi] runs no iteration
             for (int it = l > q.blk_hi || l < q.blk_lo ? q.iters : 0; it < q.iters; it++)
                 for (int col = 0; col < 4; col++) {
-                    if (q.limit >= 0 && s >= q.limit) break;
+                    if (stopped()) break;
                     if (s < q.s0) {  // band mode: sub-sweeps of earlier launches
                         s++;
                         continue;
@@ -964,7 +1008,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     // ---- pixel level, P x P colouring (Q11) --------------
     for (int it = 0; it < q.iters; it++)
         for (int col = 0; col < P * P; col++) {
-            if (q.limit >= 0 && s >= q.limit) break;
+            if (stopped()) break;
             if (s < q.s0) {
                 s++;
                 continue;
@@ -1430,6 +1474,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
 
     // ---- outputs: int32 labels of the owned tiles --------------------------
     if (q.band) return;  // band mode: seeds_band_finish emits the band's rows
+    if (blockIdx.x == 0 && tid == 0 && q.done) *q.done = s;
     for (int ti = 0; ti < ntl; ti++) {
         const GridTile t = c.tiles[ti];
         const uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
@@ -1448,7 +1493,7 @@ template <typename BinT>
 __global__ void __launch_bounds__(256) k_band_seed(const uint8_t *img, const int32_t *init, int W, int H, int C,
                                                    int bpc, int L, int nx, int B, int K, const int *bxof,
                                                    const int *byof, uint16_t *lab, int lpitch, BinT *binsp,
-                                                   int bpitch, int *Hb, int *Ab)
+                                                   int bpitch, int *Hb, int *Ab, int *err)
 {
     const long long N = (long long)W * H;
     for (long long base = (long long)blockIdx.x * blockDim.x; base < N; base += (long long)gridDim.x * blockDim.x) {
@@ -1460,7 +1505,7 @@ __global__ void __launch_bounds__(256) k_band_seed(const uint8_t *img, const int
             int b = 0;
             for (int ch = 0; ch < C; ch++) b = b * bpc + (((int)img[p * C + ch] * bpc) >> 8);
             binsp[(long long)y * bpitch + x] = (BinT)b;
-            k = init ? init[p] : (byof[y] >> L) * nx + (bxof[x] >> L);
+            k = init ? checked_label(init[p], K, err) : (byof[y] >> L) * nx + (bxof[x] >> L);
             lab[(long long)(y + 2) * lpitch + x + 2] = (uint16_t)k;
             key = k * B + b;
         }

@@ -11,8 +11,8 @@
 // which holds the state after s-2, both the deltas of s-1 (replayed from the
 // previous sub-sweep's records) and its own deltas -- so (Hy, Ay) is the
 // state after s when the kernel ends and the next sub-sweep swaps roles.
-// One kernel per sub-sweep (graph mode) or one cluster barrier per sub-sweep
-// (resident mode); that is the only ordering point.
+// One kernel per sub-sweep (graph mode) or one grid barrier per sub-sweep
+// (grid mode, seeds_grid.cuh); that is the only ordering point.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -20,7 +20,7 @@
 namespace seeds {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int SMALL_ALPHA = 16;       // resident mode: blocks up to this many pixels, one thread per block
+constexpr int SMALL_ALPHA = 16;       // k_block_small: scratch column per thread (blocks up to 16 px)
 constexpr int GRAPH_SMALL_ALPHA = 4;  // graph mode: the same for blocks up to 4 pixels (finest levels)
 
 // A histogram delta: superpixel k loses `count` pixels of bin `bin` to n.
@@ -172,7 +172,18 @@ struct SeedArgs {
     void *bins;
     uint16_t *lab;        // nullptr when the block phase builds the labels later
     int *H, *A;
+    int *err;             // bit 0 set when a warm-start label is outside [0, K)
 };
+
+// A warm-start label outside [0, K) (the precondition of seeds_batch,
+// PAPER.md:259-262) is counted as label 0 -- every later index stays in
+// bounds -- and flags the run: the host reports SEEDS_ESTATE at its next sync.
+__device__ __forceinline__ int checked_label(int k, int K, int *err)
+{
+    if ((unsigned)k < (unsigned)K) return k;
+    atomicOr(err, 1);
+    return 0;
+}
 
 // Pixels t0 + threadIdx.x, t0 + T + threadIdx.x, ... of frame f (t0, T warp-uniform).
 template <typename BinT>
@@ -190,7 +201,7 @@ __device__ __forceinline__ void seed_pixels(const SeedArgs &a, int f, long long 
             int b = 0;
             for (int c = 0; c < a.C; c++) b = b * a.bpc + (((int)v[c] * a.bpc) >> 8);
             bins[(long long)f * a.N + p] = (BinT)b;
-            if (a.init) label = a.init[(long long)f * a.N + p];
+            if (a.init) label = checked_label(a.init[(long long)f * a.N + p], a.K, a.err);
             else label = (a.byof[y] >> a.L) * a.nx + (a.bxof[x] >> a.L);
             if (a.lab) a.lab[(long long)f * a.N + p] = (uint16_t)label;
             key = label * a.B + b;
@@ -619,9 +630,8 @@ __global__ void __launch_bounds__(256) k_pixel_tile(SweepParams p, int tiles_x, 
 
 
 // ---------------------------------------------------------------------------
-// Helpers shared by the persistent kernels (grid mode, seeds_grid.cuh, and
-// resident mode, seeds_resident.cuh): their label planes carry a sentinel
-// border, so label reads need no bounds test.
+// Helpers of the persistent kernel (grid mode, seeds_grid.cuh): its label
+// planes carry a sentinel border, so label reads need no bounds test.
 // ---------------------------------------------------------------------------
 
 // SM clock read that memory operations are not moved across (debug traces).

@@ -26,7 +26,8 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish",
            "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics", "seeds_set_colour_space",
            "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks", "seeds_set_compactness",
-           "seeds_set_edge_prior", "seeds_batch_host_warm"]
+           "seeds_set_edge_prior", "seeds_batch_host_warm", "seeds_validate_labels", "seeds_set_validate",
+           "seeds_set_time_budget", "seeds_last_subsweeps"]
 
 
 class _Metrics(ctypes.Structure):
@@ -46,7 +47,7 @@ class Info(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "width", "height", "channels", "nx", "ny", "k_actual", "levels_eff", "grid_x", "grid_y",
         "colour_period", "bins_total", "bin_bytes", "subsweeps", "max_block_area",
-        "kernels_per_run", "exec_mode", "cluster_size", "grid_ctas", "grid_tiles")] + [
+        "kernels_per_run", "exec_mode", "grid_ctas", "grid_tiles")] + [
         ("workspace_bytes_per_frame", ctypes.c_size_t)]
 
 
@@ -79,6 +80,10 @@ def load(path: str = LIB_PATH):
         "seeds_set_host_chunks": ([vp, i], i),
         "seeds_set_compactness": ([vp, i], i),
         "seeds_set_edge_prior": ([vp, i], i),
+        "seeds_validate_labels": ([vp, vp, i, vp, vp], i),
+        "seeds_set_validate": ([vp, i], i),
+        "seeds_set_time_budget": ([vp, ctypes.c_longlong], i),
+        "seeds_last_subsweeps": ([vp, vp, vp], i),
         "seeds_rgb_to_lab": ([vp, vp, ctypes.c_longlong, vp, vp], i),
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
@@ -128,7 +133,6 @@ class Geometry:
     max_block_area: int
     kernels_per_run: int
     exec_mode: int
-    cluster_size: int
     grid_ctas: int
     grid_tiles: int
     workspace_bytes_per_frame: int
@@ -204,13 +208,30 @@ class Seeds:
                                           labels_out.data_ptr(), _stream_ptr(stream)))
         return labels_out
 
+    def _host_frames(self, images, labels_out) -> int:
+        """Frames of a host call; the buffers must match exactly (the C side
+        copies n*H*W*C bytes in and n*H*W int32 out)."""
+        if not (isinstance(images, np.ndarray) and images.dtype == np.uint8 and images.flags.c_contiguous):
+            raise TypeError("images must be a C-contiguous uint8 numpy array")
+        fr = self.width * self.height * self.channels
+        n = images.size // fr
+        if n < 1 or n * fr != images.size:
+            raise ValueError("images do not hold whole frames of the context's size")
+        if not (isinstance(labels_out, np.ndarray) and labels_out.dtype == np.int32
+                and labels_out.flags.c_contiguous and labels_out.flags.writeable):
+            raise TypeError("labels_out must be a writeable C-contiguous int32 numpy array")
+        if labels_out.size != n * self.width * self.height:
+            raise ValueError(f"labels_out holds {labels_out.size} values, the call writes {n * self.width * self.height}")
+        return n
+
     def batch_host(self, images: np.ndarray, labels_out: np.ndarray, init_labels=None, stream=None):
         """Host-memory entry point (copies in, runs, copies out, synchronises)."""
-        n = images.size // (self.width * self.height * self.channels)
-        assert images.flags.c_contiguous and images.dtype == np.uint8
-        assert labels_out.flags.c_contiguous and labels_out.dtype == np.int32
+        n = self._host_frames(images, labels_out)
         init_ptr = None
         if init_labels is not None:
+            if not (isinstance(init_labels, np.ndarray) and init_labels.dtype == np.int32
+                    and init_labels.flags.c_contiguous and init_labels.size == labels_out.size):
+                raise TypeError("init_labels must be a C-contiguous int32 numpy array of n*H*W values")
             init_ptr = init_labels.ctypes.data
         self._check(self._lib.seeds_batch_host(self._ctx, images.ctypes.data, n, init_ptr,
                                                labels_out.ctypes.data, _stream_ptr(stream)))
@@ -220,9 +241,7 @@ class Seeds:
         """Next frames of n video streams from host memory, each warm-started
         from the previous host call's labels still on the device
         (seeds_batch_host_warm)."""
-        n = images.size // (self.width * self.height * self.channels)
-        assert images.flags.c_contiguous and images.dtype == np.uint8
-        assert labels_out.flags.c_contiguous and labels_out.dtype == np.int32
+        n = self._host_frames(images, labels_out)
         self._check(self._lib.seeds_batch_host_warm(self._ctx, images.ctypes.data, n, labels_out.ctypes.data,
                                                     _stream_ptr(stream)))
         return labels_out
@@ -244,7 +263,7 @@ class Seeds:
         return out
 
     KINDS = ("seed", "block", "pixel", "emit", "frame")
-    MODES = {"auto": 0, "graph": 1, "resident": 2, "grid": 3}
+    MODES = {"auto": 0, "graph": 1, "grid": 3}
 
     def set_mode(self, mode: str):
         self._check(self._lib.seeds_set_mode(self._ctx, self.MODES[mode]))
@@ -267,11 +286,11 @@ class Seeds:
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.KINDS)}
 
     def debug_trace(self, enable: bool = True, n_sm: int | None = None):
-        """Resident / grid mode: per-CTA clock64 stamps [cta, phase, slot] (include/seeds.h)."""
+        """Grid mode: per-CTA clock64 stamps [cta, phase, slot] (include/seeds.h)."""
         if n_sm is None:
             import torch
             n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-        cs = max(4 * n_sm, self.info.cluster_size)
+        cs = 4 * n_sm
         n = cs * (self.info.subsweeps + 4) * 16
         out = np.zeros(n, np.int64)
         self._check(self._lib.seeds_debug_trace(self._ctx, int(enable), out.ctypes.data if enable else None, n))
@@ -329,6 +348,41 @@ class Seeds:
         self._check(self._lib.seeds_metrics(self._ctx, labels.data_ptr(), gt.data_ptr(), int(n_segments), int(eps),
                                             ctypes.byref(out), _stream_ptr(stream)))
         return {f: getattr(out, f) for f, _ in _Metrics._fields_}
+
+    def validate_labels(self, labels, stream=None) -> tuple:
+        """Check (n, H, W) / (H, W) int32 CUDA labels form valid partitions
+        (include/seeds.h seeds_validate_labels): returns (out_of_range,
+        first_missing, first_split); raises SeedsError(SEEDS_ESTATE) if invalid."""
+        import torch
+        if not (isinstance(labels, torch.Tensor) and labels.is_cuda and labels.dtype == torch.int32
+                and labels.is_contiguous()):
+            raise TypeError("labels must be a contiguous int32 CUDA tensor")
+        n = labels.numel() // (self.width * self.height)
+        if n < 1 or n * self.width * self.height != labels.numel():
+            raise ValueError("labels do not hold whole frames of the context's size")
+        rep = np.zeros(3, np.int64)
+        st = self._lib.seeds_validate_labels(self._ctx, labels.data_ptr(), n, rep.ctypes.data, _stream_ptr(stream))
+        if st not in (0, -5):
+            self._check(st)
+        out = tuple(int(v) for v in rep)
+        if st == -5:
+            raise SeedsError(st, self._lib.seeds_last_error(self._ctx).decode())
+        return out
+
+    def set_validate(self, on: bool = True):
+        """Validate warm-start labels before every run (include/seeds.h seeds_set_validate)."""
+        self._check(self._lib.seeds_set_validate(self._ctx, int(bool(on))))
+
+    def set_time_budget(self, budget_us: int):
+        """Anytime termination after budget_us microseconds (0 = off;
+        include/seeds.h seeds_set_time_budget)."""
+        self._check(self._lib.seeds_set_time_budget(self._ctx, int(budget_us)))
+
+    def last_subsweeps(self, stream=None) -> int:
+        """Sub-sweeps the last run performed (include/seeds.h seeds_last_subsweeps)."""
+        out = ctypes.c_int()
+        self._check(self._lib.seeds_last_subsweeps(self._ctx, ctypes.byref(out), _stream_ptr(stream)))
+        return out.value
 
     def debug_limit(self, max_subsweeps: int):
         self._check(self._lib.seeds_debug_limit(self._ctx, max_subsweeps))

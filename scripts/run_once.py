@@ -5,7 +5,7 @@ import numpy as np, torch
 from paper_1309_3848_b200 import configs
 from paper_1309_3848_b200.seeds import Seeds
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-mode = sys.argv[2] if len(sys.argv) > 2 else "resident"
+mode = sys.argv[2] if len(sys.argv) > 2 else "grid"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 nfr = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 imgs = configs.frames(cfg, n=nfr)

@@ -1,4 +1,4 @@
-"""Per-CTA clock64 trace of one resident / grid run: work and barrier cycles
+"""Per-CTA clock64 trace of one grid-mode run: work and barrier cycles
 per sub-sweep (max / min over CTAs), summarised per phase group.
 Usage: [NF=frames] trace.py [cfg] [mode] [HxW crop]"""
 import os
@@ -12,7 +12,7 @@ from paper_1309_3848_b200 import configs  # noqa: E402
 from paper_1309_3848_b200.seeds import Seeds  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-mode = sys.argv[2] if len(sys.argv) > 2 else "resident"
+mode = sys.argv[2] if len(sys.argv) > 2 else "grid"
 NF = int(os.environ.get("NF", "1"))  # frames per run (multi-tile plans)
 img = configs.frames(cfg, n=NF)
 img = img[0] if NF == 1 else img

@@ -37,7 +37,7 @@ def torch_cuda():
 
 
 @pytest.mark.parametrize("case", CASES, ids=[f"case{c[0]}" for c in CASES])
-@pytest.mark.parametrize("mode", ["grid", "grid128", "graph", "resident"])
+@pytest.mark.parametrize("mode", ["grid", "grid128", "graph"])
 def test_random_case(torch_cuda, orc, monkeypatch, case, mode):
     """grid128: grid mode on the 128-thread plans with two pixels per lane in
     the segment path (SEEDS_GRID_NT=128, SEEDS_SEG2=1)."""

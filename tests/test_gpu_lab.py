@@ -49,7 +49,7 @@ def test_conversion_every_colour(torch_cuda, orc):
     s.close()
 
 
-@pytest.mark.parametrize("mode", ["grid", "graph", "resident"])
+@pytest.mark.parametrize("mode", ["grid", "graph"])
 @pytest.mark.parametrize("cfg", ["c1", "c2"])
 def test_lab_runs(torch_cuda, orc, cfg, mode):
     from paper_1309_3848_b200.seeds import SeedsError

@@ -19,7 +19,7 @@ def torch_cuda():
     return torch
 
 
-MODES = ["graph", "resident", "grid"]
+MODES = ["graph", "grid"]
 
 
 @pytest.fixture(params=MODES)
@@ -179,15 +179,12 @@ def test_host_entry_point(torch_cuda, orc):
 
 
 def test_modes_resolved(torch_cuda):
-    """A c2 frame fits a co-schedulable cluster (resident mode) and a grid tile
-    plan (grid mode, the AUTO choice); every mode reports its launch count."""
+    """A c2 frame fits a grid tile plan (grid mode, the AUTO choice); every
+    mode reports its launch count; the removed resident mode (2) is rejected."""
     from paper_1309_3848_b200.seeds import Seeds
     s = Seeds(481, 321, 3, 200, 4, 5, 1, 4)
-    print("cluster size", s.info.cluster_size, "mode", s.info.exec_mode)
-    assert 1 <= s.info.cluster_size <= 16
     assert s.info.exec_mode == 3 and s.info.kernels_per_run == 1
-    s.set_mode("resident")
-    assert s.info.exec_mode == 2 and s.info.kernels_per_run == 1
+    assert s._lib.seeds_set_mode(s._ctx, 2) == -1
     s.set_mode("graph")
     assert s.info.exec_mode == 1 and s.info.kernels_per_run == 107
     s.set_mode("grid")
@@ -246,7 +243,7 @@ def test_alternating_batch_sizes(torch_cuda, orc):
     s.close()
 
 
-@pytest.mark.parametrize("mode", ["auto", "resident"])
+@pytest.mark.parametrize("mode", ["auto"])
 @pytest.mark.parametrize("big_first", [True, False])
 def test_interleaved_contexts_same_kernel(torch_cuda, orc, big_first, mode):
     """Two contexts with the same parameters (so the same k_grid
@@ -257,8 +254,6 @@ def test_interleaved_contexts_same_kernel(torch_cuda, orc, big_first, mode):
     torch = torch_cuda
     p = configs.params("c3")
     big = configs.frames("c3", n=1)[0]
-    if mode == "resident":
-        big = np.ascontiguousarray(big[:160, :240])
     small = np.ascontiguousarray(big[:96, :128])
     ps = dict(p, n_superpixels=max(4, p["n_superpixels"] * 96 * 128 // (big.shape[0] * big.shape[1])))
     mk = lambda f, q: Seeds(f.shape[1], f.shape[0], 3, *[q[k] for k in (
