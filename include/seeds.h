@@ -299,6 +299,27 @@ seeds_status seeds_last_subsweeps(seeds_ctx *ctx, int *subsweeps_host, void *str
  * bisect a divergence against the oracle's max_subsweeps. */
 seeds_status seeds_debug_limit(seeds_ctx *ctx, int max_subsweeps);
 
+/* seeds_debug_k5 -- unit test of the block colour test K5 as the grid kernel
+ * runs it on G = 2^gshift-lane warp segments (Prop. 1, PAPER.md:553-563,
+ * reading Q18 R1; seeds_grid.cuh k5_segment), context-free.  Proposal e
+ * (0 <= e < n) moves a block out of superpixel 0 of its own tables:
+ *   H        device int32 [n][5][B]: histograms of superpixels 0..4
+ *   A        device int32 [n][5]: their sizes
+ *   bins     device int32 [n][64]: the block's pixel bins (first alpha[e])
+ *   alpha    device int32 [n]: block size, 1 .. G (threads 512) or 2G (128)
+ *   cand     device int32 [n][4]: candidate labels in W, E, N, S order, 1..4,
+ *            or -1 for no candidate in that slot
+ *   threads  512 or 128 (the two grid-kernel plans; 128 packs two pixels per
+ *            lane), narrow = 1 takes the 32-bit segment reductions the kernel
+ *            uses when N < 2^27 (valid only if every sum stays < 2^32)
+ *   acc_out  device int32 [n]: the first accepted candidate label, or -1
+ * Enqueued on `stream`; SEEDS_EINVAL for bad sizes, SEEDS_ECUDA on a launch
+ * error.  Preconditions (as in a real run): H[e][0][b] >= the block's count
+ * of bin b, A[e][0] > alpha[e], A[e][n] >= 1. */
+seeds_status seeds_debug_k5(const int32_t *H, const int32_t *A, int B, const int32_t *bins, const int32_t *alpha,
+                            const int32_t *cand, int n, int threads, int gshift, int narrow, int32_t *acc_out,
+                            void *stream);
+
 /* seeds_debug_trace -- grid mode only: enable (1) per-CTA clock64
  * stamps of every sub-sweep (slot 0 work finished, 1 barrier passed; grid mode
  * also 2 replayed, 3 staged, 4 filtered, 5 decided; 8.. detail builds), copy

@@ -1816,6 +1816,26 @@ seeds_status seeds_set_validate(seeds_ctx *ctx, int on)
     return SEEDS_OK;
 }
 
+seeds_status seeds_debug_k5(const int32_t *H, const int32_t *A, int B, const int32_t *bins, const int32_t *alpha,
+                            const int32_t *cand, int n, int threads, int gshift, int narrow, int32_t *acc_out,
+                            void *stream)
+{
+    if (!H || !A || !bins || !alpha || !cand || !acc_out || n < 0 || B < 1 || gshift < 0 || gshift > 5 ||
+        (threads != GRID_THREADS && threads != GRID_THREADS_SMALL))
+        return SEEDS_EINVAL;
+    if (n == 0) return SEEDS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int per_cta = threads / 32 * (32 >> gshift);
+    const unsigned g = (unsigned)std::min((n + per_cta - 1) / per_cta, 148 * 8);
+    if (threads == GRID_THREADS)
+        k_k5_test<GRID_THREADS><<<g, GRID_THREADS, 0, st>>>(H, A, B, bins, alpha, cand, n, gshift, narrow, acc_out);
+    else
+        k_k5_test<GRID_THREADS_SMALL><<<g, GRID_THREADS_SMALL, 0, st>>>(H, A, B, bins, alpha, cand, n, gshift, narrow,
+                                                                         acc_out);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SEEDS_OK : SEEDS_ECUDA;
+}
+
 seeds_status seeds_set_time_budget(seeds_ctx *ctx, long long budget_us)
 {
     if (!ctx || budget_us < 0 || budget_us > (1LL << 40)) return SEEDS_EINVAL;

@@ -37,6 +37,12 @@ namespace seeds {
 // latencies).
 constexpr int GRID_THREADS = 512;
 constexpr int STOP_NONE = 0x7F7F7F7F;  // "no stop" (a byte-wise memset value)
+// Acquire side of the grid barrier: 1 (default) one ld.acquire.gpu after the
+// relaxed poll, 2 a fence.acq_rel.gpu, 0 none (round 1's relaxed poll; relies
+// on every cross-CTA read bypassing L1).  DESIGN.md section 6.
+#ifndef SEEDS_BARRIER_ACQ
+#define SEEDS_BARRIER_ACQ 1
+#endif
 constexpr int GRID_THREADS_SMALL = 128;
 #ifdef SEEDS_CPS8
 constexpr int GRID_SMALL_CPS = 8;  // experiment: 8 x 128 threads per SM, 64 registers
@@ -155,11 +161,14 @@ __device__ __forceinline__ void grid_poll(unsigned *ctr, unsigned target)
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
         if (++spins > (1LL << 26)) __trap();  // a CTA that never arrives: fail loudly instead of hanging
     } while ((int)(v - target) < 0);
-#ifndef SEEDS_RELAXED_BARRIER
-    // the relaxed poll that observed every arrival + this fence = an acquire
-    // pattern: every write the other CTAs released before arriving is visible
-    // to this CTA's later (generic-proxy) reads under the PTX memory model
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#if SEEDS_BARRIER_ACQ == 1
+    // one acquire load of the counter once every arrival has been observed: it
+    // reads the last value of the release sequence of every CTA's red.release,
+    // so every write another CTA made before arriving is visible to this CTA's
+    // later reads under the PTX memory model
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+#elif SEEDS_BARRIER_ACQ == 2
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // relaxed poll + fence: the same, as a fence pattern
 #endif
 }
 __device__ __forceinline__ void grid_arrive(unsigned *ctr, unsigned &target)
@@ -384,6 +393,167 @@ __device__ __forceinline__ U128 mul_u128(U128 x, unsigned long long m)
     return U128{x.lo * m, __umul64hi(x.lo, m) + x.hi * m};
 }
 __device__ __forceinline__ bool lt_u128(U128 a, U128 b) { return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo); }
+
+// K5 on one G-lane segment of the block path (Prop. 1, R1):
+// lane si of the segment holds the bins b (pixel si) and, on 128-thread plans,
+// b2 (pixel si + G) of a block of alpha pixels (-1: none).  Equal bins are
+// merged with __match_any_sync per slot plus a cross count between the slots;
+// each distinct bin's leader gathers H[k][b], H[n][b] for the four candidates
+// and forms min(H alpha, l A) terms; segmented shuffle reductions give N_k and
+// N_n[d] (32-bit halves when `narrow`: every sum < 2^32, i.e. N < 2^27 with
+// alpha <= 32); the first candidate with N_n (A_k - alpha) > N_k A_n (exact
+// 128-bit products) is returned, or -1.  The emit path reads leader / leader2
+// and the merged counts lb / l2.  `h` supplies ldA(buf, k) and ldH(buf, k, b)
+// (GridCta in k_grid; plain tables in the k_k5_test unit kernel).
+struct SegK5 {
+    int acc, lb, l2;
+    bool leader, leader2;
+};
+template <int NT, class HA>
+__device__ __forceinline__ SegK5 k5_segment(const HA &h, int ob, bool ok, int alpha, int G, int seg, int si, int sbase,
+                                            int lane, int k, const Neigh &nb, int b, int b2, bool narrow)
+{
+    int acc = -1;
+    const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : (seg << 16) | b);
+    // second slot (warp-uniform): its bins, how many of them equal my
+    // first bin, and whether my second bin is some lane's first one
+    const bool two = NT <= 128 && __any_sync(FULL, b2 >= 0);
+    unsigned m2 = 0;
+    int x01 = 0;
+    bool in0 = false;
+    if (two) {
+        m2 = __match_any_sync(FULL, b2 < 0 ? -1 - lane : (seg << 16) | b2);
+        // only lanes j < alpha - G of a segment hold a second pixel:
+        // broadcast each one's bin to its segment
+        const unsigned segmask = G == 32 ? FULL : ((1u << G) - 1) << sbase;
+        const int jmax = (int)__reduce_max_sync(FULL, (unsigned)max(alpha - G, 0));
+#pragma unroll 1
+        for (int j = 0; j < jmax; j++) {
+            const int v1 = __shfl_sync(FULL, b2, sbase + j);
+            const bool hit = b >= 0 && v1 == b;
+            x01 += hit;
+            const unsigned hm = __ballot_sync(FULL, hit) & segmask;
+            if (si == j) in0 = hm != 0;
+        }
+    }
+    const bool leader = b >= 0 && lane == __ffs(m) - 1;
+    const bool leader2 = b2 >= 0 && !in0 && lane == __ffs(m2) - 1;
+    const int l2 = leader2 ? __popc(m2) : 0;
+    // one gather round: a lane leads the bin of its first pixel, else
+    // (if any) a bin only second pixels hold; a lane leading both
+    // takes the second one in a (rare) extra round
+    const bool use2 = leader2 && !leader;
+    const int gb = use2 ? b2 : b < 0 ? 0 : b;
+    const int lb = use2 ? l2 : __popc(m) + x01;
+    unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
+    int Ak = 1, An[4] = {1, 1, 1, 1};
+    if (ok) {
+        Ak = h.ldA(ob, k);
+        const int hk = h.ldH(ob, k, gb);
+        int hn[4];
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const int n = (nb.valid >> d & 1) ? nb.v[d] : k;
+            An[d] = h.ldA(ob, n);
+            hn[d] = h.ldH(ob, n, gb);
+        }
+        if (leader || use2) {
+            const long long al = alpha, lc = lb;
+            const long long uu = (hk - lc) * al, vv = lc * (Ak - al);
+            Nk = (unsigned long long)(uu < vv ? uu : vv);
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                const long long un = (long long)hn[d] * al, vn = lc * An[d];
+                Nn[d] = (nb.valid >> d & 1) ? (unsigned long long)(un < vn ? un : vn) : 0ull;
+            }
+        }
+    }
+    if (leader && leader2) {
+        const long long al = alpha, lc = l2;
+        const long long hk = h.ldH(ob, k, b2);
+        const long long uu = (hk - lc) * al, vv = lc * (Ak - al);
+        Nk += (unsigned long long)(uu < vv ? uu : vv);
+#pragma unroll
+        for (int d = 0; d < 4; d++)
+            if (nb.valid >> d & 1) {
+                const long long un = (long long)h.ldH(ob, nb.v[d], b2) * al, vn = lc * An[d];
+                Nn[d] += (unsigned long long)(un < vn ? un : vn);
+            }
+    }
+    if (narrow) {
+        // alpha <= 32: each sum is at most alpha A < 32 N < 2^32, so the
+        // segment reductions run on 32-bit halves (half the shuffles)
+        unsigned nk = (unsigned)Nk, nn[4];
+#pragma unroll
+        for (int d = 0; d < 4; d++) nn[d] = (unsigned)Nn[d];
+        for (int o = G >> 1; o >= 1; o >>= 1) {
+            nk += __shfl_xor_sync(FULL, nk, o);
+#pragma unroll
+            for (int d = 0; d < 4; d++) nn[d] += __shfl_xor_sync(FULL, nn[d], o);
+        }
+        Nk = nk;
+#pragma unroll
+        for (int d = 0; d < 4; d++) Nn[d] = nn[d];
+    } else {
+        for (int o = G >> 1; o >= 1; o >>= 1) {
+            Nk += __shfl_xor_sync(FULL, Nk, o);
+#pragma unroll
+            for (int d = 0; d < 4; d++) Nn[d] += __shfl_xor_sync(FULL, Nn[d], o);
+        }
+    }
+    if (ok) {
+#pragma unroll
+        for (int d = 0; d < 4; d++)
+            if (acc < 0 && (nb.valid >> d & 1) &&
+                gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
+                acc = nb.v[d];
+    }
+
+    return SegK5{acc, lb, l2, leader, leader2};
+}
+
+// Unit test of k5_segment (seeds_debug_k5): proposal e moves a block of
+// alpha[e] <= 64 pixels with bins bins[64 e ..] out of superpixel 0 of its own
+// table (H[e][5][B], A[e][5]) towards candidates cand[4 e ..] (W, E, N, S slots,
+// labels 1..4 or -1); one G-lane segment per proposal, exactly as in k_grid's
+// block path.  acc_out[e] = the accepted candidate or -1.
+struct K5Tables {
+    const int *H, *A;
+    int B;
+    __device__ __forceinline__ int ldA(int, int k) const { return A[k]; }
+    __device__ __forceinline__ int ldH(int, int k, int b) const { return H[(long long)k * B + b]; }
+};
+template <int NT>
+__global__ void __launch_bounds__(NT) k_k5_test(const int *H, const int *A, int B, const int *bins, const int *alpha,
+                                                const int *cand, int nprop, int gs, int narrow, int *acc_out)
+{
+    const int lane = threadIdx.x & 31, G = 1 << gs;
+    const int segs = 32 >> gs, seg = lane >> gs, si = lane & (G - 1), sbase = lane & ~(G - 1);
+    const int warps = gridDim.x * (NT / 32), gw = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+    for (int base = gw * segs; base < nprop; base += warps * segs) {
+        const int e = base + seg;
+        const bool ok = e < nprop;
+        Neigh nb;
+        nb.valid = 0;
+        nb.mask = 0;
+        int al = 0, b = -1, b2 = -1;
+        K5Tables h{H, A, B};
+        if (ok) {
+            h.H = H + (long long)e * 5 * B;
+            h.A = A + (long long)e * 5;
+            al = alpha[e];
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                nb.v[d] = cand[4 * e + d];
+                nb.valid |= (nb.v[d] >= 0) << d;
+            }
+            if (si < al) b = bins[64 * e + si];
+            if (NT <= 128 && si + G < al) b2 = bins[64 * e + si + G];
+        }
+        const SegK5 r = k5_segment<NT>(h, 0, ok, al, G, seg, si, sbase, lane, 0, nb, b, b2, narrow != 0);
+        if (ok && si == 0) acc_out[e] = r.acc;
+    }
+}
 
 template <typename BinT, int GAMMA, int P, int NT, int MEANS>
 __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_constant__ GridParams qp)
@@ -691,100 +861,11 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                     const int dy = div_small(si + G, rw, 1.0f / (float)rw);
                                     b2 = c.bin(xa + si + G - dy * rw, ya + dy);
                                 }
-                                const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : (seg << 16) | b);
-                                // second slot (warp-uniform): its bins, how many of them equal my
-                                // first bin, and whether my second bin is some lane's first one
-                                const bool two = NT <= 128 && __any_sync(FULL, b2 >= 0);
-                                unsigned m2 = 0;
-                                int x01 = 0;
-                                bool in0 = false;
-                                if (two) {
-                                    m2 = __match_any_sync(FULL, b2 < 0 ? -1 - lane : (seg << 16) | b2);
-                                    // only lanes j < alpha - G of a segment hold a second pixel:
-                                    // broadcast each one's bin to its segment
-                                    const unsigned segmask = G == 32 ? FULL : ((1u << G) - 1) << sbase;
-                                    const int jmax = (int)__reduce_max_sync(FULL, (unsigned)max(alpha - G, 0));
-#pragma unroll 1
-                                    for (int j = 0; j < jmax; j++) {
-                                        const int v1 = __shfl_sync(FULL, b2, sbase + j);
-                                        const bool hit = b >= 0 && v1 == b;
-                                        x01 += hit;
-                                        const unsigned hm = __ballot_sync(FULL, hit) & segmask;
-                                        if (si == j) in0 = hm != 0;
-                                    }
-                                }
-                                const bool leader = b >= 0 && lane == __ffs(m) - 1;
-                                const bool leader2 = b2 >= 0 && !in0 && lane == __ffs(m2) - 1;
-                                const int l2 = leader2 ? __popc(m2) : 0;
-                                // one gather round: a lane leads the bin of its first pixel, else
-                                // (if any) a bin only second pixels hold; a lane leading both
-                                // takes the second one in a (rare) extra round
-                                const bool use2 = leader2 && !leader;
-                                const int gb = use2 ? b2 : b < 0 ? 0 : b;
-                                const int lb = use2 ? l2 : __popc(m) + x01;
-                                unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
-                                int Ak = 1, An[4] = {1, 1, 1, 1};
-                                if (ok) {
-                                    Ak = c.ldA(ob, k);
-                                    const int hk = c.ldH(ob, k, gb);
-                                    int hn[4];
-#pragma unroll
-                                    for (int d = 0; d < 4; d++) {
-                                        const int n = (nb.valid >> d & 1) ? nb.v[d] : k;
-                                        An[d] = c.ldA(ob, n);
-                                        hn[d] = c.ldH(ob, n, gb);
-                                    }
-                                    if (leader || use2) {
-                                        const long long al = alpha, lc = lb;
-                                        const long long uu = (hk - lc) * al, vv = lc * (Ak - al);
-                                        Nk = (unsigned long long)(uu < vv ? uu : vv);
-#pragma unroll
-                                        for (int d = 0; d < 4; d++) {
-                                            const long long un = (long long)hn[d] * al, vn = lc * An[d];
-                                            Nn[d] = (nb.valid >> d & 1) ? (unsigned long long)(un < vn ? un : vn) : 0ull;
-                                        }
-                                    }
-                                }
-                                if (leader && leader2) {
-                                    const long long al = alpha, lc = l2;
-                                    const long long hk = c.ldH(ob, k, b2);
-                                    const long long uu = (hk - lc) * al, vv = lc * (Ak - al);
-                                    Nk += (unsigned long long)(uu < vv ? uu : vv);
-#pragma unroll
-                                    for (int d = 0; d < 4; d++)
-                                        if (nb.valid >> d & 1) {
-                                            const long long un = (long long)c.ldH(ob, nb.v[d], b2) * al, vn = lc * An[d];
-                                            Nn[d] += (unsigned long long)(un < vn ? un : vn);
-                                        }
-                                }
-                                if (q.N < (1LL << 27)) {
-                                    // alpha <= 32: each sum is at most alpha A < 32 N < 2^32, so the
-                                    // segment reductions run on 32-bit halves (half the shuffles)
-                                    unsigned nk = (unsigned)Nk, nn[4];
-#pragma unroll
-                                    for (int d = 0; d < 4; d++) nn[d] = (unsigned)Nn[d];
-                                    for (int o = G >> 1; o >= 1; o >>= 1) {
-                                        nk += __shfl_xor_sync(FULL, nk, o);
-#pragma unroll
-                                        for (int d = 0; d < 4; d++) nn[d] += __shfl_xor_sync(FULL, nn[d], o);
-                                    }
-                                    Nk = nk;
-#pragma unroll
-                                    for (int d = 0; d < 4; d++) Nn[d] = nn[d];
-                                } else {
-                                    for (int o = G >> 1; o >= 1; o >>= 1) {
-                                        Nk += __shfl_xor_sync(FULL, Nk, o);
-#pragma unroll
-                                        for (int d = 0; d < 4; d++) Nn[d] += __shfl_xor_sync(FULL, Nn[d], o);
-                                    }
-                                }
-                                if (ok) {
-#pragma unroll
-                                    for (int d = 0; d < 4; d++)
-                                        if (acc < 0 && (nb.valid >> d & 1) &&
-                                            gt_prod(Nn[d], (unsigned long long)(Ak - alpha), Nk, (unsigned long long)An[d]))
-                                            acc = nb.v[d];
-                                }
+                                const SegK5 r5 = k5_segment<NT>(c, ob, ok, alpha, G, seg, si, sbase, lane, k, nb, b, b2,
+                                                                q.N < (1LL << 27));
+                                acc = r5.acc;
+                                const bool leader = r5.leader, leader2 = r5.leader2;
+                                const int lb = r5.lb, l2 = r5.l2;
                                 count_moves(acc >= 0 && si == 0);
                                 const int nrec = acc >= 0 ? (int)leader + (int)leader2 : 0;
                                 const int slot = append_warp(rcount(ob), nrec);

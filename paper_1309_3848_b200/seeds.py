@@ -27,7 +27,7 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics", "seeds_set_colour_space",
            "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks", "seeds_set_compactness",
            "seeds_set_edge_prior", "seeds_batch_host_warm", "seeds_validate_labels", "seeds_set_validate",
-           "seeds_set_time_budget", "seeds_last_subsweeps"]
+           "seeds_set_time_budget", "seeds_last_subsweeps", "seeds_debug_k5"]
 
 
 class _Metrics(ctypes.Structure):
@@ -84,6 +84,7 @@ def load(path: str = LIB_PATH):
         "seeds_set_validate": ([vp, i], i),
         "seeds_set_time_budget": ([vp, ctypes.c_longlong], i),
         "seeds_last_subsweeps": ([vp, vp, vp], i),
+        "seeds_debug_k5": ([vp, vp, i, vp, vp, vp, i, i, i, i, vp, vp], i),
         "seeds_rgb_to_lab": ([vp, vp, ctypes.c_longlong, vp, vp], i),
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
@@ -116,6 +117,26 @@ def _stream_ptr(stream) -> int | None:
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+def debug_k5(H, A, bins, alpha, cand, threads: int, gshift: int, narrow: bool, stream=None):
+    """Unit test entry of the block colour test K5 (include/seeds.h
+    seeds_debug_k5): int32 CUDA tensors H (n, 5, B), A (n, 5), bins (n, 64),
+    alpha (n,), cand (n, 4) -> int32 CUDA tensor (n,) of accepted labels / -1."""
+    import torch
+    lib = load()
+    ts = (H, A, bins, alpha, cand)
+    if not all(isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int32 and t.is_contiguous() for t in ts):
+        raise TypeError("every table must be a contiguous int32 CUDA tensor")
+    n, _, B = H.shape
+    if A.shape != (n, 5) or bins.shape != (n, 64) or alpha.shape != (n,) or cand.shape != (n, 4):
+        raise ValueError("table shapes")
+    out = torch.full((n,), -2, dtype=torch.int32, device=H.device)
+    st = lib.seeds_debug_k5(H.data_ptr(), A.data_ptr(), B, bins.data_ptr(), alpha.data_ptr(), cand.data_ptr(), n,
+                            threads, gshift, int(bool(narrow)), out.data_ptr(), _stream_ptr(stream))
+    if st != 0:
+        raise SeedsError(st)
+    return out
 
 
 @dataclass
