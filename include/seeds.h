@@ -326,7 +326,9 @@ seeds_status seeds_debug_k5(const int32_t *H, const int32_t *A, int B, const int
  * them to host_out[min(cap, ctas*(subsweeps+4)*16)] (int64, layout [cta][phase][16],
  * ctas = 4 #SM), or disable (0) and free the buffer.
  * Synchronises the device when host_out is given.  Diagnostic; not part of
- * the hot path. */
+ * the hot path: only a library built with -DSEEDS_TRACE records stamps
+ * (scripts/build_trace.sh); the default build returns SEEDS_ESTATE for
+ * enable = 1. */
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap);
 
 /* seeds_stats -- accepted moves per sub-sweep of frame `frame` of the last

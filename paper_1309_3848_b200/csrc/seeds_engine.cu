@@ -1626,6 +1626,12 @@ seeds_status seeds_set_mode(seeds_ctx *ctx, int mode)
 seeds_status seeds_debug_trace(seeds_ctx *ctx, int enable, long long *host_out, int cap)
 {
     if (!ctx) return SEEDS_EINVAL;
+#ifndef SEEDS_TRACE
+    if (enable) {
+        snprintf(ctx->err, sizeof ctx->err, "built without -DSEEDS_TRACE (scripts/build_trace.sh builds a tracing library)");
+        return SEEDS_ESTATE;
+    }
+#endif
     const size_t n = (size_t)(4 * ctx->n_sm) * (ctx->S + 4) * 16;
     if (enable && !ctx->d_trace) {
         CK(cudaMalloc(&ctx->d_trace, n * sizeof(long long)));

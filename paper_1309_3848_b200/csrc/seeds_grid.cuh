@@ -574,7 +574,9 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
 
     for (int i = tid; i < q.ntab * TW; i += NT) c.tabs[i] = 0;
     if (tid < 4) c.misc[tid] = 0;
-    if (tid == 8) c.misc[8] = STOP_NONE;  // sub-sweeps after which the anytime budget stops the run
+    // misc[8]: the sub-sweeps after which the run stops -- seeds_debug_limit's
+    // count, lowered by the anytime budget at a barrier (one shared load per check)
+    if (tid == 8) c.misc[8] = q.limit >= 0 ? min(q.limit, STOP_NONE) : STOP_NONE;
     if (tid < 8) c.rem[tid] = c_removable[tid];
     const int ntl = blockIdx.x < q.ntiles ? (q.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // tiles of this CTA
     for (int i = tid; i < ntl; i += NT) c.tiles[i] = q.tiles[blockIdx.x + (long long)i * gridDim.x];
@@ -644,7 +646,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
             if (q.budget_ns > 0) {
                 int v;
                 asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(q.stop) : "memory");
-                c.misc[8] = v;
+                c.misc[8] = min(c.misc[8], v);
             }
         }
         __syncthreads();
@@ -652,13 +654,18 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     if (!q.band) boundary(0);
 
     int s = 0;
-    auto stopped = [&]() { return (q.limit >= 0 && s >= q.limit) || s >= c.misc[8]; };
+    auto stopped = [&]() { return s >= c.misc[8]; };
     // debug trace [cta][phase][8]: 0 work done, 1 barrier passed, 2 replayed,
     // 3 last tile staged, 4 last tile filtered, 5 last tile decided
     // slots 6, 7, 15: per sub-sweep sums over the CTA's tiles of the staging
     // wait, the filter and the decide phases
+    // (compiled in only with -DSEEDS_TRACE: the production kernel carries no
+    // per-phase bookkeeping)
+#ifdef SEEDS_TRACE
     long long t_last = 0, acc_w = 0, acc_f = 0, acc_d = 0;
+#endif
     auto stamp = [&](int phase, int which) {
+#ifdef SEEDS_TRACE
         if (!q.trace || tid != 0) return;
         const long long now = clk64();
         long long *row = q.trace + ((long long)blockIdx.x * (q.S + 4) + phase) * 16;
@@ -674,6 +681,10 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
             row[15] = acc_d;
             acc_w = acc_f = acc_d = 0;
         }
+#else
+        (void)phase;
+        (void)which;
+#endif
     };
     stamp(0, 1);
     auto count_moves = [&](bool moved) {

@@ -14,7 +14,9 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libseeds.so")
+# SEEDS_LIB: another build of the same library (A/B measurements, the tracing
+# build of scripts/build_trace.sh); the default is the in-tree libseeds.so
+LIB_PATH = os.environ.get("SEEDS_LIB") or os.path.join(_PKG, "libseeds.so")
 
 _STATUS = {0: "ok", -1: "invalid argument", -2: "out of memory", -3: "CUDA error",
            -4: "NCCL error", -5: "invalid state", -6: "problem exceeds an integer width"}

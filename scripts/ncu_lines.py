@@ -1,18 +1,32 @@
-"""Aggregate an ncu 'source --print-source cuda,sass' CSV per CUDA source line."""
-import csv, sys
-rows = list(csv.reader(open(sys.argv[1])))
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-hdr = None; cur = None; out = []
+"""Aggregate an ncu source page (cuda,sass) by CUDA source line: warp-stall
+samples, instructions executed; usage: ncu_lines.py report.ncu-rep [top]"""
+import csv
+import io
+import subprocess
+import sys
+
+rep = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr = None
+lines = []
+fname = ""
 for r in rows:
-    if len(r) == 2 and r[0] in ('File Path', 'File Name'): cur = r[1].split('/')[-1]; continue
-    if r and r[0] == 'Line No': hdr = r; continue
-    if hdr is None or len(r) < len(hdr) or r[2] != '-': continue
-    d = dict(zip(hdr[4:], r[4:]))
-    stalls = {h: int(v) for h, v in zip(hdr[32:49], r[32:49]) if v.isdigit() and int(v) > 0}
-    try: out.append((int(r[4]), int(r[7]), cur, r[0], r[1].strip()[:90], stalls))
-    except ValueError: pass
-ts = sum(o[0] for o in out); ti = sum(o[1] for o in out)
-print("samples", ts, "warp-instructions", ti)
-for o in sorted(out, key=lambda o: -o[0])[:top]:
-    st = ' '.join(f"{k[6:]}={v}" for k, v in sorted(o[5].items(), key=lambda kv: -kv[1])[:3])
-    print(f"{o[0]:>6} {100*o[0]/ts:5.1f}% inst {o[1]:>9} {o[2]}:{o[3]} {o[4]} | {st}")
+    if r and r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+    elif r and r[0] == "Line No":
+        hdr = r
+    elif hdr and r and r[0] not in ("", "Function Name"):
+        d = dict(zip(hdr[:2] + ["addr", "sass"] + hdr[4:], r))
+        try:
+            lines.append((int(d["Warp Stall Sampling (All Samples)"]), int(d["Instructions Executed"] or 0),
+                          fname, int(r[0]), r[1].strip()[:90]))
+        except (ValueError, KeyError):
+            pass
+tot = sum(x[0] for x in lines) or 1
+lines.sort(reverse=True)
+print(f"total samples {tot}")
+for s, ins, f, ln, src in lines[:top]:
+    print(f"{100 * s / tot:5.1f}% {s:7d} {ins:10d} {f}:{ln:<5d} {src}")
