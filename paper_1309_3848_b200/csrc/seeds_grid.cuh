@@ -330,6 +330,16 @@ struct GridCta {
     {
         return __ldcg((buf ? Hf1 : Hf0) + (long long)k * q.B + b);
     }
+    // the same, issued only when p (ldcg_if): no L2 request for an empty slot
+    __device__ __forceinline__ int ldH_if(bool p, int buf, int k, int b) const
+    {
+        return ldcg_if(p, (buf ? Hf1 : Hf0) + (long long)k * q.B + b);
+    }
+    __device__ __forceinline__ int ldA_if(bool p, int buf, int k) const
+    {
+        if (q.acache) return sA[k];
+        return ldcg_if(p, (buf ? Af1 : Af0) + k);
+    }
     __device__ __forceinline__ void set(int x, int y, int v) const
     {
         glab[(long long)(y + 2) * q.lpitch + x + 2] = (uint16_t)v;
@@ -449,13 +459,13 @@ __device__ __forceinline__ SegK5 k5_segment(const HA &h, int ob, bool ok, int al
     int Ak = 1, An[4] = {1, 1, 1, 1};
     if (ok) {
         Ak = h.ldA(ob, k);
-        const int hk = h.ldH(ob, k, gb);
+        const int hk = h.ldH_if(leader || use2, ob, k, gb);
         int hn[4];
 #pragma unroll
         for (int d = 0; d < 4; d++) {
             const int n = (nb.valid >> d & 1) ? nb.v[d] : k;
-            An[d] = h.ldA(ob, n);
-            hn[d] = h.ldH(ob, n, gb);
+            An[d] = h.ldA_if(nb.valid >> d & 1, ob, n);
+            hn[d] = h.ldH_if((nb.valid >> d & 1) && (leader || use2), ob, n, gb);
         }
         if (leader || use2) {
             const long long al = alpha, lc = lb;
@@ -522,6 +532,8 @@ struct K5Tables {
     int B;
     __device__ __forceinline__ int ldA(int, int k) const { return A[k]; }
     __device__ __forceinline__ int ldH(int, int k, int b) const { return H[(long long)k * B + b]; }
+    __device__ __forceinline__ int ldA_if(bool p, int, int k) const { return p ? A[k] : 0; }
+    __device__ __forceinline__ int ldH_if(bool p, int, int k, int b) const { return p ? H[(long long)k * B + b] : 0; }
 };
 template <int NT>
 __global__ void __launch_bounds__(NT) k_k5_test(const int *H, const int *A, int B, const int *bins, const int *alpha,
@@ -915,7 +927,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                 const long long Ak = c.ldA(ob, k);
                                 long long An[4];
 #pragma unroll
-                                for (int d = 0; d < 4; d++) An[d] = c.ldA(ob, (nb.valid >> d & 1) ? nb.v[d] : k);
+                                for (int d = 0; d < 4; d++) An[d] = c.ldA_if(nb.valid >> d & 1, ob, (nb.valid >> d & 1) ? nb.v[d] : k);
                                 for (int i0 = wi * 32; i0 < alpha; i0 += GT) {
                                     const int i = i0 + lane;
                                     int b = -1;
@@ -937,7 +949,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                     const long long hk = c.ldH(ob, k, b);
                                     long long hn[4];
 #pragma unroll
-                                    for (int d = 0; d < 4; d++) hn[d] = c.ldH(ob, (nb.valid >> d & 1) ? nb.v[d] : k, b);
+                                    for (int d = 0; d < 4; d++) hn[d] = c.ldH_if(nb.valid >> d & 1, ob, (nb.valid >> d & 1) ? nb.v[d] : k, b);
                                     const long long u = (hk - lc) * alpha, v = lc * (Ak - alpha);
                                     Nk += (unsigned long long)(u < v ? u : v);
 #pragma unroll
@@ -1021,7 +1033,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                 const long long Ak = c.ldA(ob, k);
                                 long long An[4];
 #pragma unroll
-                                for (int d = 0; d < 4; d++) An[d] = c.ldA(ob, (nb.valid >> d & 1) ? nb.v[d] : k);
+                                for (int d = 0; d < 4; d++) An[d] = c.ldA_if(nb.valid >> d & 1, ob, (nb.valid >> d & 1) ? nb.v[d] : k);
                                 for (int i0 = 0; i0 < alpha; i0 += 32) {
                                     const int i = i0 + lane;
                                     int b = -1;
@@ -1043,7 +1055,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                     const long long hk = c.ldH(ob, k, b);
                                     long long hn[4];
 #pragma unroll
-                                    for (int d = 0; d < 4; d++) hn[d] = c.ldH(ob, (nb.valid >> d & 1) ? nb.v[d] : k, b);
+                                    for (int d = 0; d < 4; d++) hn[d] = c.ldH_if(nb.valid >> d & 1, ob, (nb.valid >> d & 1) ? nb.v[d] : k, b);
                                     const long long u = (hk - lc) * alpha, v = lc * (Ak - alpha);
                                     Nk += (unsigned long long)(u < v ? u : v);
 #pragma unroll
@@ -1333,8 +1345,8 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                     for (int d = 0; d < 4; d++) {
                         u.v[d] = nb.v[d];
                         const int n = (nb.valid >> d & 1) ? nb.v[d] : u.k;
-                        u.hn[d] = c.ldH(ob, n, u.j);
-                        u.An[d] = c.ldA(ob, n);
+                        u.hn[d] = c.ldH_if(nb.valid >> d & 1, ob, n, u.j);
+                        u.An[d] = c.ldA_if(nb.valid >> d & 1, ob, n);
                     }
                 };
                 // Prop. 2 for every candidate (bit d: candidate d passes; reads only

@@ -121,6 +121,19 @@ __device__ __forceinline__ Neigh neighbourhood(const uint16_t *m, int w, int h, 
 }
 
 // a*b > c*d for non-negative 64-bit operands, exactly (128-bit products).
+// An L2-coherent gather issued only when p holds (a predicated ld.global.cg;
+// 0 otherwise): the candidate slots without a candidate and the bin slots a
+// small block does not use send no request to L2, while every issued load
+// still goes out back to back (no branch between them).
+__device__ __forceinline__ int ldcg_if(bool p, const int *a)
+{
+    int v = 0;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cg.s32 %0, [%1];\n\t}"
+        : "+r"(v)
+        : "l"(a), "r"((unsigned)p));
+    return v;
+}
+
 __device__ __forceinline__ bool gt_prod(unsigned long long a, unsigned long long b, unsigned long long c,
                                         unsigned long long d)
 {
@@ -841,13 +854,13 @@ __device__ __forceinline__ int block_t4(const Ctx &c, int ob, int k, const Neigh
     const long long Ak = c.ldA(ob, k);
     long long An[4], hk[4], hn[4][4];
 #pragma unroll
-    for (int d = 0; d < 4; d++) An[d] = c.ldA(ob, nn[d]);
+    for (int d = 0; d < 4; d++) An[d] = c.ldA_if(nb.valid >> d & 1, ob, nn[d]);
 #pragma unroll
     for (int i = 0; i < 4; i++) {
         const int b = bv[i] < 0 ? 0 : bv[i];
-        hk[i] = c.ldH(ob, k, b);
+        hk[i] = c.ldH_if(cnt[i] != 0, ob, k, b);
 #pragma unroll
-        for (int d = 0; d < 4; d++) hn[i][d] = c.ldH(ob, nn[d], b);
+        for (int d = 0; d < 4; d++) hn[i][d] = c.ldH_if(cnt[i] != 0 && (nb.valid >> d & 1), ob, nn[d], b);
     }
     unsigned long long Nk = 0, Nn[4] = {0, 0, 0, 0};
     const long long al = alpha;
