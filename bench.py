@@ -443,6 +443,68 @@ def cpu_baseline(name, budget_s=10.0, means_iters=0, colour="rgb", compact=False
             "single_thread": single}
 
 
+def cpu_info():
+    """Host CPU model and core count (the cpu_baseline
+    states the host it ran on)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "affinity_cores": host_cores()}
+
+
+def measure_extra(name, steps, flush, stream, torch):
+    """One more config measured in the same process (the `extra` map of the
+    bench line): device-resident steps timed with CUDA
+    events on the launching stream, L2 flushed between steps, per-launch
+    profile events for the roofline, traffic from the committed ncu capture."""
+    wl = Workload(name, 0, 1)
+    s = wl.make_context()
+    info = s.info
+    wl.setup(torch, s)
+    for _ in range(3):
+        wl.step(s, stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(i & 0xFF)
+        ev[i][0].record(stream)
+        wl.step(s, stream)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    s.profile(True)
+    prof = None
+    for i in range(min(steps, 5)):
+        flush.fill_(i & 0xFF)
+        wl.step(s, stream)
+        prof = s.profile_collect(stream=stream)
+    s.profile(False)
+    ms_launch, nl = prof["frame"]
+    avg_us = 1e3 * ms_launch / max(1, nl)
+    ab = wl.algorithmic_bytes(info) / len(wl.groups)
+    hbm, hbm_src = peaks()
+    achieved = ab / (avg_us / 1e6) / 1e9
+    traffic = None
+    try:
+        ent = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(f"{name}/grid", {}).get("frame")
+        traffic = ent.get("dram_bytes") if isinstance(ent, dict) else ent
+    except Exception:
+        pass
+    out = {"workload": wl.describe(info), "value": wl.frames_per_step * wl.N / (ms / 1e3) / 1e6, "unit": UNIT,
+           "ms_per_step": ms, "steps": steps,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                        "traffic": traffic, "kernel": "frame", "avg_launch_us": avg_us,
+                        "algorithmic_bytes_per_launch": ab, "peak_source": hbm_src},
+           "gpu_launches": info.kernels_per_run * len(wl.groups) * steps}
+    s.close()
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -488,8 +550,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic",
             "config": {"workload": f"{name}: {note} per step, oracle COL schedule"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle",
-                             "sample": f"{args.steps} steps, each {note}"},
+            "cpu_baseline": dict({"value": v, "unit": UNIT, "cores": workers, "kind": "oracle",
+                                  "sample": f"{args.steps} steps, each {note}"}, **cpu_info()),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -511,6 +573,9 @@ def main():
                     help="lab: the 8-bit CIELAB pre-pass inside the timed run (reading M3)")
     ap.add_argument("--compact", action="store_true", help="the compactness prior at the pixel level (reading M5)")
     ap.add_argument("--edge", type=int, default=0, help="the edge prior with this colour threshold (reading M6)")
+    ap.add_argument("--extra", default="auto",
+                    help="comma-separated configs measured in the same run into the line's `extra` map "
+                         "(auto: c3,c5 on a default one-GPU c2 run; none: off)")
     ap.add_argument("--means-iters", type=int, default=0,
                     help="SPM means post-processing: the last M pixel iterations use the means test (reading M1)")
     args = ap.parse_args()
@@ -701,9 +766,17 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
         }
+        extra = args.extra
+        if extra == "auto":
+            extra = "c3,c5" if (name == "c2" and world == 1 and default_path and args.mode == "auto") else "none"
+        if extra != "none":
+            line["extra"] = {}
+            for x in extra.split(","):
+                line["extra"][x] = measure_extra(x, min(args.steps, 10), flush, stream, torch)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(name, args.cpu_budget, args.means_iters, args.colour, args.compact,
                                                 args.edge)
+            line["cpu_baseline"].update(cpu_info())
         out = json.dumps(line)
         print(out)
         if args.json_out:

@@ -274,6 +274,16 @@ typedef struct {
 seeds_status seeds_metrics(seeds_ctx *ctx, const int32_t *labels, const int32_t *gt, int n_segments, int eps,
                            seeds_metrics_t *out, void *stream);
 
+/* seeds_debug_block_hist -- out != NULL: every later cold grid-mode run also
+ * writes the histograms of the top-level blocks (level L_eff - 1: the four
+ * blocks composing each superpixel) that its seed counted
+ * in shared memory before summing them into H, to out (device int32,
+ * [n_frames][(grid_x >> (L_eff-1)) * (grid_y >> (L_eff-1)) blocks, row-major]
+ * [B]; cells of empty (block, bin) pairs are not written -- zero the buffer
+ * first).  For pin P1b on the GPU (tests/test_gpu_seed.py).  NULL turns it off.
+ * SEEDS_EINVAL for L_eff = 0 or a row-band ctx; SEEDS_ESTATE in graph mode. */
+seeds_status seeds_debug_block_hist(seeds_ctx *ctx, int32_t *out);
+
 /* seeds_set_time_budget -- anytime termination (S5.4: the
  * hill climbing "can be stopped at any time", with "a time budget on the
  * fly").  budget_us > 0: every later run stops at the first sub-sweep boundary

@@ -40,11 +40,12 @@ struct GraphKey {
     int blk_lo = 0, blk_hi = 0;
     int compact = 0, edge_tau = 0;
     long long budget = 0;
+    const void *dbg_blk = nullptr;
     bool operator==(const GraphKey &o) const
     {
         return img == o.img && init == o.init && out == o.out && nf == o.nf && limit == o.limit && prof == o.prof &&
                mode == o.mode && miters == o.miters && colour == o.colour && blk_lo == o.blk_lo && blk_hi == o.blk_hi &&
-               compact == o.compact && edge_tau == o.edge_tau && budget == o.budget;
+               compact == o.compact && edge_tau == o.edge_tau && budget == o.budget && dbg_blk == o.dbg_blk;
     }
 };
 
@@ -182,6 +183,7 @@ struct seeds_ctx {
     // anytime termination (seeds_set_time_budget): d_err[1] = stop boundary, d_err[2] = sub-sweeps run
     long long budget_ns = 0;
     bool last_dynamic = false;
+    int *dbg_blk = nullptr;  // seeds_debug_block_hist: caller's buffer for the top-level block histograms
 };
 
 
@@ -606,7 +608,7 @@ static bool default_levels(const seeds_ctx *c) { return c->blk_lo == 0 && c->blk
 // the extended pixel path (k_grid<..., 1>): means post-processing or the compactness prior
 static bool ext_pixel(const seeds_ctx *c) { return c->miters > 0 || c->compact || c->edge_tau > 0; }
 // options that only grid mode implements
-static bool grid_only(const seeds_ctx *c) { return ext_pixel(c) || !default_levels(c) || c->budget_ns > 0; }
+static bool grid_only(const seeds_ctx *c) { return ext_pixel(c) || !default_levels(c) || c->budget_ns > 0 || c->dbg_blk; }
 
 static int resolved_mode(seeds_ctx *c, int nf)
 {
@@ -1022,7 +1024,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         }
         q.tiles = c->d_tiles;
         q.rec = c->d_grec;
-        if (!res) {  // padded bin planes for the TMA
+        {  // padded bin planes: written by the seed kernel, staged by the TMA (or copied once into resident bins)
             q.bpitch = c->bb == 1 ? (c->W + 15) / 16 * 16 : (c->W + 7) / 8 * 8;
             q.binsp_fs = (long long)q.bpitch * c->H;
             const size_t bytes = (size_t)c->cap_frames * q.binsp_fs * c->bb;
@@ -1078,10 +1080,11 @@ static cudaError_t launch_grid_nt(seeds_ctx *ctx, const GridParams &q, cudaStrea
 static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
                                  cudaStream_t st)
 {
-    for (int i = 0; i < 2; i++) {
-        CK(cudaMemsetAsync(ctx->d_H[i], 0, (size_t)nf * ctx->H_fs * 4, st));
-        CK(cudaMemsetAsync(ctx->d_A[i], 0, (size_t)nf * ctx->Afs * 4, st));
-    }
+    if (init)  // a cold seed writes every histogram row and size itself (k_seed_cells)
+        for (int i = 0; i < 2; i++) {
+            CK(cudaMemsetAsync(ctx->d_H[i], 0, (size_t)nf * ctx->H_fs * 4, st));
+            CK(cudaMemsetAsync(ctx->d_A[i], 0, (size_t)nf * ctx->Afs * 4, st));
+        }
     if (ctx->miters > 0)
         for (int i = 0; i < 2; i++) CK(cudaMemsetAsync(ctx->d_S[i], 0, (size_t)nf * ctx->Afs * 4 * sizeof(long long), st));
     if (ctx->compact) CK(cudaMemsetAsync(ctx->d_csum, 0, (size_t)nf * ctx->Afs * 4 * sizeof(long long), st));
@@ -1113,11 +1116,24 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     q.moves = ctx->d_moves;
     q.sync = ctx->d_sync;
     q.trace = ctx->d_trace;
+    q.dbg_blk = ctx->dbg_blk;
+    q.dbg_ntop = ctx->L > 0 ? (long long)(ctx->GX >> (ctx->L - 1)) * (ctx->GY >> (ctx->L - 1)) : 0;
     q.budget_ns = ctx->budget_ns;
     q.stop = ctx->d_err + 1;
     q.done = ctx->d_err + 2;
     CK(cudaMemsetAsync(ctx->d_err + 1, 0x7F, 4, st));  // STOP_NONE
     ctx->ev_used = 0;
+    CK(prof_begin(ctx, st, SEEDS_KIND_SEED));
+    {
+        const dim3 g((unsigned)ctx->K, (unsigned)nf);
+        const size_t sm = init ? 0 : (size_t)4 * ctx->B * sizeof(int);
+        if (ctx->bb == 1)
+            k_seed_cells<uint8_t><<<g, 256, sm, st>>>(q);
+        else
+            k_seed_cells<uint16_t><<<g, 256, sm, st>>>(q);
+        CK(cudaGetLastError());
+    }
+    CK(prof_end(ctx, st));
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
     cudaError_t e;
     if (ctx->grid_nt == GRID_THREADS)
@@ -1126,6 +1142,13 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
         e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
                            : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid launch");
+    CK(prof_end(ctx, st));
+    CK(prof_begin(ctx, st, SEEDS_KIND_EMIT));
+    {
+        k_emit_planes<<<(unsigned)(nf * ctx->H), ctx->W >= 256 ? 256 : 128, 0, st>>>(ctx->d_labp, ctx->labp_fs, ctx->lpitch,
+                                                                                   ctx->W, ctx->H, out);
+        CK(cudaGetLastError());
+    }
     CK(prof_end(ctx, st));
     const bool blocks = init == nullptr && ctx->L > 0;
     const int total = (blocks ? 4 * block_levels_run(ctx) * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
@@ -1287,6 +1310,7 @@ static seeds_status run(seeds_ctx *ctx, const uint8_t *img, const int32_t *init,
     key.compact = ctx->compact;
     key.edge_tau = ctx->edge_tau;
     key.budget = ctx->budget_ns;
+    key.dbg_blk = ctx->dbg_blk;
     key.colour = ctx->colour;
     seeds_ctx::GraphEntry *hit = nullptr;
     for (auto &g : ctx->graphs)
@@ -1376,6 +1400,9 @@ seeds_status seeds_create(int width, int height, int channels, int n_superpixels
     // shared-memory opt-in of the block kernels (set outside any graph capture)
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block_large<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block_large<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    // the seed kernel's four block histograms: 4 B ints, up to 64 KB (B <= 4096)
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_seed_cells<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_seed_cells<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, ctx->dev);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_err, 16);
@@ -1534,7 +1561,7 @@ seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *o)
         o->grid_ctas = ok ? m->grid_G : 0;
         o->grid_tiles = ok ? m->gp.ntiles : 0;
     }
-    o->kernels_per_run = (o->exec_mode == SEEDS_MODE_GRAPH ? ctx->kernels_per_run : 1) +
+    o->kernels_per_run = (o->exec_mode == SEEDS_MODE_GRAPH ? ctx->kernels_per_run : 3) +  // grid: seed, k_grid, emit
                          (ctx->colour == SEEDS_COLOUR_LAB ? 1 : 0);  // + the LAB pre-pass
     o->workspace_bytes_per_frame = (size_t)ctx->N * (ctx->bb + 2) +
                                    (size_t)(((long long)ctx->GX * ctx->GY + 7) / 8 * 8) * 4 +
@@ -1840,6 +1867,18 @@ seeds_status seeds_debug_k5(const int32_t *H, const int32_t *A, int B, const int
                                                                          acc_out);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? SEEDS_OK : SEEDS_ECUDA;
+}
+
+seeds_status seeds_debug_block_hist(seeds_ctx *ctx, int32_t *out)
+{
+    if (!ctx) return SEEDS_EINVAL;
+    if (out && (ctx->L < 1 || ctx->banded)) return SEEDS_EINVAL;
+    if (out && ctx->mode == SEEDS_MODE_GRAPH) {
+        snprintf(ctx->err, sizeof ctx->err, "the block-histogram output is written by the grid-mode seed");
+        return SEEDS_ESTATE;
+    }
+    ctx->dbg_blk = out;
+    return SEEDS_OK;
 }
 
 seeds_status seeds_set_time_budget(seeds_ctx *ctx, long long budget_us)

@@ -131,6 +131,10 @@ struct GridParams {
     // sub-sweeps run.
     long long budget_ns;
     int *stop, *done;
+    // debug (seeds_debug_block_hist): the cold seed's top-level block histograms,
+    // [frame][dbg_ntop = (GX >> (L-1)) (GY >> (L-1)) blocks, row-major][B], or nullptr
+    int *dbg_blk;
+    long long dbg_ntop;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer()
@@ -606,42 +610,17 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     };
     __syncthreads();
 
-    // ---- seed: bins (reading Q1), labels (grid, or warm
-    // start, reading O9) and the histogram counts (Eq. 6) into both buffers,
-    // warp-aggregated on the (label, bin) key
-    for (int ti = 0; ti < (q.band ? 0 : ntl); ti++) {
-        const GridTile t = c.tiles[ti];
-        const int tw = t.X1 - t.X0;
-        BinT *tb = q.bins_res ? c.sbins + t.boff : static_cast<BinT *>(q.binsp) + (long long)t.f * q.binsp_fs;
-        uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
-        int *H0 = q.Hb[0] + (long long)t.f * q.H_fs, *H1 = q.Hb[1] + (long long)t.f * q.H_fs;
-        int *A0 = q.Ab[0] + (long long)t.f * q.A_fs, *A1 = q.Ab[1] + (long long)t.f * q.A_fs;
-        const long long fN = (long long)t.f * q.N;
-        for (int y = t.Y0 + wid; y < t.Y1; y += NW) {
-            const int gy = (q.byof[y] >> q.L) * q.nx;
-            for (int x0 = t.X0; x0 < t.X1; x0 += 32) {
-                const int x = x0 + lane;
-                int key = -1, k = -1, b = 0;
-                if (x < t.X1) {
-                    const uint8_t *v = q.img + (fN + (long long)y * W + x) * q.C;
-                    for (int ch = 0; ch < q.C; ch++) b = b * q.bpc + (((int)v[ch] * q.bpc) >> 8);
-                    if (q.bins_res) tb[(y - t.Y0) * tw + x - t.X0] = (BinT)b;
-                    else tb[(long long)y * q.bpitch + x] = (BinT)b;
-                    k = q.init ? checked_label(q.init[fN + (long long)y * W + x], q.K, q.err) : gy + (q.bxof[x] >> q.L);
-                    gl[(long long)(y + 2) * q.lpitch + x + 2] = (uint16_t)k;
-                    key = k * B + b;
-                }
-                unsigned m = __match_any_sync(FULL, key);
-                if (x < t.X1 && lane == __ffs(m) - 1) {
-                    atomicAdd(H0 + key, __popc(m));
-                    atomicAdd(H1 + key, __popc(m));
-                }
-                m = __match_any_sync(FULL, k);
-                if (x < t.X1 && lane == __ffs(m) - 1) {
-                    atomicAdd(A0 + k, __popc(m));
-                    atomicAdd(A1 + k, __popc(m));
-                }
-            }
+    // ---- the seed ran before this launch (k_seed_cells): bins, labels and the
+    // histograms are in global memory.  Plans that keep their tiles' bins in
+    // shared memory for the whole run copy them in once (coalesced rows).
+    if (q.bins_res && !q.band) {
+        for (int ti = 0; ti < ntl; ti++) {
+            const GridTile t = c.tiles[ti];
+            const int tw = t.X1 - t.X0;
+            BinT *tb = c.sbins + t.boff;
+            const BinT *src = static_cast<const BinT *>(q.binsp) + (long long)t.f * q.binsp_fs;
+            for (int y = t.Y0 + wid; y < t.Y1; y += NW)
+                for (int x = t.X0 + lane; x < t.X1; x += 32) tb[(y - t.Y0) * tw + x - t.X0] = src[(long long)y * q.bpitch + x];
         }
     }
     // Grid barrier at a sub-sweep boundary, after which `next` sub-sweeps are
@@ -663,7 +642,6 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
         }
         __syncthreads();
     };
-    if (!q.band) boundary(0);
 
     int s = 0;
     auto stopped = [&]() { return s >= c.misc[8]; };
@@ -698,6 +676,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
         (void)which;
 #endif
     };
+    __syncthreads();  // the resident bins are in place
     stamp(0, 1);
     auto count_moves = [&](bool moved) {
         const unsigned mv = __ballot_sync(FULL, moved);
@@ -1576,16 +1555,140 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
             end_subsweep();
         }
 
-    // ---- outputs: int32 labels of the owned tiles --------------------------
+    // ---- outputs: the int32 labels are written by k_emit_planes, the next
+    // launch on the stream (a streaming kernel at full occupancy)
     if (q.band) return;  // band mode: seeds_band_finish emits the band's rows
     if (blockIdx.x == 0 && tid == 0 && q.done) *q.done = s;
-    for (int ti = 0; ti < ntl; ti++) {
-        const GridTile t = c.tiles[ti];
-        const uint16_t *gl = q.lab + (long long)t.f * q.lab_fs;
-        int32_t *o = q.out + (long long)t.f * q.N;
-        for (int y = t.Y0 + wid; y < t.Y1; y += NW)
-            for (int x = t.X0 + lane; x < t.X1; x += 32)
-                o[(long long)y * W + x] = __ldcg(gl + (long long)(y + 2) * q.lpitch + x + 2);
+}
+
+// Emit (a12): int32 labels of nf frames from the padded u16 label planes --
+// one thread per output pixel, grid-stride, coalesced in both planes.
+// One CTA per output row (blockIdx.x = frame * H + y): no index division.
+__global__ void __launch_bounds__(256) k_emit_planes(const uint16_t *lab, long long lab_fs, int lpitch, int W, int H,
+                                                    int32_t *out)
+{
+    const int f = blockIdx.x / H, y = blockIdx.x - f * H;
+    const uint16_t *src = lab + (long long)f * lab_fs + (long long)(y + 2) * lpitch + 2;
+    int32_t *dst = out + ((long long)f * H + y) * W;
+    for (int x = threadIdx.x; x < W; x += blockDim.x) dst[x] = __ldcg(src + x);
+}
+
+// The seeding kernel of grid mode (a1-a3 of SURVEY.md 8(a)): one CTA per
+// superpixel cell of the initial grid (reading O2) and frame.
+// It quantises the cell's pixels (reading Q1) into the padded bin plane, writes
+// their labels into the padded label plane and counts the histograms.
+//  * Cold start: the cell is exactly superpixel k = cy nx + cx.  Its four
+//    top-level blocks (level L_eff - 1) are counted in shared memory
+//    (privatised; warp-aggregated atomics on the (block, bin) key), and the
+//    superpixel's histogram is written as the sum of the histograms of its
+//    composing blocks -- one plain store per bin into both
+//    snapshot buffers: the row belongs to this CTA alone, so no global atomic
+//    and no memset of H is needed.
+//  * Warm start (reading O9): labels come from init (range-checked); counts go
+//    to global memory with warp-aggregated atomics (H zeroed beforehand).
+template <typename BinT>
+__global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
+{
+    extern __shared__ int shist[];  // [4][B] top-level block histograms (cold)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int cell = blockIdx.x, f = blockIdx.y;
+    const int cx = cell % q.nx, cy = cell / q.nx, L = q.L, B = q.B, W = q.W;
+    const bool cold = q.init == nullptr;
+    const int x0 = q.colstart[cx << L], x1 = q.colstart[(cx + 1) << L];
+    const int y0 = q.rowstart[cy << L], y1 = q.rowstart[(cy + 1) << L];
+    const int xm = L > 0 ? q.colstart[(2 * cx + 1) << (L - 1)] : x1;  // the top-level block split
+    const int ym = L > 0 ? q.rowstart[(2 * cy + 1) << (L - 1)] : y1;
+    int *H0 = q.Hb[0] + (long long)f * q.H_fs, *H1 = q.Hb[1] + (long long)f * q.H_fs;
+    int *A0 = q.Ab[0] + (long long)f * q.A_fs, *A1 = q.Ab[1] + (long long)f * q.A_fs;
+    BinT *bp = static_cast<BinT *>(q.binsp) + (long long)f * q.binsp_fs;
+    uint16_t *gl = q.lab + (long long)f * q.lab_fs;
+    const long long fN = (long long)f * q.N;
+    if (cold) {
+        for (int i = tid; i < 4 * B; i += blockDim.x) shist[i] = 0;
+        __syncthreads();
+    }
+    // four pixels per thread in flight: every load of a batch is issued before
+    // the first use (the cell is walked as one flat index, row-major)
+    constexpr int U = 4;
+    const int cw = x1 - x0, area = cw * (y1 - y0);
+    const float inv = 1.0f / (float)cw;
+    for (int base = 0; base < area; base += U * (int)blockDim.x) {
+        int px[U], py[U];
+        uint32_t rgb[U];
+        int lk[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = base + u * (int)blockDim.x + tid;
+            px[u] = -1;
+            rgb[u] = 0;
+            lk[u] = cell;
+            if (i < area) {
+                const int dy = div_small(i, cw, inv);
+                px[u] = x0 + i - dy * cw;
+                py[u] = y0 + dy;
+                const uint8_t *v = q.img + (fN + (long long)py[u] * W + px[u]) * q.C;
+                for (int ch = 0; ch < q.C; ch++) rgb[u] |= (uint32_t)v[ch] << (8 * ch);
+                if (!cold) lk[u] = q.init[fN + (long long)py[u] * W + px[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const bool in = px[u] >= 0;
+            const int x = px[u], y = py[u];
+            int b = 0, k = cell;
+            if (in) {
+                for (int ch = 0; ch < q.C; ch++) b = b * q.bpc + (((int)(rgb[u] >> (8 * ch) & 0xFF) * q.bpc) >> 8);
+                bp[(long long)y * q.bpitch + x] = (BinT)b;
+                if (!cold) k = checked_label(lk[u], q.K, q.err);
+                gl[(long long)(y + 2) * q.lpitch + x + 2] = (uint16_t)k;
+            }
+            if (cold) {
+                const int key = in ? ((y >= ym ? 2 : 0) + (x >= xm ? 1 : 0)) * B + b : -1;
+                const unsigned m = __match_any_sync(FULL, key);
+                if (in && lane == __ffs(m) - 1) atomicAdd(&shist[key], __popc(m));
+            } else {
+                const int key = in ? k * B + b : -1;
+                unsigned m = __match_any_sync(FULL, key);
+                if (in && lane == __ffs(m) - 1) {
+                    atomicAdd(H0 + key, __popc(m));
+                    atomicAdd(H1 + key, __popc(m));
+                }
+                m = __match_any_sync(FULL, in ? k : -1);
+                if (in && lane == __ffs(m) - 1) {
+                    atomicAdd(A0 + k, __popc(m));
+                    atomicAdd(A1 + k, __popc(m));
+                }
+            }
+        }
+    }
+    if (!cold) return;
+    __syncthreads();
+    // H[k] = the sum of the four top-level block histograms; A[k] = its total
+    __shared__ int wsum[8];
+    int tot = 0;
+    const int tbx = 2 * cx, tby = 2 * cy, gtx = L > 0 ? q.GX >> (L - 1) : 0;
+    for (int bb = tid; bb < B; bb += blockDim.x) {
+        const int h0 = shist[bb], h1 = shist[B + bb], h2 = shist[2 * B + bb], h3 = shist[3 * B + bb];
+        const int v = h0 + h1 + h2 + h3;
+        H0[(long long)cell * B + bb] = v;
+        H1[(long long)cell * B + bb] = v;
+        tot += v;
+        if (q.dbg_blk && L > 0) {  // debug (pin P1b on the GPU): the top-level block histograms
+            int *d = q.dbg_blk + (long long)f * q.dbg_ntop * B;
+            d[((long long)tby * gtx + tbx) * B + bb] = h0;
+            d[((long long)tby * gtx + tbx + 1) * B + bb] = h1;
+            d[((long long)(tby + 1) * gtx + tbx) * B + bb] = h2;
+            d[((long long)(tby + 1) * gtx + tbx + 1) * B + bb] = h3;
+        }
+    }
+    tot = __reduce_add_sync(FULL, tot);
+    if (lane == 0) wsum[wid] = tot;
+    __syncthreads();
+    if (tid == 0) {
+        int a = 0;
+        for (int w = 0; w < (int)(blockDim.x / 32); w++) a += wsum[w];
+        A0[cell] = a;
+        A1[cell] = a;
     }
 }
 

@@ -29,7 +29,8 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics", "seeds_set_colour_space",
            "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks", "seeds_set_compactness",
            "seeds_set_edge_prior", "seeds_batch_host_warm", "seeds_validate_labels", "seeds_set_validate",
-           "seeds_set_time_budget", "seeds_last_subsweeps", "seeds_debug_k5"]
+           "seeds_set_time_budget", "seeds_last_subsweeps", "seeds_debug_k5",
+           "seeds_debug_block_hist"]
 
 
 class _Metrics(ctypes.Structure):
@@ -87,6 +88,7 @@ def load(path: str = LIB_PATH):
         "seeds_set_time_budget": ([vp, ctypes.c_longlong], i),
         "seeds_last_subsweeps": ([vp, vp, vp], i),
         "seeds_debug_k5": ([vp, vp, i, vp, vp, vp, i, i, i, i, vp, vp], i),
+        "seeds_debug_block_hist": ([vp, vp], i),
         "seeds_rgb_to_lab": ([vp, vp, ctypes.c_longlong, vp, vp], i),
         "seeds_stats": ([vp, i, vp, i, vp], i),
         "seeds_sync": ([vp, vp], i),
@@ -105,6 +107,8 @@ def load(path: str = LIB_PATH):
         "seeds_last_error": ([vp], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
+        if path != os.path.join(_PKG, "libseeds.so") and not hasattr(lib, name):
+            continue  # an older A/B build (SEEDS_LIB) may lack newer entry points
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res
@@ -395,6 +399,12 @@ class Seeds:
     def set_validate(self, on: bool = True):
         """Validate warm-start labels before every run (include/seeds.h seeds_set_validate)."""
         self._check(self._lib.seeds_set_validate(self._ctx, int(bool(on))))
+
+    def debug_block_hist(self, out=None):
+        """out: a zeroed (n, n_top_blocks, B) int32 CUDA tensor that later cold
+        runs fill with the seed's top-level block histograms (None: off;
+        include/seeds.h seeds_debug_block_hist)."""
+        self._check(self._lib.seeds_debug_block_hist(self._ctx, None if out is None else out.data_ptr()))
 
     def set_time_budget(self, budget_us: int):
         """Anytime termination after budget_us microseconds (0 = off;

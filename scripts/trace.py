@@ -50,6 +50,9 @@ if (cur[:, :, 8] != 0).any():
     parts.update({"d.pre": cur[:, :, 13], "d.xy": cur[:, :, 14], "d.ring": cur[:, :, 11], "d.bin": cur[:, :, 12], "d.gath": cur[:, :, 8], "d.dec": cur[:, :, 9],
                   "d.emit": cur[:, :, 10]})
 have_parts = mode == "grid"
+seed = tr[:, 0, 1] - tr[:, 0, 2]
+if (tr[:, 0, 2] != 0).all():
+    print(f"    seed: max {seed.max():7.0f} mean {seed.mean():7.0f} cycles (launch start to the first barrier passed)")
 groups = [(f"level {l}", 4 * I) for l in range(L - 1, -1, -1)] + [("pixel", P * P * I)]
 i = 0
 for name, n in groups:

@@ -183,12 +183,12 @@ def test_modes_resolved(torch_cuda):
     mode reports its launch count; the removed resident mode (2) is rejected."""
     from paper_1309_3848_b200.seeds import Seeds
     s = Seeds(481, 321, 3, 200, 4, 5, 1, 4)
-    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 1
+    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 3  # seed, k_grid, emit
     assert s._lib.seeds_set_mode(s._ctx, 2) == -1
     s.set_mode("graph")
     assert s.info.exec_mode == 1 and s.info.kernels_per_run == 107
     s.set_mode("grid")
-    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 1
+    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 3
 
 
 def test_two_contexts_on_two_streams(torch_cuda, orc):
