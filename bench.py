@@ -171,9 +171,12 @@ class Clocks:
 
 
 class BandWorkload:
-    """c5 as row bands: this rank refines band `rank` of `world` of the frame."""
+    """c5 in row-band mode (include/seeds.h): across ranks, this rank refines
+    band `rank` of `world` (one GPU each; the exchange runs inside the kernel
+    over peer memory, bootstrapped once through NCCL); on one rank with
+    --bands K, all K bands in one launch on this GPU."""
 
-    def __init__(self, name, rank, world):
+    def __init__(self, name, rank, world, local_bands=1):
         self.name = name
         c = self.c = configs.CONFIGS[name]
         self.p = configs.params(name)
@@ -181,28 +184,31 @@ class BandWorkload:
         self.N = self.W * self.H
         self.img = configs.frames(name, n=1)[0]
         self.rank, self.world = rank, world
+        self.local_bands = local_bands
         self.frames_per_step = 1
         self.scaling = "strong"
-        self.parallelism = f"row bands/{world}"
+        self.parallelism = f"row bands/{world}" if world > 1 else f"{local_bands} row bands in one launch"
         self.nf = 1
         self.groups = [None]  # one run per step
 
     def make_context(self):
-        from paper_1309_3848_b200.seeds import SeedsBand
         p = self.p
-        return SeedsBand(self.W, self.H, self.C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
-                         p["smoothness_prior"], p["iters_per_level"], self.rank, self.world)
+        args = (self.W, self.H, self.C, p["n_superpixels"], p["n_levels"], p["bins_per_channel"],
+                p["smoothness_prior"], p["iters_per_level"])
+        if self.world > 1:
+            from paper_1309_3848_b200 import bands
+            return bands.make_band(*args, bootstrap="nccl")
+        from paper_1309_3848_b200.seeds import SeedsBands
+        return SeedsBands(*args, self.local_bands)
 
     def describe(self, info):
         p = self.p
-        return (f"{self.name}: one {self.W}x{self.H} RGB Voronoi mosaic as {self.world} row bands (this rank: rows "
+        return (f"{self.name}: one {self.W}x{self.H} RGB Voronoi mosaic as {self.s.n_bands} row bands (this rank: rows "
                 f"{self.s.row0}..{self.s.row1}), K={p['n_superpixels']} (K_act={info.k_actual}), "
                 f"L={info.levels_eff}, I={p['iters_per_level']}, B={info.bins_total}, gamma={p['smoothness_prior']}")
 
     def setup(self, torch, s):
-        from paper_1309_3848_b200.bands import DistExchange
         self.s = s
-        self.ex = DistExchange()
         self.d_in = torch.from_numpy(self.img).cuda()
         self.d_out = torch.zeros((self.H, self.W), dtype=torch.int32, device="cuda")
         self.h_in = torch.from_numpy(self.img).pin_memory()
@@ -211,13 +217,11 @@ class BandWorkload:
         self.d_tmp_out = torch.zeros_like(self.d_out)
 
     def step(self, s, stream):
-        from paper_1309_3848_b200 import bands
-        bands.dist_run(s, self.d_in, self.d_out, exchange=self.ex, stream=stream)
+        s.run(self.d_in, labels_out=self.d_out, stream=stream)
 
     def host_step(self, s, stream):
-        from paper_1309_3848_b200 import bands
         self.d_tmp_in.copy_(self.h_in, non_blocking=True)
-        bands.dist_run(s, self.d_tmp_in, self.d_tmp_out, exchange=self.ex, stream=stream)
+        s.run(self.d_tmp_in, labels_out=self.d_tmp_out, stream=stream)
         self.h_out[s.row0:s.row1].copy_(self.d_tmp_out[s.row0:s.row1], non_blocking=True)
         stream.synchronize()
 
@@ -568,7 +572,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--json-out", default=None)
-    ap.add_argument("--bands", action="store_true", help="c5: row-band mode even on one rank")
+    ap.add_argument("--bands", type=int, default=0,
+                    help="c5 on one rank: row-band mode with this many bands in one launch (multi-rank c5 always bands)")
     ap.add_argument("--colour", default="rgb", choices=["rgb", "lab"],
                     help="lab: the 8-bit CIELAB pre-pass inside the timed run (reading M3)")
     ap.add_argument("--compact", action="store_true", help="the compactness prior at the pixel level (reading M5)")
@@ -596,13 +601,8 @@ def main():
     from paper_1309_3848_b200.seeds import Seeds
 
     name = args.config
-    banded = name == "c5" and (world > 1 or args.bands)
-    if banded and not dist:
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
-    wl = BandWorkload(name, rank, world) if banded else Workload(name, rank, world)
+    banded = name == "c5" and (world > 1 or args.bands > 0)
+    wl = BandWorkload(name, rank, world, max(1, args.bands)) if banded else Workload(name, rank, world)
     p = wl.p
     s = wl.make_context()
     if not banded:
@@ -653,21 +653,18 @@ def main():
     value = px_all / (tot_ms_max / 1e3) / 1e6
     runs_per_step = len(wl.groups)
     launches = info.kernels_per_run * runs_per_step * args.steps
-    if banded:  # seed + per sub-sweep (apply records + grid launch) + emit
-        launches = (2 + 2 * s.subsweeps) * args.steps
+    if banded:  # seed + k_grid + one emit per band of this process
+        launches = (2 + (s.n_bands if s.band < 0 else 1)) * args.steps
 
     # ---- per-kernel timing pass (event pairs inside the graph) ------------
     kp = min(args.steps, 20)
-    if banded:  # one grid launch per sub-sweep; the whole step is the unit
-        prof = {"frame": (tot_ms_max / args.steps * kp, kp)}
-    else:
-        s.profile(True)
-        prof = None
-        for i in range(kp):
-            flush.fill_(i & 0xFF)
-            wl.step(s, stream)
-            prof = s.profile_collect(stream=stream)
-        s.profile(False)
+    s.profile(True)
+    prof = None
+    for i in range(kp):
+        flush.fill_(i & 0xFF)
+        wl.step(s, stream)
+        prof = s.profile_collect(stream=stream)
+    s.profile(False)
     torch.cuda.synchronize()
     ab = algorithmic_bytes(info, wl.C, wl.nf, wl.N, p["iters_per_level"])
     ab["frame"] = wl.algorithmic_bytes(info) / runs_per_step  # per launch (a warm run has no block levels)
@@ -754,7 +751,8 @@ def main():
                        "edge_tau": args.edge,
                        "grid_ctas": info.grid_ctas, "grid_tiles_per_frame": info.grid_tiles,
                        "parallelism": wl.parallelism,
-                       "exchange": "NCCL all-gather of delta records + halo send/recv per sub-sweep" if banded else None,
+                       "exchange": ("inside the persistent kernel: owner-band histogram updates and halo label rows "
+                                    "through peer memory, one counter barrier per sub-sweep") if banded else None,
                        "l2": "512 MiB buffer rewritten between timed steps (outside events)"},
             "frames_per_s": wl.frames_per_step * world * args.steps / (tot_ms_max / 1e3),
             "e2e_hbm_frac": (fb * args.steps / (tot_ms_max / 1e3) / 1e9) / hbm,

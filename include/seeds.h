@@ -52,7 +52,7 @@ typedef enum {
     SEEDS_EINVAL = -1, /* an argument is out of its documented range */
     SEEDS_ENOMEM = -2, /* a device or pinned-host allocation failed */
     SEEDS_ECUDA = -3,  /* a CUDA runtime error; seeds_last_error() has the text */
-    SEEDS_ENCCL = -4,  /* reserved (the row-band exchange is done by the caller) */
+    SEEDS_ENCCL = -4,  /* NCCL missing or failed (seeds_nccl_unique_id, seeds_create_banded bootstrap) */
     SEEDS_ESTATE = -5, /* call out of order (e.g. read_state before any run) */
     SEEDS_ERANGE = -6  /* the problem exceeds an integer width (see seeds_create) */
 } seeds_status;
@@ -387,90 +387,83 @@ seeds_status seeds_profile(seeds_ctx *ctx, int enable);
 seeds_status seeds_profile_collect(seeds_ctx *ctx, void *stream, double *ms_out, long long *launches_out);
 
 /* ---------------------------------------------------------------------------
- * Row-band mode: one very large frame refined by n_bands cooperating contexts
- * (one per GPU / rank), BASELINE.json configs[4] and SURVEY.md section 8(e).
- * Band b owns the pixel rows of superpixel rows [b*ny/n, (b+1)*ny/n) (whole
- * superpixel rows, so every block of every level lies in one band).  Every
- * band keeps a full replica of the histograms and the full label plane, but
- * decides only its own rows.  The caller drives the schedule:
- *
- *   seeds_band_seed(ctx, image, init)            every rank, the whole frame
- *   for s in 0 .. subsweeps-1:
- *     seeds_band_subsweep(ctx, s, all_records_of_s-1, n, my_records, my_n)
- *     exchange: all-gather the records (the concatenation of every band's
- *       records, in any order); send seeds_band_halo(get) top rows to band
- *       b-1 and bottom rows to band b+1, seeds_band_halo(put) what arrives
- *   seeds_band_finish(ctx, all_records_of_last, n, labels_out)  this band's rows
- *
- * The records are the sparse histogram deltas of a sub-sweep (opaque,
- * record_bytes each); applying every band's records keeps every replica equal
- * to the one-GPU state, so any n_bands gives bit-identical results
- * (tests/test_bands.py).  Sub-sweep s of the snapshot schedule (reading O7)
- * reads the histograms after sub-sweep s-1 and the labels within 2 rows of
- * the band, which is what the exchange provides.
+ * Row-band mode: one very large frame refined as n_bands bands of whole
+ * superpixel rows (BASELINE.json configs[4], SURVEY.md section 8(e) "v3
+ * fused").  Band b owns the pixel rows of superpixel
+ * rows [b*ny/n, (b+1)*ny/n) -- every block of every level lies in one band --
+ * and the superpixels of the grid cells in those rows: it keeps their
+ * histograms and sizes (one owner per superpixel, no replicas) and a label
+ * plane of its rows plus two halo rows on each side.  Inside the one
+ * persistent kernel every read and update of H[k], A[k] goes to k's owner and
+ * a label written within two rows of a band edge is also written into the
+ * neighbour's plane (peer memory over NVLink across devices); one barrier per
+ * sub-sweep (the grid barrier in one process; across devices a system-scope
+ * counter barrier after it).  No host round trip per sub-sweep.  Every
+ * n_bands gives the one-GPU result bit for bit (tests/test_bands.py).
+ * Grid mode only; means post-processing, priors, LAB, block-level ranges and
+ * the time budget are single-GPU features (SEEDS_EINVAL on a band context).
  * ------------------------------------------------------------------------- */
 
-/* seeds_create_banded -- as seeds_create, plus band (0 <= band < n_bands) and
- * n_bands (1 .. ny, the superpixel rows).  SEEDS_EINVAL also for a band of
+/* The bands a context can hold / ranks a run can span. */
+#define SEEDS_MAX_BANDS 8
+
+/* seeds_create_bands -- every band of a run in this process, on the current
+ * device, refined by one launch (the single-GPU form of the band exchange:
+ * peer buffers are other buffers of the same device).  As seeds_create, plus
+ * n_bands in 1 .. min(SEEDS_MAX_BANDS, ny); SEEDS_EINVAL also for a band of
  * fewer than 2 pixel rows; SEEDS_ERANGE if no grid-mode tile plan fits. */
+seeds_status seeds_create_bands(int width, int height, int channels, int n_superpixels, int n_levels,
+                                int bins_per_channel, int smoothness_prior, int iters_per_level, int n_bands,
+                                seeds_ctx **out);
+
+/* seeds_nccl_unique_id -- a new NCCL unique id (128 bytes at id) for the
+ * bootstrap of seeds_create_banded: rank 0 creates it and the caller
+ * distributes it.  NCCL is loaded at run time (libnccl.so.2); SEEDS_ENCCL if
+ * it is missing or fails. */
+seeds_status seeds_nccl_unique_id(void *id);
+
+/* seeds_create_banded -- band `rank` of a `world`-rank run, one rank per
+ * device (the current one).  Allocates this band's buffers and maps every
+ * other rank's through CUDA IPC: with nccl_id (from seeds_nccl_unique_id, the
+ * same on every rank) the library exchanges the handles itself (one NCCL
+ * all-gather, then the communicator is destroyed; NCCL errors are
+ * SEEDS_ENCCL); with nccl_id = NULL and world > 1 the caller exchanges
+ * seeds_band_export blobs with its own transport and calls
+ * seeds_band_connect.  world = 1 needs neither.  Every rank must then call
+ * seeds_band_run the same number of times (the kernels wait for each other at
+ * every sub-sweep; a rank that never arrives traps the others' kernels after
+ * ~2^26 polls instead of hanging).  Errors as seeds_create_bands. */
 seeds_status seeds_create_banded(int width, int height, int channels, int n_superpixels, int n_levels,
-                                 int bins_per_channel, int smoothness_prior, int iters_per_level, int band,
-                                 int n_bands, seeds_ctx **out);
+                                 int bins_per_channel, int smoothness_prior, int iters_per_level, int rank, int world,
+                                 const void *nccl_id, seeds_ctx **out);
 
-/* seeds_band_info -- the band's pixel rows [*row0, *row1), the most records one
- * sub-sweep of the band can emit (*record_capacity) and their size in bytes.
- * Any pointer may be NULL. */
-seeds_status seeds_band_info(const seeds_ctx *ctx, int *row0, int *row1, long long *record_capacity,
-                             int *record_bytes);
+/* seeds_band_export -- this rank's bootstrap blob (CUDA IPC handles of its
+ * label plane, histogram / size buffers and barrier words) into blob[cap];
+ * *len receives its size (blob = NULL: size only).  SEEDS_EINVAL for a
+ * context not made by seeds_create_banded or cap too small. */
+seeds_status seeds_band_export(seeds_ctx *ctx, void *blob, size_t cap, size_t *len);
 
-/* seeds_band_seed -- quantise and label the WHOLE frame and count its
- * histograms (every band does the same, so the replicas start equal).
- *   image_u8     device, height*width*channels bytes (the whole frame)
- *   init_labels  NULL (cold: grid) or device height*width int32 (warm start:
- *                no block levels, reading O9) */
-seeds_status seeds_band_seed(seeds_ctx *ctx, const uint8_t *image_u8, const int32_t *init_labels, void *stream);
+/* seeds_band_connect -- map the peers' buffers from every rank's blob, in rank
+ * order (world * len bytes, this rank's own included).  SEEDS_EINVAL for a
+ * blob of another run or rank; SEEDS_ECUDA if a handle cannot be opened (e.g.
+ * no peer access between the devices). */
+seeds_status seeds_band_connect(seeds_ctx *ctx, const void *blobs, int world);
 
-/* seeds_band_subsweep -- apply records_in (device, *n_in records: every band's
- * records of sub-sweep s-1; NULL for s = 0) to the histograms, then run
- * sub-sweep s (0 <= s < subsweeps of the seeded run) on this band's rows,
- * writing its records to records_out (device, capacity from seeds_band_info)
- * and their count to *n_out (device int32).  SEEDS_ESTATE before a seed or for
- * s out of range. */
-seeds_status seeds_band_subsweep(seeds_ctx *ctx, int s, const void *records_in, const int32_t *n_in,
-                                 void *records_out, int32_t *n_out, void *stream);
+/* seeds_band_info -- the pixel rows [*row0, *row1) this context refines (one
+ * process: the whole frame), the number of bands and this context's band (-1:
+ * every band).  Any pointer may be NULL. */
+seeds_status seeds_band_info(const seeds_ctx *ctx, int *row0, int *row1, int *n_bands, int *band);
 
-/* seeds_band_halo -- put = 0: copy this band's first two rows to top and its
- * last two rows to bottom (device, 2*width uint16 each; either may be NULL).
- * put = 1: write top into the two rows above the band and bottom into the two
- * rows below it (ignored at the image border). */
-seeds_status seeds_band_halo(seeds_ctx *ctx, int put, uint16_t *top, uint16_t *bottom, void *stream);
-
-/* seeds_band_finish -- apply records_in (every band's records of the last
- * sub-sweep; may be NULL) and write this band's rows of the int32 labels into
- * labels_out (device, height*width; other rows untouched).  seeds_read_state
- * then returns this band's replica of the histograms (equal on every band). */
-seeds_status seeds_band_finish(seeds_ctx *ctx, const void *records_in, const int32_t *n_in, int32_t *labels_out,
-                               void *stream);
-
-/* seeds_validate_labels -- is every frame of `labels` a valid partition
- * (the set S -- every superpixel one non-empty, spatially
- * connected blob; 4-connectivity, reading Q8)?  Runs a union-find connected-
- * components pass on the GPU (seeds_validate.cuh) and synchronises `stream`.
- *   labels       device, n_frames*height*width int32
- *   report_host  NULL or host long long[3]: labels outside [0, K_act); the
- *                first missing superpixel as frame*K_act + k (-1: none); the
- *                first superpixel of more than one component, likewise
- * SEEDS_OK if valid, SEEDS_ESTATE (seeds_last_error names the first defect)
- * if not, SEEDS_EINVAL for NULL labels or n_frames < 1. */
-seeds_status seeds_validate_labels(seeds_ctx *ctx, const int32_t *labels, int n_frames, long long *report_host,
-                                   void *stream);
-
-/* seeds_set_validate -- on = 1: every later seeds_batch / seeds_batch_host with
- * init_labels first runs seeds_validate_labels on them (synchronising) and
- * returns its SEEDS_ESTATE without running; 0 (default) turns it off.  The
- * SEEDS_ESTATE check of the batch contract ("checked in debug
- * mode").  SEEDS_EINVAL for on not 0/1. */
-seeds_status seeds_set_validate(seeds_ctx *ctx, int on);
+/* seeds_band_run -- refine one frame in row-band mode (enqueued on `stream`).
+ *   image_u8     device, height*width*channels bytes: the WHOLE frame (every
+ *                rank holds it; each seeds and bins only its own cells)
+ *   init_labels  NULL (cold: grid) or device height*width int32 (warm start)
+ *   labels_out   device, height*width int32: this context's rows are written
+ * seeds_read_state then returns the rows of the superpixels this context owns
+ * (one process: all of them); seeds_batch / seeds_iterate with one frame do
+ * the same as seeds_band_run.  SEEDS_ESTATE before seeds_band_connect. */
+seeds_status seeds_band_run(seeds_ctx *ctx, const uint8_t *image_u8, const int32_t *init_labels,
+                            int32_t *labels_out, void *stream);
 
 /* seeds_sync -- wait for `stream` and report any pending CUDA error. */
 seeds_status seeds_sync(seeds_ctx *ctx, void *stream);

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <dlfcn.h>
 #include <mutex>
 #include <climits>
 #include <cmath>
@@ -134,17 +135,20 @@ struct seeds_ctx {
     bool grid_ok = false;
     int grid_G = 0;
     int grid_nt = 512;     // threads per CTA of the plan
-    // row-band mode (seeds_create_banded): band `band` of `band_n`, top-unit rows
-    // [band_u0, band_u1) = pixel rows [band_y0, band_y1); record list + count
-    bool banded = false;
-    int band = 0, band_n = 1, band_u0 = 0, band_u1 = 0, band_y0 = 0, band_y1 = 0;
-    GRec *d_brec = nullptr;
-    int *d_bcount = nullptr;
-    long long brec_cap = 0;
-    int band_total = 0;    // sub-sweeps of the seeded run (cold or warm)
-    bool band_seeded = false;
-    bool band_warm = false;
-    const int32_t *band_init = nullptr;
+    // row-band mode: nbands bands of one frame, band b =
+    // superpixel rows [bj[b], bj[b+1]) = top-unit rows [bu[b], bu[b+1]) = pixel
+    // rows [by[b], by[b+1]) = superpixels [bk[b], bk[b+1]).  seeds_create_bands:
+    // every band in this process (bself = -1, one launch); seeds_create_banded:
+    // band bself of nbands ranks, one device each (bsys), the peers' buffers
+    // mapped through CUDA IPC.
+    bool banded = false, bsys = false;
+    int nbands = 0, bself = -1;
+    int bj[SEEDS_MAX_BANDS + 1] = {}, bu[SEEDS_MAX_BANDS + 1] = {}, by[SEEDS_MAX_BANDS + 1] = {},
+        bk[SEEDS_MAX_BANDS + 1] = {};
+    uint16_t *b_lab[SEEDS_MAX_BANDS] = {};
+    int *b_H[SEEDS_MAX_BANDS][2] = {}, *b_A[SEEDS_MAX_BANDS][2] = {};
+    unsigned *b_ctl[SEEDS_MAX_BANDS] = {};  // per band: [0] band-arrival counter, [1] bar_base, [2] go
+    bool b_mapped[SEEDS_MAX_BANDS] = {};    // IPC-mapped (closed at destroy) rather than allocated here
     size_t grid_smem = 0;
     GridParams gp{};
     // tile plans of the last few batch sizes (plan_grid): the active one is
@@ -662,11 +666,13 @@ static int grid_occupancy_m(size_t smem)
     }
     return n;
 }
-// both variants (with and without the means post-processing) get the opt-in
+// every variant (plain, extended pixel path, row-band mode) gets the opt-in
 template <typename BinT, int GAMMA, int P, int NT>
 static int grid_occupancy(size_t smem)
 {
-    return std::min(grid_occupancy_m<BinT, GAMMA, P, NT, 0>(smem), grid_occupancy_m<BinT, GAMMA, P, NT, 1>(smem));
+    return std::min(std::min(grid_occupancy_m<BinT, GAMMA, P, NT, VAR_PLAIN>(smem),
+                             grid_occupancy_m<BinT, GAMMA, P, NT, VAR_EXT>(smem)),
+                    grid_occupancy_m<BinT, GAMMA, P, NT, VAR_BAND>(smem));
 }
 
 template <int NT>
@@ -723,6 +729,14 @@ static bool encode_tmaps(seeds_ctx *c, GridParams &q)
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return false;
+        // row-band mode: one map per band plane this launch stages from
+        for (int b = 0; c->banded && b < c->nbands; b++) {
+            if (c->bself >= 0 && b != c->bself) continue;
+            if (enc(&q.tm_lab_b[b], CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, c->b_lab[b], dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return false;
+        }
     }
     if (!q.bins_res) {
         const cuuint64_t dims[3] = {(cuuint64_t)q.bpitch, (cuuint64_t)c->H, (cuuint64_t)c->cap_frames};
@@ -817,7 +831,20 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     const int TX = c->L > 0 ? c->GX >> Lm : c->W, TY = c->L > 0 ? c->GY >> Lm : c->H;
     auto ux = [&](int i) { return c->L > 0 ? c->colstart[(size_t)i << Lm] : i; };
     auto uy = [&](int j) { return c->L > 0 ? c->rowstart[(size_t)j << Lm] : j; };
-    const int UY0 = c->banded ? c->band_u0 : 0, TYb = c->banded ? c->band_u1 - c->band_u0 : TY;
+    // the row ranges tiled: the whole frame, or (row-band mode) every band of
+    // this launch -- tiles never straddle a band edge; a tile's band in .pad
+    struct Rng {
+        int u0, u1, band;
+    };
+    std::vector<Rng> rng;
+    if (c->banded) {
+        for (int b = 0; b < c->nbands; b++)
+            if (c->bself < 0 || b == c->bself) rng.push_back({c->bu[b], c->bu[b + 1], b});
+    } else {
+        rng.push_back({0, TY, 0});
+    }
+    int TYb = 0;
+    for (const Rng &r : rng) TYb = std::max(TYb, r.u1 - r.u0);
     int muw = 0, muh = 0;
     for (int i = 0; i < TX; i++) muw = std::max(muw, ux(i + 1) - ux(i));
     for (int j = 0; j < TY; j++) muh = std::max(muh, uy(j + 1) - uy(j));
@@ -867,7 +894,9 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     int ba = 0, bb_ = 0;
     for (int a : size_candidates(TX))
         for (int b : size_candidates(TYb)) {
-            const long long T = (long long)nf * ((TX + a - 1) / a) * ((TYb + b - 1) / b);
+            long long rows = 0;
+            for (const Rng &r : rng) rows += (r.u1 - r.u0 + b - 1) / b;
+            const long long T = (long long)nf * ((TX + a - 1) / a) * rows;
             const long long G = std::min<long long>(nsm, T);
             const long long tw = (long long)a * muw, th = (long long)b * muh;
             if ((tw + 4 + 14) / 8 * 8 > 256 || th + 4 > 256) continue;  // TMA box limits (aligned start)
@@ -884,14 +913,16 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         }
     if (!ba) return false;
     // tiles of one frame, then their per-tile capacities
-    const int ntx = (TX + ba - 1) / ba, nty = (TYb + bb_ - 1) / bb_;
+    const int ntx = (TX + ba - 1) / ba;
     std::vector<GridTile> ft;
     std::vector<long long> tpx, tq, tr;
-    for (int ty = 0; ty < nty; ty++)
+    for (const Rng &r : rng)
+    for (int ty = 0; ty < (r.u1 - r.u0 + bb_ - 1) / bb_; ty++)
         for (int tx = 0; tx < ntx; tx++) {
             GridTile t{};
+            t.pad = r.band;
             const int i0 = tx * ba, i1 = std::min(TX, (tx + 1) * ba);
-            const int j0 = UY0 + ty * bb_, j1 = UY0 + std::min(TYb, (ty + 1) * bb_);
+            const int j0 = r.u0 + ty * bb_, j1 = std::min(r.u1, r.u0 + (ty + 1) * bb_);
             t.X0 = ux(i0); t.X1 = ux(i1); t.Y0 = uy(j0); t.Y1 = uy(j1);
             t.BX0 = i0 << Lm; t.BX1 = i1 << Lm; t.BY0 = j0 << Lm; t.BY1 = j1 << Lm;
             const long long w = t.X1 - t.X0, h = t.Y1 - t.Y0;
@@ -955,7 +986,6 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     // round trip, so it is preferred over shared-memory-resident bins
     for (int opt = 0; opt < 4; opt++) {
         const int rs = opt < 2, res = !(opt & 1);
-        if (c->banded && (rs || res)) continue;  // band mode: bins from k_band_seed, records to the host
         size_t off = 0;
         q.o_stage = (unsigned)off; off = align128(off + 2 * (size_t)q.stage_bytes);
         q.o_bins = (unsigned)off;  off = align128(off + (res ? (size_t)max_cpx * c->bb : 2 * (size_t)q.bins_bytes));
@@ -967,7 +997,8 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.o_scr = (unsigned)off;   off = align16(off + (need_tab ? (size_t)(nt / 32) * 6 * 8 : 0));
         // A cache (two copies of K_pad ints) when it leaves room for the tables
         q.acache = 0;
-        if (!getenv_off("SEEDS_GRID_ACACHE") &&
+        // (row-band mode: A lives with its owner band -- the cache only with one band)
+        if ((!c->banded || c->nbands == 1) && !getenv_off("SEEDS_GRID_ACACHE") &&
             align16(off + 2 * (size_t)c->Afs * 4) + (need_tab ? tabw : 0) <= limit) {
             q.acache = 1;
             q.o_acache = (unsigned)off;
@@ -981,9 +1012,6 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         if (occ < cps) continue;
         q.bins_res = res;
         q.rec_smem = rs;
-        q.band = 0;  // whole-run launch: every sub-sweep (seeds_band_subsweep overrides these)
-        q.s0 = 0;
-        q.s1 = -1;
         q.filt2 = !getenv_off("SEEDS_FILT2");
         q.blk_lo = 0;  // every block level (enqueue_grid applies seeds_set_block_levels)
         q.blk_hi = 1 << 20;
@@ -1075,16 +1103,27 @@ static cudaError_t launch_grid_nt(seeds_ctx *ctx, const GridParams &q, cudaStrea
                       : launch_grid_t<uint16_t, 0, 2, NT, MEANS>(ctx, q, st);
 }
 
+// The row-band kernel variant runs for several bands or across devices; one
+// band in one process is the ordinary run (its buffers are the context's).
+static bool band_kernel(const seeds_ctx *c) { return c->banded && (c->bsys || c->nbands > 1); }
+
 // Enqueue one grid-mode run: zero the histograms, move counters and the barrier
 // counter, then the single persistent launch.
 static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
                                  cudaStream_t st)
 {
-    if (init)  // a cold seed writes every histogram row and size itself (k_seed_cells)
+    if (init) {  // a cold seed writes every histogram row and size itself (k_seed_cells)
         for (int i = 0; i < 2; i++) {
             CK(cudaMemsetAsync(ctx->d_H[i], 0, (size_t)nf * ctx->H_fs * 4, st));
             CK(cudaMemsetAsync(ctx->d_A[i], 0, (size_t)nf * ctx->Afs * 4, st));
         }
+        for (int b = 0; ctx->banded && b < ctx->nbands; b++)  // every band buffer of this process
+            if (!ctx->b_mapped[b] && ctx->b_H[b][0] != ctx->d_H[0])
+                for (int i = 0; i < 2; i++) {
+                    CK(cudaMemsetAsync(ctx->b_H[b][i], 0, (size_t)ctx->H_fs * 4, st));
+                    CK(cudaMemsetAsync(ctx->b_A[b][i], 0, (size_t)ctx->Afs * 4, st));
+                }
+    }
     if (ctx->miters > 0)
         for (int i = 0; i < 2; i++) CK(cudaMemsetAsync(ctx->d_S[i], 0, (size_t)nf * ctx->Afs * 4 * sizeof(long long), st));
     if (ctx->compact) CK(cudaMemsetAsync(ctx->d_csum, 0, (size_t)nf * ctx->Afs * 4 * sizeof(long long), st));
@@ -1117,6 +1156,27 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     q.sync = ctx->d_sync;
     q.trace = ctx->d_trace;
     q.dbg_blk = ctx->dbg_blk;
+    q.nbands = ctx->banded ? ctx->nbands : 0;
+    q.bsys = ctx->bsys;
+    q.bself = ctx->bself;
+    for (int b = 0; ctx->banded && b < ctx->nbands; b++) {
+        q.pH[b][0] = ctx->b_H[b][0];
+        q.pH[b][1] = ctx->b_H[b][1];
+        q.pA[b][0] = ctx->b_A[b][0];
+        q.pA[b][1] = ctx->b_A[b][1];
+        q.plab[b] = ctx->b_lab[b];
+        q.pbar[b] = ctx->b_ctl[b];
+    }
+    for (int b = 0; ctx->banded && b <= SEEDS_MAX_BANDS; b++) {
+        q.by[b] = b <= ctx->nbands ? ctx->by[b] : INT_MAX;
+        q.bk[b] = b < ctx->nbands ? ctx->bk[b] : INT_MAX;  // band_owner: no band at or past nbands
+    }
+    if (ctx->banded) {
+        const int own = ctx->bself >= 0 ? ctx->bself : 0;
+        q.bar_base = ctx->b_ctl[own] + 1;
+        q.go = ctx->b_ctl[own] + 2;
+        CK(cudaMemsetAsync(q.go, 0, 4, st));  // (the counters [0], [1] persist across runs)
+    }
     q.dbg_ntop = ctx->L > 0 ? (long long)(ctx->GX >> (ctx->L - 1)) * (ctx->GY >> (ctx->L - 1)) : 0;
     q.budget_ns = ctx->budget_ns;
     q.stop = ctx->d_err + 1;
@@ -1125,28 +1185,45 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     ctx->ev_used = 0;
     CK(prof_begin(ctx, st, SEEDS_KIND_SEED));
     {
-        const dim3 g((unsigned)ctx->K, (unsigned)nf);
+        const int cells = ctx->banded && ctx->bsys ? ctx->bk[ctx->bself + 1] - ctx->bk[ctx->bself] : ctx->K;
+        const dim3 g((unsigned)cells, (unsigned)nf);
         const size_t sm = init ? 0 : (size_t)4 * ctx->B * sizeof(int);
-        if (ctx->bb == 1)
-            k_seed_cells<uint8_t><<<g, 256, sm, st>>>(q);
-        else
-            k_seed_cells<uint16_t><<<g, 256, sm, st>>>(q);
+        if (band_kernel(ctx)) {
+            if (ctx->bb == 1) k_seed_cells<uint8_t, 1><<<g, 256, sm, st>>>(q);
+            else k_seed_cells<uint16_t, 1><<<g, 256, sm, st>>>(q);
+        } else {
+            if (ctx->bb == 1) k_seed_cells<uint8_t, 0><<<g, 256, sm, st>>>(q);
+            else k_seed_cells<uint16_t, 0><<<g, 256, sm, st>>>(q);
+        }
         CK(cudaGetLastError());
     }
     CK(prof_end(ctx, st));
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
     cudaError_t e;
     if (ctx->grid_nt == GRID_THREADS)
-        e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS, 1>(ctx, q, st) : launch_grid_nt<GRID_THREADS, 0>(ctx, q, st);
+        e = band_kernel(ctx) ? launch_grid_nt<GRID_THREADS, VAR_BAND>(ctx, q, st)
+            : ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS, VAR_EXT>(ctx, q, st)
+                             : launch_grid_nt<GRID_THREADS, VAR_PLAIN>(ctx, q, st);
     else
-        e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
-                           : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
+        e = band_kernel(ctx) ? launch_grid_nt<GRID_THREADS_SMALL, VAR_BAND>(ctx, q, st)
+            : ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS_SMALL, VAR_EXT>(ctx, q, st)
+                             : launch_grid_nt<GRID_THREADS_SMALL, VAR_PLAIN>(ctx, q, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid launch");
     CK(prof_end(ctx, st));
     CK(prof_begin(ctx, st, SEEDS_KIND_EMIT));
     {
-        k_emit_planes<<<(unsigned)(nf * ctx->H), ctx->W >= 256 ? 256 : 128, 0, st>>>(ctx->d_labp, ctx->labp_fs, ctx->lpitch,
-                                                                                   ctx->W, ctx->H, out);
+        const int nt = ctx->W >= 256 ? 256 : 128;
+        if (!ctx->banded) {
+            k_emit_planes<<<(unsigned)(nf * ctx->H), nt, 0, st>>>(ctx->d_labp, ctx->labp_fs, ctx->lpitch, ctx->W, ctx->H, 0,
+                                                                  ctx->H, out);
+        } else {  // each band's rows from its own plane (across devices: this rank's band)
+            for (int b = 0; b < ctx->nbands; b++) {
+                if (ctx->bself >= 0 && b != ctx->bself) continue;
+                const int rows = ctx->by[b + 1] - ctx->by[b];
+                k_emit_planes<<<(unsigned)rows, nt, 0, st>>>(ctx->b_lab[b], ctx->labp_fs, ctx->lpitch, ctx->W, ctx->H,
+                                                             ctx->by[b], rows, out);
+            }
+        }
         CK(cudaGetLastError());
     }
     CK(prof_end(ctx, st));
@@ -1401,8 +1478,10 @@ seeds_status seeds_create(int width, int height, int channels, int n_superpixels
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block_large<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_block_large<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     // the seed kernel's four block histograms: 4 B ints, up to 64 KB (B <= 4096)
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_seed_cells<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_seed_cells<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_seed_cells<uint8_t, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_seed_cells<uint16_t, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_seed_cells<uint8_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_seed_cells<uint16_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, ctx->dev);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_err, 16);
@@ -1420,6 +1499,7 @@ seeds_status seeds_batch(seeds_ctx *ctx, const uint8_t *images, int n_frames, co
                          int32_t *labels_out, void *stream)
 {
     if (!ctx || !images || !labels_out || n_frames < 1 || n_frames > 65535) return SEEDS_EINVAL;
+    if (ctx->banded && n_frames != 1) return SEEDS_EINVAL;  // row-band mode: one frame (seeds_band_run)
     return run(ctx, images, init_labels, labels_out, n_frames, (cudaStream_t)stream);
 }
 
@@ -1577,6 +1657,19 @@ seeds_status seeds_read_state(seeds_ctx *ctx, int frame, int32_t *hist_out, int3
     seeds_status sd = settle_done(ctx, st);
     if (sd != SEEDS_OK) return sd;
     const int b = ctx->last_final;
+    if (ctx->banded) {  // each superpixel's row from its owner band (across devices: this rank's rows)
+        for (int r = 0; r < ctx->nbands; r++) {
+            if (ctx->bself >= 0 && r != ctx->bself) continue;
+            const size_t k0 = ctx->bk[r], nk = ctx->bk[r + 1] - ctx->bk[r];
+            if (hist_out)
+                CK(cudaMemcpyAsync(hist_out + k0 * ctx->B, ctx->b_H[r][b] + k0 * ctx->B, nk * ctx->B * 4,
+                                   cudaMemcpyDeviceToDevice, st));
+            if (sizes_out)
+                CK(cudaMemcpyAsync(sizes_out + k0, ctx->b_A[r][b] + k0, nk * 4, cudaMemcpyDeviceToDevice, st));
+        }
+        CK(cudaStreamSynchronize(st));
+        return check_err(ctx);
+    }
     if (hist_out)
         CK(cudaMemcpyAsync(hist_out, ctx->d_H[b] + (size_t)frame * ctx->H_fs, (size_t)ctx->H_fs * 4,
                            cudaMemcpyDeviceToDevice, st));
@@ -1923,11 +2016,22 @@ void seeds_destroy(seeds_ctx *ctx)
     void *ptrs[] = {ctx->d_colstart, ctx->d_rowstart, ctx->d_bxof, ctx->d_byof, ctx->d_bins, ctx->d_lab,
                     ctx->d_M[0], ctx->d_M[1], ctx->d_H[0], ctx->d_H[1], ctx->d_A[0], ctx->d_A[1], ctx->d_S[0], ctx->d_S[1],
                     ctx->d_rec[0], ctx->d_rec[1], ctx->d_cnt, ctx->d_moves, ctx->d_img_stage,
-                    ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp, ctx->d_bcount,
+                    ctx->d_labp, ctx->d_sync, ctx->d_grec, ctx->d_tiles, ctx->d_binsp,
                     ctx->d_init_stage, ctx->d_out_stage, ctx->d_met_key, ctx->d_met_cnt, ctx->d_met_acc,
                     ctx->d_lab_tab, ctx->d_labimg, ctx->d_err, ctx->d_cc_par, ctx->d_cc_roots, ctx->d_vout};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    // row-band mode: the other bands' buffers (allocated here, or peers' mapped)
+    for (int b = 0; ctx->banded && b < ctx->nbands; b++) {
+        void *bp[] = {ctx->b_lab[b], ctx->b_H[b][0], ctx->b_H[b][1], ctx->b_A[b][0], ctx->b_A[b][1], ctx->b_ctl[b]};
+        for (int i = 0; i < 6; i++) {
+            if (!bp[i]) continue;
+            if (i < 5 && bp[i] == (i == 0 ? (void *)ctx->d_labp : i < 3 ? (void *)ctx->d_H[i - 1] : (void *)ctx->d_A[i - 3]))
+                continue;  // this band's own buffers (freed above)
+            if (ctx->b_mapped[b]) cudaIpcCloseMemHandle(bp[i]);
+            else cudaFree(bp[i]);
+        }
+    }
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
@@ -1939,173 +2043,260 @@ void seeds_destroy(seeds_ctx *ctx)
 // ---------------------------------------------------------------------------
 // Row-band mode (include/seeds.h)
 // ---------------------------------------------------------------------------
-seeds_status seeds_create_banded(int width, int height, int channels, int n_superpixels, int n_levels,
-                                 int bins_per_channel, int smoothness_prior, int iters_per_level, int band,
-                                 int n_bands, seeds_ctx **out)
+
+// Band geometry: band b = superpixel rows [b ny / n, (b+1) ny / n) (whole rows,
+// so every block of every level lies in one band).
+static seeds_status band_geometry(seeds_ctx *ctx, int n)
 {
-    if (!out || n_bands < 1 || band < 0 || band >= n_bands) return SEEDS_EINVAL;
+    if (n < 1 || n > SEEDS_MAX_BANDS || n > ctx->ny) return SEEDS_EINVAL;
+    for (int b = 0; b <= n; b++) {
+        const int j = (int)((long long)b * ctx->ny / n);
+        ctx->bj[b] = j;
+        ctx->by[b] = ctx->rowstart[(size_t)j << ctx->L];
+        ctx->bu[b] = ctx->L > 0 ? 2 * j : ctx->by[b];
+        ctx->bk[b] = j * ctx->nx;
+    }
+    for (int b = 0; b < n; b++)
+        if (ctx->by[b + 1] - ctx->by[b] < 2) return SEEDS_EINVAL;  // the halo logic needs >= 2 rows per band
+    ctx->banded = true;
+    ctx->nbands = n;
+    ctx->mode = SEEDS_MODE_GRID;
+    return SEEDS_OK;
+}
+
+// This process's band buffers: band `b` reuses the context's own plane and
+// histogram buffers; the other bands of a one-process run get their own.
+static seeds_status band_alloc(seeds_ctx *ctx, int b, bool own)
+{
+    if (own) {
+        ctx->b_lab[b] = ctx->d_labp;
+        for (int i = 0; i < 2; i++) {
+            ctx->b_H[b][i] = ctx->d_H[i];
+            ctx->b_A[b][i] = ctx->d_A[i];
+        }
+    } else {
+        CK(cudaMalloc(&ctx->b_lab[b], (size_t)ctx->labp_fs * 2));
+        CK(cudaMemset(ctx->b_lab[b], 0xFF, (size_t)ctx->labp_fs * 2));  // sentinel border
+        for (int i = 0; i < 2; i++) {
+            CK(cudaMalloc(&ctx->b_H[b][i], (size_t)ctx->H_fs * 4));
+            CK(cudaMalloc(&ctx->b_A[b][i], (size_t)ctx->Afs * 4));
+        }
+    }
+    CK(cudaMalloc(&ctx->b_ctl[b], 16));
+    CK(cudaMemset(ctx->b_ctl[b], 0, 16));
+    return SEEDS_OK;
+}
+
+struct SeedsNcclId {  // ncclUniqueId (128 bytes)
+    char internal[128];
+};
+
+// What a rank publishes to its peers: CUDA IPC handles of its band's plane,
+// histogram / size buffers and barrier words.
+struct BandBlob {
+    int magic, rank, world, pad;
+    cudaIpcMemHandle_t lab, H0, H1, A0, A1, ctl;
+};
+constexpr int BAND_MAGIC = 0x5EED5BAD;
+
+// NCCL, loaded at run time (bootstrap of seeds_create_banded only): the
+// library links no NCCL, and without one the multi-rank path reports SEEDS_ENCCL.
+struct NcclApi {
+    void *h = nullptr;
+    int (*getUniqueId)(void *) = nullptr;
+    int (*commInitRank)(void **, int, SeedsNcclId, int) = nullptr;
+    int (*allGather)(const void *, void *, size_t, int, void *, cudaStream_t) = nullptr;
+    int (*commDestroy)(void *) = nullptr;
+    const char *(*errStr)(int) = nullptr;
+};
+static NcclApi *nccl_api()
+{
+    static NcclApi api;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    if (api.h) return &api;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return nullptr;
+    api.getUniqueId = (int (*)(void *))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (int (*)(void **, int, SeedsNcclId, int))dlsym(h, "ncclCommInitRank");
+    api.allGather = (int (*)(const void *, void *, size_t, int, void *, cudaStream_t))dlsym(h, "ncclAllGather");
+    api.commDestroy = (int (*)(void *))dlsym(h, "ncclCommDestroy");
+    api.errStr = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
+    if (!api.getUniqueId || !api.commInitRank || !api.allGather || !api.commDestroy) return nullptr;
+    api.h = h;
+    return &api;
+}
+
+extern "C" {
+
+seeds_status seeds_nccl_unique_id(void *id)
+{
+    if (!id) return SEEDS_EINVAL;
+    NcclApi *a = nccl_api();
+    if (!a) return SEEDS_ENCCL;
+    return a->getUniqueId(id) == 0 ? SEEDS_OK : SEEDS_ENCCL;
+}
+
+seeds_status seeds_create_bands(int width, int height, int channels, int n_superpixels, int n_levels,
+                                int bins_per_channel, int smoothness_prior, int iters_per_level, int n_bands,
+                                seeds_ctx **out)
+{
+    if (!out) return SEEDS_EINVAL;
     seeds_ctx *ctx = nullptr;
     seeds_status st = seeds_create(width, height, channels, n_superpixels, n_levels, bins_per_channel,
                                    smoothness_prior, iters_per_level, &ctx);
     if (st != SEEDS_OK) return st;
-    if (n_bands > ctx->ny) {
-        seeds_destroy(ctx);
-        return SEEDS_EINVAL;
+    st = band_geometry(ctx, n_bands);
+    if (st == SEEDS_OK) st = ensure_frames(ctx, 1);
+    for (int b = 0; st == SEEDS_OK && b < n_bands; b++) st = band_alloc(ctx, b, b == 0);
+    ctx->bself = -1;
+    ctx->bsys = false;
+    if (st == SEEDS_OK && !plan_grid(ctx, 1)) {
+        snprintf(ctx->err, sizeof ctx->err, "no grid-mode tile plan fits the bands");
+        st = SEEDS_ERANGE;
     }
-    // bands are runs of whole superpixel rows, so every block of every level
-    // lies in one band
-    const int j0 = (int)((long long)band * ctx->ny / n_bands), j1 = (int)((long long)(band + 1) * ctx->ny / n_bands);
-    ctx->banded = true;
-    ctx->band = band;
-    ctx->band_n = n_bands;
-    ctx->band_y0 = ctx->rowstart[(size_t)j0 << ctx->L];
-    ctx->band_y1 = ctx->rowstart[(size_t)j1 << ctx->L];
-    ctx->band_u0 = ctx->L > 0 ? 2 * j0 : ctx->band_y0;
-    ctx->band_u1 = ctx->L > 0 ? 2 * j1 : ctx->band_y1;
-    if (ctx->band_y1 - ctx->band_y0 < 2) {
+    if (st != SEEDS_OK) {
         seeds_destroy(ctx);
-        return SEEDS_EINVAL;
-    }
-    ctx->mode = SEEDS_MODE_GRID;
-    ctx->brec_cap = (long long)(ctx->band_y1 - ctx->band_y0) * ctx->W + 32;
-    cudaError_t e = cudaMalloc(&ctx->d_bcount, 16);
-    if (e != cudaSuccess) {
-        seeds_destroy(ctx);
-        return e == cudaErrorMemoryAllocation ? SEEDS_ENOMEM : SEEDS_ECUDA;
-    }
-    if (!plan_grid(ctx, 1)) {
-        snprintf(ctx->err, sizeof ctx->err, "no grid-mode tile plan fits the band");
-        seeds_destroy(ctx);
-        return SEEDS_ERANGE;
+        return st;
     }
     *out = ctx;
     return SEEDS_OK;
 }
 
-seeds_status seeds_band_info(const seeds_ctx *ctx, int *row0, int *row1, long long *record_capacity,
-                             int *record_bytes)
+seeds_status seeds_band_export(seeds_ctx *ctx, void *blob, size_t cap, size_t *len)
+{
+    if (!ctx || !ctx->banded || ctx->bself < 0) return SEEDS_EINVAL;
+    if (len) *len = sizeof(BandBlob);
+    if (!blob) return SEEDS_OK;
+    if (cap < sizeof(BandBlob)) return SEEDS_EINVAL;
+    BandBlob x{};
+    const int r = ctx->bself;
+    x.magic = BAND_MAGIC;
+    x.rank = r;
+    x.world = ctx->nbands;
+    CK(cudaIpcGetMemHandle(&x.lab, ctx->b_lab[r]));
+    CK(cudaIpcGetMemHandle(&x.H0, ctx->b_H[r][0]));
+    CK(cudaIpcGetMemHandle(&x.H1, ctx->b_H[r][1]));
+    CK(cudaIpcGetMemHandle(&x.A0, ctx->b_A[r][0]));
+    CK(cudaIpcGetMemHandle(&x.A1, ctx->b_A[r][1]));
+    CK(cudaIpcGetMemHandle(&x.ctl, ctx->b_ctl[r]));
+    memcpy(blob, &x, sizeof x);
+    return SEEDS_OK;
+}
+
+seeds_status seeds_band_connect(seeds_ctx *ctx, const void *blobs, int world)
+{
+    if (!ctx || !ctx->banded || ctx->bself < 0 || !blobs || world != ctx->nbands) return SEEDS_EINVAL;
+    const BandBlob *x = static_cast<const BandBlob *>(blobs);
+    for (int r = 0; r < world; r++)
+        if (x[r].magic != BAND_MAGIC || x[r].rank != r || x[r].world != world) {
+            snprintf(ctx->err, sizeof ctx->err, "blob %d is not rank %d's of a %d-rank run", r, r, world);
+            return SEEDS_EINVAL;
+        }
+    for (int r = 0; r < world; r++) {
+        if (r == ctx->bself || ctx->b_mapped[r]) continue;
+        const unsigned fl = cudaIpcMemLazyEnablePeerAccess;
+        CK(cudaIpcOpenMemHandle((void **)&ctx->b_lab[r], x[r].lab, fl));
+        CK(cudaIpcOpenMemHandle((void **)&ctx->b_H[r][0], x[r].H0, fl));
+        CK(cudaIpcOpenMemHandle((void **)&ctx->b_H[r][1], x[r].H1, fl));
+        CK(cudaIpcOpenMemHandle((void **)&ctx->b_A[r][0], x[r].A0, fl));
+        CK(cudaIpcOpenMemHandle((void **)&ctx->b_A[r][1], x[r].A1, fl));
+        CK(cudaIpcOpenMemHandle((void **)&ctx->b_ctl[r], x[r].ctl, fl));
+        ctx->b_mapped[r] = true;
+    }
+    drop_graphs(ctx);
+    return SEEDS_OK;
+}
+
+seeds_status seeds_create_banded(int width, int height, int channels, int n_superpixels, int n_levels,
+                                 int bins_per_channel, int smoothness_prior, int iters_per_level, int rank, int world,
+                                 const void *nccl_id, seeds_ctx **out)
+{
+    if (!out || world < 1 || rank < 0 || rank >= world) return SEEDS_EINVAL;
+    seeds_ctx *ctx = nullptr;
+    seeds_status st = seeds_create(width, height, channels, n_superpixels, n_levels, bins_per_channel,
+                                   smoothness_prior, iters_per_level, &ctx);
+    if (st != SEEDS_OK) return st;
+    st = band_geometry(ctx, world);
+    if (st == SEEDS_OK) st = ensure_frames(ctx, 1);
+    if (st == SEEDS_OK) st = band_alloc(ctx, rank, true);
+    ctx->bself = rank;
+    ctx->bsys = true;
+    if (st == SEEDS_OK && !plan_grid(ctx, 1)) {
+        snprintf(ctx->err, sizeof ctx->err, "no grid-mode tile plan fits the band");
+        st = SEEDS_ERANGE;
+    }
+    if (st == SEEDS_OK && (world == 1 || nccl_id)) {
+        // bootstrap: every rank's IPC handles to every rank (one all-gather)
+        std::vector<BandBlob> all(world);
+        BandBlob mine{};
+        st = seeds_band_export(ctx, &mine, sizeof mine, nullptr);
+        if (st == SEEDS_OK && world == 1) all[0] = mine;
+        if (st == SEEDS_OK && world > 1) {
+            NcclApi *a = nccl_api();
+            void *comm = nullptr;
+            void *dev = nullptr;
+            SeedsNcclId id;
+            memcpy(&id, nccl_id, sizeof id);
+            if (!a) {
+                snprintf(ctx->err, sizeof ctx->err, "libnccl.so.2 not found");
+                st = SEEDS_ENCCL;
+            } else if (int r = a->commInitRank(&comm, world, id, rank)) {
+                snprintf(ctx->err, sizeof ctx->err, "ncclCommInitRank: %s", a->errStr ? a->errStr(r) : "error");
+                st = SEEDS_ENCCL;
+            } else {
+                const size_t bytes = sizeof(BandBlob);
+                cudaError_t e = cudaMalloc(&dev, bytes * (world + 1));
+                if (e == cudaSuccess) e = cudaMemcpy(dev, &mine, bytes, cudaMemcpyHostToDevice);
+                if (e != cudaSuccess) {
+                    st = cuda_fail(ctx, e, "band bootstrap buffer");
+                } else if (int r2 = a->allGather(dev, (char *)dev + bytes, bytes, 0 /* ncclInt8 */, comm, ctx->cap_stream)) {
+                    snprintf(ctx->err, sizeof ctx->err, "ncclAllGather: %s", a->errStr ? a->errStr(r2) : "error");
+                    st = SEEDS_ENCCL;
+                } else {
+                    e = cudaStreamSynchronize(ctx->cap_stream);
+                    if (e == cudaSuccess) e = cudaMemcpy(all.data(), (char *)dev + bytes, bytes * world, cudaMemcpyDeviceToHost);
+                    if (e != cudaSuccess) st = cuda_fail(ctx, e, "band bootstrap copy");
+                }
+                if (dev) cudaFree(dev);
+                a->commDestroy(comm);
+            }
+        }
+        if (st == SEEDS_OK) st = seeds_band_connect(ctx, all.data(), world);
+    }
+    if (st != SEEDS_OK) {
+        seeds_destroy(ctx);
+        return st;
+    }
+    *out = ctx;
+    return SEEDS_OK;
+}
+
+seeds_status seeds_band_info(const seeds_ctx *ctx, int *row0, int *row1, int *n_bands, int *band)
 {
     if (!ctx || !ctx->banded) return SEEDS_EINVAL;
-    if (row0) *row0 = ctx->band_y0;
-    if (row1) *row1 = ctx->band_y1;
-    if (record_capacity) *record_capacity = ctx->brec_cap;
-    if (record_bytes) *record_bytes = (int)sizeof(GRec);
+    const int b0 = ctx->bself >= 0 ? ctx->bself : 0, b1 = ctx->bself >= 0 ? ctx->bself + 1 : ctx->nbands;
+    if (row0) *row0 = ctx->by[b0];
+    if (row1) *row1 = ctx->by[b1];
+    if (n_bands) *n_bands = ctx->nbands;
+    if (band) *band = ctx->bself;
     return SEEDS_OK;
 }
 
-seeds_status seeds_band_seed(seeds_ctx *ctx, const uint8_t *image_u8, const int32_t *init_labels, void *stream)
+seeds_status seeds_band_run(seeds_ctx *ctx, const uint8_t *image_u8, const int32_t *init_labels, int32_t *labels_out,
+                            void *stream)
 {
-    if (!ctx || !ctx->banded || !image_u8) return SEEDS_EINVAL;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (!plan_grid(ctx, 1)) return SEEDS_ESTATE;
-    seeds_status r = ensure_labimg(ctx, 1);
-    if (r != SEEDS_OK) return r;
-    image_u8 = enqueue_lab(ctx, image_u8, 1, st);
-    CK(cudaMemsetAsync(ctx->d_H[0], 0, (size_t)ctx->H_fs * 4, st));
-    CK(cudaMemsetAsync(ctx->d_A[0], 0, (size_t)ctx->K * 4, st));
-    CK(cudaMemsetAsync(ctx->d_moves, 0, (size_t)(ctx->S + 1) * 4, st));
-    const GridParams &q = ctx->gp;
-    const dim3 g(grid1(ctx->N, 256, 1));
-    if (ctx->bb == 1)
-        k_band_seed<uint8_t><<<g, 256, 0, st>>>(image_u8, init_labels, ctx->W, ctx->H, ctx->C, ctx->bpc, ctx->L,
-                                                ctx->nx, ctx->B, ctx->K, ctx->d_bxof, ctx->d_byof, ctx->d_labp,
-                                                ctx->lpitch, (uint8_t *)q.binsp, q.bpitch, ctx->d_H[0], ctx->d_A[0], ctx->d_err);
-    else
-        k_band_seed<uint16_t><<<g, 256, 0, st>>>(image_u8, init_labels, ctx->W, ctx->H, ctx->C, ctx->bpc, ctx->L,
-                                                 ctx->nx, ctx->B, ctx->K, ctx->d_bxof, ctx->d_byof, ctx->d_labp,
-                                                 ctx->lpitch, (uint16_t *)q.binsp, q.bpitch, ctx->d_H[0], ctx->d_A[0], ctx->d_err);
-    CK(cudaGetLastError());
-    ctx->band_total = (init_labels ? 0 : 4 * ctx->L * ctx->iters) + ctx->P * ctx->P * ctx->iters;
-    ctx->band_seeded = true;
-    ctx->last_nf = 1;
-    ctx->last_final = 0;
-    ctx->last_done = 0;
-    ctx->ran = true;
-    ctx->band_warm = init_labels != nullptr;
-    ctx->band_init = init_labels;
-    return SEEDS_OK;
+    if (!ctx || !ctx->banded || !image_u8 || !labels_out) return SEEDS_EINVAL;
+    for (int b = 0; b < ctx->nbands; b++)
+        if (!ctx->b_lab[b]) {
+            snprintf(ctx->err, sizeof ctx->err, "band %d not connected (seeds_band_connect)", b);
+            return SEEDS_ESTATE;
+        }
+    return run(ctx, image_u8, init_labels, labels_out, 1, (cudaStream_t)stream);
 }
 
-seeds_status seeds_band_subsweep(seeds_ctx *ctx, int s, const void *records_in, const int32_t *n_in,
-                                 void *records_out, int32_t *n_out, void *stream)
-{
-    if (!ctx || !ctx->banded || !records_out || !n_out) return SEEDS_EINVAL;
-    if (!ctx->band_seeded || s < 0 || s >= ctx->band_total) return SEEDS_ESTATE;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (records_in && n_in) {
-        k_apply_records<<<ctx->n_sm, 256, 0, st>>>((const GRec *)records_in, n_in, ctx->B, ctx->d_H[0], ctx->d_A[0]);
-        CK(cudaGetLastError());
-    }
-    CK(cudaMemsetAsync(n_out, 0, 4, st));
-    CK(cudaMemsetAsync(ctx->d_sync, 0, 16, st));
-    GridParams q = ctx->gp;
-    q.img = nullptr; q.out = nullptr;
-    q.init = ctx->band_init;  // only tested against NULL: a warm run has no block levels
-    q.W = ctx->W; q.H = ctx->H; q.C = ctx->C; q.bpc = ctx->bpc; q.B = ctx->B; q.K = ctx->K; q.nx = ctx->nx;
-    q.L = ctx->L; q.iters = ctx->iters; q.limit = -1; q.S = ctx->S; q.nf = 1;
-    q.colstart = ctx->d_colstart; q.rowstart = ctx->d_rowstart; q.bxof = ctx->d_bxof; q.byof = ctx->d_byof;
-    q.lab = ctx->d_labp; q.lab_fs = ctx->labp_fs; q.lpitch = ctx->lpitch;
-    q.bins = ctx->d_bins; q.N = ctx->N;
-    for (int i = 0; i < 2; i++) {
-        q.Hb[i] = ctx->d_H[0];
-        q.Ab[i] = ctx->d_A[0];
-    }
-    q.H_fs = ctx->H_fs;
-    q.A_fs = ctx->Afs;
-    q.moves = ctx->d_moves;
-    q.sync = ctx->d_sync;
-    q.trace = nullptr;
-    q.band = 1;
-    q.s0 = s;
-    q.s1 = s + 1;
-    q.rec_out = (GRec *)records_out;
-    q.rec_count = n_out;
-    cudaError_t e;
-    if (ctx->grid_nt == GRID_THREADS)
-        e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS, 1>(ctx, q, st) : launch_grid_nt<GRID_THREADS, 0>(ctx, q, st);
-    else
-        e = ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS_SMALL, 1>(ctx, q, st)
-                           : launch_grid_nt<GRID_THREADS_SMALL, 0>(ctx, q, st);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid (band) launch");
-    ctx->last_done = s + 1;
-    return SEEDS_OK;
-}
-
-seeds_status seeds_band_halo(seeds_ctx *ctx, int put, uint16_t *top, uint16_t *bottom, void *stream)
-{
-    if (!ctx || !ctx->banded) return SEEDS_EINVAL;
-    cudaStream_t st = (cudaStream_t)stream;
-    const size_t pitch = (size_t)ctx->lpitch * 2, row = (size_t)ctx->W * 2;
-    auto at = [&](int y) { return ctx->d_labp + (size_t)(y + 2) * ctx->lpitch + 2; };
-    if (!put) {  // this band's first and last two rows
-        if (top) CK(cudaMemcpy2DAsync(top, row, at(ctx->band_y0), pitch, row, 2, cudaMemcpyDeviceToDevice, st));
-        if (bottom)
-            CK(cudaMemcpy2DAsync(bottom, row, at(ctx->band_y1 - 2), pitch, row, 2, cudaMemcpyDeviceToDevice, st));
-    } else {  // the neighbours' rows into this band's halo (none beyond the image)
-        if (top && ctx->band > 0)
-            CK(cudaMemcpy2DAsync(at(ctx->band_y0 - 2), pitch, top, row, row, 2, cudaMemcpyDeviceToDevice, st));
-        if (bottom && ctx->band + 1 < ctx->band_n)
-            CK(cudaMemcpy2DAsync(at(ctx->band_y1), pitch, bottom, row, row, 2, cudaMemcpyDeviceToDevice, st));
-    }
-    return SEEDS_OK;
-}
-
-seeds_status seeds_band_finish(seeds_ctx *ctx, const void *records_in, const int32_t *n_in, int32_t *labels_out,
-                               void *stream)
-{
-    if (!ctx || !ctx->banded || !labels_out) return SEEDS_EINVAL;
-    if (!ctx->band_seeded) return SEEDS_ESTATE;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (records_in && n_in) {  // the last sub-sweep's records
-        k_apply_records<<<ctx->n_sm, 256, 0, st>>>((const GRec *)records_in, n_in, ctx->B, ctx->d_H[0], ctx->d_A[0]);
-        CK(cudaGetLastError());
-    }
-    const long long n = (long long)(ctx->band_y1 - ctx->band_y0) * ctx->W;
-    k_band_emit<<<grid1(n, 256, 1), 256, 0, st>>>(ctx->d_labp, ctx->lpitch, ctx->W, ctx->band_y0, ctx->band_y1,
-                                                  labels_out);
-    CK(cudaGetLastError());
-    return SEEDS_OK;
-}
+}  // extern "C"
 
 const char *seeds_status_string(seeds_status s)
 {

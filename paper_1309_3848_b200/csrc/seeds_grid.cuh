@@ -35,7 +35,13 @@ namespace seeds {
 // the run is latency-bound) or 128 (four CTAs per SM; plans whose CTAs own
 // several tiles, so that four independent tile pipelines hide each other's
 // latencies).
+#ifndef SEEDS_MAX_BANDS
+#define SEEDS_MAX_BANDS 8
+#endif
 constexpr int GRID_THREADS = 512;
+// k_grid variants (template parameter VAR): the plain refinement, the
+// extended pixel path (means post-processing, priors), the row-band mode
+constexpr int VAR_PLAIN = 0, VAR_EXT = 1, VAR_BAND = 2;
 constexpr int STOP_NONE = 0x7F7F7F7F;  // "no stop" (a byte-wise memset value)
 // Acquire side of the grid barrier: 1 (default) one ld.acquire.gpu after the
 // relaxed poll, 2 a fence.acq_rel.gpu, 0 none (round 1's relaxed poll; relies
@@ -110,18 +116,10 @@ struct GridParams {
     int tx_bytes;                 // bytes one tile's TMA loads deliver (label box + bin box)
     int bw, bbw, bh;              // TMA boxes: label box bw x bh, bin box bbw x (bh - 4)
     int tiles_per_cta, q_cap, ntab, GX, GY, bins_res, rec_smem;
-    // row-band mode (one band of a multi-rank run): the
-    // launch runs sub-sweeps [s0, s1) of its own tiles against a single
-    // histogram buffer (0) that the host keeps current between launches,
-    // appends its delta records to rec_out / rec_count and applies none;
-    // the seed is done by k_band_seed.
-    int band, s0, s1;
     // A cache: each tile's staging also bulk-copies the sizes A of its frame
     // (snapshot buffer) into shared memory, so decisions read A there
     int acache;
     unsigned o_acache;
-    GRec *rec_out;
-    int *rec_count;
     float invGX, invGY;
     // anytime termination: with budget_ns > 0, CTA 0 compares
     // the device clock with the launch start at every sub-sweep boundary and,
@@ -135,7 +133,38 @@ struct GridParams {
     // [frame][dbg_ntop = (GX >> (L-1)) (GY >> (L-1)) blocks, row-major][B], or nullptr
     int *dbg_blk;
     long long dbg_ntop;
+    // row-band mode (k_grid<..., VAR_BAND>): one frame
+    // refined as nbands bands of whole superpixel rows.  Band b owns pixel rows
+    // [by[b], by[b+1]) and superpixels [bk[b], bk[b+1]) (the grid cells of its
+    // rows), and keeps the histograms of the superpixels it owns (pH[b], pA[b]:
+    // full-size buffers, only the owned rows used) and a label plane of its
+    // rows plus two halo rows each side (plab[b]).  Every read and update of
+    // H[k] / A[k] goes to k's owner; a label written within two rows of a band
+    // edge is also written into the neighbour's plane.  In one process on one
+    // GPU (bsys = 0) every band is in this launch (a tile's band in GridTile.
+    // pad) and the ordinary grid barrier separates sub-sweeps; across devices
+    // (bsys = 1: this launch is band `bself`, the peers' buffers are mapped
+    // peer memory) CTA 0 joins the ranks after the local barrier: a sys-scope
+    // release add on every band's counter, an acquire poll of its own.
+    int nbands, bsys, bself;
+    int by[SEEDS_MAX_BANDS + 1], bk[SEEDS_MAX_BANDS + 1];
+    int *pH[SEEDS_MAX_BANDS][2], *pA[SEEDS_MAX_BANDS][2];
+    uint16_t *plab[SEEDS_MAX_BANDS];
+    unsigned *pbar[SEEDS_MAX_BANDS];  // every band's band-arrival counter (monotonic across runs)
+    unsigned *bar_base;               // this band's: the counter value of its last completed barrier
+    unsigned *go;                     // local: the release word of the cross-device barrier
+    CUtensorMap tm_lab_b[SEEDS_MAX_BANDS];
 };
+
+// the band owning superpixel k (bands own contiguous id ranges; bk[b] is
+// INT_MAX for b >= nbands, so the sum needs no loop bound)
+__device__ __forceinline__ int band_owner(const GridParams &q, int k)
+{
+    int o = 0;
+#pragma unroll
+    for (int b = 1; b < SEEDS_MAX_BANDS; b++) o += k >= q.bk[b];
+    return o;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer()
 {
@@ -174,6 +203,17 @@ __device__ __forceinline__ void grid_poll(unsigned *ctr, unsigned target)
 #elif SEEDS_BARRIER_ACQ == 2
     asm volatile("fence.acq_rel.gpu;" ::: "memory");  // relaxed poll + fence: the same, as a fence pattern
 #endif
+}
+// the cross-device counterpart: relaxed sys-scope polls, then one acquire load
+__device__ __forceinline__ void sys_poll(unsigned *ctr, unsigned target)
+{
+    unsigned v;
+    long long spins = 0;
+    do {
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        if (++spins > (1LL << 26)) __trap();  // a rank that never arrives: fail loudly instead of hanging
+    } while ((int)(v - target) < 0);
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
 }
 __device__ __forceinline__ void grid_arrive(unsigned *ctr, unsigned &target)
 {
@@ -238,9 +278,10 @@ __device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *tm, int 
         : "memory");
 }
 
-template <typename BinT>
+template <typename BinT, int BAND = 0>
 struct GridCta {
     const GridParams &q;
+    int tband;         // the current tile's band (row-band mode)
     uint16_t *stage0;  // two TMA stage buffers: a tile's labels + 2-pixel halo, pitch bw
     BinT *sbins;       // bins: every owned tile (bins_res) or two TMA stage buffers
     uint32_t *rem;     // removable-ring LUT (8 words, reading Q8)
@@ -294,7 +335,8 @@ struct GridCta {
             tbp = q.bbw;
             bx0 = X0 & ~(16 / (int)sizeof(BinT) - 1);
         }
-        glab = q.lab + (long long)f * q.lab_fs;
+        if (BAND) tband = t.pad;
+        glab = (BAND ? q.plab[t.pad] : q.lab) + (long long)f * q.lab_fs;
         Hf0 = q.Hb[0] + (long long)f * q.H_fs;
         Hf1 = q.Hb[1] + (long long)f * q.H_fs;
         Af0 = q.Ab[0] + (long long)f * q.A_fs;
@@ -318,40 +360,65 @@ struct GridCta {
             bulk_load(sAc + (size_t)slot * q.A_fs, (ob ? q.Ab[1] : q.Ab[0]) + (long long)t.f * q.A_fs,
                       (unsigned)(q.A_fs * 4), &mbar[slot]);
         // box starts must be 16-byte aligned in x (the TMA faults otherwise)
-        tma_load3(reinterpret_cast<unsigned char *>(stage0) + slot * q.stage_bytes, tm_lab, t.X0 & ~7, t.Y0, t.f,
-                  &mbar[slot]);
+        tma_load3(reinterpret_cast<unsigned char *>(stage0) + slot * q.stage_bytes, BAND ? &q.tm_lab_b[t.pad] : tm_lab,
+                  t.X0 & ~7, t.Y0, t.f, &mbar[slot]);
         if (!q.bins_res)
             tma_load3(reinterpret_cast<unsigned char *>(sbins) + slot * q.bins_bytes, tm_bins,
                       t.X0 & ~(16 / (int)sizeof(BinT) - 1), t.Y0, t.f, &mbar[slot]);
     }
     // Histogram reads of a decision (the snapshot buffer ob of the sub-sweep)
+    // row-band mode: superpixel k's rows live with its owner band (one frame)
+    __device__ __forceinline__ const int *hrow(int buf, int k) const
+    {
+        if (BAND) return q.pH[band_owner(q, k)][buf] + (long long)k * q.B;
+        return (buf ? Hf1 : Hf0) + (long long)k * q.B;
+    }
+    __device__ __forceinline__ const int *aptr(int buf, int k) const
+    {
+        if (BAND) return q.pA[band_owner(q, k)][buf] + k;
+        return (buf ? Af1 : Af0) + k;
+    }
     __device__ __forceinline__ int ldA(int buf, int k) const
     {
-        if (q.acache) return sA[k];
-        return __ldcg((buf ? Af1 : Af0) + k);
+        if (q.acache) return sA[k];  // (row-band mode: only with one band, whose buffers are the context's)
+        return __ldcg(aptr(buf, k));
     }
-    __device__ __forceinline__ int ldH(int buf, int k, int b) const
-    {
-        return __ldcg((buf ? Hf1 : Hf0) + (long long)k * q.B + b);
-    }
+    __device__ __forceinline__ int ldH(int buf, int k, int b) const { return __ldcg(hrow(buf, k) + b); }
     // the same, issued only when p (ldcg_if): no L2 request for an empty slot
-    __device__ __forceinline__ int ldH_if(bool p, int buf, int k, int b) const
-    {
-        return ldcg_if(p, (buf ? Hf1 : Hf0) + (long long)k * q.B + b);
-    }
+    __device__ __forceinline__ int ldH_if(bool p, int buf, int k, int b) const { return ldcg_if(p, hrow(buf, k) + b); }
     __device__ __forceinline__ int ldA_if(bool p, int buf, int k) const
     {
         if (q.acache) return sA[k];
-        return ldcg_if(p, (buf ? Af1 : Af0) + k);
+        return ldcg_if(p, aptr(buf, k));
     }
     __device__ __forceinline__ void set(int x, int y, int v) const
     {
-        glab[(long long)(y + 2) * q.lpitch + x + 2] = (uint16_t)v;
+        const long long o = (long long)(y + 2) * q.lpitch + x + 2;
+        glab[o] = (uint16_t)v;
+        if (BAND) {  // within two rows of a band edge: the neighbour's halo too
+            if (tband > 0 && y < q.by[tband] + 2) {
+                q.plab[tband - 1][o] = (uint16_t)v;
+                misc[9] = 1;  // peer memory written in this sub-sweep (cross-device barrier)
+            }
+            if (tband + 1 < q.nbands && y >= q.by[tband + 1] - 2) {
+                q.plab[tband + 1][o] = (uint16_t)v;
+                misc[9] = 1;
+            }
+        }
     }
 };
 
+template <int BAND = 0>
 __device__ __forceinline__ void gdelta(const GridParams &q, int buf, int f, int k, int n, int b, int count)
 {
+    if (BAND) {  // each superpixel's counts at its owner band (one frame)
+        const int ok = band_owner(q, k), on = band_owner(q, n);
+        atomicAdd(q.pH[ok][buf] + (long long)k * q.B + b, -count);
+        atomicAdd(q.pH[on][buf] + (long long)n * q.B + b, count);
+        atomicAdd(q.pA[ok][buf] + k, -count);
+        atomicAdd(q.pA[on][buf] + n, count);
+        return;
+    }
     int *H = (buf ? q.Hb[1] : q.Hb[0]) + (long long)f * q.H_fs;
     int *A = (buf ? q.Ab[1] : q.Ab[0]) + (long long)f * q.A_fs;
     atomicAdd(H + (long long)k * q.B + b, -count);
@@ -576,16 +643,17 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
 {
     extern __shared__ __align__(128) uint32_t smem[];
     const GridParams &q = qp;
-    GridCta<BinT> c(q, reinterpret_cast<unsigned char *>(smem), &qp.tm_lab, &qp.tm_bins);
+    constexpr bool EXT = MEANS == VAR_EXT, BAND = MEANS == VAR_BAND;
+    GridCta<BinT, BAND> c(q, reinterpret_cast<unsigned char *>(smem), &qp.tm_lab, &qp.tm_bins);
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int W = q.W, B = q.B;
     const int TW = 2 * B + 2;  // warp table words
     unsigned target = 0;
-    GRec *const rec0 = q.band ? q.rec_out : q.rec_smem ? reinterpret_cast<GRec *>(reinterpret_cast<unsigned char *>(smem) + q.o_rec)
+    GRec *const rec0 = q.rec_smem ? reinterpret_cast<GRec *>(reinterpret_cast<unsigned char *>(smem) + q.o_rec)
                                   : q.rec + (long long)blockIdx.x * 2 * q.rec_cap;
-    GRec *const rec1 = q.band ? q.rec_out : rec0 + q.rec_cap;
-    auto rcount = [&](int b) { return q.band ? q.rec_count : &c.misc[b]; };
+    GRec *const rec1 = rec0 + q.rec_cap;
+    auto rcount = [&](int b) { return &c.misc[b]; };
     auto rec_list = [&](int b) { return b ? rec1 : rec0; };
 
     for (int i = tid; i < q.ntab * TW; i += NT) c.tabs[i] = 0;
@@ -593,6 +661,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     // misc[8]: the sub-sweeps after which the run stops -- seeds_debug_limit's
     // count, lowered by the anytime budget at a barrier (one shared load per check)
     if (tid == 8) c.misc[8] = q.limit >= 0 ? min(q.limit, STOP_NONE) : STOP_NONE;
+    if (tid == 9) c.misc[9] = 0;  // row-band mode: this CTA wrote peer memory since the last barrier
     if (tid < 8) c.rem[tid] = c_removable[tid];
     const int ntl = blockIdx.x < q.ntiles ? (q.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // tiles of this CTA
     for (int i = tid; i < ntl; i += NT) c.tiles[i] = q.tiles[blockIdx.x + (long long)i * gridDim.x];
@@ -606,14 +675,14 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     // from the parameters each time so that nothing stays live across the run
     auto means_sub = [&](int s_) {
         const int nlev = q.init == nullptr ? max(0, min(q.blk_hi, q.L - 1) - q.blk_lo + 1) : 0;
-        return MEANS && s_ >= 4 * nlev * q.iters + (q.iters - q.miters) * P * P;
+        return EXT && s_ >= 4 * nlev * q.iters + (q.iters - q.miters) * P * P;
     };
     __syncthreads();
 
     // ---- the seed ran before this launch (k_seed_cells): bins, labels and the
     // histograms are in global memory.  Plans that keep their tiles' bins in
     // shared memory for the whole run copy them in once (coalesced rows).
-    if (q.bins_res && !q.band) {
+    if (q.bins_res) {
         for (int ti = 0; ti < ntl; ti++) {
             const GridTile t = c.tiles[ti];
             const int tw = t.X1 - t.X0;
@@ -626,14 +695,37 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     // Grid barrier at a sub-sweep boundary, after which `next` sub-sweeps are
     // done; it carries the anytime stop decision (q.budget_ns).
     const unsigned long long t_start = globaltimer();
+    // Across devices (row-band mode, q.bsys) the local barrier is followed by
+    // the ranks' one: once every local CTA arrived, CTA 0 adds one to every
+    // band's counter (sys-scope release); every CTA then waits for nbands
+    // arrivals on its own band's counter (sys-scope acquire).  The counters
+    // only grow; *bar_base carries the last target from run to run.
+    unsigned btarget = 0;
+    if (BAND && q.bsys && tid == 0)
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(btarget) : "l"(q.bar_base) : "memory");
     auto boundary = [&](int next) {
         __syncthreads();
         target += gridDim.x;
         if (tid == 0) {
             if (q.budget_ns > 0 && blockIdx.x == 0 && (long long)(globaltimer() - t_start) >= q.budget_ns)
                 asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(q.stop), "r"(next) : "memory");
-            grid_signal(q.sync);
-            grid_poll(q.sync, target);
+            if (BAND && q.bsys) {
+                if (c.misc[9]) {  // this CTA's writes to peer memory first (its local ones go with the local barrier)
+                    asm volatile("fence.acq_rel.sys;" ::: "memory");
+                    c.misc[9] = 0;
+                }
+                grid_signal(q.sync);
+                if (blockIdx.x == 0) {
+                    grid_poll(q.sync, target);
+                    for (int r = 0; r < q.nbands; r++)
+                        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(q.pbar[r]) : "memory");
+                }
+                btarget += q.nbands;
+                sys_poll(q.pbar[q.bself], btarget);
+            } else {
+                grid_signal(q.sync);
+                grid_poll(q.sync, target);
+            }
             if (q.budget_ns > 0) {
                 int v;
                 asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(q.stop) : "memory");
@@ -677,6 +769,39 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
 #endif
     };
     __syncthreads();  // the resident bins are in place
+    if (BAND && q.bsys) {
+        boundary(0);  // every rank's seed (and its halo rows in our plane) is done, its buffers zeroed
+        if (q.init) {
+            // warm start across devices: the histogram counts of this band's rows,
+            // to each label's owner band (warp-aggregated atomics), then one more
+            // barrier before any decision reads them
+            for (int ti = 0; ti < ntl; ti++) {
+                const GridTile t = c.tiles[ti];
+                const uint16_t *gl = q.plab[t.pad];
+                const BinT *bp = static_cast<const BinT *>(q.binsp);
+                for (int y = t.Y0 + wid; y < t.Y1; y += NW)
+                    for (int x0 = t.X0; x0 < t.X1; x0 += 32) {
+                        const int x = x0 + lane;
+                        const bool in = x < t.X1;
+                        const int k = in ? (int)gl[(long long)(y + 2) * q.lpitch + x + 2] : -1;
+                        const int b = in ? (int)bp[(long long)y * q.bpitch + x] : 0;
+                        const int o = in ? band_owner(q, k) : 0;
+                        unsigned m = __match_any_sync(FULL, in ? k * B + b : -1);
+                        if (in && lane == __ffs(m) - 1) {
+                            atomicAdd(q.pH[o][0] + (long long)k * B + b, __popc(m));
+                            atomicAdd(q.pH[o][1] + (long long)k * B + b, __popc(m));
+                            if (o != q.bself) c.misc[9] = 1;
+                        }
+                        m = __match_any_sync(FULL, k);
+                        if (in && lane == __ffs(m) - 1) {
+                            atomicAdd(q.pA[o][0] + k, __popc(m));
+                            atomicAdd(q.pA[o][1] + k, __popc(m));
+                        }
+                    }
+            }
+            boundary(0);
+        }
+    }
     stamp(0, 1);
     auto count_moves = [&](bool moved) {
         const unsigned mv = __ballot_sync(FULL, moved);
@@ -686,14 +811,16 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     // buffer yb and reset the list that sub-sweep s fills.
     auto begin_subsweep = [&](int yb) {
         if (tid == 0 && ntl > 0) c.issue(c.tiles[0], 0, (yb ^ 1));  // overlaps the replay
-        const int nrec = q.band ? 0 : c.misc[yb];
+        const int nrec = c.misc[yb];
         const GRec *r = rec_list(yb);
         for (int e = tid; e < nrec; e += NT) {
             const GRec x = r[e];
-            gdelta(q, yb, (int)x.f, x.kn & 0xFFFF, x.kn >> 16, x.bc & 0xFFFF, x.bc >> 16);
+            gdelta<BAND>(q, yb, (int)x.f, x.kn & 0xFFFF, x.kn >> 16, x.bc & 0xFFFF, x.bc >> 16);
+            if (BAND && q.bsys && (band_owner(q, x.kn & 0xFFFF) != q.bself || band_owner(q, x.kn >> 16) != q.bself))
+                c.misc[9] = 1;
             if (means_sub(s - 1)) gdelta_s(q, yb, (int)x.f, x.kn & 0xFFFF, x.kn >> 16, x.pad);
         }
-        if (tid == 0 && !q.band) c.misc[yb ^ 1] = 0;  // list yb^1 was last read before the barrier
+        if (tid == 0) c.misc[yb ^ 1] = 0;  // list yb^1 was last read before the barrier
         __syncthreads();  // the reset precedes every append of this sub-sweep
         stamp(s + 1, 2);
     };
@@ -728,7 +855,8 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     // A move k -> n of `count` pixels of bin b: record + histogram deltas.
     auto emit = [&](GRec *r, int slot, int k, int n, int b, int count, int yb) {
         r[slot] = GRec{(uint32_t)k | ((uint32_t)n << 16), (uint32_t)b | ((uint32_t)count << 16), (uint32_t)c.f, 0u};
-        if (!q.band) gdelta(q, yb, c.f, k, n, b, count);
+        gdelta<BAND>(q, yb, c.f, k, n, b, count);
+        if (BAND && q.bsys && (band_owner(q, k) != q.bself || band_owner(q, n) != q.bself)) c.misc[9] = 1;
     };
 
     const bool blocks = q.init == nullptr && q.L > 0;
@@ -741,13 +869,8 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
             for (int it = l > q.blk_hi || l < q.blk_lo ? q.iters : 0; it < q.iters; it++)
                 for (int col = 0; col < 4; col++) {
                     if (stopped()) break;
-                    if (s < q.s0) {  // band mode: sub-sweeps of earlier launches
-                        s++;
-                        continue;
-                    }
-                    if (q.s1 >= 0 && s >= q.s1) break;
                     const int cx = col & 1, cy = col >> 1;
-                    const int ob = q.band ? 0 : s & 1, yb_ = ob ^ 1;
+                    const int ob = s & 1, yb_ = ob ^ 1;
                     begin_subsweep(yb_);
                     for (int ti = 0; ti < ntl; ti++) {
                         if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1, ob);
@@ -1092,12 +1215,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     for (int it = 0; it < q.iters; it++)
         for (int col = 0; col < P * P; col++) {
             if (stopped()) break;
-            if (s < q.s0) {
-                s++;
-                continue;
-            }
-            if (q.s1 >= 0 && s >= q.s1) break;
-            if (MEANS && it == q.iters - q.miters && col == 0) {
+            if (EXT && it == q.iters - q.miters && col == 0) {
                 // channel sums S[k][c] of the current labels into both buffers
                 // (reading M1): warp-aggregated per label, then combined per CTA in a
                 // small direct-mapped table (key = frame << 16 | label) kept in the
@@ -1174,7 +1292,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                 }
                 grid_barrier(q.sync, target);
             }
-            if (MEANS && q.compact && col == 0) {
+            if (EXT && q.compact && col == 0) {
                 // reading M5: centres of gravity of the current labels for this pixel
                 // iteration -- coordinate sums per label (warp-aggregated, then one set
                 // of atomics per label and CTA through a shared-memory table), a grid
@@ -1240,7 +1358,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                 grid_barrier(q.sync, target);
             }
             const int cx = col % P, cy = col / P;
-            const int ob = q.band ? 0 : s & 1, yb_ = ob ^ 1;
+            const int ob = s & 1, yb_ = ob ^ 1;
             begin_subsweep(yb_);
             for (int ti = 0; ti < ntl; ti++) {
                 if (tid == 0 && ti + 1 < ntl) c.issue(c.tiles[ti + 1], (ti + 1) & 1, ob);
@@ -1415,7 +1533,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                         c.set(u.xy & 0xFFFF, u.xy >> 16, u.acc);
                     }
                 };
-                if (MEANS && (q.compact || q.edge_tau || it >= q.iters - q.miters)) {
+                if (EXT && (q.compact || q.edge_tau || it >= q.iters - q.miters)) {
                     // extended pixel sub-sweep: one thread per unit, no move across a colour
                     // edge with the edge prior (reading M6); the first candidate (W, E, N, S)
                     // passing the colour test -- the means test in the means iterations
@@ -1557,17 +1675,18 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
 
     // ---- outputs: the int32 labels are written by k_emit_planes, the next
     // launch on the stream (a streaming kernel at full occupancy)
-    if (q.band) return;  // band mode: seeds_band_finish emits the band's rows
     if (blockIdx.x == 0 && tid == 0 && q.done) *q.done = s;
+    if (BAND && q.bsys && blockIdx.x == 0 && tid == 0) *q.bar_base = btarget;  // the next run continues from here
 }
 
 // Emit (a12): int32 labels of nf frames from the padded u16 label planes --
 // one thread per output pixel, grid-stride, coalesced in both planes.
-// One CTA per output row (blockIdx.x = frame * H + y): no index division.
+// One CTA per output row (blockIdx.x = frame * nrows + row - y0; rows
+// [y0, y0 + nrows) of every frame): no per-pixel index division.
 __global__ void __launch_bounds__(256) k_emit_planes(const uint16_t *lab, long long lab_fs, int lpitch, int W, int H,
-                                                    int32_t *out)
+                                                    int y0, int nrows, int32_t *out)
 {
-    const int f = blockIdx.x / H, y = blockIdx.x - f * H;
+    const int f = blockIdx.x / nrows, y = y0 + blockIdx.x - f * nrows;
     const uint16_t *src = lab + (long long)f * lab_fs + (long long)(y + 2) * lpitch + 2;
     int32_t *dst = out + ((long long)f * H + y) * W;
     for (int x = threadIdx.x; x < W; x += blockDim.x) dst[x] = __ldcg(src + x);
@@ -1586,22 +1705,27 @@ __global__ void __launch_bounds__(256) k_emit_planes(const uint16_t *lab, long l
 //    and no memset of H is needed.
 //  * Warm start (reading O9): labels come from init (range-checked); counts go
 //    to global memory with warp-aggregated atomics (H zeroed beforehand).
-template <typename BinT>
+template <typename BinT, int BAND>
 __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
 {
     extern __shared__ int shist[];  // [4][B] top-level block histograms (cold)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int cell = blockIdx.x, f = blockIdx.y;
+    // row-band mode: the cells of this launch's bands (all of them in one
+    // process; band bself's across devices), each seeded into its owner band
+    const int cell = BAND && q.bsys ? q.bk[q.bself] + blockIdx.x : blockIdx.x, f = blockIdx.y;
+    const int band = BAND ? band_owner(q, cell) : 0;
     const int cx = cell % q.nx, cy = cell / q.nx, L = q.L, B = q.B, W = q.W;
     const bool cold = q.init == nullptr;
     const int x0 = q.colstart[cx << L], x1 = q.colstart[(cx + 1) << L];
     const int y0 = q.rowstart[cy << L], y1 = q.rowstart[(cy + 1) << L];
     const int xm = L > 0 ? q.colstart[(2 * cx + 1) << (L - 1)] : x1;  // the top-level block split
     const int ym = L > 0 ? q.rowstart[(2 * cy + 1) << (L - 1)] : y1;
-    int *H0 = q.Hb[0] + (long long)f * q.H_fs, *H1 = q.Hb[1] + (long long)f * q.H_fs;
-    int *A0 = q.Ab[0] + (long long)f * q.A_fs, *A1 = q.Ab[1] + (long long)f * q.A_fs;
+    int *H0 = (BAND ? q.pH[band][0] : q.Hb[0]) + (long long)f * q.H_fs;
+    int *H1 = (BAND ? q.pH[band][1] : q.Hb[1]) + (long long)f * q.H_fs;
+    int *A0 = (BAND ? q.pA[band][0] : q.Ab[0]) + (long long)f * q.A_fs;
+    int *A1 = (BAND ? q.pA[band][1] : q.Ab[1]) + (long long)f * q.A_fs;
     BinT *bp = static_cast<BinT *>(q.binsp) + (long long)f * q.binsp_fs;
-    uint16_t *gl = q.lab + (long long)f * q.lab_fs;
+    uint16_t *gl = (BAND ? q.plab[band] : q.lab) + (long long)f * q.lab_fs;
     const long long fN = (long long)f * q.N;
     if (cold) {
         for (int i = tid; i < 4 * B; i += blockDim.x) shist[i] = 0;
@@ -1640,23 +1764,39 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
                 for (int ch = 0; ch < q.C; ch++) b = b * q.bpc + (((int)(rgb[u] >> (8 * ch) & 0xFF) * q.bpc) >> 8);
                 bp[(long long)y * q.bpitch + x] = (BinT)b;
                 if (!cold) k = checked_label(lk[u], q.K, q.err);
-                gl[(long long)(y + 2) * q.lpitch + x + 2] = (uint16_t)k;
+                const long long o = (long long)(y + 2) * q.lpitch + x + 2;
+                gl[o] = (uint16_t)k;
+                if (BAND) {  // rows within two of a band edge: the neighbour's halo too
+                    if (band > 0 && y < q.by[band] + 2) q.plab[band - 1][o] = (uint16_t)k;
+                    if (band + 1 < q.nbands && y >= q.by[band + 1] - 2) q.plab[band + 1][o] = (uint16_t)k;
+                }
             }
-            if (cold) {
+            if (BAND && !cold && q.bsys) {
+                // across devices the owners' buffers are zeroed by their own
+                // ranks: k_grid counts warm labels after its first barrier
+            } else if (cold) {
                 const int key = in ? ((y >= ym ? 2 : 0) + (x >= xm ? 1 : 0)) * B + b : -1;
                 const unsigned m = __match_any_sync(FULL, key);
                 if (in && lane == __ffs(m) - 1) atomicAdd(&shist[key], __popc(m));
             } else {
                 const int key = in ? k * B + b : -1;
+                int *h0 = H0, *h1 = H1, *a0 = A0, *a1 = A1;
+                if (BAND && in) {  // a warm label's counts go to its owner band
+                    const int o = band_owner(q, k);
+                    h0 = q.pH[o][0];
+                    h1 = q.pH[o][1];
+                    a0 = q.pA[o][0];
+                    a1 = q.pA[o][1];
+                }
                 unsigned m = __match_any_sync(FULL, key);
                 if (in && lane == __ffs(m) - 1) {
-                    atomicAdd(H0 + key, __popc(m));
-                    atomicAdd(H1 + key, __popc(m));
+                    atomicAdd(h0 + key, __popc(m));
+                    atomicAdd(h1 + key, __popc(m));
                 }
                 m = __match_any_sync(FULL, in ? k : -1);
                 if (in && lane == __ffs(m) - 1) {
-                    atomicAdd(A0 + k, __popc(m));
-                    atomicAdd(A1 + k, __popc(m));
+                    atomicAdd(a0 + k, __popc(m));
+                    atomicAdd(a1 + k, __popc(m));
                 }
             }
         }
@@ -1689,62 +1829,6 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
         for (int w = 0; w < (int)(blockDim.x / 32); w++) a += wsum[w];
         A0[cell] = a;
         A1[cell] = a;
-    }
-}
-
-// Band mode seed (every rank seeds the whole frame, the image being
-// replicated): bins into the padded bin plane, grid or warm-start labels into
-// the padded label plane, and the histogram counts (Eq. 6) of every pixel into
-// buffer 0 -- one thread per pixel, atomics warp-aggregated on (label, bin).
-template <typename BinT>
-__global__ void __launch_bounds__(256) k_band_seed(const uint8_t *img, const int32_t *init, int W, int H, int C,
-                                                   int bpc, int L, int nx, int B, int K, const int *bxof,
-                                                   const int *byof, uint16_t *lab, int lpitch, BinT *binsp,
-                                                   int bpitch, int *Hb, int *Ab, int *err)
-{
-    const long long N = (long long)W * H;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < N; base += (long long)gridDim.x * blockDim.x) {
-        const long long p = base + threadIdx.x;
-        const int lane = threadIdx.x & 31;
-        int key = -1, k = -1;
-        if (p < N) {
-            const int y = (int)(p / W), x = (int)(p - (long long)y * W);
-            int b = 0;
-            for (int ch = 0; ch < C; ch++) b = b * bpc + (((int)img[p * C + ch] * bpc) >> 8);
-            binsp[(long long)y * bpitch + x] = (BinT)b;
-            k = init ? checked_label(init[p], K, err) : (byof[y] >> L) * nx + (bxof[x] >> L);
-            lab[(long long)(y + 2) * lpitch + x + 2] = (uint16_t)k;
-            key = k * B + b;
-        }
-        unsigned m = __match_any_sync(FULL, key);
-        if (p < N && lane == __ffs(m) - 1) atomicAdd(Hb + key, __popc(m));
-        m = __match_any_sync(FULL, k);
-        if (p < N && lane == __ffs(m) - 1) atomicAdd(Ab + k, __popc(m));
-    }
-}
-
-// Band mode: int32 labels of pixel rows [y0, y1) from the padded label plane.
-__global__ void __launch_bounds__(256) k_band_emit(const uint16_t *lab, int lpitch, int W, int y0, int y1, int32_t *out)
-{
-    const long long n = (long long)(y1 - y0) * W;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const int y = y0 + (int)(i / W), x = (int)(i - (long long)(y - y0) * W);
-        out[(long long)y * W + x] = lab[(long long)(y + 2) * lpitch + x + 2];
-    }
-}
-
-// Band mode: apply every rank's delta records of the previous sub-sweep to this
-// rank's histogram replica (buffer 0), in any order (integer sums commute).
-__global__ void __launch_bounds__(256) k_apply_records(const GRec *r, const int *n, int B, int *Hb, int *Ab)
-{
-    const int cnt = *n;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
-        const GRec x = r[e];
-        const int k = x.kn & 0xFFFF, nn = x.kn >> 16, b = x.bc & 0xFFFF, c = x.bc >> 16;
-        atomicSub(Hb + (long long)k * B + b, c);
-        atomicAdd(Hb + (long long)nn * B + b, c);
-        atomicSub(Ab + k, c);
-        atomicAdd(Ab + nn, c);
     }
 }
 

@@ -25,7 +25,7 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_read_state", "seeds_debug_limit", "seeds_stats", "seeds_sync", "seeds_destroy",
            "seeds_profile", "seeds_profile_collect", "seeds_set_mode", "seeds_debug_trace",
            "seeds_status_string", "seeds_last_error", "seeds_create_banded", "seeds_band_info",
-           "seeds_band_seed", "seeds_band_subsweep", "seeds_band_halo", "seeds_band_finish",
+           "seeds_create_bands", "seeds_nccl_unique_id", "seeds_band_export", "seeds_band_connect", "seeds_band_run",
            "seeds_set_means_iters", "seeds_read_sums", "seeds_metrics", "seeds_set_colour_space",
            "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks", "seeds_set_compactness",
            "seeds_set_edge_prior", "seeds_batch_host_warm", "seeds_validate_labels", "seeds_set_validate",
@@ -97,12 +97,13 @@ def load(path: str = LIB_PATH):
         "seeds_debug_trace": ([vp, i, vp, i], i),
         "seeds_profile_collect": ([vp, vp, vp, vp], i),
         "seeds_destroy": ([vp], None),
-        "seeds_create_banded": ([i] * 10 + [ctypes.POINTER(vp)], i),
+        "seeds_create_banded": ([i] * 10 + [vp, ctypes.POINTER(vp)], i),
+        "seeds_create_bands": ([i] * 9 + [ctypes.POINTER(vp)], i),
+        "seeds_nccl_unique_id": ([vp], i),
+        "seeds_band_export": ([vp, vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)], i),
+        "seeds_band_connect": ([vp, vp, i], i),
         "seeds_band_info": ([vp, vp, vp, vp, vp], i),
-        "seeds_band_seed": ([vp, vp, vp, vp], i),
-        "seeds_band_subsweep": ([vp, i, vp, vp, vp, vp, vp], i),
-        "seeds_band_halo": ([vp, i, vp, vp, vp], i),
-        "seeds_band_finish": ([vp, vp, vp, vp, vp], i),
+        "seeds_band_run": ([vp, vp, vp, vp, vp], i),
         "seeds_status_string": ([i], ctypes.c_char_p),
         "seeds_last_error": ([vp], ctypes.c_char_p),
     }
@@ -424,50 +425,85 @@ class Seeds:
         self._check(self._lib.seeds_sync(self._ctx, _stream_ptr(stream)))
 
 
-class SeedsBand(Seeds):
-    """One band of a row-band run (seeds_create_banded ... seeds_band_finish).
-    The schedule and the exchange between bands are driven by ``bands.py``."""
+def nccl_unique_id() -> bytes:
+    """A new NCCL unique id (128 bytes) for SeedsBand's bootstrap (rank 0
+    creates it, the caller distributes it; include/seeds.h seeds_nccl_unique_id)."""
+    lib = load()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.seeds_nccl_unique_id(buf)
+    if st != 0:
+        raise SeedsError(st)
+    return buf.raw
+
+
+class _BandMixin:
+    """Row-band run of one frame (include/seeds.h "Row-band mode")."""
+
+    def _band_init(self):
+        r0, r1, nb, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        self._check(self._lib.seeds_band_info(self._ctx, ctypes.byref(r0), ctypes.byref(r1), ctypes.byref(nb),
+                                              ctypes.byref(b)))
+        self.row0, self.row1, self.n_bands, self.band = r0.value, r1.value, nb.value, b.value
+
+    def run(self, image, init_labels=None, labels_out=None, stream=None):
+        """(H, W, C) uint8 CUDA tensor (the whole frame) [+ (H, W) int32 warm-start
+        labels] -> (H, W) int32 CUDA tensor; this context's rows are written."""
+        import torch
+        self._frames(image)
+        if labels_out is None:
+            labels_out = torch.zeros((self.height, self.width), dtype=torch.int32, device=image.device)
+        self._check(self._lib.seeds_band_run(self._ctx, image.data_ptr(),
+                                             None if init_labels is None else init_labels.data_ptr(),
+                                             labels_out.data_ptr(), _stream_ptr(stream)))
+        return labels_out
+
+
+class SeedsBands(_BandMixin, Seeds):
+    """Every band of a row-band run in this process, one launch on the current
+    device (seeds_create_bands)."""
 
     def __init__(self, width: int, height: int, channels: int, n_superpixels: int, n_levels: int,
-                 bins_per_channel: int, smoothness_prior: int, iters_per_level: int, band: int,
-                 n_bands: int):
+                 bins_per_channel: int, smoothness_prior: int, iters_per_level: int, n_bands: int):
         self._lib = load()
         self._ctx = ctypes.c_void_p()
-        st = self._lib.seeds_create_banded(width, height, channels, n_superpixels, n_levels,
-                                           bins_per_channel, int(smoothness_prior), iters_per_level,
-                                           band, n_bands, ctypes.byref(self._ctx))
+        st = self._lib.seeds_create_bands(width, height, channels, n_superpixels, n_levels, bins_per_channel,
+                                          int(smoothness_prior), iters_per_level, n_bands, ctypes.byref(self._ctx))
         if st != 0:
             raise SeedsError(st)
         self.width, self.height, self.channels = width, height, channels
-        self.band, self.n_bands = band, n_bands
-        self.iters = iters_per_level
         self._refresh()
-        r0, r1, cap, rb = ctypes.c_int(), ctypes.c_int(), ctypes.c_longlong(), ctypes.c_int()
-        self._check(self._lib.seeds_band_info(self._ctx, ctypes.byref(r0), ctypes.byref(r1),
-                                              ctypes.byref(cap), ctypes.byref(rb)))
-        self.row0, self.row1, self.record_capacity, self.record_bytes = r0.value, r1.value, cap.value, rb.value
-        self.subsweeps = 0
+        self._band_init()
 
-    def seed(self, image, init_labels=None, stream=None):
-        self._frames(image)
-        self._check(self._lib.seeds_band_seed(self._ctx, image.data_ptr(),
-                                              None if init_labels is None else init_labels.data_ptr(),
-                                              _stream_ptr(stream)))
-        P = self.info.colour_period
-        self.subsweeps = (0 if init_labels is not None else 4 * self.info.levels_eff * self.iters) + P * P * self.iters
 
-    def subsweep(self, s: int, records_in, n_in, records_out, n_out, stream=None):
-        self._check(self._lib.seeds_band_subsweep(
-            self._ctx, s, None if records_in is None else records_in.data_ptr(),
-            None if n_in is None else n_in.data_ptr(), records_out.data_ptr(), n_out.data_ptr(),
-            _stream_ptr(stream)))
+class SeedsBand(_BandMixin, Seeds):
+    """Band `rank` of a `world`-rank row-band run, one device per rank
+    (seeds_create_banded).  nccl_id (bytes from nccl_unique_id(), the same on
+    every rank): the library exchanges the ranks' CUDA IPC handles itself;
+    None with world > 1: call connect() with every rank's export() blob."""
 
-    def halo(self, put: bool, top, bottom, stream=None):
-        self._check(self._lib.seeds_band_halo(self._ctx, int(put), None if top is None else top.data_ptr(),
-                                              None if bottom is None else bottom.data_ptr(),
-                                              _stream_ptr(stream)))
+    def __init__(self, width: int, height: int, channels: int, n_superpixels: int, n_levels: int,
+                 bins_per_channel: int, smoothness_prior: int, iters_per_level: int, rank: int, world: int,
+                 nccl_id: bytes | None = None):
+        self._lib = load()
+        self._ctx = ctypes.c_void_p()
+        idbuf = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
+        st = self._lib.seeds_create_banded(width, height, channels, n_superpixels, n_levels, bins_per_channel,
+                                           int(smoothness_prior), iters_per_level, rank, world, idbuf,
+                                           ctypes.byref(self._ctx))
+        if st != 0:
+            raise SeedsError(st)
+        self.width, self.height, self.channels = width, height, channels
+        self._refresh()
+        self._band_init()
 
-    def finish(self, records_in, n_in, labels_out, stream=None):
-        self._check(self._lib.seeds_band_finish(
-            self._ctx, None if records_in is None else records_in.data_ptr(),
-            None if n_in is None else n_in.data_ptr(), labels_out.data_ptr(), _stream_ptr(stream)))
+    def export(self) -> bytes:
+        n = ctypes.c_size_t()
+        self._check(self._lib.seeds_band_export(self._ctx, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        self._check(self._lib.seeds_band_export(self._ctx, buf, n.value, ctypes.byref(n)))
+        return buf.raw
+
+    def connect(self, blobs):
+        """blobs: every rank's export(), in rank order."""
+        data = b"".join(blobs)
+        self._check(self._lib.seeds_band_connect(self._ctx, data, len(blobs)))
