@@ -43,6 +43,22 @@ constexpr int GRID_THREADS = 512;
 // extended pixel path (means post-processing, priors), the row-band mode
 constexpr int VAR_PLAIN = 0, VAR_EXT = 1, VAR_BAND = 2;
 constexpr int STOP_NONE = 0x7F7F7F7F;  // "no stop" (a byte-wise memset value)
+// Bounds-checked build (-DSEEDS_CHECKED, scripts/build_checked.sh): every
+// histogram / size index, label-plane write, staged-tile read and record slot
+// of k_grid is range-checked and a violation traps (the launch fails with an
+// error instead of touching memory it does not own) -- the stand-in for
+// compute-sanitizer memcheck, which this GPU pool does not allow.
+#ifdef SEEDS_CHECKED
+#define SEEDS_CHECK(cond) \
+    do {                  \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define SEEDS_CHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 // Acquire side of the grid barrier: 1 (default) one ld.acquire.gpu after the
 // relaxed poll, 2 a fence.acq_rel.gpu, 0 none (round 1's relaxed poll; relies
 // on every cross-CTA read bypassing L1).  DESIGN.md section 6.
@@ -344,9 +360,14 @@ struct GridCta {
     }
     __device__ __forceinline__ const uint16_t *cell(int x, int y) const
     {
+        SEEDS_CHECK(y >= Y0 - 2 && y < Y1 + 2 && x + 2 - sx0 >= 0 && x + 2 - sx0 < sp && (y - Y0 + 2) < q.bh);
         return stage + (y - Y0 + 2) * sp + (x + 2 - sx0);
     }
-    __device__ __forceinline__ int bin(int x, int y) const { return tb[(y - Y0) * tbp + (x - bx0)]; }
+    __device__ __forceinline__ int bin(int x, int y) const
+    {
+        SEEDS_CHECK(x >= X0 && x < X1 && y >= Y0 && y < Y1);
+        return tb[(y - Y0) * tbp + (x - bx0)];
+    }
     // level-0 block column / row starts: colstart[i] = floor(i W / GX) (reading O2)
     __device__ __forceinline__ int colx(int i) const { return div_small(i * q.W, q.GX, q.invGX); }
     __device__ __forceinline__ int rowy(int j) const { return div_small(j * q.H, q.GY, q.invGY); }
@@ -370,11 +391,13 @@ struct GridCta {
     // row-band mode: superpixel k's rows live with its owner band (one frame)
     __device__ __forceinline__ const int *hrow(int buf, int k) const
     {
+        SEEDS_CHECK(k >= 0 && k < q.K && (buf == 0 || buf == 1));
         if (BAND) return q.pH[band_owner(q, k)][buf] + (long long)k * q.B;
         return (buf ? Hf1 : Hf0) + (long long)k * q.B;
     }
     __device__ __forceinline__ const int *aptr(int buf, int k) const
     {
+        SEEDS_CHECK(k >= 0 && k < q.K);
         if (BAND) return q.pA[band_owner(q, k)][buf] + k;
         return (buf ? Af1 : Af0) + k;
     }
@@ -393,6 +416,7 @@ struct GridCta {
     }
     __device__ __forceinline__ void set(int x, int y, int v) const
     {
+        SEEDS_CHECK(x >= X0 && x < X1 && y >= Y0 && y < Y1 && v >= 0 && v < q.K);
         const long long o = (long long)(y + 2) * q.lpitch + x + 2;
         glab[o] = (uint16_t)v;
         if (BAND) {  // within two rows of a band edge: the neighbour's halo too
@@ -411,6 +435,8 @@ struct GridCta {
 template <int BAND = 0>
 __device__ __forceinline__ void gdelta(const GridParams &q, int buf, int f, int k, int n, int b, int count)
 {
+    SEEDS_CHECK(k >= 0 && k < q.K && n >= 0 && n < q.K && k != n && b >= 0 && b < q.B && count > 0 && f >= 0 &&
+                f < q.nf);
     if (BAND) {  // each superpixel's counts at its owner band (one frame)
         const int ok = band_owner(q, k), on = band_owner(q, n);
         atomicAdd(q.pH[ok][buf] + (long long)k * q.B + b, -count);
@@ -854,6 +880,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
     };
     // A move k -> n of `count` pixels of bin b: record + histogram deltas.
     auto emit = [&](GRec *r, int slot, int k, int n, int b, int count, int yb) {
+        SEEDS_CHECK(slot >= 0 && slot < q.rec_cap);
         r[slot] = GRec{(uint32_t)k | ((uint32_t)n << 16), (uint32_t)b | ((uint32_t)count << 16), (uint32_t)c.f, 0u};
         gdelta<BAND>(q, yb, c.f, k, n, b, count);
         if (BAND && q.bsys && (band_owner(q, k) != q.bself || band_owner(q, n) != q.bself)) c.misc[9] = 1;
@@ -1643,6 +1670,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                         }
                         slot = __shfl_sync(FULL, slot, 0) + __popc(mv & ((1u << lane) - 1));
                         if (u.acc >= 0) {
+                            SEEDS_CHECK(slot >= 0 && slot < q.rec_cap);
                             rec_list(ob)[slot] = GRec{(uint32_t)u.k | ((uint32_t)u.acc << 16), (uint32_t)u.j | (1u << 16),
                                                       (uint32_t)c.f, rgba};
                             gdelta(q, yb_, c.f, u.k, u.acc, u.j, 1);
@@ -1687,9 +1715,13 @@ __global__ void __launch_bounds__(256) k_emit_planes(const uint16_t *lab, long l
                                                     int y0, int nrows, int32_t *out)
 {
     const int f = blockIdx.x / nrows, y = y0 + blockIdx.x - f * nrows;
-    const uint16_t *src = lab + (long long)f * lab_fs + (long long)(y + 2) * lpitch + 2;
+    const uint16_t *src = lab + (long long)f * lab_fs + (long long)(y + 2) * lpitch + 2;  // 4-byte aligned
     int32_t *dst = out + ((long long)f * H + y) * W;
-    for (int x = threadIdx.x; x < W; x += blockDim.x) dst[x] = __ldcg(src + x);
+    for (int x = 2 * threadIdx.x; x < W; x += 2 * blockDim.x) {  // two labels per 32-bit load
+        const unsigned v = __ldcg(reinterpret_cast<const unsigned *>(src + x));
+        dst[x] = (int32_t)(v & 0xFFFF);
+        if (x + 1 < W) dst[x + 1] = (int32_t)(v >> 16);
+    }
 }
 
 // The seeding kernel of grid mode (a1-a3 of SURVEY.md 8(a)): one CTA per
@@ -1735,7 +1767,9 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
     // the first use (the cell is walked as one flat index, row-major)
     constexpr int U = 4;
     const int cw = x1 - x0, area = cw * (y1 - y0);
-    const float inv = 1.0f / (float)cw;
+    // the thread's position walks the flat index by blockDim.x at a time
+    const int stx = (int)blockDim.x % cw, sty = (int)blockDim.x / cw;
+    int wx = x0 + tid % cw, wy = y0 + tid / cw;
     for (int base = 0; base < area; base += U * (int)blockDim.x) {
         int px[U], py[U];
         uint32_t rgb[U];
@@ -1747,12 +1781,17 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
             rgb[u] = 0;
             lk[u] = cell;
             if (i < area) {
-                const int dy = div_small(i, cw, inv);
-                px[u] = x0 + i - dy * cw;
-                py[u] = y0 + dy;
+                px[u] = wx;
+                py[u] = wy;
                 const uint8_t *v = q.img + (fN + (long long)py[u] * W + px[u]) * q.C;
                 for (int ch = 0; ch < q.C; ch++) rgb[u] |= (uint32_t)v[ch] << (8 * ch);
                 if (!cold) lk[u] = q.init[fN + (long long)py[u] * W + px[u]];
+            }
+            wx += stx;
+            wy += sty;
+            if (wx >= x1) {
+                wx -= cw;
+                wy++;
             }
         }
 #pragma unroll
@@ -1776,8 +1815,12 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
                 // ranks: k_grid counts warm labels after its first barrier
             } else if (cold) {
                 const int key = in ? ((y >= ym ? 2 : 0) + (x >= xm ? 1 : 0)) * B + b : -1;
-                const unsigned m = __match_any_sync(FULL, key);
-                if (in && lane == __ffs(m) - 1) atomicAdd(&shist[key], __popc(m));
+                if (sizeof(BinT) == 1) {  // few bins (<= 256): runs of equal keys, aggregate them
+                    const unsigned m = __match_any_sync(FULL, key);
+                    if (in && lane == __ffs(m) - 1) atomicAdd(&shist[key], __popc(m));
+                } else if (in) {  // many bins: keys mostly distinct, plain shared atomics are cheaper
+                    atomicAdd(&shist[key], 1);
+                }
             } else {
                 const int key = in ? k * B + b : -1;
                 int *h0 = H0, *h1 = H1, *a0 = A0, *a1 = A1;
