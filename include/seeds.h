@@ -205,7 +205,7 @@ seeds_status seeds_set_colour_space(seeds_ctx *ctx, int space);
 seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pixels, uint8_t *lab_out,
                               void *stream);
 
-/* seeds_set_compactness -- the compactness prior (PAPER.md:853-863: "minimize
+/* seeds_set_compactness -- the compactness prior (PAPER.md:867-868: "minimize
  * the distance between the pixels on the superpixel boundary and the center of
  * gravity of the superpixel"), reading M5: every later run's pixel-level moves
  * k -> n also need the pixel strictly nearer (squared Euclidean, integers) to
@@ -216,13 +216,13 @@ seeds_status seeds_rgb_to_lab(seeds_ctx *ctx, const uint8_t *rgb, long long n_pi
  *   SEEDS_ESTATE  the ctx is forced to graph mode (grid mode only) */
 seeds_status seeds_set_compactness(seeds_ctx *ctx, int on);
 
-/* seeds_set_edge_prior -- the edge prior (PAPER.md:863-866: "If a boundary is near
+/* seeds_set_edge_prior -- the edge prior (PAPER.md:868-871: "If a boundary is near
  * an edge, it snaps to this edge and is no longer updated"), reading M6: an edge
  * separates 4-adjacent pixels whose colours (in the colour space in effect)
  * differ by more than tau (sum of absolute channel differences); at the pixel
  * level a pixel with a differently labelled 4-neighbour across an edge does not
  * move.  With smoothness_prior = 1 and the compactness prior this is the
- * paper's combined prior (PAPER.md:866-868).  tau = 0 (default) turns it off.
+ * paper's combined prior (PAPER.md:872).  tau = 0 (default) turns it off.
  *   SEEDS_EINVAL  tau outside 0..1020, or a row-band ctx
  *   SEEDS_ESTATE  the ctx is forced to graph mode (grid mode only) */
 seeds_status seeds_set_edge_prior(seeds_ctx *ctx, int tau);

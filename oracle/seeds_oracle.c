@@ -477,7 +477,7 @@ static int decide_block(st_t *s, int *M, int w, int h, int l, int bi, int bj, in
 }
 
 /* decide for pixel (x, y) on the label plane. */
-/* Compactness prior (PAPER.md:853-863: "minimize the distance between the
+/* Compactness prior (PAPER.md:867-868: "minimize the distance between the
  * pixels on the superpixel boundary and the center of gravity of the
  * superpixel"), reading M5: a pixel-level move k -> n also needs p strictly
  * nearer (squared Euclidean, integers) to n's centre of gravity than to k's,
@@ -508,7 +508,7 @@ static int compact_test(const st_t *s, int x, int y, int k, int n)
     return dxn * dxn + dyn * dyn < dxk * dxk + dyk * dyk;
 }
 
-/* Edge prior (PAPER.md:863-866: "If a boundary is near an edge, it snaps to
+/* Edge prior (PAPER.md:868-871: "If a boundary is near an edge, it snaps to
  * this edge and is no longer updated from there on forward"), reading M6: an
  * edge separates 4-adjacent pixels whose colours differ by more than edge_tau
  * (sum of the absolute channel differences, 8-bit units); at the pixel level a

@@ -92,7 +92,7 @@ def test_edge_prior(torch_cuda, orc, cfg, gamma, tau):
 
 
 def test_combined_prior(torch_cuda, orc):
-    """3x3 smoothing + compactness + edge snapping (PAPER.md:866-868), on a c3
+    """3x3 smoothing + compactness + edge snapping (PAPER.md:872), on a c3
     batch (multi-tile plans) and with the LAB pre-pass."""
     p = configs.params("c3")
     check(torch_cuda, orc, configs.frames("c3", n=12), p, compact=True, edge=60)

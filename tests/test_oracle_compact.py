@@ -1,5 +1,5 @@
 """Pins of the oracle's compactness prior (PAPER.md:
-853-863; reading M5 in DESIGN.md): at the pixel level a move k -> n also needs
+867-868; reading M5 in DESIGN.md): at the pixel level a move k -> n also needs
 the pixel strictly nearer to n's centre of gravity than to k's, the centres
 (rounded to the nearest pixel) taken at the start of each pixel iteration.
 Whole sub-sweeps are predicted from the definitions: histograms recounted with

@@ -1,4 +1,4 @@
-"""Pins of the oracle's edge prior (SURVEY.md 8(f) rank 4; PAPER.md:863-866;
+"""Pins of the oracle's edge prior (SURVEY.md 8(f) rank 4; PAPER.md:868-871;
 reading M6 in DESIGN.md): at the pixel level a pixel whose differently labelled
 4-neighbour lies across a colour edge (channel L1 difference > tau) does not
 move.  Whole pixel sub-sweeps are predicted from the definitions (histograms
