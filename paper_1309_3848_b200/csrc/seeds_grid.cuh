@@ -910,7 +910,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                         const int uw = ifirst < bx1 ? (bx1 - ifirst + 1) / 2 : 0;
                         const int uh = jfirst < by1 ? (by1 - jfirst + 1) / 2 : 0;
                         const int nunits = uw * uh;
-                        const float inv_uw = 1.0f / (float)max(uw, 1);
+                        const float inv_uw = rcp_small(max(uw, 1));
                         auto rect = [&](int u, int &bi, int &bj, int &xa, int &xb, int &ya, int &yb) {
                             const int tj = div_small(u, uw, inv_uw);
                             bi = ifirst + 2 * (u - tj * uw);
@@ -1008,11 +1008,11 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                 const bool ok = nb.valid && c.removable_s(nb.mask);
                                 int b = -1, b2 = -1;
                                 if (ok && si < alpha) {
-                                    const int dy = div_small(si, rw, 1.0f / (float)rw);
+                                    const int dy = div_small(si, rw, rcp_small(rw));
                                     b = c.bin(xa + si - dy * rw, ya + dy);
                                 }
                                 if (NT <= 128 && ok && si + G < alpha) {  // two pixels per lane: 128-thread plans only
-                                    const int dy = div_small(si + G, rw, 1.0f / (float)rw);
+                                    const int dy = div_small(si + G, rw, rcp_small(rw));
                                     b2 = c.bin(xa + si + G - dy * rw, ya + dy);
                                 }
                                 const SegK5 r5 = k5_segment<NT>(c, ob, ok, alpha, G, seg, si, sbase, lane, k, nb, b, b2,
@@ -1027,11 +1027,11 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                     if (leader) emit(rec_list(ob), slot, k, acc, b, (int)lb, yb_);
                                     if (leader2) emit(rec_list(ob), slot + (int)leader, k, acc, b2, l2, yb_);
                                     if (si < alpha) {
-                                        const int dy = div_small(si, rw, 1.0f / (float)rw);
+                                        const int dy = div_small(si, rw, rcp_small(rw));
                                         c.set(xa + si - dy * rw, ya + dy, acc);
                                     }
                                     if (NT <= 128 && si + G < alpha) {
-                                        const int dy = div_small(si + G, rw, 1.0f / (float)rw);
+                                        const int dy = div_small(si + G, rw, rcp_small(rw));
                                         c.set(xa + si + G - dy * rw, ya + dy, acc);
                                     }
                                 }
@@ -1053,7 +1053,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                 const Neigh nb = ring_at(a, c.sp, xb - xa, (yb - ya) * c.sp);
                                 if (!nb.valid || !c.removable_s(nb.mask)) continue;
                                 const int rw = xb - xa, alpha = rw * (yb - ya);
-                                const float inv = 1.0f / (float)rw;
+                                const float inv = rcp_small(rw);
                                 // candidate sizes first: their loads overlap the histogram build
                                 const long long Ak = c.ldA(ob, k);
                                 long long An[4];
@@ -1159,7 +1159,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                                 const Neigh nb = ring_at(a, c.sp, xb - xa, (yb - ya) * c.sp);
                                 if (!nb.valid || !c.removable_s(nb.mask)) continue;
                                 const int rw = xb - xa, alpha = rw * (yb - ya);
-                                const float inv = 1.0f / (float)rw;
+                                const float inv = rcp_small(rw);
                                 // candidate sizes first: their loads overlap the histogram build
                                 const long long Ak = c.ldA(ob, k);
                                 long long An[4];
@@ -1398,7 +1398,7 @@ __global__ void __launch_bounds__(NT, grid_cps<NT>()) k_grid(const __grid_consta
                 const int uw = xfirst < t.X1 ? (t.X1 - xfirst + P - 1) / P : 0;
                 const int uh = yfirst < t.Y1 ? (t.Y1 - yfirst + P - 1) / P : 0;
                 const int nunits = uw * uh;
-                const float inv_uw = 1.0f / (float)max(uw, 1);
+                const float inv_uw = rcp_small(max(uw, 1));
                 auto unit_xy = [&](int u, int &x, int &y) {
                     const int tj = div_small(u, uw, inv_uw);
                     x = xfirst + P * (u - tj * uw);

@@ -658,6 +658,10 @@ __device__ __forceinline__ long long clk64()
 // per-level block strategies of the persistent kernels
 enum { BK_T4 = 0, BK_T16 = 1, BK_WARP = 2 };
 
+// 1 / d for div_small: the hardware reciprocal (MUFU.RCP, ~1 ulp) -- a full
+// IEEE division would add a slow-path branch, and div_small corrects +-1 anyway.
+__device__ __forceinline__ float rcp_small(int d) { return __fdividef(1.0f, (float)d); }
+
 // q = t / d for small non-negative t, d (< 2^22) with a float reciprocal and
 // an exact correction.
 __device__ __forceinline__ int div_small(int t, int d, float inv)
