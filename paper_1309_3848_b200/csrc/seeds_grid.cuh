@@ -68,6 +68,8 @@ constexpr int STOP_NONE = 0x7F7F7F7F;  // "no stop" (a byte-wise memset value)
 constexpr int GRID_THREADS_SMALL = 128;
 #ifdef SEEDS_CPS8
 constexpr int GRID_SMALL_CPS = 8;  // experiment: 8 x 128 threads per SM, 64 registers
+#elif defined(SEEDS_CPS6)
+constexpr int GRID_SMALL_CPS = 6;  // experiment: 6 x 128 threads per SM, 80 registers
 #else
 constexpr int GRID_SMALL_CPS = 4;
 #endif
