@@ -136,3 +136,85 @@ def test_random_feature_combination(torch_cuda, orc, case):
             h, a = s.read_state(f)
             np.testing.assert_array_equal(h.cpu().numpy(), r.hist, err_msg=f"hist frame {f}")
     s.close()
+
+
+# ----------------------------------------------------------------------------
+# Round 2 features under random shapes: row bands in one launch (1-8 bands,
+# cold and warm, 1-4 channels, u8 and u16 bins) and the anytime budget replay.
+# ----------------------------------------------------------------------------
+BRNG = np.random.default_rng(20261020)
+BAND_CASES = []
+for i in range(24):
+    W = int(BRNG.integers(24, 320))
+    H = int(BRNG.integers(24, 240))
+    C = int(BRNG.integers(1, 4))
+    bpc = int(BRNG.choice([2, 3, 4, 5, 8] if C <= 2 else [2, 4, 5, 8]))
+    K = int(BRNG.integers(4, max(5, W * H // 150)))
+    L = int(BRNG.integers(0, 5))
+    gamma = int(BRNG.integers(0, 2))
+    iters = int(BRNG.integers(1, 4))
+    nb = int(BRNG.integers(1, 9))
+    warm = bool(BRNG.integers(0, 3) == 0)
+    BAND_CASES.append((i, W, H, C, bpc, K, L, gamma, iters, nb, warm))
+
+
+@pytest.mark.parametrize("case", BAND_CASES, ids=[f"band{c[0]}" for c in BAND_CASES])
+def test_random_bands(torch_cuda, orc, case):
+    """seeds_create_bands with a random band count: labels, histograms and
+    sizes equal the oracle's one-GPU run (warm cases start from the oracle's
+    cold result of the previous frame)."""
+    from paper_1309_3848_b200.seeds import SeedsBands, SeedsError
+    torch = torch_cuda
+    i, W, H, C, bpc, K, L, gamma, iters, nb, warm = case
+    p = dict(n_superpixels=K, n_levels=L, bins_per_channel=bpc, smoothness_prior=gamma, iters_per_level=iters)
+    f = [mosaic.mosaic(W, H, int(BRNG.integers(2, 25)), 9.0, seed=5000 + 10 * i + t, C=C, grad=20.0)
+         for t in range(2)]
+    nb = max(1, min(nb, orc.geometry(W, H, K, L)[1]))  # at most one band per superpixel row
+    try:
+        s = SeedsBands(W, H, C, K, L, bpc, gamma, iters, nb)
+    except SeedsError:
+        pytest.skip("band count or geometry rejected (bands of < 2 rows, more bands than superpixel rows)")
+    init = orc.run(f[0], **p).labels if warm else None
+    img = f[1]
+    lab = s.run(torch.from_numpy(np.ascontiguousarray(img)).cuda(),
+                None if init is None else torch.from_numpy(init).cuda()).cpu().numpy()
+    h, a = s.read_state(0)
+    r = orc.run(img, **p, init_labels=init)
+    np.testing.assert_array_equal(lab, r.labels)
+    np.testing.assert_array_equal(h.cpu().numpy(), r.hist)
+    np.testing.assert_array_equal(a.cpu().numpy(), r.sizes)
+    s.close()
+
+
+@pytest.mark.parametrize("case", CASES[:16], ids=[f"budget{c[0]}" for c in CASES[:16]])
+def test_random_budget_replay(torch_cuda, orc, case):
+    """Random budgets (5-60% of a measured run): the run stops at some
+    sub-sweep r and equals the oracle's run with max_subsweeps = r."""
+    from paper_1309_3848_b200.seeds import Seeds, SeedsError
+    torch = torch_cuda
+    i, W, H, C, bpc, K, L, gamma, iters, nf, warm = case
+    if iters == 0:
+        pytest.skip("no sub-sweeps to stop in")
+    p = dict(n_superpixels=K, n_levels=L, bins_per_channel=bpc, smoothness_prior=gamma, iters_per_level=iters)
+    img = mosaic.mosaic(W, H, 12, 10.0, seed=7000 + i, C=C, grad=20.0)
+    try:
+        s = Seeds(W, H, C, K, L, bpc, gamma, iters)
+        s.set_mode("grid")
+    except SeedsError:
+        pytest.skip("no grid plan / geometry rejected")
+    d = torch.from_numpy(img).cuda()
+    for _ in range(2):
+        s.iterate(d)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    s.iterate(d)
+    b.record()
+    torch.cuda.synchronize()
+    frac = float(BRNG.uniform(0.05, 0.6))
+    s.set_time_budget(max(1, int(a.elapsed_time(b) * 1000 * frac)))
+    lab = s.iterate(d).cpu().numpy()
+    rr = s.last_subsweeps()
+    ref = orc.run(img, **p, max_subsweeps=rr)
+    np.testing.assert_array_equal(lab, ref.labels)
+    np.testing.assert_array_equal(s.read_state(0)[0].cpu().numpy(), ref.hist)
+    s.close()
