@@ -20,6 +20,7 @@
 #include "../../include/seeds.h"
 #include "seeds_kernels.cuh"
 #include "seeds_grid.cuh"
+#include "seeds_tile1.cuh"
 #include "seeds_metrics.cuh"
 #include "seeds_lab.cuh"
 #include "seeds_validate.cuh"
@@ -752,6 +753,62 @@ static bool encode_tmaps(seeds_ctx *c, GridParams &q)
 
 static bool plan_try(seeds_ctx *c, int nf, int nt);
 
+// k_tile1 (seeds_tile1.cuh): one 512-thread CTA per tile, every tile on its
+// own CTA, the plain refinement (no means / priors, no row bands).
+template <typename BinT, int GAMMA, int P>
+static int tile1_occupancy(size_t smem)
+{
+    auto k = k_tile1<BinT, GAMMA, P>;
+    static int optin[MAX_DEVICES] = {};
+    if (!raise_optin((const void *)k, optin, smem)) return 0;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, T1_THREADS, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+static int tile1_occupancy_for(const seeds_ctx *c, size_t smem)
+{
+    if (c->bb == 1) return c->gamma ? tile1_occupancy<uint8_t, 1, 3>(smem) : tile1_occupancy<uint8_t, 0, 2>(smem);
+    return c->gamma ? tile1_occupancy<uint16_t, 1, 3>(smem) : tile1_occupancy<uint16_t, 0, 2>(smem);
+}
+// Its shared-memory layout (q.t1_*): records, class tables, block units,
+// histogram item slots (G per block of a level), pixel positions, the tile's
+// bins, the per-block state of multi-warp classes (G > 32), the build tables
+// of blocks larger than 32 pixels (a B-word count table per warp) -- or q.t1 =
+// 0 when the plan has several tiles per CTA or the layout does not fit.
+static void tile1_layout(seeds_ctx *c, GridParams &q, int nt, long long T, int G, long long units, long long items,
+                         long long maxcls, long long max_px, const int (&gs)[16])
+{
+    q.t1 = 0;
+    if (nt != T1_THREADS || T > G || getenv_off("SEEDS_TILE1") || c->L > T1_MAX_CLS / 4 || units > 65535)
+        return;
+    const int NW = T1_THREADS / 32;
+    bool big = false;
+    for (int l = 0; l < c->L; l++) {
+        q.t1_gs[l] = gs[l];
+        q.t1_am[l] = max_block_area(c, l);
+        big = big || q.t1_am[l] > 32;
+    }
+    size_t off = 0;
+    q.t1_o_misc = (unsigned)off;  off = align16(off + 128);
+    q.t1_o_rec = (unsigned)off;   off = align16(off + 2 * (size_t)q.rec_cap * 8);
+    q.t1_o_cls = (unsigned)off;   off = align16(off + T1_MAX_CLS * sizeof(T1Class) + 9 * sizeof(T1PClass));
+    q.t1_o_units = (unsigned)off; off = align16(off + (size_t)(units + 1) * sizeof(T1Unit));
+    q.t1_o_items = (unsigned)off; off = align16(off + (size_t)items * 8);
+    q.t1_o_pos = (unsigned)off;   off = align16(off + (size_t)max_px * 4);
+    q.t1_nst = (int)maxcls;
+    q.t1_o_st = (unsigned)off;    off = align16(off + (size_t)maxcls * sizeof(T1State));
+    q.t1_o_bins = (unsigned)off;  off = align16(off + (size_t)max_px * c->bb);
+    q.t1_tabw = big ? NW * c->B : 0;
+    q.t1_o_tab = (unsigned)off;   off = align16(off + (size_t)q.t1_tabw * 4);
+    if (off > 227 * 1024) return;
+    if (tile1_occupancy_for(c, off) < 1) return;
+    q.t1_smem = (unsigned)off;
+    q.t1 = 1;
+}
+
 // Plan for nf frames: one 512-thread CTA per SM, unless that leaves CTAs with
 // several tiles -- then four 128-thread CTAs per SM (each with its own tiles
 // and TMA pipeline) when such a plan fits.
@@ -916,6 +973,13 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     const int ntx = (TX + ba - 1) / ba;
     std::vector<GridTile> ft;
     std::vector<long long> tpx, tq, tr;
+    // the single-tile kernel's per-tile maxima (k_tile1): block units over all
+    // (level, class), an upper bound of their histogram items, units of the
+    // largest class
+    long long t1_units = 0, t1_items = 0, t1_maxcls = 0;
+    int t1_gs[16] = {};  // log2 of its lanes per block: G >= min(largest block area, B)
+    for (int l = 0; l < c->L && l < 16; l++)
+        while ((1 << t1_gs[l]) < std::min(max_block_area(c, l), c->B)) t1_gs[l]++;
     for (const Rng &r : rng)
     for (int ty = 0; ty < (r.u1 - r.u0 + bb_ - 1) / bb_; ty++)
         for (int tx = 0; tx < ntx; tx++) {
@@ -927,6 +991,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
             t.BX0 = i0 << Lm; t.BX1 = i1 << Lm; t.BY0 = j0 << Lm; t.BY1 = j1 << Lm;
             const long long w = t.X1 - t.X0, h = t.Y1 - t.Y0;
             long long qc = ((w + c->P - 1) / c->P) * ((h + c->P - 1) / c->P), rc = qc;
+            long long tu = 0, ti = 0;
             for (int l = 0; l < c->L; l++) {
                 const int bx0 = t.BX0 >> l, bx1 = t.BX1 >> l, by0 = t.BY0 >> l, by1 = t.BY1 >> l;
                 for (int cy = 0; cy < 2; cy++)
@@ -944,8 +1009,13 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
                         }
                         qc = std::max(qc, units);
                         rc = std::max(rc, sum);
+                        tu += units;
+                        ti += units << t1_gs[std::min(l, 15)];
+                        if (t1_gs[std::min(l, 15)] > 5) t1_maxcls = std::max(t1_maxcls, units);
                     }
             }
+            t1_units = std::max(t1_units, tu);
+            t1_items = std::max(t1_items, ti);
             ft.push_back(t);
             tpx.push_back(w * h);
             tq.push_back(qc);
@@ -1069,6 +1139,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
             q.binsp = c->d_binsp;
         }
         if (!encode_tmaps(c, q)) return false;
+        tile1_layout(c, q, nt, T, G, t1_units, t1_items, t1_maxcls, (long long)max_tw * max_th, t1_gs);
         c->grid_G = G;
         c->grid_smem = smem;
         c->grid_nt = nt;
@@ -1106,6 +1177,38 @@ static cudaError_t launch_grid_nt(seeds_ctx *ctx, const GridParams &q, cudaStrea
 // The row-band kernel variant runs for several bands or across devices; one
 // band in one process is the ordinary run (its buffers are the context's).
 static bool band_kernel(const seeds_ctx *c) { return c->banded && (c->bsys || c->nbands > 1); }
+
+// k_tile1 runs a single-tile plan's plain refinement (no means / priors, one
+// band, no phase trace: seeds_debug_trace stays with k_grid)
+static bool use_tile1(const seeds_ctx *c, const GridParams &q)
+{
+#ifdef SEEDS_TRACE
+    return q.t1 && !band_kernel(c) && !ext_pixel(c);  // (the tracing build stamps k_tile1 too)
+#else
+    return q.t1 && !band_kernel(c) && !ext_pixel(c) && !q.trace;
+#endif
+}
+template <typename BinT, int GAMMA, int P>
+static cudaError_t launch_tile1_t(seeds_ctx *ctx, const GridParams &q, cudaStream_t st)
+{
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3(ctx->grid_G);
+    cfg.blockDim = dim3(T1_THREADS);
+    cfg.dynamicSmemBytes = q.t1_smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_tile1<BinT, GAMMA, P>, q);
+}
+static cudaError_t launch_tile1(seeds_ctx *ctx, const GridParams &q, cudaStream_t st)
+{
+    if (ctx->bb == 1)
+        return ctx->gamma ? launch_tile1_t<uint8_t, 1, 3>(ctx, q, st) : launch_tile1_t<uint8_t, 0, 2>(ctx, q, st);
+    return ctx->gamma ? launch_tile1_t<uint16_t, 1, 3>(ctx, q, st) : launch_tile1_t<uint16_t, 0, 2>(ctx, q, st);
+}
 
 // Enqueue one grid-mode run: zero the histograms, move counters and the barrier
 // counter, then the single persistent launch.
@@ -1200,7 +1303,9 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     CK(prof_end(ctx, st));
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
     cudaError_t e;
-    if (ctx->grid_nt == GRID_THREADS)
+    if (use_tile1(ctx, q))
+        e = launch_tile1(ctx, q, st);
+    else if (ctx->grid_nt == GRID_THREADS)
         e = band_kernel(ctx) ? launch_grid_nt<GRID_THREADS, VAR_BAND>(ctx, q, st)
             : ext_pixel(ctx) ? launch_grid_nt<GRID_THREADS, VAR_EXT>(ctx, q, st)
                              : launch_grid_nt<GRID_THREADS, VAR_PLAIN>(ctx, q, st);

@@ -172,6 +172,12 @@ struct GridParams {
     unsigned *bar_base;               // this band's: the counter value of its last completed barrier
     unsigned *go;                     // local: the release word of the cross-device barrier
     CUtensorMap tm_lab_b[SEEDS_MAX_BANDS];
+    // single-tile kernel (k_tile1, seeds_tile1.cuh): t1 = its layout fits; its
+    // shared-memory offsets, table width (words) and bytes
+    int t1, t1_tabw, t1_nst;
+    int t1_gs[16], t1_am[16];  // per level: log2 G (lanes per block), the largest block area
+    unsigned t1_o_misc, t1_o_rec, t1_o_units, t1_o_items, t1_o_cls, t1_o_pos, t1_o_st, t1_o_bins, t1_o_tab;
+    unsigned t1_smem;
 };
 
 // the band owning superpixel k (bands own contiguous id ranges; bk[b] is

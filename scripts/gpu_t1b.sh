@@ -1,0 +1,13 @@
+# k_tile1 iteration: parity (c1/c2 + fuzz), bench A/B, phase trace
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q > gpurun_out/t1_pytest.log 2>&1; echo "exit $?" >> gpurun_out/t1_pytest.log
+for cfg in c2 c1; do
+for v in 1 0 1; do
+  rm -f /tmp/b.json
+  SEEDS_TILE1=$v timeout 120 python bench.py --steps 30 --warmup 5 --config $cfg --no-cpu-baseline --json-out /tmp/b.json > /tmp/b.log 2>&1
+  python -c "import json;d=json.load(open('/tmp/b.json'));print('$cfg tile1=$v', round(d['value'],1),'Mpx/s', round(d['ms_per_step'],4),'ms')" 2>/dev/null || tail -3 /tmp/b.log
+done; done > gpurun_out/t1_bench.txt 2>&1
+export SEEDS_LIB=scripts/alt_trace.so
+for cfg in c2 c1; do
+echo "== $cfg tile1"; timeout 120 python scripts/trace.py $cfg grid 2>&1 | tail -7
+done > gpurun_out/trace_t1.txt 2>&1

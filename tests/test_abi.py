@@ -61,7 +61,7 @@ def test_persistent_kernels_use_no_local_memory():
     """The grid kernels keep their hot state in registers or shared
     memory (ptxas -v of the in-tree build, paper_1309_3848_b200/ptxas_info.txt):
     no stack at all for the default grid kernels
-    (template flag 0); the extended-pixel instantiations (means post-processing,
+    (template flag 0) and the single-tile kernels (k_tile1); the extended-pixel instantiations (means post-processing,
     priors) may keep a cold loop counter (at most 16 bytes) in local memory --
     the grid barrier does not invalidate L1, which once made a spilled register
     unsafe across it."""
@@ -72,7 +72,7 @@ def test_persistent_kernels_use_no_local_memory():
     seen = 0
     for b in blocks:
         name = b.split("'", 1)[0]
-        if "k_grid" not in name:
+        if "k_grid" not in name and "k_tile1" not in name:
             continue
         seen += 1
         m = re.search(r"(\d+) bytes stack frame, (\d+) bytes spill stores, (\d+) bytes spill loads", b)
@@ -81,4 +81,4 @@ def test_persistent_kernels_use_no_local_memory():
             assert int(m.group(1)) <= 16, (name, m.group(0))
         else:
             assert m.groups() == ("0", "0", "0"), (name, m.group(0))
-    assert seen >= 8
+    assert seen >= 12
