@@ -779,7 +779,7 @@ static int tile1_occupancy_for(const seeds_ctx *c, size_t smem)
 // of blocks larger than 32 pixels (a B-word count table per warp) -- or q.t1 =
 // 0 when the plan has several tiles per CTA or the layout does not fit.
 static void tile1_layout(seeds_ctx *c, GridParams &q, int nt, long long T, int G, long long units, long long items,
-                         long long maxcls, long long max_px, const int (&gs)[16])
+                         long long maxcls, long long max_px, const int (&gs)[16], long long ncell)
 {
     q.t1 = 0;
     if (nt != T1_THREADS || T > G || getenv_off("SEEDS_TILE1") || c->L > T1_MAX_CLS / 4 || units > 65535)
@@ -794,16 +794,21 @@ static void tile1_layout(seeds_ctx *c, GridParams &q, int nt, long long T, int G
     size_t off = 0;
     q.t1_o_misc = (unsigned)off;  off = align16(off + 128);
     q.t1_o_rec = (unsigned)off;   off = align16(off + 2 * (size_t)q.rec_cap * 8);
-    q.t1_o_cls = (unsigned)off;   off = align16(off + T1_MAX_CLS * sizeof(T1Class) + 9 * sizeof(T1PClass));
-    q.t1_o_units = (unsigned)off; off = align16(off + (size_t)(units + 1) * sizeof(T1Unit));
+    if (!q.t1_static || !q.t1_sstride) return;
+    q.t1_o_static = (unsigned)off; off = align16(off + q.t1_sstride);
     q.t1_o_items = (unsigned)off; off = align16(off + (size_t)items * 8);
-    q.t1_o_pos = (unsigned)off;   off = align16(off + (size_t)max_px * 4);
     q.t1_nst = (int)maxcls;
     q.t1_o_st = (unsigned)off;    off = align16(off + (size_t)maxcls * sizeof(T1State));
     q.t1_o_bins = (unsigned)off;  off = align16(off + (size_t)max_px * c->bb);
     q.t1_tabw = big ? NW * c->B : 0;
     q.t1_o_tab = (unsigned)off;   off = align16(off + (size_t)q.t1_tabw * 4);
     if (off > 227 * 1024) return;
+    // the fused cold seed's per-tile (cell, bin) counts and cell sizes, when they fit
+    q.t1_o_seed = (unsigned)off;
+    q.t1_ncell = (int)ncell;
+    const size_t seed_bytes = align16((size_t)ncell * (c->B + 1) * 4);
+    q.t1_seedok = !getenv_off("SEEDS_TILE1_SEED") && off + seed_bytes <= 227 * 1024;
+    if (q.t1_seedok) off += seed_bytes;
     if (tile1_occupancy_for(c, off) < 1) return;
     q.t1_smem = (unsigned)off;
     q.t1 = 1;
@@ -880,6 +885,73 @@ static bool plan_grid(seeds_ctx *c, int nf)
     c->grec_bytes = slot->grec_bytes;
     c->grid_nf = nf;
     return c->grid_ok = slot->ok;
+}
+
+// k_tile1's static per-tile tables (seeds_tile1.cuh T1Head): class tables,
+// block geometry (T1Unit.pad = its class) and pixel positions of every tile of
+// one frame, at a common stride; built once per plan, uploaded after the
+// plan's tiles, and copied into shared memory by each CTA at launch.
+static size_t tile1_static(const seeds_ctx *c, const std::vector<GridTile> &ft, const int (&gs)[16],
+                           std::vector<unsigned char> &blob, unsigned &b_units, unsigned &b_pos)
+{
+    const int L = c->L, P = c->P;
+    long long mu = 0, mp = 0;
+    for (const GridTile &t : ft) {
+        long long nu = 0;
+        for (int l = 0; l < L; l++) {
+            const long long bw = (t.BX1 >> l) - (t.BX0 >> l), bh = (t.BY1 >> l) - (t.BY0 >> l);
+            nu += bw * bh;
+        }
+        mu = std::max(mu, nu);
+        mp = std::max(mp, (long long)(t.X1 - t.X0) * (t.Y1 - t.Y0));
+    }
+    b_units = (unsigned)align16(sizeof(T1Head) + T1_MAX_CLS * sizeof(T1Class) + 9 * sizeof(T1PClass));
+    b_pos = (unsigned)align16(b_units + (size_t)mu * sizeof(T1Unit));
+    const size_t stride = align16(b_pos + (size_t)mp * 4);
+    blob.assign(stride * ft.size(), 0);
+    for (size_t ti = 0; ti < ft.size(); ti++) {
+        const GridTile &t = ft[ti];
+        unsigned char *b = blob.data() + ti * stride;
+        T1Head *h = reinterpret_cast<T1Head *>(b);
+        T1Class *cls = reinterpret_cast<T1Class *>(b + sizeof(T1Head));
+        T1PClass *pcls = reinterpret_cast<T1PClass *>(b + sizeof(T1Head) + T1_MAX_CLS * sizeof(T1Class));
+        T1Unit *un = reinterpret_cast<T1Unit *>(b + b_units);
+        uint32_t *pos = reinterpret_cast<uint32_t *>(b + b_pos);
+        int uo = 0, io = 0;
+        for (int l = 0; l < L; l++) {
+            const int bx0 = t.BX0 >> l, bx1 = t.BX1 >> l, by0 = t.BY0 >> l, by1 = t.BY1 >> l;
+            for (int col = 0; col < 4; col++) {
+                const int cx = col & 1, cy = col >> 1;
+                const int ifirst = bx0 + ((bx0 & 1) != cx), jfirst = by0 + ((by0 & 1) != cy);
+                const int uw = ifirst < bx1 ? (bx1 - ifirst + 1) / 2 : 0;
+                const int uh = jfirst < by1 ? (by1 - jfirst + 1) / 2 : 0;
+                cls[l * 4 + col] = T1Class{uo, uw * uh, uw, ifirst, jfirst, io, 0, 0};
+                for (int u = 0; u < uw * uh; u++) {
+                    const int bi = ifirst + 2 * (u % uw), bj = jfirst + 2 * (u / uw);
+                    const int xa = c->colstart[(size_t)bi << l], xb = c->colstart[(size_t)(bi + 1) << l];
+                    const int ya = c->rowstart[(size_t)bj << l], yb = c->rowstart[(size_t)(bj + 1) << l];
+                    un[uo + u] = T1Unit{(uint16_t)xa, (uint16_t)ya, (uint16_t)(xb - xa), (uint16_t)(yb - ya),
+                                        (uint32_t)((xb - xa) * (yb - ya)), (uint32_t)(l * 4 + col)};
+                }
+                uo += uw * uh;
+                io += (uw * uh) << gs[l];
+            }
+        }
+        int po = 0;
+        for (int col = 0; col < P * P; col++) {
+            const int cx = col % P, cy = col / P;
+            const int xfirst = t.X0 + (((cx - t.X0) % P) + P) % P;
+            const int yfirst = t.Y0 + (((cy - t.Y0) % P) + P) % P;
+            const int uw = xfirst < t.X1 ? (t.X1 - xfirst + P - 1) / P : 0;
+            const int uh = yfirst < t.Y1 ? (t.Y1 - yfirst + P - 1) / P : 0;
+            pcls[col] = T1PClass{po, uw * uh, uw, xfirst, yfirst, 0};
+            for (int u = 0; u < uw * uh; u++)
+                pos[po + u] = (uint32_t)(xfirst + P * (u % uw)) | (uint32_t)(yfirst + P * (u / uw)) << 16;
+            po += uw * uh;
+        }
+        *h = T1Head{uo, po, io, {0, 0, 0, 0, 0}};
+    }
+    return stride;
 }
 
 static bool plan_try(seeds_ctx *c, int nf, int nt)
@@ -976,7 +1048,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     // the single-tile kernel's per-tile maxima (k_tile1): block units over all
     // (level, class), an upper bound of their histogram items, units of the
     // largest class
-    long long t1_units = 0, t1_items = 0, t1_maxcls = 0;
+    long long t1_units = 0, t1_items = 0, t1_maxcls = 0, t1_ncell = 0;
     int t1_gs[16] = {};  // log2 of its lanes per block: G >= min(largest block area, B)
     for (int l = 0; l < c->L && l < 16; l++)
         while ((1 << t1_gs[l]) < std::min(max_block_area(c, l), c->B)) t1_gs[l]++;
@@ -1015,6 +1087,12 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
                     }
             }
             t1_units = std::max(t1_units, tu);
+            {  // superpixel cells of the initial grid the tile overlaps (the fused seed's tables)
+                const int Lq = c->L;
+                const long long ncx = (c->bxof[t.X1 - 1] >> Lq) - (c->bxof[t.X0] >> Lq) + 1;
+                const long long ncy = (c->byof[t.Y1 - 1] >> Lq) - (c->byof[t.Y0] >> Lq) + 1;
+                t1_ncell = std::max(t1_ncell, ncx * ncy);
+            }
             t1_items = std::max(t1_items, ti);
             ft.push_back(t);
             tpx.push_back(w * h);
@@ -1094,21 +1172,40 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         q.rec_cap = rec_cap;
         q.ntiles = (int)T;
         // device buffers: tiles, records
-        if (c->tiles_cap < tiles.size()) {
+        // k_tile1's static tables (one-tile-per-CTA plans) follow the tiles in the same allocation
+        std::vector<unsigned char> t1blob;
+        unsigned t1_bu = 0, t1_bp = 0;
+        const size_t t1_stride = nt == T1_THREADS && T <= G ? tile1_static(c, ft, t1_gs, t1blob, t1_bu, t1_bp) : 0;
+        const size_t tiles_bytes = align16(tiles.size() * sizeof(GridTile));
+        const size_t alloc_n = (tiles_bytes + t1blob.size() + sizeof(GridTile) - 1) / sizeof(GridTile);
+        if (c->tiles_cap < alloc_n) {
             if (c->d_tiles) cudaFree(c->d_tiles);
             c->d_tiles = nullptr;
             c->tiles_cap = 0;
-            if (cudaMalloc(&c->d_tiles, tiles.size() * sizeof(GridTile)) != cudaSuccess) {
+            if (cudaMalloc(&c->d_tiles, alloc_n * sizeof(GridTile)) != cudaSuccess) {
                 cudaGetLastError();
                 return false;
             }
-            c->tiles_cap = tiles.size();
+            c->tiles_cap = alloc_n;
         }
         if (cudaMemcpy(c->d_tiles, tiles.data(), tiles.size() * sizeof(GridTile), cudaMemcpyHostToDevice) !=
             cudaSuccess) {
             cudaGetLastError();
             return false;
         }
+        q.t1_static = nullptr;
+        if (!t1blob.empty()) {
+            unsigned char *dst = reinterpret_cast<unsigned char *>(c->d_tiles) + tiles_bytes;
+            q.t1_static = dst;
+            if (cudaMemcpy(dst, t1blob.data(), t1blob.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+        }
+        q.t1_sstride = (unsigned)t1_stride;
+        q.t1_b_units = t1_bu;
+        q.t1_b_pos = t1_bp;
+        q.t1_nft = (int)ft.size();
         const size_t rb = rs ? 16 : (size_t)G * 2 * rec_cap * sizeof(GRec);
         if (c->grec_bytes < rb) {
             if (c->d_grec) cudaFree(c->d_grec);
@@ -1139,7 +1236,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
             q.binsp = c->d_binsp;
         }
         if (!encode_tmaps(c, q)) return false;
-        tile1_layout(c, q, nt, T, G, t1_units, t1_items, t1_maxcls, (long long)max_tw * max_th, t1_gs);
+        tile1_layout(c, q, nt, T, G, t1_units, t1_items, t1_maxcls, (long long)max_tw * max_th, t1_gs, t1_ncell);
         c->grid_G = G;
         c->grid_smem = smem;
         c->grid_nt = nt;
@@ -1286,6 +1383,11 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
     q.done = ctx->d_err + 2;
     CK(cudaMemsetAsync(ctx->d_err + 1, 0x7F, 4, st));  // STOP_NONE
     ctx->ev_used = 0;
+    // single-tile plans (k_tile1): a cold run is seeded inside the launch, and
+    // the launch writes the int32 labels itself
+    const bool t1 = use_tile1(ctx, q);
+    q.t1_seed = t1 && !init && !ctx->dbg_blk && q.t1_seedok;
+    if (!q.t1_seed) {
     CK(prof_begin(ctx, st, SEEDS_KIND_SEED));
     {
         const int cells = ctx->banded && ctx->bsys ? ctx->bk[ctx->bself + 1] - ctx->bk[ctx->bself] : ctx->K;
@@ -1301,9 +1403,10 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
         CK(cudaGetLastError());
     }
     CK(prof_end(ctx, st));
+    }
     CK(prof_begin(ctx, st, SEEDS_KIND_FRAME));
     cudaError_t e;
-    if (use_tile1(ctx, q))
+    if (t1)
         e = launch_tile1(ctx, q, st);
     else if (ctx->grid_nt == GRID_THREADS)
         e = band_kernel(ctx) ? launch_grid_nt<GRID_THREADS, VAR_BAND>(ctx, q, st)
@@ -1315,6 +1418,7 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
                              : launch_grid_nt<GRID_THREADS_SMALL, VAR_PLAIN>(ctx, q, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_grid launch");
     CK(prof_end(ctx, st));
+    if (!t1) {
     CK(prof_begin(ctx, st, SEEDS_KIND_EMIT));
     {
         const int nt = ctx->W >= 256 ? 256 : 128;
@@ -1332,6 +1436,7 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
         CK(cudaGetLastError());
     }
     CK(prof_end(ctx, st));
+    }
     const bool blocks = init == nullptr && ctx->L > 0;
     const int total = (blocks ? 4 * block_levels_run(ctx) * ctx->iters : 0) + ctx->P * ctx->P * ctx->iters;
     ctx->last_done = ctx->limit >= 0 ? std::min(ctx->limit, total) : total;
@@ -1746,7 +1851,9 @@ seeds_status seeds_query(const seeds_ctx *ctx, seeds_info *o)
         o->grid_ctas = ok ? m->grid_G : 0;
         o->grid_tiles = ok ? m->gp.ntiles : 0;
     }
-    o->kernels_per_run = (o->exec_mode == SEEDS_MODE_GRAPH ? ctx->kernels_per_run : 3) +  // grid: seed, k_grid, emit
+    // grid: seed, k_grid, emit -- or one k_tile1 launch (a cold run of a single-tile plan)
+    const int grid_kernels = o->grid_ctas && use_tile1(ctx, ctx->gp) && ctx->gp.t1_seedok && !ctx->dbg_blk ? 1 : 3;
+    o->kernels_per_run = (o->exec_mode == SEEDS_MODE_GRAPH ? ctx->kernels_per_run : grid_kernels) +
                          (ctx->colour == SEEDS_COLOUR_LAB ? 1 : 0);  // + the LAB pre-pass
     o->workspace_bytes_per_frame = (size_t)ctx->N * (ctx->bb + 2) +
                                    (size_t)(((long long)ctx->GX * ctx->GY + 7) / 8 * 8) * 4 +

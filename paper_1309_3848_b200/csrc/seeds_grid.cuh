@@ -175,8 +175,18 @@ struct GridParams {
     // single-tile kernel (k_tile1, seeds_tile1.cuh): t1 = its layout fits; its
     // shared-memory offsets, table width (words) and bytes
     int t1, t1_tabw, t1_nst;
+    int t1_seed;     // this run seeds in k_tile1's prologue (cold start): quantise, grid labels, histograms
+    int t1_seedok;   // the layout has room for the seed's per-tile cell tables (t1_ncell cells)
+    int t1_ncell;
+    unsigned t1_o_seed;
     int t1_gs[16], t1_am[16];  // per level: log2 G (lanes per block), the largest block area
-    unsigned t1_o_misc, t1_o_rec, t1_o_units, t1_o_items, t1_o_cls, t1_o_pos, t1_o_st, t1_o_bins, t1_o_tab;
+    unsigned t1_o_misc, t1_o_rec, t1_o_static, t1_o_items, t1_o_st, t1_o_bins, t1_o_tab;
+    // the static tables (host-built, seeds_engine.cu tile1_static): frame-0
+    // tile i's blob at t1_static + i t1_sstride; units / positions at these
+    // offsets inside a blob; t1_nft tiles per frame
+    const unsigned char *t1_static;
+    unsigned t1_sstride, t1_b_units, t1_b_pos;
+    int t1_nft;
     unsigned t1_smem;
 };
 
@@ -227,6 +237,18 @@ __device__ __forceinline__ void grid_poll(unsigned *ctr, unsigned target)
 #elif SEEDS_BARRIER_ACQ == 2
     asm volatile("fence.acq_rel.gpu;" ::: "memory");  // relaxed poll + fence: the same, as a fence pattern
 #endif
+}
+// Poll with acquire loads (no final load after the count is reached): for
+// kernels that keep nothing in L1 (k_tile1), each poll's L1 invalidation costs
+// nothing, and the barrier saves one L2 round trip.
+__device__ __forceinline__ void grid_poll_acq(unsigned *ctr, unsigned target)
+{
+    unsigned v;
+    long long spins = 0;
+    do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        if (++spins > (1LL << 26)) __trap();  // a CTA that never arrives: fail loudly instead of hanging
+    } while ((int)(v - target) < 0);
 }
 // the cross-device counterpart: relaxed sys-scope polls, then one acquire load
 __device__ __forceinline__ void sys_poll(unsigned *ctr, unsigned target)

@@ -27,6 +27,9 @@
 //    pixels j, j + G, ...).  One phase, no CTA barrier, when G <= 32; blocks of
 //    G > 32 lanes (several warps) add their warp sums in shared memory and
 //    decide after one CTA barrier.
+//  * A cold run is seeded in the prologue (quantise, grid labels, per-tile
+//    (cell, bin) counts in shared memory, one atomic each into H and A) and
+//    the tile's int32 labels are written in the epilogue: one launch per run.
 //  * A pixel sub-sweep is one thread per unit: 5x5 window (or ring) loads,
 //    ring test, bin, gathers, Prop. 2 while the gathers are in flight, the
 //    colour test, the emit.
@@ -49,7 +52,12 @@ __device__ __forceinline__ Neigh ring_at_g(const uint16_t *a, int k, long long p
                   __ldcg(a + dyb - 1), __ldcg(a - 1), __ldcg(a - pitch - 1));
 }
 
-// a block unit: its rectangle and area
+// header of a tile's static tables (host-built): block units, pixel positions,
+// item slots; then the class tables, the pixel classes, the units, the positions
+struct T1Head {
+    int nunits, npos, nitems, pad[5];
+};
+// a block unit: its rectangle and area (pad: its (level, class) index)
 struct T1Unit {
     uint16_t xa, ya, rw, rh;
     uint32_t alpha, pad;
@@ -80,15 +88,17 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
     unsigned char *sb = reinterpret_cast<unsigned char *>(smem);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int B = q.B;
-    int *misc = reinterpret_cast<int *>(sb + q.t1_o_misc);  // [0], [1] record counts, [8] stop, [10], [11] build
+    int *misc = reinterpret_cast<int *>(sb + q.t1_o_misc);  // [0], [1] record counts, [8] stop
     uint32_t *rem = reinterpret_cast<uint32_t *>(sb + q.t1_o_misc + 64);
     uint2 *rec0 = reinterpret_cast<uint2 *>(sb + q.t1_o_rec);
     uint2 *rec1 = rec0 + q.rec_cap;
-    T1Unit *units = reinterpret_cast<T1Unit *>(sb + q.t1_o_units);
+    unsigned char *stat = sb + q.t1_o_static;  // the tile's static tables (T1Head ...)
+    const T1Head *head = reinterpret_cast<const T1Head *>(stat);
+    const T1Class *cls = reinterpret_cast<const T1Class *>(stat + sizeof(T1Head));
+    const T1PClass *pcls = reinterpret_cast<const T1PClass *>(stat + sizeof(T1Head) + T1_MAX_CLS * sizeof(T1Class));
+    const T1Unit *units = reinterpret_cast<const T1Unit *>(stat + q.t1_b_units);
+    const uint32_t *ppos = reinterpret_cast<const uint32_t *>(stat + q.t1_b_pos);
     uint2 *items = reinterpret_cast<uint2 *>(sb + q.t1_o_items);
-    T1Class *cls = reinterpret_cast<T1Class *>(sb + q.t1_o_cls);
-    T1PClass *pcls = reinterpret_cast<T1PClass *>(sb + q.t1_o_cls + T1_MAX_CLS * sizeof(T1Class));
-    uint32_t *ppos = reinterpret_cast<uint32_t *>(sb + q.t1_o_pos);
     T1State *st = reinterpret_cast<T1State *>(sb + q.t1_o_st);
     BinT *sbin = reinterpret_cast<BinT *>(sb + q.t1_o_bins);
     uint32_t *tab = reinterpret_cast<uint32_t *>(sb + q.t1_o_tab);  // build of blocks > 32 px: per warp B counts
@@ -118,77 +128,130 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
     auto lab_at = [&](int x, int y) -> const uint16_t * { return glab + (long long)y * lp + x; };
     auto sbin_at = [&](int x, int y) -> int { return (int)sbin[(y - t.Y0) * tw + (x - t.X0)]; };
 
+    // grid barrier outside the sub-sweep schedule (the fused seed's two)
+    unsigned target = 0;
+    auto gbar = [&]() {
+        __syncthreads();
+        target += gridDim.x;
+        if (tid == 0) {
+            grid_signal(q.sync);
+            grid_poll_acq(q.sync, target);
+        }
+        __syncthreads();
+    };
     if (tid < 16) misc[tid] = 0;
     if (tid < 8) rem[tid] = c_removable[tid];
+    // cold start seeded here (q.t1_seed): every CTA zeroes a
+    // slice of the histogram / size buffers, quantises its tile (reading Q1)
+    // into the shared bins, writes the grid labels (reading O2) and counts the
+    // tile's pixels per (cell, bin) in shared memory; after a grid barrier the
+    // counts go to H and A with one atomic per non-zero entry, and a second
+    // barrier (before the first sub-sweep) publishes them
+    const int Lq = q.L;
+    int cxa = 0, cya = 0, ncx = 1, ncl = 0;
+    int *sh = reinterpret_cast<int *>(sb + q.t1_o_seed);  // [ncell][B] counts, then [ncell] sizes
+    if (q.t1_seed) {
+        for (long long i = (long long)blockIdx.x * NT + tid; i < (long long)q.nf * q.H_fs; i += (long long)gridDim.x * NT) {
+            q.Hb[0][i] = 0;
+            q.Hb[1][i] = 0;
+        }
+        for (long long i = (long long)blockIdx.x * NT + tid; i < (long long)q.nf * q.A_fs; i += (long long)gridDim.x * NT) {
+            q.Ab[0][i] = 0;
+            q.Ab[1][i] = 0;
+        }
+        if (has) {
+            cxa = __ldg(q.bxof + t.X0) >> Lq;
+            cya = __ldg(q.byof + t.Y0) >> Lq;
+            ncx = (__ldg(q.bxof + t.X1 - 1) >> Lq) - cxa + 1;
+            ncl = ncx * ((__ldg(q.byof + t.Y1 - 1) >> Lq) - cya + 1);
+        }
+        for (int i = tid; i < ncl * (B + 1); i += NT) sh[i] = 0;
+    }
     __syncthreads();
     if (tid == 8) misc[8] = q.limit >= 0 ? min(q.limit, STOP_NONE) : STOP_NONE;
     const bool blocks = q.init == nullptr && q.L > 0;
     const int L = blocks ? q.L : 0;
     // ---- prologue ------------------------------------------------------------
-    // class tables (thread 0; 4 L + P^2 entries)
-    if (tid == 0 && has) {
-        int uo = 0, io = 0;
-        for (int l = 0; l < L; l++) {
-            const int bx0 = t.BX0 >> l, bx1 = t.BX1 >> l, by0 = t.BY0 >> l, by1 = t.BY1 >> l;
-            for (int col = 0; col < 4; col++) {
-                const int cx = col & 1, cy = col >> 1;
-                const int ifirst = bx0 + ((bx0 & 1) != cx), jfirst = by0 + ((by0 & 1) != cy);
-                const int uw = ifirst < bx1 ? (bx1 - ifirst + 1) / 2 : 0;
-                const int uh = jfirst < by1 ? (by1 - jfirst + 1) / 2 : 0;
-                cls[l * 4 + col] = T1Class{uo, uw * uh, uw, ifirst, jfirst, io, 0, 0};
-                uo += uw * uh;
-                io += (uw * uh) << q.t1_gs[l];
-            }
-        }
-        misc[10] = uo;
-        misc[12] = io;
-        int po = 0;
-        for (int col = 0; col < P * P; col++) {
-            const int cx = col % P, cy = col / P;
-            const int xfirst = t.X0 + (((cx - t.X0) % P) + P) % P;
-            const int yfirst = t.Y0 + (((cy - t.Y0) % P) + P) % P;
-            const int uw = xfirst < t.X1 ? (t.X1 - xfirst + P - 1) / P : 0;
-            const int uh = yfirst < t.Y1 ? (t.Y1 - yfirst + P - 1) / P : 0;
-            pcls[col] = T1PClass{po, uw * uh, uw, xfirst, yfirst, 0};
-            po += uw * uh;
-        }
-        misc[11] = po;
+    // the tile's static tables (class tables, block geometry, pixel positions;
+    // built by the host once per plan) -- one 16-byte load per thread or two
+    if (has) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(q.t1_static + (size_t)(blockIdx.x % q.t1_nft) * q.t1_sstride);
+        uint4 *dst = reinterpret_cast<uint4 *>(stat);
+        for (int i = tid; i < (int)(q.t1_sstride / 16); i += NT) dst[i] = __ldg(src + i);
     }
     // the tile's bins (constant for the whole run) into shared memory
-    if (has)
+    if (has && q.t1_seed) {
+        // the tile walked as one flat index, four pixels per thread in flight
+        const long long fN = (long long)f * q.N;
+        const int th = t.Y1 - t.Y0, tpx = tw * th;
+        constexpr int U = 4;
+        for (int base = 0; base < tpx; base += U * NT) {
+            uint32_t rgb[U];
+            int cxs[U], cys[U], xs[U], ys[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int i = base + u * NT + tid;
+                rgb[u] = 0;
+                xs[u] = -1;
+                ys[u] = 0;
+                cxs[u] = cys[u] = 0;
+                if (i < tpx) {
+                    const int dy = i / tw;
+                    xs[u] = t.X0 + i - dy * tw;
+                    ys[u] = t.Y0 + dy;
+                    const uint8_t *v = q.img + (fN + (long long)ys[u] * q.W + xs[u]) * q.C;
+                    for (int ch = 0; ch < q.C; ch++) rgb[u] |= (uint32_t)__ldg(v + ch) << (8 * ch);
+                    cxs[u] = __ldg(q.bxof + xs[u]);
+                    cys[u] = __ldg(q.byof + ys[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const bool in = xs[u] >= 0;
+                int b = 0, lc = 0;
+                if (in) {
+                    for (int ch = 0; ch < q.C; ch++) b = b * q.bpc + (((int)(rgb[u] >> (8 * ch) & 0xFF) * q.bpc) >> 8);
+                    sbin[(ys[u] - t.Y0) * tw + xs[u] - t.X0] = (BinT)b;
+                    const int cx = cxs[u] >> Lq, cy = cys[u] >> Lq;
+                    glab[(long long)ys[u] * lp + xs[u]] = (uint16_t)(cy * q.nx + cx);
+                    lc = (cy - cya) * ncx + (cx - cxa);
+                }
+                unsigned m = __match_any_sync(FULL, in ? lc * B + b : -1);
+                if (in && lane == __ffs(m) - 1) atomicAdd(&sh[lc * B + b], __popc(m));
+                m = __match_any_sync(FULL, in ? lc : -1);
+                if (in && lane == __ffs(m) - 1) atomicAdd(&sh[ncl * B + lc], __popc(m));
+            }
+        }
+    } else if (has) {
         for (int y = t.Y0 + wid; y < t.Y1; y += NW) {
             const BinT *src = static_cast<const BinT *>(q.binsp) + (long long)f * q.binsp_fs + (long long)y * q.bpitch;
             for (int x = t.X0 + lane; x < t.X1; x += 32) sbin[(y - t.Y0) * tw + x - t.X0] = src[x];
         }
+    }
+    stamp(0, 3);
+    if (q.t1_seed) {
+        gbar();  // every slice of H and A is zero
+        stamp(0, 4);
+        for (int i = tid; i < ncl * (B + 1); i += NT) {
+            const int v = sh[i];
+            if (!v) continue;
+            const int lc = i < ncl * B ? i / B : i - ncl * B;
+            const int k = (cya + lc / ncx) * q.nx + cxa + lc % ncx;
+            if (i < ncl * B) {
+                const int b = i - lc * B;
+                atomicAdd(H0 + (long long)k * B + b, v);
+                atomicAdd(H1 + (long long)k * B + b, v);
+            } else {
+                atomicAdd(A0 + k, v);
+                atomicAdd(A1 + k, v);
+            }
+        }
+    }
     for (int i = tid; i < q.t1_nst * 5; i += NT) st[i / 5].sum[i % 5] = 0;
     __syncthreads();
-    const int nunits = has ? misc[10] : 0, nitems = has ? misc[12] : 0;
-    // class of block unit g (classes are contiguous in g)
-    auto class_of = [&](int g) {
-        int ci = 0;
-        while (ci + 1 < 4 * L && cls[ci + 1].uoff <= g) ci++;
-        return ci;
-    };
-    // unit geometry (level-0 block starts: colstart[i] = floor(i W / GX), reading O2)
-    for (int g = tid; g < nunits; g += NT) {
-        const int ci = class_of(g);
-        const T1Class c = cls[ci];
-        const int l = ci >> 2, u = g - c.uoff;
-        const int bi = c.ifirst + 2 * (u % c.uw), bj = c.jfirst + 2 * (u / c.uw);
-        const int xa = q.colstart[bi << l], xb = q.colstart[(bi + 1) << l];
-        const int ya = q.rowstart[bj << l], yb = q.rowstart[(bj + 1) << l];
-        units[g] = T1Unit{(uint16_t)xa, (uint16_t)ya, (uint16_t)(xb - xa), (uint16_t)(yb - ya),
-                          (uint32_t)((xb - xa) * (yb - ya)), 0u};
-    }
+    stamp(0, 5);
+    const int nitems = has ? head->nitems : 0;
     for (int i = tid; i < nitems; i += NT) items[i] = make_uint2(0u, 0u);  // empty slots: count 0
-    // pixel positions of every pixel class
-    for (int g = tid; g < (has ? misc[11] : 0); g += NT) {
-        int ci = 0;
-        while (ci + 1 < P * P && pcls[ci + 1].poff <= g) ci++;
-        const T1PClass c = pcls[ci];
-        const int u = g - c.poff;
-        ppos[g] = (uint32_t)(c.xfirst + P * (u % c.uw)) | (uint32_t)(c.yfirst + P * (u / c.uw)) << 16;
-    }
     if (q.t1_tabw)
         for (int i = tid; i < q.t1_tabw; i += NT) tab[i] = 0;
     __syncthreads();
@@ -196,7 +259,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
     // at most 32 pixels one per S-lane segment (S = the power of two >= the
     // largest area; equal bins merged by __match_any_sync), larger ones one warp
     // each (warp-aggregated counts in the warp's table)
-    for (int l = 0; l < L; l++) {
+    for (int l = 0; l < (has ? L : 0); l++) {
         const int g0 = cls[4 * l].uoff, g1 = cls[4 * l + 3].uoff + cls[4 * l + 3].n;
         const int gs = q.t1_gs[l];
         if (q.t1_am[l] <= 32) {
@@ -207,8 +270,8 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
                 const int e = base + lane, g = g0 + (e >> ss), i = e & (S - 1);
                 int b = -1, ci = 0;
                 if (g < g1) {
-                    ci = class_of(g);
                     const T1Unit un = units[g];
+                    ci = (int)un.pad;
                     if (i < (int)un.alpha) {
                         const int dy = i / un.rw;
                         b = sbin_at(un.xa + i - dy * un.rw, un.ya + dy);
@@ -228,7 +291,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
             uint32_t *wt = tab + (size_t)wid * B;
             for (int g = g0 + wid; g < g1; g += NW) {
                 const T1Unit un = units[g];
-                const int ci = class_of(g);
+                const int ci = (int)un.pad;
                 const int u = g - cls[ci].uoff, al = (int)un.alpha, rw = un.rw;
                 uint2 *it = items + cls[ci].ioff + (u << gs);
                 int nd = 0;
@@ -257,11 +320,12 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
             }
         }
     }
-    __syncthreads();
+    stamp(0, 6);
+    if (q.t1_seed) gbar();  // every tile's counts are in H and A, its labels in the plane
+    else __syncthreads();
     stamp(0, 1);
 
     // ---- the refinement ------------------------------------------------------
-    unsigned target = 0;
     const unsigned long long t_start = globaltimer();
     int s = 0;
     auto stopped = [&]() { return s >= misc[8]; };
@@ -279,7 +343,11 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
             if (q.budget_ns > 0 && blockIdx.x == 0 && (long long)(globaltimer() - t_start) >= q.budget_ns)
                 asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(q.stop), "r"(s + 1) : "memory");
             grid_signal(q.sync);
-            grid_poll(q.sync, target);
+#ifdef SEEDS_T1_ACQ_POLL
+            grid_poll_acq(q.sync, target);
+#else
+            grid_poll(q.sync, target);  // relaxed polls + one acquire load: measured faster than acquire polls
+#endif
             if (q.budget_ns > 0) {
                 int v;
                 asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(q.stop) : "memory");
@@ -333,6 +401,8 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
     // ---- block levels, largest first ---------------------
     for (int l = L - 1; l >= 0; l--) {
         const int gs = q.t1_gs[l], G = 1 << gs;
+        // every K5 sum of the level is at most alpha A_n <= alpha_max N
+        const bool narrow = (unsigned long long)q.t1_am[l] * (unsigned long long)q.N < (1ull << 32);
         for (int it = l > q.blk_hi || l < q.blk_lo ? q.iters : 0; it < q.iters; it++)
             for (int col = 0; col < 4; col++) {
                 if (stopped()) break;
@@ -386,12 +456,27 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
                             sm[1 + d] = (valid >> d & 1) ? (unsigned long long)(un_ < vn ? un_ : vn) : 0ull;
                         }
                     }
-                    // N_k, N_n: butterfly over the block's lanes (all of the warp when G >= 32)
+                    // N_k, N_n: butterfly over the block's lanes (all of the warp when G >= 32),
+                    // on 32-bit halves when every sum fits (alpha A <= alpha_max N < 2^32)
+                    if (narrow) {
+                        uint32_t sv[5];
 #pragma unroll
-                    for (int o = 16; o >= 1; o >>= 1) {
-                        if (o >= G) continue;
+                        for (int d = 0; d < 5; d++) sv[d] = (uint32_t)sm[d];
 #pragma unroll
-                        for (int d = 0; d < 5; d++) sm[d] += __shfl_xor_sync(FULL, sm[d], o);
+                        for (int o = 16; o >= 1; o >>= 1) {
+                            if (o >= G) continue;
+#pragma unroll
+                            for (int d = 0; d < 5; d++) sv[d] += __shfl_xor_sync(FULL, sv[d], o);
+                        }
+#pragma unroll
+                        for (int d = 0; d < 5; d++) sm[d] = sv[d];
+                    } else {
+#pragma unroll
+                        for (int o = 16; o >= 1; o >>= 1) {
+                            if (o >= G) continue;
+#pragma unroll
+                            for (int d = 0; d < 5; d++) sm[d] += __shfl_xor_sync(FULL, sm[d], o);
+                        }
                     }
                     if (G > 32) {  // several warps per block: their sums meet in shared memory
                         if (lane == 0 && valid) {
@@ -554,6 +639,29 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
             stamp(s + 1, 2);
             boundary(yb, 0);
         }
+    // ---- output (a12): the tile's int32 labels (its own writes, final here)
+    if (has) {  // flat over the tile, four labels per thread in flight
+        int32_t *out = q.out + (long long)f * q.N;
+        const int tpx = tw * (t.Y1 - t.Y0);
+        constexpr int U = 4;
+        for (int base = 0; base < tpx; base += U * NT) {
+            int v[U];
+            long long o[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int i = base + u * NT + tid;
+                o[u] = -1;
+                if (i < tpx) {
+                    const int dy = i / tw, x = t.X0 + i - dy * tw, y = t.Y0 + dy;
+                    o[u] = (long long)y * q.W + x;
+                    v[u] = __ldcg(lab_at(x, y));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (o[u] >= 0) out[o[u]] = v[u];
+        }
+    }
     if (blockIdx.x == 0 && tid == 0 && q.done) *q.done = s;
 }
 

@@ -179,16 +179,18 @@ def test_host_entry_point(torch_cuda, orc):
 
 
 def test_modes_resolved(torch_cuda):
-    """A c2 frame fits a grid tile plan (grid mode, the AUTO choice); every
-    mode reports its launch count; the removed resident mode (2) is rejected."""
+    """A c2 frame fits a grid tile plan (grid mode, the AUTO choice) with one
+    tile per CTA, so a cold run is one k_tile1 launch (seed and int32 output
+    inside it); every mode reports its launch count; the removed resident mode
+    (2) is rejected."""
     from paper_1309_3848_b200.seeds import Seeds
     s = Seeds(481, 321, 3, 200, 4, 5, 1, 4)
-    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 3  # seed, k_grid, emit
+    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 1  # k_tile1
     assert s._lib.seeds_set_mode(s._ctx, 2) == -1
     s.set_mode("graph")
     assert s.info.exec_mode == 1 and s.info.kernels_per_run == 107
     s.set_mode("grid")
-    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 3
+    assert s.info.exec_mode == 3 and s.info.kernels_per_run == 1
 
 
 def test_two_contexts_on_two_streams(torch_cuda, orc):
