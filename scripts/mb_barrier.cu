@@ -82,6 +82,30 @@ __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned *flags, uns
                 if (V == 8) __nanosleep(32);
             }
         }
+    } else if (V == 11) {
+        // the kernels' scheme: red.release + relaxed polls + one ld.acquire
+        if (threadIdx.x == 0) {
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+            while ((int)(ld_relaxed(ctr) - target) < 0) {}
+            (void)ld_acquire(ctr);
+        }
+    } else if (V >= 12 && V <= 15) {
+        // sub-counters on separate lines: CTA b releases into ctr[32 (1 + b % G)];
+        // warp 0 polls the G sub-counters (relaxed), sums them, then one
+        // acquire fence (V 12: G 16, V 13: G 8, V 14: G 32, V 15: G 16 with
+        // ld.acquire polls)
+        constexpr int G = V == 13 ? 8 : V == 14 ? 32 : 16;
+        if (threadIdx.x == 0)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr + 32 * (1 + blockIdx.x % G)) : "memory");
+        if (threadIdx.x < 32) {
+            for (;;) {
+                unsigned v = 0;
+                if (threadIdx.x < G) v = V == 15 ? ld_acquire(ctr + 32 * (1 + threadIdx.x)) : ld_relaxed(ctr + 32 * (1 + threadIdx.x));
+                v = __reduce_add_sync(0xffffffffu, v);
+                if ((int)(v - target) >= 0) break;
+            }
+            if (V != 15 && threadIdx.x < G) (void)ld_acquire(ctr + 32 * (1 + threadIdx.x));
+        }
     } else if (V == 10) {
         if (threadIdx.x == 0) {
             asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
@@ -182,7 +206,7 @@ void run(int nsm, unsigned *ctr, unsigned *flags, int *data, long long *out, int
     const int iters = 1000;
     long long h[256];
     for (int rep = 0; rep < 2; rep++) {
-        cudaMemset(ctr, 0, 32 * 4 * 32);
+        cudaMemset(ctr, 0, 32 * 4 * 40);
         cudaMemset(flags, 0, 256 * 4);
         void *args[] = {&ctr, &flags, &data, (void *)&iters, &mode, &out};
         cudaError_t e = cudaLaunchCooperativeKernel((void *)k_bar<V>, nsm, nthr, args, 0, 0);
@@ -229,13 +253,13 @@ int main()
     unsigned *ctr, *flags;
     int *data;
     long long *out, h[4];
-    cudaMalloc(&ctr, 32 * 4 * 32);
+    cudaMalloc(&ctr, 32 * 4 * 40);
     cudaMalloc(&flags, 256 * 4);
     cudaMalloc(&data, (nsm * 2048 + 8192) * 4);
     cudaMemset(data, 0, (nsm * 2048 + 8192) * 4);
     cudaMalloc(&out, 256 * 8);
     for (int mode = 0; mode < 2; mode++) {
-        cudaMemset(ctr, 0, 32 * 4 * 32);
+        cudaMemset(ctr, 0, 32 * 4 * 40);
         const int iters = 200;
         void *args[] = {&ctr, &flags, &data, (void *)&iters, &mode, &out};
         cudaLaunchCooperativeKernel((void *)k_hot, nsm, 512, args, 0, 0);
@@ -252,6 +276,22 @@ int main()
     k_lat<<<1, 1>>>(data, 2000, out);
     cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
     printf("L2 (ldcg) dependent-load latency: %lld cycles\n", h[0]);
+    for (int n : {136, nsm}) {
+        run<0>(n, ctr, flags, data, out, 1);
+        run<2>(n, ctr, flags, data, out, 1);
+        run<3>(n, ctr, flags, data, out, 1);
+        run<4>(n, ctr, flags, data, out, 1);
+        run<7>(n, ctr, flags, data, out, 1);
+        run<10>(n, ctr, flags, data, out, 0);
+        run<11>(n, ctr, flags, data, out, 0);
+        run<11>(n, ctr, flags, data, out, 1);
+        for (int m = 0; m < 2; m++) {
+            run<12>(n, ctr, flags, data, out, m);
+            run<13>(n, ctr, flags, data, out, m);
+            run<14>(n, ctr, flags, data, out, m);
+            run<15>(n, ctr, flags, data, out, m);
+        }
+    }
     run_cluster<8>(out);
     run_cluster<12>(out);
     run_cluster<16>(out);
