@@ -114,6 +114,15 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
         (void)which;
 #endif
     };
+    // globaltimer (ns; one clock for every SM) -- tracing builds only
+    auto stampg = [&](int phase, int which) {
+#ifdef SEEDS_TRACE
+        if (q.trace && tid == 0) q.trace[((long long)blockIdx.x * (q.S + 4) + phase) * 16 + which] = (long long)globaltimer();
+#else
+        (void)phase;
+        (void)which;
+#endif
+    };
     stamp(0, 2);
     const bool has = blockIdx.x < q.ntiles;
     GridTile t{};
@@ -336,6 +345,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
     auto boundary = [&](int yb, int zero_n) {
         __syncthreads();
         stamp(s + 1, 0);
+        stampg(s + 1, 7);
         target += gridDim.x;
         for (int i = tid; i < zero_n * 5; i += NT) st[i / 5].sum[i % 5] = 0;
         if (tid == 0) {
@@ -356,6 +366,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
         }
         __syncthreads();
         stamp(s + 1, 1);
+        stampg(s + 1, 6);
         s++;
     };
     // replay the previous sub-sweep's records into buffer yb

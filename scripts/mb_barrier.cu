@@ -106,6 +106,22 @@ __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned *flags, uns
             }
             if (V != 15 && threadIdx.x < G) (void)ld_acquire(ctr + 32 * (1 + threadIdx.x));
         }
+    } else if (V >= 16 && V <= 18) {
+        // replicated counter: every CTA adds 1 to each of R replicas (one fence,
+        // then R relaxed adds by R lanes: a release pattern each); CTA b polls
+        // only replica b % R (relaxed), then one acquire load of it -- the polls
+        // of a line drop R-fold (V 16: R 8, V 17: R 16, V 18: R 4)
+        constexpr int R = V == 16 ? 8 : V == 17 ? 16 : 4;
+        if (threadIdx.x < 32) {
+            if (threadIdx.x == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            __syncwarp();
+            if (threadIdx.x < R) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(ctr + 32 * (1 + threadIdx.x)) : "memory");
+            if (threadIdx.x == 0) {
+                unsigned *c = ctr + 32 * (1 + blockIdx.x % R);
+                while ((int)(ld_relaxed(c) - target) < 0) {}
+                (void)ld_acquire(c);
+            }
+        }
     } else if (V == 10) {
         if (threadIdx.x == 0) {
             asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
@@ -285,6 +301,12 @@ int main()
         run<10>(n, ctr, flags, data, out, 0);
         run<11>(n, ctr, flags, data, out, 0);
         run<11>(n, ctr, flags, data, out, 1);
+        for (int m = 0; m < 2; m++) {
+            run<11>(n, ctr, flags, data, out, m);
+            run<16>(n, ctr, flags, data, out, m);
+            run<17>(n, ctr, flags, data, out, m);
+            run<18>(n, ctr, flags, data, out, m);
+        }
         for (int m = 0; m < 2; m++) {
             run<12>(n, ctr, flags, data, out, m);
             run<13>(n, ctr, flags, data, out, m);
