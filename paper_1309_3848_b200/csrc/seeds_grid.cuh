@@ -200,6 +200,25 @@ __device__ __forceinline__ int band_owner(const GridParams &q, int k)
     return o;
 }
 
+// H / A gathers of k_grid: plain L1-allocating loads (SEEDS_GRID_L1H=0: .cg)
+// -- correct because every grid barrier ends with an acquire load (an L1
+// invalidation) and nothing gathered in a sub-sweep is written in it; repeated
+// rows and sizes then hit L1 (c3 -0.1%, c4 -0.4%, c5 -0.2%)
+#ifndef SEEDS_GRID_L1H
+#define SEEDS_GRID_L1H 1
+#endif
+__device__ __forceinline__ int gld(const int *p) { return SEEDS_GRID_L1H ? *p : __ldcg(p); }
+__device__ __forceinline__ int gld_if(bool p, const int *a)
+{
+    if (!SEEDS_GRID_L1H) return ldcg_if(p, a);
+    int v = 0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.s32 %0, [%1];\n\t}"
+                 : "+r"(v)
+                 : "l"(a), "r"((unsigned)p)
+                 : "memory");
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long globaltimer()
 {
     unsigned long long t;
@@ -434,15 +453,15 @@ struct GridCta {
     __device__ __forceinline__ int ldA(int buf, int k) const
     {
         if (q.acache) return sA[k];  // (row-band mode: only with one band, whose buffers are the context's)
-        return __ldcg(aptr(buf, k));
+        return gld(aptr(buf, k));
     }
-    __device__ __forceinline__ int ldH(int buf, int k, int b) const { return __ldcg(hrow(buf, k) + b); }
+    __device__ __forceinline__ int ldH(int buf, int k, int b) const { return gld(hrow(buf, k) + b); }
     // the same, issued only when p (ldcg_if): no L2 request for an empty slot
-    __device__ __forceinline__ int ldH_if(bool p, int buf, int k, int b) const { return ldcg_if(p, hrow(buf, k) + b); }
+    __device__ __forceinline__ int ldH_if(bool p, int buf, int k, int b) const { return gld_if(p, hrow(buf, k) + b); }
     __device__ __forceinline__ int ldA_if(bool p, int buf, int k) const
     {
         if (q.acache) return sA[k];
-        return ldcg_if(p, aptr(buf, k));
+        return gld_if(p, aptr(buf, k));
     }
     __device__ __forceinline__ void set(int x, int y, int v) const
     {
