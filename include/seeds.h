@@ -132,7 +132,7 @@ seeds_status seeds_batch(seeds_ctx *ctx, const uint8_t *images, int n_frames,
 /* seeds_batch_host -- seeds_batch from and to HOST memory: copies the frames
  * in, runs, copies the labels out and synchronises `stream`.  Pinned host
  * buffers give the fastest copies; pageable ones work.  init_labels_host may
- * be NULL (cold).  A batch of several frames is cut into 2-4 equal chunks
+ * be NULL (cold).  A batch of several frames is cut into 2-16 equal chunks
  * (seeds_set_host_chunks) whose copies in and out run on two copy streams
  * while the neighbouring chunks are refined; the frames being independent, the
  * labels are those of one seeds_batch.  After a chunked call the context holds
@@ -153,10 +153,30 @@ seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_
 seeds_status seeds_batch_host_warm(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
                                    int32_t *labels_out_host, void *stream);
 
+/* seeds_video_host -- n_steps time steps of n_streams video streams, from and
+ * to HOST memory, in one call: step 0 cold (or, continue_prev = 1, warm from
+ * this context's labels of the previous seeds_batch_host / _warm / video call,
+ * which must have had n_frames = n_streams, else SEEDS_ESTATE), every later
+ * step warm-started from the previous step's labels on the device (reading O9:
+ * video is named as an input at PAPER.md:943; BASELINE.json's c4 seeds each
+ * frame's labels from the previous frame's result); the copy in of step t + 1
+ * and the copy out of step t - 1 overlap
+ * the refinement of step t (two copy streams, double-buffered staging).
+ *   images_host      n_steps x n_streams x H x W x C uint8, time-major
+ *                    (stream i of step t at index t * n_streams + i)
+ *   labels_out_host  n_steps x n_streams x H x W int32, the same order
+ * Equals n_steps calls of seeds_batch_host_warm (the first seeds_batch_host
+ * when continue_prev = 0) frame for frame; the chain then continues
+ * (seeds_batch_host_warm or continue_prev = 1).  Synchronises `stream`.
+ * SEEDS_EINVAL for NULL buffers, n_streams outside 1..65535, n_steps < 1 or
+ * continue_prev outside 0..1.  Pinned host buffers give the fastest copies. */
+seeds_status seeds_video_host(seeds_ctx *ctx, const uint8_t *images_host, int n_streams, int n_steps,
+                              int continue_prev, int32_t *labels_out_host, void *stream);
+
 /* seeds_set_host_chunks -- chunks of the seeds_batch_host pipeline: 0 (default)
  * picks the largest of 4, 3, 2 dividing n_frames; 1 turns the pipeline off
- * (one copy in, one run, one copy out); 2..4 the largest count <= chunks
- * dividing n_frames.  SEEDS_EINVAL outside 0..4. */
+ * (one copy in, one run, one copy out); 2..16 the largest count <= chunks
+ * dividing n_frames.  SEEDS_EINVAL outside 0..16. */
 seeds_status seeds_set_host_chunks(seeds_ctx *ctx, int chunks);
 
 /* seeds_query -- derived geometry and sizes (see seeds_info). */

@@ -86,7 +86,7 @@ struct seeds_ctx {
     cudaStream_t cap_stream = nullptr;
     // seeds_batch_host pipeline: copy-in / copy-out streams and chunk events
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-    cudaEvent_t pev[16] = {};
+    cudaEvent_t pev[40] = {};  // [0, 16) copy-in chunks, [16, 32) runs, 32.. video steps, 38 start, 39 end
     int host_chunks = 0;  // seeds_set_host_chunks (0 = automatic)
     int host_prev_nf = 0; // frames of the last successful host call (its labels stay in d_out_stage)
     // instantiated runs, keyed by their pointers / sizes (least recently used dropped)
@@ -1762,8 +1762,8 @@ static seeds_status batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n
         }
         const int m = n_frames / nc;
         const size_t fi = (size_t)ctx->N * ctx->C, fo = (size_t)ctx->N * 4;
-        CK(cudaEventRecord(ctx->pev[15], st));  // the staging buffers are free once earlier work on st is done
-        CK(cudaStreamWaitEvent(ctx->h2d_stream, ctx->pev[15], 0));
+        CK(cudaEventRecord(ctx->pev[38], st));  // the staging buffers are free once earlier work on st is done
+        CK(cudaStreamWaitEvent(ctx->h2d_stream, ctx->pev[38], 0));
         for (int i = 0; i < nc; i++) {
             const size_t f0 = (size_t)i * m;
             CK(cudaMemcpyAsync(ctx->d_img_stage + f0 * fi, images_host + f0 * fi, m * fi, cudaMemcpyHostToDevice,
@@ -1779,13 +1779,13 @@ static seeds_status batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n
             seeds_status r = run(ctx, ctx->d_img_stage + f0 * fi, has_init ? ctx->d_init_stage + f0 * ctx->N : nullptr,
                                  ctx->d_out_stage + f0 * ctx->N, m, st);
             if (r != SEEDS_OK) return r;
-            CK(cudaEventRecord(ctx->pev[4 + i], st));
-            CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->pev[4 + i], 0));
+            CK(cudaEventRecord(ctx->pev[16 + i], st));
+            CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->pev[16 + i], 0));
             CK(cudaMemcpyAsync(labels_out_host + f0 * ctx->N, ctx->d_out_stage + f0 * ctx->N, m * fo,
                                cudaMemcpyDeviceToHost, ctx->d2h_stream));
         }
-        CK(cudaEventRecord(ctx->pev[14], ctx->d2h_stream));
-        CK(cudaStreamWaitEvent(st, ctx->pev[14], 0));
+        CK(cudaEventRecord(ctx->pev[39], ctx->d2h_stream));
+        CK(cudaStreamWaitEvent(st, ctx->pev[39], 0));
         CK(cudaStreamSynchronize(st));
         ctx->ran = false;  // the context's state is that of the last chunk only (seeds_read_state: ESTATE)
         return check_err(ctx);
@@ -1830,9 +1830,95 @@ seeds_status seeds_batch_host_warm(seeds_ctx *ctx, const uint8_t *images_host, i
     return r;
 }
 
+// seeds_video_host: n_steps time steps of n_streams video streams from and to
+// host memory, each step warm-started from the previous one's labels on the
+// device (reading O9), the copy in of step t + 1 and the copy out of step t - 1
+// overlapping the refinement of step t (copy streams + events, double-buffered
+// staging: images in d_img_stage's two halves, labels alternating between
+// d_out_stage and d_init_stage).
+seeds_status seeds_video_host(seeds_ctx *ctx, const uint8_t *images_host, int n_streams, int n_steps,
+                              int continue_prev, int32_t *labels_out_host, void *stream)
+{
+    if (!ctx || !images_host || !labels_out_host || n_streams < 1 || n_streams > 65535 || n_steps < 1 ||
+        (continue_prev != 0 && continue_prev != 1))
+        return SEEDS_EINVAL;
+    if (continue_prev && ctx->host_prev_nf != n_streams) {
+        snprintf(ctx->err, sizeof ctx->err, "seeds_video_host: the previous host call had %d frames, not %d",
+                 ctx->host_prev_nf, n_streams);
+        return SEEDS_ESTATE;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t m = (size_t)n_streams, fi = (size_t)ctx->N * ctx->C, fo = (size_t)ctx->N * 4;
+    if ((size_t)ctx->stage_frames < 2 * m) {  // two steps of staging (the previous labels carried over)
+        CK(cudaStreamSynchronize(st));
+        uint8_t *img = nullptr;
+        int32_t *out = nullptr, *init = nullptr;
+        CK(cudaMalloc(&img, 2 * m * fi));
+        CK(cudaMalloc(&out, 2 * m * fo));
+        CK(cudaMalloc(&init, 2 * m * fo));
+        if (continue_prev) CK(cudaMemcpy(out, ctx->d_out_stage, m * fo, cudaMemcpyDeviceToDevice));
+        if (ctx->d_img_stage) cudaFree(ctx->d_img_stage);
+        if (ctx->d_out_stage) cudaFree(ctx->d_out_stage);
+        if (ctx->d_init_stage) cudaFree(ctx->d_init_stage);
+        ctx->d_img_stage = img;
+        ctx->d_out_stage = out;
+        ctx->d_init_stage = init;
+        ctx->stage_frames = (int)(2 * m);
+    }
+    if (!ctx->h2d_stream) {
+        CK(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+        for (auto &ev : ctx->pev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    ctx->host_prev_nf = 0;  // a failure ends the chain
+    uint8_t *img[2] = {ctx->d_img_stage, ctx->d_img_stage + m * fi};
+    int32_t *out[2] = {ctx->d_out_stage, ctx->d_init_stage};
+    const int o = continue_prev;  // step t writes out[(t + o) & 1]; out[0] holds the previous call's labels
+    cudaEvent_t *h2d_done = ctx->pev + 32, *run_done = ctx->pev + 34, *d2h_done = ctx->pev + 36;
+    CK(cudaEventRecord(ctx->pev[38], st));  // the staging buffers are free once earlier work on st is done
+    CK(cudaStreamWaitEvent(ctx->h2d_stream, ctx->pev[38], 0));
+    CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->pev[38], 0));
+    CK(cudaMemcpyAsync(img[0], images_host, m * fi, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    CK(cudaEventRecord(h2d_done[0], ctx->h2d_stream));
+    for (int t = 0; t < n_steps; t++) {
+        const int b = t & 1, ob = (t + o) & 1;
+        if (t + 1 < n_steps) {  // prefetch step t + 1 into the other image buffer (read by step t - 1)
+            if (t >= 1) CK(cudaStreamWaitEvent(ctx->h2d_stream, run_done[b ^ 1], 0));
+            CK(cudaMemcpyAsync(img[b ^ 1], images_host + (size_t)(t + 1) * m * fi, m * fi, cudaMemcpyHostToDevice,
+                               ctx->h2d_stream));
+            CK(cudaEventRecord(h2d_done[b ^ 1], ctx->h2d_stream));
+        }
+        CK(cudaStreamWaitEvent(st, h2d_done[b], 0));
+        if (t >= 2) CK(cudaStreamWaitEvent(st, d2h_done[ob], 0));  // step t - 2's labels are out
+        const int32_t *init = t > 0 || o ? out[ob ^ 1] : nullptr;
+        seeds_status r = run(ctx, img[b], init, out[ob], n_streams, st);
+        if (r != SEEDS_OK) {
+            cudaStreamSynchronize(ctx->h2d_stream);
+            cudaStreamSynchronize(ctx->d2h_stream);
+            return r;
+        }
+        CK(cudaEventRecord(run_done[b], st));
+        CK(cudaStreamWaitEvent(ctx->d2h_stream, run_done[b], 0));
+        CK(cudaMemcpyAsync(labels_out_host + (size_t)t * m * ctx->N, out[ob], m * fo, cudaMemcpyDeviceToHost,
+                           ctx->d2h_stream));
+        CK(cudaEventRecord(d2h_done[ob], ctx->d2h_stream));
+    }
+    const int last = (n_steps - 1 + o) & 1;
+    if (last == 1) {  // the chain continues from d_out_stage (seeds_batch_host_warm / continue_prev)
+        CK(cudaStreamWaitEvent(st, d2h_done[0], 0));  // (step n_steps - 2's labels are out of out[0])
+        CK(cudaMemcpyAsync(out[0], out[1], m * fo, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaEventRecord(ctx->pev[39], ctx->d2h_stream));
+    CK(cudaStreamWaitEvent(st, ctx->pev[39], 0));
+    CK(cudaStreamSynchronize(st));
+    seeds_status r = check_err(ctx);
+    if (r == SEEDS_OK) ctx->host_prev_nf = n_streams;
+    return r;
+}
+
 seeds_status seeds_set_host_chunks(seeds_ctx *ctx, int chunks)
 {
-    if (!ctx || chunks < 0 || chunks > 4) return SEEDS_EINVAL;
+    if (!ctx || chunks < 0 || chunks > 16) return SEEDS_EINVAL;
     ctx->host_chunks = chunks;
     return SEEDS_OK;
 }

@@ -30,7 +30,7 @@ EXPORTS = ["seeds_create", "seeds_iterate", "seeds_batch", "seeds_batch_host", "
            "seeds_rgb_to_lab", "seeds_set_block_levels", "seeds_set_host_chunks", "seeds_set_compactness",
            "seeds_set_edge_prior", "seeds_batch_host_warm", "seeds_validate_labels", "seeds_set_validate",
            "seeds_set_time_budget", "seeds_last_subsweeps", "seeds_debug_k5",
-           "seeds_debug_block_hist"]
+           "seeds_debug_block_hist", "seeds_video_host"]
 
 
 class _Metrics(ctypes.Structure):
@@ -72,6 +72,7 @@ def load(path: str = LIB_PATH):
         "seeds_batch": ([vp, vp, i, vp, vp, vp], i),
         "seeds_batch_host": ([vp, vp, i, vp, vp, vp], i),
         "seeds_batch_host_warm": ([vp, vp, i, vp, vp], i),
+        "seeds_video_host": ([vp, vp, i, i, i, vp, vp], i),
         "seeds_query": ([vp, ctypes.POINTER(Info)], i),
         "seeds_read_state": ([vp, i, vp, vp, vp], i),
         "seeds_debug_limit": ([vp, i], i),
@@ -272,6 +273,19 @@ class Seeds:
         n = self._host_frames(images, labels_out)
         self._check(self._lib.seeds_batch_host_warm(self._ctx, images.ctypes.data, n, labels_out.ctypes.data,
                                                     _stream_ptr(stream)))
+        return labels_out
+
+    def video_host(self, images: np.ndarray, labels_out: np.ndarray, continue_prev: bool = False, stream=None):
+        """n_steps x n_streams video frames (time-major, uint8 (T, n, H, W, C))
+        from host memory in one call, each step warm-started from the previous
+        one's labels (seeds_video_host); labels_out int32 (T, n, H, W)."""
+        if not (isinstance(images, np.ndarray) and images.ndim >= 4):
+            raise TypeError("images must be a (T, n, H, W[, C]) uint8 numpy array")
+        T, n = images.shape[0], images.shape[1]
+        if self._host_frames(images, labels_out) != T * n:
+            raise ValueError("images must hold T x n whole frames")
+        self._check(self._lib.seeds_video_host(self._ctx, images.ctypes.data, n, T, int(bool(continue_prev)),
+                                               labels_out.ctypes.data, _stream_ptr(stream)))
         return labels_out
 
     def read_state(self, frame: int = 0, stream=None):

@@ -1,4 +1,5 @@
-"""profiles/ncu_traffic.json from ncu --set full captures of one k_grid launch:
+"""profiles/ncu_traffic.json from ncu --set full captures of one refinement launch (k_tile1 for
+the single-tile c2 plan, k_grid for c3-c5):
 DRAM bytes (read + write) and warp instructions per launch, per config."""
 import csv
 import json
@@ -23,7 +24,8 @@ def raw(path):
             "launch_us": t * (1e3 if tu == "ms" else 1.0)}
 
 
-res = {"_source": "ncu --set full --clock-control none of one k_grid launch (scripts/make_traffic.py); "
+res = {"_source": "ncu --set full --clock-control none of one refinement launch (scripts/make_traffic.py): "
+                  "c2 k_tile1 (seed, refinement and int32 labels in one launch), c3-c5 k_grid; "
                   "c3 and c4 are cold batch launches (c4: one 8-frame time step)"}
 for arg in sys.argv[1:]:
     key, path = arg.split("=")

@@ -169,6 +169,25 @@ def test_multi_tile_plans_are_deterministic(torch_cuda):
         s.close()
 
 
+def test_c4_video_host_matches_device(torch_cuda):
+    """The c4 video (8 clips x 4 frames) through one seeds_video_host call
+    (pinned buffers, copies overlapping the runs): identical to the device
+    entry point chained frame by frame with explicit previous labels."""
+    torch = torch_cuda
+    cl = configs.clips("c4")[:, :4]
+    p = configs.params("c4")
+    s = ctx(cl.shape[2:], p, "auto")
+    video = torch.from_numpy(np.ascontiguousarray(cl.transpose(1, 0, 2, 3, 4))).pin_memory()  # time x clip
+    out = torch.empty(video.shape[:4], dtype=torch.int32).pin_memory()
+    s.video_host(video.numpy(), out.numpy())
+    prev = None
+    for t in range(video.shape[0]):
+        ref = s.batch(video[t].cuda(), init_labels=prev)
+        np.testing.assert_array_equal(out[t].numpy(), ref.cpu().numpy())
+        prev = ref.clone()
+    s.close()
+
+
 def test_c4_host_warm_chain_matches_device(torch_cuda):
     """The c4 video (8 clips) through seeds_batch_host_warm, frame 0 cold, then
     frames 1-3 warm from the labels the previous host call left on the device

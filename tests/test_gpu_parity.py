@@ -311,6 +311,51 @@ def test_batch_host_warm_chain(torch_cuda, orc, chunks):
     s.close()
 
 
+def test_video_host_chain(torch_cuda, orc):
+    """seeds_video_host: three time steps of four streams from host memory in
+    one call (copies of neighbouring steps overlapping each step's run), every
+    step after the first warm-started from the previous one (reading O9); equals
+    the oracle's warm chain frame by frame.  A second call with continue_prev
+    continues the chain, as does a following seeds_batch_host_warm; continuing
+    with another stream count, or without a previous host call, is SEEDS_ESTATE."""
+    from paper_1309_3848_b200.seeds import Seeds, SeedsError
+    f = configs.frames("c2", n=16)
+    p = configs.params("c2")
+    video = np.ascontiguousarray(f[:12].reshape(3, 4, *f.shape[1:]))  # time x stream
+    s = Seeds(f.shape[2], f.shape[1], 3, *[p[k] for k in (
+        "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    out = np.empty(video.shape[:4], np.int32)
+    with pytest.raises(SeedsError):
+        s.video_host(video, out, continue_prev=True)
+    s.video_host(video, out)
+    prev = [None] * 4
+    for t in range(3):
+        for i in range(4):
+            r = orc.run(video[t, i], **p, init_labels=prev[i]).labels
+            np.testing.assert_array_equal(out[t, i], r)
+            prev[i] = r
+    # continue the chain: three more steps (their labels end in the second buffer and are carried back
+    # for the next call), then one host_warm step
+    more = np.ascontiguousarray(np.stack([video[1], video[0], video[2]]))
+    out2 = np.empty(more.shape[:4], np.int32)
+    s.video_host(more, out2, continue_prev=True)
+    for t in range(3):
+        for i in range(4):
+            r = orc.run(more[t, i], **p, init_labels=prev[i]).labels
+            np.testing.assert_array_equal(out2[t, i], r)
+            prev[i] = r
+    one = np.empty((4,) + f.shape[1:3], np.int32)
+    s.batch_host_warm(np.ascontiguousarray(video[2]), one)
+    for i in range(4):
+        np.testing.assert_array_equal(one[i], orc.run(video[2, i], **p, init_labels=prev[i]).labels)
+    with pytest.raises(SeedsError):  # another stream count cannot continue this chain
+        s.video_host(np.ascontiguousarray(f[:2].reshape(1, 2, *f.shape[1:])), np.empty((1, 2) + f.shape[1:3], np.int32),
+                     continue_prev=True)
+    with pytest.raises(ValueError):
+        s.video_host(video, np.empty((3, 4, 2, 2), np.int32))
+    s.close()
+
+
 @pytest.mark.parametrize("nt", ["512", "128"])
 @pytest.mark.parametrize("seg2", ["0", "1"])
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c4"])
