@@ -281,18 +281,26 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
         }
     }
     for (int i = tid; i < q.t1_nst * 5; i += NT) st[i / 5].sum[i % 5] = 0;
-    __syncthreads();
-    stamp(0, 5);
+    __syncthreads();  // (the static tables, copied in the prologue, are complete)
     const int nitems = has ? head->nitems : 0;
     for (int i = tid; i < nitems; i += NT) items[i] = make_uint2(0u, 0u);  // empty slots: count 0
     if (q.t1_tabw)
         for (int i = tid; i < q.t1_tabw; i += NT) tab[i] = 0;
     __syncthreads();
+    stamp(0, 5);
+    // a cold run arrives at the grid barrier that publishes the seed's counts
+    // now (after the CTA barrier, every thread's flush is in) and waits for it
+    // after the item build, which only reads this tile's bins
+    if (q.t1_seed) {
+        target += gridDim.x;
+        if (tid == 0) grid_signal(q.sync);
+    }
     // block histograms as (bin, count) items at slots ioff + u G + rank: blocks of
     // at most 32 pixels one per S-lane segment (S = the power of two >= the
     // largest area; equal bins merged by __match_any_sync), larger ones one warp
     // each (warp-aggregated counts in the warp's table)
     for (int l = 0; l < (has ? L : 0); l++) {
+        stamp(0, 7 + l);
         const int g0 = cls[4 * l].uoff, g1 = cls[4 * l + 3].uoff + cls[4 * l + 3].n;
         const int gs = q.t1_gs[l];
         if (q.t1_am[l] <= 32) {
@@ -320,6 +328,47 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
                     items[cls[ci].ioff + (u << gs) + rank] = make_uint2((uint32_t)u | (uint32_t)b << 16, (uint32_t)__popc(m));
                 }
             }
+        } else if (g1 - g0 <= NW) {
+            // a few large blocks (the top levels): every thread counts pixels of the
+            // level's blocks, taken as one flat range, into block bi's B-word table
+            // (warp-aggregated per (block, bin)); then warp bi compacts table bi into
+            // the block's item slots and clears it.  Balanced over all warps, where
+            // one warp per block would walk a top-level block alone.
+            __syncthreads();  // (a lower level's per-warp tables are in use until here)
+            const int nbk = g1 - g0;
+            int tot = 0;
+            for (int bk = 0; bk < nbk; bk++) tot += (int)units[g0 + bk].alpha;
+            for (int e0 = 0; e0 < tot; e0 += NT) {
+                const int e = e0 + tid;
+                int b = -1, bi = 0;
+                if (e < tot) {
+                    int off = e;
+                    while (off >= (int)units[g0 + bi].alpha) off -= (int)units[g0 + bi++].alpha;
+                    const T1Unit un = units[g0 + bi];
+                    const int dy = off / un.rw;
+                    b = sbin_at(un.xa + off - dy * un.rw, un.ya + dy);
+                }
+                const unsigned m = __match_any_sync(FULL, b < 0 ? -1 - lane : (bi << 16 | b));
+                if (b >= 0 && lane == __ffs(m) - 1) atomicAdd(&tab[(size_t)bi * B + b], (unsigned)__popc(m));
+            }
+            __syncthreads();
+            if (wid < nbk) {
+                const int g = g0 + wid, ci = (int)units[g].pad, u = g - cls[ci].uoff;
+                uint2 *it = items + cls[ci].ioff + (u << gs);
+                uint32_t *bt = tab + (size_t)wid * B;
+                int nd = 0;
+                for (int j0 = 0; j0 < B; j0 += 32) {
+                    const int bin = j0 + lane;
+                    const uint32_t cnt = bin < B ? bt[bin] : 0u;
+                    const unsigned nz = __ballot_sync(FULL, cnt != 0u);
+                    if (cnt) {
+                        it[nd + __popc(nz & ((1u << lane) - 1))] = make_uint2((uint32_t)u | (uint32_t)bin << 16, cnt);
+                        bt[bin] = 0u;
+                    }
+                    nd += __popc(nz);
+                }
+            }
+            __syncthreads();
         } else {
             uint32_t *wt = tab + (size_t)wid * B;
             for (int g = g0 + wid; g < g1; g += NW) {
@@ -354,8 +403,8 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_tile1(const __grid_constant__
         }
     }
     stamp(0, 6);
-    if (q.t1_seed) gbar();  // every tile's counts are in H and A, its labels in the plane
-    else __syncthreads();
+    if (q.t1_seed && tid == 0) grid_poll(q.sync, target);  // every tile's counts are in H and A, its labels in the plane
+    __syncthreads();
     stamp(0, 1);
 
     // ---- the refinement ------------------------------------------------------

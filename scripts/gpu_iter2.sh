@@ -1,0 +1,5 @@
+# parity + fuzz on the in-tree build, A/B against scripts/alt_head.so (c2, c1), prologue trace
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py tests/test_gpu_seed.py -x -q > gpurun_out/it_pytest.log 2>&1; echo "exit $?" >> gpurun_out/it_pytest.log
+ALTS=scripts/alt_head.so CFGS="c2 c1" bash scripts/gpu_ab.sh > gpurun_out/it_ab.txt 2>&1
+SEEDS_LIB=scripts/alt_trace.so timeout 200 python scripts/trace_prologue.py c2 > gpurun_out/it_prologue.txt 2>&1

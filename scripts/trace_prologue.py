@@ -30,3 +30,9 @@ for a, b, n in names:
     v = r0[:, b] - r0[:, a]
     print(f"{n:18s} mean {v.mean():8.0f} max {v.max():8.0f} min {v.min():8.0f}")
 print(f"{'total':18s} mean {(r0[:, 1] - r0[:, 2]).mean():8.0f}")
+# per level of the item build (stamps 7 + l at each level's start, thread 0's view)
+L = s.info.levels_eff
+pts = [5] + [7 + l for l in range(L)] + [6]
+for a, b in zip(pts[:-1], pts[1:]):
+    v = r0[:, b] - r0[:, a]
+    print(f"  item build {a}->{b}: mean {v.mean():7.0f} max {v.max():7.0f}")
