@@ -181,6 +181,7 @@ struct seeds_ctx {
     // device status word: bit 0 = a warm-start label outside [0, K) (kernels
     // set it with atomicOr; check_err reports and clears it after a sync)
     int *d_err = nullptr;
+    int *h_err = nullptr;  // page-locked copy of d_err[0] (host entry points)
     // label validation (seeds_validate_labels, seeds_set_validate)
     bool validate = false;
     int *d_cc_par = nullptr, *d_cc_roots = nullptr;
@@ -207,6 +208,23 @@ static seeds_status cuda_fail(seeds_ctx *c, cudaError_t e, const char *what)
 // After a synchronisation: report (and clear) a status the kernels flagged
 // since the last check -- SEEDS_ESTATE for warm-start labels outside [0, K)
 // (include/seeds.h seeds_batch).
+// The same for the host entry points, without a blocking copy: the error word
+// is copied on `st` into page-locked memory before the stream synchronisation
+// that ends the call (enqueue_err), then read here (err_after_sync).
+static cudaError_t enqueue_err(seeds_ctx *ctx, cudaStream_t st)
+{
+    return cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, st);
+}
+static seeds_status err_after_sync(seeds_ctx *ctx)
+{
+    if (!ctx->h_err[0]) return SEEDS_OK;
+    ctx->h_err[0] = 0;
+    CK(cudaMemset(ctx->d_err, 0, sizeof(int)));
+    snprintf(ctx->err, sizeof ctx->err,
+             "init_labels held a label outside [0, K_act) (counted as label 0; the run's output is not meaningful)");
+    return SEEDS_ESTATE;
+}
+
 static seeds_status check_err(seeds_ctx *ctx)
 {
     int h = 0;
@@ -1696,6 +1714,8 @@ seeds_status seeds_create(int width, int height, int channels, int n_superpixels
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_err, 16);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, 16);
+    if (e == cudaSuccess) e = cudaHostAlloc(&ctx->h_err, 16, cudaHostAllocDefault);
+    if (e == cudaSuccess) ctx->h_err[0] = 0;
     if (e != cudaSuccess) {
         seeds_status st = e == cudaErrorMemoryAllocation ? SEEDS_ENOMEM : SEEDS_ECUDA;
         seeds_destroy(ctx);
@@ -1786,13 +1806,14 @@ static seeds_status batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n
         }
         CK(cudaEventRecord(ctx->pev[39], ctx->d2h_stream));
         CK(cudaStreamWaitEvent(st, ctx->pev[39], 0));
+        CK(enqueue_err(ctx, st));
         CK(cudaStreamSynchronize(st));
         ctx->ran = false;  // the context's state is that of the last chunk only (seeds_read_state: ESTATE)
-        return check_err(ctx);
+        return err_after_sync(ctx);
     }
+    const int32_t *init = has_init ? ctx->d_init_stage : nullptr;
     CK(cudaMemcpyAsync(ctx->d_img_stage, images_host, (size_t)n_frames * ctx->N * ctx->C,
                        cudaMemcpyHostToDevice, st));
-    const int32_t *init = has_init ? ctx->d_init_stage : nullptr;
     if (init_labels_host && !warm)
         CK(cudaMemcpyAsync(ctx->d_init_stage, init_labels_host, (size_t)n_frames * ctx->N * 4,
                            cudaMemcpyHostToDevice, st));
@@ -1800,8 +1821,9 @@ static seeds_status batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n
     if (r != SEEDS_OK) return r;
     CK(cudaMemcpyAsync(labels_out_host, ctx->d_out_stage, (size_t)n_frames * ctx->N * 4, cudaMemcpyDeviceToHost,
                        st));
+    CK(enqueue_err(ctx, st));
     CK(cudaStreamSynchronize(st));
-    return check_err(ctx);
+    return err_after_sync(ctx);
 }
 
 seeds_status seeds_batch_host(seeds_ctx *ctx, const uint8_t *images_host, int n_frames,
@@ -1910,8 +1932,9 @@ seeds_status seeds_video_host(seeds_ctx *ctx, const uint8_t *images_host, int n_
     }
     CK(cudaEventRecord(ctx->pev[39], ctx->d2h_stream));
     CK(cudaStreamWaitEvent(st, ctx->pev[39], 0));
+    CK(enqueue_err(ctx, st));
     CK(cudaStreamSynchronize(st));
-    seeds_status r = check_err(ctx);
+    seeds_status r = err_after_sync(ctx);
     if (r == SEEDS_OK) ctx->host_prev_nf = n_streams;
     return r;
 }
@@ -2335,6 +2358,7 @@ void seeds_destroy(seeds_ctx *ctx)
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
     for (auto &ev : ctx->pev)
         if (ev) cudaEventDestroy(ev);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
     delete ctx;
 }
 

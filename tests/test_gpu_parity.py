@@ -311,6 +311,30 @@ def test_batch_host_warm_chain(torch_cuda, orc, chunks):
     s.close()
 
 
+def test_batch_host_pinned_single_frames(torch_cuda, orc):
+    """seeds_batch_host / _warm on single frames in page-locked host buffers,
+    then from pageable ones: a warm chain equal to the oracle's frame by frame."""
+    torch = torch_cuda
+    from paper_1309_3848_b200.seeds import Seeds
+    f = configs.frames("c2", n=3)
+    p = configs.params("c2")
+    s = Seeds(f.shape[2], f.shape[1], 3, *[p[k] for k in (
+        "n_superpixels", "n_levels", "bins_per_channel", "smoothness_prior", "iters_per_level")])
+    hin = torch.from_numpy(np.ascontiguousarray(f[:1])).pin_memory()
+    hout = torch.full((1,) + f.shape[1:3], -1, dtype=torch.int32).pin_memory()
+    s.batch_host(hin.numpy(), hout.numpy())
+    r0 = orc.run(f[0], **p).labels
+    np.testing.assert_array_equal(hout[0].numpy(), r0)
+    hin.copy_(torch.from_numpy(f[1:2]))
+    s.batch_host_warm(hin.numpy(), hout.numpy())
+    r1 = orc.run(f[1], **p, init_labels=r0).labels
+    np.testing.assert_array_equal(hout[0].numpy(), r1)
+    out = np.empty((1,) + f.shape[1:3], np.int32)  # pageable buffers, the same chain
+    s.batch_host_warm(np.ascontiguousarray(f[2:3]), out)
+    np.testing.assert_array_equal(out[0], orc.run(f[2], **p, init_labels=r1).labels)
+    s.close()
+
+
 def test_video_host_chain(torch_cuda, orc):
     """seeds_video_host: three time steps of four streams from host memory in
     one call (copies of neighbouring steps overlapping each step's run), every
