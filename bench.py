@@ -765,6 +765,10 @@ def main():
                        "compact": args.compact,
                        "edge_tau": args.edge,
                        "grid_ctas": info.grid_ctas, "grid_tiles_per_frame": info.grid_tiles,
+                       # the refinement kernel the roofline's "frame" launch is: one k_tile1 launch per
+                       # cold run when every CTA owns one tile, else seed + k_grid + emit
+                       "refine_kernel": ("k_tile1" if mode_name == "grid" and info.kernels_per_run == 1 else
+                                         "k_grid" if mode_name.startswith("grid") else "graph kernels"),
                        "parallelism": wl.parallelism,
                        "exchange": ("inside the persistent kernel: owner-band histogram updates and halo label rows "
                                     "through peer memory, one counter barrier per sub-sweep") if banded else None,
