@@ -642,8 +642,8 @@ static int resolved_mode(seeds_ctx *c, int nf)
 // ---------------------------------------------------------------------------
 // Grid mode (seeds_grid.cuh): tile plan for a batch of nf frames.  Tiles are
 // rectangles of a x b top-level blocks (pixels when L = 0); the plan takes the
-// (a, b) with the least pixels on the busiest CTA (tiles go round-robin to
-// min(#SM, #tiles) CTAs), then the least halo.  Shared memory per CTA: the
+// (a, b) with the least cost on the busiest CTA (tiles go round-robin to
+// min(#SM, #tiles) CTAs): its pixels, its tiles' halos and a fixed cost per tile.  Shared memory per CTA: the
 // staged labels of one tile (+ 2-pixel halo), the bins of all its tiles when
 // they fit (else of one tile, restaged every sub-sweep), the unit queue, the
 // warp tables of the large-block path and the block geometry.
@@ -1039,6 +1039,17 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     const size_t fixed = 128 + 16 + (need_tab ? tabw : 0);
     double best = 1e300;
     int ba = 0, bb_ = 0;
+    // Fixed cost of a tile in pixel equivalents: every tile of a CTA is a
+    // dependent chain per sub-sweep (TMA wait, filter pass, decide, CTA barriers),
+    // so fewer, larger tiles win at equal pixels per CTA.  Measured
+    // (profiles/r02/tile_cost_sweep.txt): 300-20000 all give the same plans,
+    // c5 26.7 -> 22.4 ms, c3 19.3 -> 18.0 ms, c2 / c4 plans unchanged; 0 is
+    // round 2's pixel-and-halo-only score.  SEEDS_TILE_COST / SEEDS_HALO_W
+    // override it (A/B measurements).
+    double tile_cost = 1000;
+    if (const char *v = getenv("SEEDS_TILE_COST")) tile_cost = atof(v);
+    double halo_w = 4.0;
+    if (const char *v = getenv("SEEDS_HALO_W")) halo_w = atof(v);
     for (int a : size_candidates(TX))
         for (int b : size_candidates(TYb)) {
             long long rows = 0;
@@ -1051,7 +1062,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
             const size_t minimal = stage + 2 * align128((size_t)(tw + 32) * th * c->bb) + align16((size_t)tw * th * 4) + fixed;
             if (minimal > limit) continue;
             const long long per = (T + G - 1) / G;
-            const double score = (double)per * tw * th + 4.0 * per * (tw + th + 4);
+            const double score = (double)per * tw * th + halo_w * per * (tw + th + 4) + tile_cost * per;
             if (score < best) {
                 best = score;
                 ba = a;
@@ -1258,6 +1269,9 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         c->grid_G = G;
         c->grid_smem = smem;
         c->grid_nt = nt;
+        if (getenv("SEEDS_PLAN_DEBUG"))
+            fprintf(stderr, "seeds plan: nf=%d nt=%d G=%d tiles=%lld tiles/cta=%d tile=%dx%d smem=%zu rec_smem=%d bins_res=%d\n",
+                    nf, nt, G, T, q.tiles_per_cta, max_tw, max_th, smem, rs, res);
         return true;
     }
     return false;
