@@ -1000,7 +1000,9 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     // old fence-based grid barrier (an L1 invalidation, CCTL.IVALL) that build
     // gave wrong c3 results; with the release / relaxed barrier it is correct
     // but only +-2% against this plan, so the spill-free plan stays.)
-    const int cps = nt == GRID_THREADS_SMALL ? GRID_SMALL_CPS : GRID_THREADS / nt;
+    int cps = nt == GRID_THREADS_SMALL ? GRID_SMALL_CPS : GRID_THREADS / nt;
+    if (const char *v = getenv("SEEDS_SMALL_CPS"); v && nt == GRID_THREADS_SMALL)  // experiments: fewer, larger CTAs' tiles
+        cps = std::max(1, std::min(GRID_SMALL_CPS, atoi(v)));
     const size_t limit = cps == 1 ? 227 * 1024 : (228 * 1024) / cps - 1024;
     const size_t tabw = (2 * (size_t)c->B + 2) * 4;
     bool need_tab = false;
