@@ -1341,6 +1341,17 @@ static cudaError_t launch_tile1(seeds_ctx *ctx, const GridParams &q, cudaStream_
     return ctx->gamma ? launch_tile1_t<uint16_t, 1, 3>(ctx, q, st) : launch_tile1_t<uint16_t, 0, 2>(ctx, q, st);
 }
 
+// k_seed_warm (word loads and stores of four pixels per thread) for a warm
+// start: three channels, rows of a multiple of four pixels, a 16-byte aligned
+// label buffer and a word-aligned image; not in row-band mode (SEEDS_WARM_VEC=0
+// keeps k_seed_cells, for A/B measurements)
+static bool warm_vec_ok(const seeds_ctx *c, const uint8_t *img, const int32_t *init)
+{
+    return init && !c->banded && c->C == 3 && c->W % 4 == 0 && ((uintptr_t)init & 15) == 0 &&
+           ((uintptr_t)img & 3) == 0 && c->lpitch % 2 == 0 && c->labp_fs % 2 == 0 && c->K <= 65536 &&
+           !getenv_off("SEEDS_WARM_VEC");
+}
+
 // Enqueue one grid-mode run: zero the histograms, move counters and the barrier
 // counter, then the single persistent launch.
 static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32_t *init, int32_t *out, int nf,
@@ -1427,7 +1438,11 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
         const int cells = ctx->banded && ctx->bsys ? ctx->bk[ctx->bself + 1] - ctx->bk[ctx->bself] : ctx->K;
         const dim3 g((unsigned)cells, (unsigned)nf);
         const size_t sm = init ? 0 : (size_t)4 * ctx->B * sizeof(int);
-        if (band_kernel(ctx)) {
+        if (warm_vec_ok(ctx, img, init)) {
+            const dim3 gr((unsigned)ctx->H, (unsigned)nf);
+            if (ctx->bb == 1) k_seed_warm<uint8_t><<<gr, 128, 0, st>>>(q);
+            else k_seed_warm<uint16_t><<<gr, 128, 0, st>>>(q);
+        } else if (band_kernel(ctx)) {
             if (ctx->bb == 1) k_seed_cells<uint8_t, 1><<<g, 256, sm, st>>>(q);
             else k_seed_cells<uint16_t, 1><<<g, 256, sm, st>>>(q);
         } else {

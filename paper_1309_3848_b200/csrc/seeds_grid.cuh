@@ -1926,4 +1926,75 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
     }
 }
 
+
+// Warm-start seed of one pixel row per CTA (a1 + a3 of a warm run, reading
+// Q13/O9: the labels come from the caller): quantise, write the bin and label
+// planes, count (label, bin) and label sizes with warp-aggregated atomics into
+// both snapshot buffers.  Each thread takes four consecutive pixels with word
+// loads and stores (the HWC image as three 32-bit words, the labels as one
+// int4, the bins as one word per four, the padded u16 labels as two words) --
+// the per-cell walk of k_seed_cells issues one load per byte.  The host uses it
+// when the row, frame and buffer alignments allow (seeds_engine.cu warm_vec_ok):
+// C = 3, W % 4 == 0, a 16-byte aligned label buffer; not in row-band mode.
+template <typename BinT>
+__global__ void __launch_bounds__(128) k_seed_warm(const GridParams q)
+{
+    const int y = blockIdx.x, f = blockIdx.y, W = q.W, B = q.B, lane = threadIdx.x & 31;
+    const long long row = (long long)f * q.N + (long long)y * W;
+    const uint32_t *img = reinterpret_cast<const uint32_t *>(q.img + row * 3);
+    const int4 *init = reinterpret_cast<const int4 *>(q.init + row);
+    BinT *bp = static_cast<BinT *>(q.binsp) + (long long)f * q.binsp_fs + (long long)y * q.bpitch;
+    uint32_t *gl = reinterpret_cast<uint32_t *>(q.lab + (long long)f * q.lab_fs + (long long)(y + 2) * q.lpitch + 2);
+    int *H0 = q.Hb[0] + (long long)f * q.H_fs, *H1 = q.Hb[1] + (long long)f * q.H_fs;
+    int *A0 = q.Ab[0] + (long long)f * q.A_fs, *A1 = q.Ab[1] + (long long)f * q.A_fs;
+    const int bpc = q.bpc, ng = W >> 2, ngr = (ng + 31) & ~31;  // warp-uniform trip count (the matches)
+    for (int g = threadIdx.x; g < ngr; g += blockDim.x) {
+        const bool in = g < ng;
+        uint32_t w0 = 0, w1 = 0, w2 = 0;
+        int4 l = make_int4(0, 0, 0, 0);
+        if (in) {
+            w0 = __ldg(img + 3 * g);
+            w1 = __ldg(img + 3 * g + 1);
+            w2 = __ldg(img + 3 * g + 2);
+            l = __ldg(init + g);
+        }
+        // bytes of the four pixels: r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
+        const uint32_t by[12] = {w0 & 0xFF, w0 >> 8 & 0xFF, w0 >> 16 & 0xFF, w0 >> 24,
+                                 w1 & 0xFF, w1 >> 8 & 0xFF, w1 >> 16 & 0xFF, w1 >> 24,
+                                 w2 & 0xFF, w2 >> 8 & 0xFF, w2 >> 16 & 0xFF, w2 >> 24};
+        int lk[4] = {l.x, l.y, l.z, l.w}, b[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            b[u] = 0;
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) b[u] = b[u] * bpc + (((int)by[3 * u + ch] * bpc) >> 8);
+            if (in) lk[u] = checked_label(lk[u], q.K, q.err);
+        }
+        if (in) {
+            if (sizeof(BinT) == 1)
+                *reinterpret_cast<uint32_t *>(bp + 4 * g) =
+                    (uint32_t)b[0] | (uint32_t)b[1] << 8 | (uint32_t)b[2] << 16 | (uint32_t)b[3] << 24;
+            else
+                *reinterpret_cast<uint2 *>(bp + 4 * g) =
+                    make_uint2((uint32_t)b[0] | (uint32_t)b[1] << 16, (uint32_t)b[2] | (uint32_t)b[3] << 16);
+            gl[2 * g] = (uint32_t)lk[0] | (uint32_t)lk[1] << 16;
+            gl[2 * g + 1] = (uint32_t)lk[2] | (uint32_t)lk[3] << 16;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int k = lk[u], key = in ? k * B + b[u] : -1;
+            unsigned m = __match_any_sync(FULL, key);
+            if (in && lane == __ffs(m) - 1) {
+                atomicAdd(H0 + key, __popc(m));
+                atomicAdd(H1 + key, __popc(m));
+            }
+            m = __match_any_sync(FULL, in ? k : -1);
+            if (in && lane == __ffs(m) - 1) {
+                atomicAdd(A0 + k, __popc(m));
+                atomicAdd(A1 + k, __popc(m));
+            }
+        }
+    }
+}
+
 }  // namespace seeds

@@ -100,3 +100,45 @@ def test_warm_seed_recounts_exactly(torch_cuda, orc, pattern):
         np.testing.assert_array_equal(a.cpu().numpy(), want.sum(1))
         np.testing.assert_array_equal(lab[fi].cpu().numpy(), init[fi])
     s.close()
+
+
+@pytest.mark.parametrize("bpc", [5, 8])
+@pytest.mark.parametrize("aligned", [True, False])
+def test_warm_seed_word_path_and_fallback(torch_cuda, orc, bpc, aligned):
+    """Warm seed of rows of a multiple of four pixels: k_seed_warm (word loads
+    of four pixels, uint8 bins for bpc=5 / uint16 for bpc=8) when the label
+    buffer is 16-byte aligned, k_seed_cells when it is not (a view one int32
+    into its allocation).  Both: H and A equal a recount of (init labels, bins),
+    the refined labels equal the oracle's warm run (PAPER.md:259-262 validity,
+    reading Q13/O9)."""
+    torch = torch_cuda
+    f = configs.frames("c1", n=2)
+    p = dict(configs.params("c1"), bins_per_channel=bpc)
+    H, W = f.shape[1:3]
+    assert W % 4 == 0
+    init = np.stack([orc.run(f[0], **p).labels, orc.run(f[1], **p).labels]).astype(np.int32)
+    s = mk(f.shape[1:], p, iters=0)
+    K, B = s.info.k_actual, s.info.bins_total
+    buf = torch.zeros(init.size + 4, dtype=torch.int32, device="cuda")
+    off = 0 if aligned else 1
+    buf[off:off + init.size] = torch.from_numpy(init.ravel()).cuda()
+    d_init = buf[off:off + init.size].view(init.shape)
+    lab = s.batch(torch.from_numpy(f).cuda(), init_labels=d_init)
+    for fi in range(2):
+        bins = bins_of(f[fi], bpc)
+        want = np.bincount((init[fi].astype(np.int64) * B + bins).ravel(), minlength=K * B).reshape(K, B)
+        h, a = s.read_state(fi)
+        np.testing.assert_array_equal(h.cpu().numpy(), want)
+        np.testing.assert_array_equal(a.cpu().numpy(), want.sum(1))
+        np.testing.assert_array_equal(lab[fi].cpu().numpy(), init[fi])
+    s.close()
+    # the whole warm run (pixel level) against the oracle
+    s = mk(f.shape[1:], p)
+    lab = s.batch(torch.from_numpy(f).cuda(), init_labels=d_init)
+    for fi in range(2):
+        r = orc.run(f[fi], **p, init_labels=init[fi])
+        h, a = s.read_state(fi)
+        np.testing.assert_array_equal(lab[fi].cpu().numpy(), r.labels)
+        np.testing.assert_array_equal(h.cpu().numpy(), r.hist)
+        np.testing.assert_array_equal(a.cpu().numpy(), r.sizes)
+    s.close()
