@@ -1438,6 +1438,8 @@ static seeds_status enqueue_grid(seeds_ctx *ctx, const uint8_t *img, const int32
         const int cells = ctx->banded && ctx->bsys ? ctx->bk[ctx->bself + 1] - ctx->bk[ctx->bself] : ctx->K;
         const dim3 g((unsigned)cells, (unsigned)nf);
         const size_t sm = init ? 0 : (size_t)4 * ctx->B * sizeof(int);
+        q.seed_vec = !init && !ctx->banded && ctx->C == 3 && ctx->W % 4 == 0 && ((uintptr_t)img & 3) == 0 &&
+                     !getenv_off("SEEDS_SEED_VEC");
         if (warm_vec_ok(ctx, img, init)) {
             const dim3 gr((unsigned)ctx->H, (unsigned)nf);
             if (ctx->bb == 1) k_seed_warm<uint8_t><<<gr, 128, 0, st>>>(q);

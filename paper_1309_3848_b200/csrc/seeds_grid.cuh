@@ -113,6 +113,7 @@ struct GridParams {
     long long S_fs;        // their frame stride (4 A_fs)
     int miters;            // the last miters pixel iterations use the means test (reading M1)
     int compact;           // compactness prior at the pixel level (reading M5)
+    int seed_vec;          // k_seed_cells (cold): word loads / stores of four pixels (C = 3, W % 4 == 0)
     int edge_tau;          // edge prior threshold (reading M6), 0 = off
     int filt2;             // 128-thread kernels: two filter units per lane (SEEDS_FILT2=0: one)
     long long *csum;       // per frame and superpixel: sum x, sum y, count (4 int64) for the centres
@@ -1814,6 +1815,66 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
         for (int i = tid; i < 4 * B; i += blockDim.x) shist[i] = 0;
         __syncthreads();
     }
+    if (!BAND && cold && q.seed_vec) {
+        // the cell as groups of four pixels at x = 0 mod 4 (those straddling the
+        // cell's left / right edge masked): the HWC image as three words per
+        // group, bins and labels stored as words when the whole group is in
+        const int gx0 = x0 >> 2, gw = ((x1 + 3) >> 2) - gx0, ng = gw * (y1 - y0), ngr = (ng + 31) & ~31;
+        const uint32_t lw = (uint32_t)cell | (uint32_t)cell << 16;
+        for (int i = tid; i < ngr; i += blockDim.x) {  // warp-uniform trip count (the matches)
+            const bool gin = i < ng;
+            const int gy = gin ? i / gw : 0;
+            const int y = y0 + gy, xb = 4 * (gx0 + (gin ? i - gy * gw : 0));
+            uint32_t w0 = 0, w1 = 0, w2 = 0;
+            if (gin) {
+                const uint32_t *v = reinterpret_cast<const uint32_t *>(q.img + (fN + (long long)y * W + xb) * 3);
+                w0 = __ldg(v);
+                w1 = __ldg(v + 1);
+                w2 = __ldg(v + 2);
+            }
+            const uint32_t by[12] = {w0 & 0xFF, w0 >> 8 & 0xFF, w0 >> 16 & 0xFF, w0 >> 24,
+                                     w1 & 0xFF, w1 >> 8 & 0xFF, w1 >> 16 & 0xFF, w1 >> 24,
+                                     w2 & 0xFF, w2 >> 8 & 0xFF, w2 >> 16 & 0xFF, w2 >> 24};
+            int b[4];
+            bool in[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                b[u] = 0;
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++) b[u] = b[u] * q.bpc + (((int)by[3 * u + ch] * q.bpc) >> 8);
+                in[u] = gin && xb + u >= x0 && xb + u < x1;
+            }
+            BinT *brow = bp + (long long)y * q.bpitch + xb;
+            uint16_t *lrow = gl + (long long)(y + 2) * q.lpitch + xb + 2;
+            if (in[0] && in[3]) {
+                if (sizeof(BinT) == 1)
+                    *reinterpret_cast<uint32_t *>(brow) =
+                        (uint32_t)b[0] | (uint32_t)b[1] << 8 | (uint32_t)b[2] << 16 | (uint32_t)b[3] << 24;
+                else
+                    *reinterpret_cast<uint2 *>(brow) =
+                        make_uint2((uint32_t)b[0] | (uint32_t)b[1] << 16, (uint32_t)b[2] | (uint32_t)b[3] << 16);
+                reinterpret_cast<uint32_t *>(lrow)[0] = lw;
+                reinterpret_cast<uint32_t *>(lrow)[1] = lw;
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (in[u]) {
+                        brow[u] = (BinT)b[u];
+                        lrow[u] = (uint16_t)cell;
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int key = in[u] ? ((y >= ym ? 2 : 0) + (xb + u >= xm ? 1 : 0)) * B + b[u] : -1;
+                if (sizeof(BinT) == 1) {
+                    const unsigned m = __match_any_sync(FULL, key);
+                    if (in[u] && lane == __ffs(m) - 1) atomicAdd(&shist[key], __popc(m));
+                } else if (in[u]) {
+                    atomicAdd(&shist[key], 1);
+                }
+            }
+        }
+    } else {
     // four pixels per thread in flight: every load of a batch is issued before
     // the first use (the cell is walked as one flat index, row-major)
     constexpr int U = 4;
@@ -1894,6 +1955,7 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
                 }
             }
         }
+    }
     }
     if (!cold) return;
     __syncthreads();
