@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/seeds.h"
+#include "tile_balance.h"
 #include "seeds_kernels.cuh"
 #include "seeds_grid.cuh"
 #include "seeds_tile1.cuh"
@@ -1149,15 +1150,51 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     q.tx_bytes = q.bw * q.bh * 2;  // + the bin box when the bins are staged (set with bins_res)
     q.tiles_per_cta = (int)((T + G - 1) / G);
     std::vector<GridTile> tiles((size_t)T);
-    for (long long t = 0; t < T; t++) {
+    // Position p of the table is slot p / G of CTA p % G, so the table's order is
+    // the assignment of tiles to CTAs: balanced by the plan score's tile cost
+    // (tile_balance.h) instead of frame order.  SEEDS_TILE_BALANCE=0 keeps frame
+    // order (A/B measurements); row-band plans keep it too (their CTAs are tied
+    // to bands).
+    std::vector<long long> order((size_t)T);
+    for (long long t = 0; t < T; t++) order[(size_t)t] = t;
+    if (T > G && nf > 1 && !c->banded && !getenv_off("SEEDS_TILE_BALANCE")) {
+        std::vector<double> cost(ft.size());
+        for (size_t i = 0; i < ft.size(); i++)
+            cost[i] = (double)tpx[i] + halo_w * ((ft[i].X1 - ft[i].X0) + (ft[i].Y1 - ft[i].Y0) + 4) + tile_cost;
+        double busiest[2];
+        order = tile_balance(cost, T, G, busiest);
+        if (getenv("SEEDS_PLAN_DEBUG"))
+            fprintf(stderr, "seeds plan: busiest CTA %.0f balanced, %.0f in frame order\n", busiest[1], busiest[0]);
+    }
+    // Experiment switch SEEDS_TILE_ORDER=rows / cols: every CTA takes a run of
+    // consecutive tiles of the row-major / column-major walk of the frames (a
+    // contiguous region per CTA) instead of every G-th tile.
+    if (const char *v = getenv("SEEDS_TILE_ORDER"); v && T > G && !c->banded && (v[0] == 'r' || v[0] == 'c')) {
+        std::vector<long long> seq;
+        seq.reserve((size_t)T);
+        const long long nft = (long long)ft.size(), nty = nft / ntx;
+        for (long long f = 0; f < nf; f++) {
+            if (v[0] == 'r') {
+                for (long long i = 0; i < nft; i++) seq.push_back(f * nft + i);
+            } else {
+                for (long long tx = 0; tx < ntx; tx++)
+                    for (long long ty = 0; ty < nty; ty++) seq.push_back(f * nft + ty * ntx + tx);
+            }
+        }
+        size_t idx = 0;
+        for (int k = 0; k < G; k++)
+            for (long long j = 0; j < (T - 1 - k) / G + 1; j++) order[(size_t)k + (size_t)j * (size_t)G] = seq[idx++];
+    }
+    for (long long p = 0; p < T; p++) {
+        const long long t = order[(size_t)p];
         const size_t i = (size_t)(t % (long long)ft.size());
         GridTile g = ft[i];
         g.f = (int)(t / (long long)ft.size());
-        const int cta = (int)(t % G);
+        const int cta = (int)(p % G);
         g.boff = (int)cpx[cta];
         cpx[cta] += tpx[i];
         crec[cta] += tr[i];
-        tiles[(size_t)t] = g;
+        tiles[(size_t)p] = g;
     }
     const long long max_cpx = *std::max_element(cpx.begin(), cpx.end());
     const long long rec_cap = *std::max_element(crec.begin(), crec.end()) + 32;
