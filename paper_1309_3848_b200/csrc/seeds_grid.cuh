@@ -1846,6 +1846,11 @@ __global__ void __launch_bounds__(256) k_seed_cells(const GridParams q)
             }
             BinT *brow = bp + (long long)y * q.bpitch + xb;
             uint16_t *lrow = gl + (long long)(y + 2) * q.lpitch + xb + 2;
+            SEEDS_CHECK(!gin || (xb >= 0 && xb + 4 <= W && (long long)y * q.bpitch + xb + 4 <= q.binsp_fs &&
+                                 (long long)(y + 2) * q.lpitch + xb + 2 + 4 <= q.lab_fs &&
+                                 (long long)(y + 1) * W <= q.N));
+#pragma unroll
+            for (int u = 0; u < 4; u++) SEEDS_CHECK(b[u] >= 0 && b[u] < B);
             if (in[0] && in[3]) {
                 if (sizeof(BinT) == 1)
                     *reinterpret_cast<uint32_t *>(brow) =
@@ -2033,6 +2038,12 @@ __global__ void __launch_bounds__(128) k_seed_warm(const GridParams q)
             if (in) lk[u] = checked_label(lk[u], q.K, q.err);
         }
         if (in) {
+            SEEDS_CHECK(4 * g + 4 <= q.bpitch && (long long)(y + 1) * q.bpitch <= q.binsp_fs &&
+                        (long long)(y + 2) * q.lpitch + 2 + 4 * g + 4 <= q.lab_fs && (long long)(y + 1) * W <= q.N);
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                SEEDS_CHECK(b[u] >= 0 && b[u] < B && lk[u] >= 0 && lk[u] < q.K &&
+                            (long long)lk[u] * B + b[u] < q.H_fs && lk[u] < q.A_fs);
             if (sizeof(BinT) == 1)
                 *reinterpret_cast<uint32_t *>(bp + 4 * g) =
                     (uint32_t)b[0] | (uint32_t)b[1] << 8 | (uint32_t)b[2] << 16 | (uint32_t)b[3] << 24;
