@@ -1053,6 +1053,7 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
     if (const char *v = getenv("SEEDS_TILE_COST")) tile_cost = atof(v);
     double halo_w = 4.0;
     if (const char *v = getenv("SEEDS_HALO_W")) halo_w = atof(v);
+    const bool plan_bal = getenv("SEEDS_PLAN_BAL") && atoi(getenv("SEEDS_PLAN_BAL")) != 0;
     for (int a : size_candidates(TX))
         for (int b : size_candidates(TYb)) {
             long long rows = 0;
@@ -1065,7 +1066,21 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
             const size_t minimal = stage + 2 * align128((size_t)(tw + 32) * th * c->bb) + align16((size_t)tw * th * 4) + fixed;
             if (minimal > limit) continue;
             const long long per = (T + G - 1) / G;
-            const double score = (double)per * tw * th + halo_w * per * (tw + th + 4) + tile_cost * per;
+            double score = (double)per * tw * th + halo_w * per * (tw + th + 4) + tile_cost * per;
+            // Experiment switch SEEDS_PLAN_BAL=1: score a multi-frame batch by what the
+            // balanced assignment reaches (the mean CTA, or what is left for the CTAs
+            // with `per` tiles when the others hold per - 1 full tiles each) instead of
+            // `per` full tiles.
+            if (plan_bal && nf > 1 && !c->banded && T > G && rng.size() == 1) {
+                const double ntx = (double)((TX + a - 1) / a), nty = (double)rows;
+                const double total = (double)nf * ((double)c->W * c->H + halo_w * ((double)c->W * nty + (double)c->H * ntx + 4 * ntx * nty) +
+                                                   tile_cost * ntx * nty);
+                const double cmax = (double)tw * th + halo_w * (tw + th + 4) + tile_cost;
+                const long long nbig = T % G;
+                double bound = total / (double)G;
+                if (nbig) bound = std::max(bound, (total - (double)(G - nbig) * (double)(per - 1) * cmax) / (double)nbig);
+                score = bound;
+            }
             if (score < best) {
                 best = score;
                 ba = a;
