@@ -1200,6 +1200,19 @@ static bool plan_try(seeds_ctx *c, int nf, int nt)
         for (int k = 0; k < G; k++)
             for (long long j = 0; j < (T - 1 - k) / G + 1; j++) order[(size_t)k + (size_t)j * (size_t)G] = seq[idx++];
     }
+    // ... =C / =P<n>: every G-th tile as in the default, but of the column-major
+    // walk / of the walk by panels of n tile columns (row-major inside a panel):
+    // the tiles worked on at the same moment form a tall block instead of a
+    // stripe over the frame's width.
+    if (const char *v = getenv("SEEDS_TILE_ORDER"); v && T > G && !c->banded && (v[0] == 'C' || v[0] == 'P')) {
+        const long long nft = (long long)ft.size(), nty = nft / ntx;
+        const long long pw = v[0] == 'P' ? std::max(1, atoi(v + 1)) : 1;
+        size_t idx = 0;
+        for (long long f = 0; f < nf; f++)
+            for (long long x0 = 0; x0 < ntx; x0 += pw)
+                for (long long ty = 0; ty < nty; ty++)
+                    for (long long tx = x0; tx < std::min<long long>(ntx, x0 + pw); tx++) order[idx++] = f * nft + ty * ntx + tx;
+    }
     for (long long p = 0; p < T; p++) {
         const long long t = order[(size_t)p];
         const size_t i = (size_t)(t % (long long)ft.size());
